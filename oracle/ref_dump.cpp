@@ -1,0 +1,410 @@
+// Golden-vector generator. TEST INFRASTRUCTURE ONLY.
+//
+// Links the unmodified reference core (compiled in place from
+// /root/reference/proj/src by oracle/Makefile into oracle/_ref/) and writes
+// JSON fixtures that pin the C restatement in oracle/espec_oracle.c:
+//   * init checksums      -> init_model            proj/src/model.cpp:38-84
+//   * the argmax-110 KAT  -> proj/tests/test_model.cpp:61-68
+//   * layer plans         -> plan_groups           proj/src/layer_plan.cpp:54-82
+//   * forward outputs     -> forward_sequential / forward_fuzzy
+//                            proj/src/draft_engine.cpp:35-133
+//   * full generations    -> generate()            proj/src/orchestrator.cpp:488-492
+//     with per-iteration traces and KV-cache checksums taken through the
+//     IterationHook (proj/include/espec/orchestrator.hpp:46-55).
+// Nothing here is shipped or measured.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <iostream>
+#include <string>
+#include <vector>
+
+#include "espec/draft_engine.hpp"
+#include "espec/errors.hpp"
+#include "espec/kv_cache.hpp"
+#include "espec/layer_plan.hpp"
+#include "espec/model.hpp"
+#include "espec/orchestrator.hpp"
+
+using namespace espec;
+using json = nlohmann::ordered_json;
+
+namespace {
+
+ModelConfig tiny(int n_layers, std::uint64_t seed, int d_model = 32, int n_heads = 2, int d_head = 16,
+                 int d_mlp = 64, int max_pos = 128) {
+    ModelConfig c;
+    c.d_model = d_model;
+    c.n_heads = n_heads;
+    c.d_head = d_head;
+    c.d_mlp = d_mlp;
+    c.n_layers = n_layers;
+    c.max_positions = max_pos;
+    c.seed = seed;
+    return c;
+}
+
+json cfg_json(const ModelConfig& c) {
+    return json{{"vocab_size", c.vocab_size}, {"d_model", c.d_model}, {"n_layers", c.n_layers},
+                {"n_heads", c.n_heads},       {"d_head", c.d_head},   {"d_mlp", c.d_mlp},
+                {"max_positions", c.max_positions}, {"norm_eps", c.norm_eps},
+                {"seed", c.seed}};
+}
+
+std::vector<Token> bos_bytes(const std::string& s) {
+    std::vector<Token> t = {kBosToken};
+    for (unsigned char c : s) t.push_back(c);
+    return t;
+}
+
+std::vector<float> as_vec(const Matrix& m) { return m.data; }
+
+// Chain prefill on a fresh/partial cache (stage + sequential pass).
+Matrix prefill(const Model& model, const std::vector<Token>& tokens, KvCache& cache, bool commit) {
+    std::vector<int> parents;
+    for (std::size_t i = 0; i < tokens.size(); ++i)
+        parents.push_back(i == 0 ? kCommittedTail : cache.committed_len() + static_cast<int>(i) - 1);
+    ForwardBatch batch;
+    batch.flat_rows = cache.stage_append(parents, false);
+    for (int r : batch.flat_rows) batch.positions.push_back(cache.position_of(r));
+    const TreeMask mask = cache.build_tree_mask();
+    batch.mask = &mask;
+    Matrix h = forward_sequential(model, embed(model, tokens), cache, batch);
+    if (commit) cache.commit_path(batch.flat_rows);
+    return h;
+}
+
+double tensor_sum(const Matrix& m) {
+    double s = 0.0;
+    for (float v : m.data) s += v;
+    return s;
+}
+
+json init_probe(const ModelConfig& cfg) {
+    const Model m = init_model(cfg);
+    json j;
+    j["config"] = cfg_json(cfg);
+    j["embedding_sum"] = tensor_sum(m.weights.embedding);
+    j["embedding_head"] = std::vector<float>(m.weights.embedding.data.begin(),
+                                             m.weights.embedding.data.begin() + 8);
+    json layers = json::array();
+    for (const auto& lw : m.weights.layers) {
+        layers.push_back(json{{"wq", tensor_sum(lw.wq)},
+                              {"wk", tensor_sum(lw.wk)},
+                              {"wv", tensor_sum(lw.wv)},
+                              {"wo", tensor_sum(lw.wo)},
+                              {"w_gate", tensor_sum(lw.w_gate)},
+                              {"w_up", tensor_sum(lw.w_up)},
+                              {"w_down", tensor_sum(lw.w_down)},
+                              {"w_down_head", std::vector<float>(lw.w_down.data.begin(),
+                                                                 lw.w_down.data.begin() + 4)}});
+    }
+    j["layers"] = layers;
+    return j;
+}
+
+// Per-layer checksum of the committed K/V rows of a cache.
+json cache_sums(const KvCache& cache) {
+    json layers = json::array();
+    for (int l = 0; l < cache.n_layers(); ++l) {
+        double ks = 0, ka = 0, vs = 0, va = 0;
+        for (int r = 0; r < cache.committed_len(); ++r) {
+            for (float v : cache.key_row(l, r)) {
+                ks += v;
+                ka += std::fabs(v);
+            }
+            for (float v : cache.value_row(l, r)) {
+                vs += v;
+                va += std::fabs(v);
+            }
+        }
+        layers.push_back(json::array({ks, ka, vs, va}));
+    }
+    return layers;
+}
+
+struct GenCase {
+    std::string name;
+    ModelConfig base;
+    int keep;  // 0 = self-draft (draft is the base model itself)
+    RunConfig run;
+    std::string prompt;
+    // Non-zero: the drafter is an independent init_model with this seed and
+    // `keep` layers (the CLI's --draft-seed path, proj/src/cli.cpp:252-257).
+    std::uint64_t draft_seed = 0;
+};
+
+RunConfig run_cfg(Algorithm a, int n, std::vector<int> widths, int lp, float temp, int max_new,
+                  std::uint64_t seed, bool calibration = true) {
+    RunConfig r;
+    r.algorithm = a;
+    r.n = n;
+    r.widths = std::move(widths);
+    r.lp_size = lp;
+    r.temperature = temp;
+    r.max_new_tokens = max_new;
+    r.seed = seed;
+    r.calibration = calibration;
+    r.workers = 1;
+    return r;
+}
+
+json run_case(const GenCase& gc) {
+    const Model base = init_model(gc.base);
+    Model draft;
+    if (gc.draft_seed != 0) {
+        ModelConfig dc = gc.base;
+        dc.n_layers = gc.keep;
+        dc.seed = gc.draft_seed;
+        draft = init_model(dc);
+    } else {
+        draft = gc.keep == 0 ? base : make_truncated_draft(base, gc.keep);
+    }
+    json iters = json::array();
+    const IterationHook hook = [&](const IterationInspection& view) {
+        iters.push_back(json{{"committed", static_cast<int>(view.committed.size())},
+                             {"draft_committed", view.draft_cache.committed_len()},
+                             {"base_committed", view.base_cache.committed_len()},
+                             {"draft_kv", cache_sums(view.draft_cache)},
+                             {"base_kv", cache_sums(view.base_cache)}});
+    };
+    json j;
+    j["name"] = gc.name;
+    j["base"] = cfg_json(gc.base);
+    j["keep"] = gc.keep;
+    j["draft_seed"] = gc.draft_seed;
+    j["run"] = json{{"algorithm", to_string(gc.run.algorithm)},
+                    {"n", gc.run.n},
+                    {"widths", gc.run.effective_widths()},
+                    {"lp_size", gc.run.lp_size},
+                    {"plan_override", gc.run.plan_override ? *gc.run.plan_override : std::string()},
+                    {"temperature", gc.run.temperature},
+                    {"max_new_tokens", gc.run.max_new_tokens},
+                    {"seed", gc.run.seed},
+                    {"calibration", gc.run.calibration}};
+    j["prompt"] = gc.prompt;
+    try {
+        const GenerateResult res = generate(
+            base, draft, gc.run,
+            {reinterpret_cast<const std::uint8_t*>(gc.prompt.data()), gc.prompt.size()}, hook);
+        j["tokens"] = res.tokens;
+        json traces = json::array();
+        for (std::size_t i = 0; i < res.report.iterations.size(); ++i) {
+            const auto& t = res.report.iterations[i];
+            json tj{{"m", t.m},
+                    {"n", t.n},
+                    {"drafted_nodes", t.drafted_nodes},
+                    {"emitted", t.emitted},
+                    {"sequential_forwards", t.sequential_forwards},
+                    {"fuzzy_forwards", t.fuzzy_forwards},
+                    {"base_forwards", t.base_forwards}};
+            for (auto& [k, v] : iters[i].items()) tj[k] = v;
+            traces.push_back(tj);
+        }
+        j["iterations"] = traces;
+        j["alpha"] = res.report.alpha;
+        j["error"] = nullptr;
+    } catch (const Error& e) {
+        j["error"] = e.what();
+    }
+    return j;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+    const std::string out_dir = argc > 1 ? argv[1] : ".";
+
+    // ---- init + numerics KATs ------------------------------------------------
+    json numerics;
+    numerics["init"] = json::array({init_probe(tiny(3, 99)), init_probe(tiny(2, 7, 64, 4, 16, 128))});
+    {
+        // proj/tests/test_model.cpp:61-68 — golden argmax 110.
+        const Model m = init_model(tiny(4, 2024));
+        KvCache cache(m.config.n_layers, m.config.d_model);
+        const Matrix h = prefill(m, bos_bytes("golden"), cache, false);
+        const Matrix logits = lm_logits(m, h);
+        const auto last = logits.row(logits.rows - 1);
+        numerics["golden_argmax"] = json{{"config", cfg_json(m.config)},
+                                         {"prompt", "golden"},
+                                         {"argmax", argmax(last)},
+                                         {"logits", std::vector<float>(last.begin(), last.end())}};
+    }
+    {
+        // Prefill K/V rows + hidden for a 2-layer d32 model.
+        const Model m = init_model(tiny(2, 7));
+        KvCache cache(m.config.n_layers, m.config.d_model);
+        const Matrix h = prefill(m, bos_bytes("ab"), cache, true);
+        json kv = json::array();
+        for (int l = 0; l < 2; ++l) {
+            std::vector<float> k, v;
+            for (int r = 0; r < cache.committed_len(); ++r) {
+                auto kr = cache.key_row(l, r);
+                auto vr = cache.value_row(l, r);
+                k.insert(k.end(), kr.begin(), kr.end());
+                v.insert(v.end(), vr.begin(), vr.end());
+            }
+            kv.push_back(json{{"k", k}, {"v", v}});
+        }
+        numerics["prefill_kv"] = json{{"config", cfg_json(m.config)},
+                                      {"prompt", "ab"},
+                                      {"hidden", as_vec(h)},
+                                      {"logits", as_vec(lm_logits(m, h))},
+                                      {"kv", kv}};
+    }
+    {
+        // proj/tests/test_model.cpp:236-269 — tree-path commit then decode.
+        const Model m = init_model(tiny(3, 43));
+        KvCache cache(m.config.n_layers, m.config.d_model);
+        prefill(m, bos_bytes("tre"), cache, true);
+        const auto roots = cache.stage_append(std::vector<int>{kCommittedTail, kCommittedTail}, false);
+        const auto kids = cache.stage_append(std::vector<int>{roots[0], roots[0]}, false);
+        const std::vector<Token> toks = {'a', 'b', 'c', 'd'};
+        ForwardBatch batch;
+        batch.flat_rows = roots;
+        batch.flat_rows.insert(batch.flat_rows.end(), kids.begin(), kids.end());
+        for (int r : batch.flat_rows) batch.positions.push_back(cache.position_of(r));
+        const TreeMask mask = cache.build_tree_mask();
+        batch.mask = &mask;
+        const Matrix tree_h = forward_sequential(m, embed(m, toks), cache, batch);
+        cache.commit_path(std::vector<int>{roots[0], kids[0]});
+        const Matrix next = prefill(m, {'e'}, cache, false);
+        numerics["tree_commit"] = json{{"config", cfg_json(m.config)},
+                                       {"tree_logits", as_vec(lm_logits(m, tree_h))},
+                                       {"next_logits", as_vec(lm_logits(m, next))}};
+    }
+    {
+        // Fuzzy vs sequential forward on a 4-token chain, 8 layers, lp 3.
+        const Model m = init_model(tiny(8, 63));
+        const std::vector<Token> toks = {kBosToken, 'f', 'u', 'z'};
+        json fz;
+        fz["config"] = cfg_json(m.config);
+        fz["tokens"] = toks;
+        for (int lp : {1, 2, 3, 4}) {
+            const LayerPlan plan = plan_groups(8, lp);
+            KvCache cache(m.config.n_layers, m.config.d_model);
+            std::vector<int> parents = {kCommittedTail, 0, 1, 2};
+            ForwardBatch batch;
+            batch.flat_rows = cache.stage_append(parents, true);
+            for (int r : batch.flat_rows) batch.positions.push_back(cache.position_of(r));
+            const TreeMask mask = cache.build_tree_mask();
+            batch.mask = &mask;
+            const Matrix h = forward_fuzzy(m, plan, embed(m, toks), cache, batch);
+            fz["lp" + std::to_string(lp)] =
+                json{{"plan", format_plan(plan)}, {"hidden", as_vec(h)}, {"logits", as_vec(lm_logits(m, h))}};
+        }
+        numerics["fuzzy"] = fz;
+    }
+    {
+        json plans = json::array();
+        const int cases[][2] = {{32, 4}, {28, 4}, {28, 8}, {24, 4}, {24, 2}, {24, 1}, {8, 2},
+                                {8, 3},  {12, 3}, {5, 2},  {2, 1},  {3, 5},  {80, 8}, {32, 8},
+                                {32, 2}, {32, 1}, {9, 4},  {10, 4}, {4, 3},  {6, 6}};
+        for (const auto& c : cases) {
+            plans.push_back(json{{"n_layers", c[0]}, {"lp", c[1]},
+                                 {"plan", format_plan(plan_groups(c[0], c[1]))}});
+        }
+        numerics["plans"] = plans;
+    }
+    {
+        std::ofstream f(out_dir + "/ref_numerics.json");
+        f << numerics.dump() << "\n";
+    }
+
+    // ---- generations ----------------------------------------------------------
+    std::vector<GenCase> cases;
+    const ModelConfig c1 = tiny(12, 7, 64, 4, 16, 128, 512);  // proj/src/cli.cpp:210-218
+    const std::vector<int> chain4 = {1, 1, 1, 1};
+    for (Algorithm a : {Algorithm::vanilla, Algorithm::sd, Algorithm::sd_tree, Algorithm::easyspec}) {
+        cases.push_back({"c1_" + to_string(a), c1, 8, run_cfg(a, 4, chain4, 2, 0.0f, 64, 1),
+                         "the quick brown fox"});
+    }
+    const ModelConfig fa = tiny(12, 21);
+    for (Algorithm a : {Algorithm::vanilla, Algorithm::sd, Algorithm::easyspec}) {
+        cases.push_back({"fixa_" + to_string(a), fa, 8, run_cfg(a, 4, chain4, 2, 0.0f, 40, 1),
+                         "Zq8#k!pL2@xR9&mW"});
+    }
+    cases.push_back({"fixa_easyspec_nocal", fa, 8,
+                     run_cfg(Algorithm::easyspec, 4, chain4, 2, 0.0f, 40, 1, false),
+                     "Zq8#k!pL2@xR9&mW"});
+    cases.push_back({"fixa_easyspec_lp4", fa, 8,
+                     run_cfg(Algorithm::easyspec, 5, {1, 1, 1, 1, 1}, 4, 0.0f, 40, 1),
+                     "Zq8#k!pL2@xR9&mW"});
+    {
+        GenCase g{"fixa_easyspec_override", fa, 8,
+                  run_cfg(Algorithm::easyspec, 4, chain4, 3, 0.0f, 40, 1), "Zq8#k!pL2@xR9&mW"};
+        g.run.plan_override = "0|1-3|4-6|7";
+        cases.push_back(g);
+    }
+    cases.push_back({"deep_easyspec_lp4", tiny(10, 77), 9,
+                     run_cfg(Algorithm::easyspec, 5, {1, 1, 1, 1, 1}, 4, 0.0f, 36, 1),
+                     "layer parallel"});
+    cases.push_back({"self_greedy", tiny(4, 83), 0,
+                     run_cfg(Algorithm::easyspec, 4, chain4, 1, 0.0f, 20, 3), "fixed point"});
+    cases.push_back({"cap7", tiny(4, 99), 0,
+                     run_cfg(Algorithm::easyspec, 4, chain4, 1, 0.0f, 7, 3), "cap"});
+    // Temperature > 0 (RNG-order parity): chains and trees.
+    cases.push_back({"t08_chain_easyspec", tiny(6, 97), 4,
+                     run_cfg(Algorithm::easyspec, 4, chain4, 2, 0.8f, 16, 3), "ranges"});
+    cases.push_back({"t08_chain_sd", tiny(6, 97), 4,
+                     run_cfg(Algorithm::sd, 4, chain4, 2, 0.8f, 16, 3), "ranges"});
+    cases.push_back({"t08_chain_vanilla", tiny(6, 97), 4,
+                     run_cfg(Algorithm::vanilla, 4, chain4, 2, 0.8f, 16, 3), "ranges"});
+    cases.push_back({"t08_tree_easyspec", tiny(6, 91), 4,
+                     run_cfg(Algorithm::easyspec, 4, {2, 2, 2, 2}, 2, 0.8f, 16, 3), "replay"});
+    cases.push_back({"t08_tree_sd_tree", tiny(6, 91), 4,
+                     run_cfg(Algorithm::sd_tree, 4, {2, 2, 2, 2}, 2, 0.8f, 16, 3), "replay"});
+    cases.push_back({"crit4_easyspec", tiny(7, 33), 5,
+                     run_cfg(Algorithm::easyspec, 3, {2, 2, 2}, 2, 0.8f, 16, 500), "calibrated"});
+    cases.push_back({"crit4_nocal", tiny(7, 33), 5,
+                     run_cfg(Algorithm::easyspec, 3, {2, 2, 2}, 2, 0.8f, 16, 500, false),
+                     "calibrated"});
+    cases.push_back({"t1_tree_wide", tiny(5, 93), 3,
+                     run_cfg(Algorithm::easyspec, 3, {3, 2, 1}, 2, 1.0f, 18, 9), "wide tree"});
+    // Greedy tree: the reference throws when a first sibling is rejected
+    // (proj/src/verifier.cpp:156-157); recorded so the oracle reproduces it.
+    cases.push_back({"greedy_tree_throws", tiny(6, 91), 4,
+                     run_cfg(Algorithm::easyspec, 4, {2, 2, 2, 2}, 2, 0.0f, 16, 3), "replay"});
+
+    // Cases with rejections (alpha < 1) so the reject/residual paths run.
+    cases.push_back({"rej_greedy_d32s21k2", tiny(8, 21, 32, 2, 16, 64, 256), 2,
+                     run_cfg(Algorithm::easyspec, 4, chain4, 2, 0.0f, 48, 1), "hello world, again"});
+    cases.push_back({"rej_greedy_sd_d32s21k2", tiny(8, 21, 32, 2, 16, 64, 256), 2,
+                     run_cfg(Algorithm::sd, 4, chain4, 2, 0.0f, 48, 1), "hello world, again"});
+    cases.push_back({"rej_greedy_vanilla_d32s21k2", tiny(8, 21, 32, 2, 16, 64, 256), 2,
+                     run_cfg(Algorithm::vanilla, 4, chain4, 2, 0.0f, 48, 1), "hello world, again"});
+    cases.push_back({"rej_greedy_d64s11k3", tiny(8, 11, 64, 4, 16, 128, 256), 3,
+                     run_cfg(Algorithm::easyspec, 4, chain4, 2, 0.0f, 48, 1), "layer parallel"});
+    {
+        GenCase g{"indep_greedy_easyspec", tiny(8, 11, 64, 4, 16, 128, 256), 5,
+                  run_cfg(Algorithm::easyspec, 5, {1, 1, 1, 1, 1}, 4, 0.0f, 40, 1), "independent"};
+        g.draft_seed = 9;
+        cases.push_back(g);
+        g.name = "indep_greedy_vanilla";
+        g.run.algorithm = Algorithm::vanilla;
+        cases.push_back(g);
+    }
+    cases.push_back({"t3_chain_easyspec", tiny(8, 5, 32, 2, 16, 64, 256), 3,
+                     run_cfg(Algorithm::easyspec, 4, chain4, 2, 3.0f, 48, 1), "the quick brown fox"});
+    cases.push_back({"t3_chain_sd", tiny(8, 5, 32, 2, 16, 64, 256), 3,
+                     run_cfg(Algorithm::sd, 4, chain4, 2, 3.0f, 48, 1), "the quick brown fox"});
+    cases.push_back({"t15_chain_easyspec_d64", tiny(8, 21, 64, 4, 16, 128, 256), 4,
+                     run_cfg(Algorithm::easyspec, 5, {1, 1, 1, 1, 1}, 4, 1.5f, 48, 2), "Zq8#k!pL2@xR9&mW"});
+    cases.push_back({"t3_tree_easyspec", tiny(8, 7, 32, 2, 16, 64, 256), 4,
+                     run_cfg(Algorithm::easyspec, 4, {2, 2, 1, 1}, 2, 3.0f, 48, 4), "tree search"});
+    cases.push_back({"t3_tree_sd_tree", tiny(8, 7, 32, 2, 16, 64, 256), 4,
+                     run_cfg(Algorithm::sd_tree, 4, {2, 2, 1, 1}, 2, 3.0f, 48, 4), "tree search"});
+    cases.push_back({"t3_tree_nocal", tiny(8, 7, 32, 2, 16, 64, 256), 4,
+                     run_cfg(Algorithm::easyspec, 4, {2, 2, 1, 1}, 2, 3.0f, 48, 4, false), "tree search"});
+
+    json gens = json::array();
+    for (const auto& gc : cases) gens.push_back(run_case(gc));
+    {
+        std::ofstream f(out_dir + "/ref_generate.json");
+        f << gens.dump() << "\n";
+    }
+    std::cout << "wrote " << out_dir << "/ref_numerics.json and ref_generate.json (" << cases.size()
+              << " generation cases)\n";
+    return 0;
+}

@@ -1,0 +1,177 @@
+/*
+ * espec_c.h — C ABI of the B200 EasySpec decode engine (libespec_b200.so).
+ *
+ * The reference (/root/reference/proj) is a C++20 static library with no
+ * FFI; its entry points are C++ functions over espec:: types. This header is
+ * the drop-in boundary that replaces them, one entry point per reference
+ * interface (cited below). Plain pointers and sizes only; nothing crosses
+ * the boundary as an exception: every call returns an espec_status and
+ * espec_last_error() carries the message (the reference's exception taxonomy,
+ * proj/include/espec/errors.hpp:11-44, maps onto the status codes).
+ *
+ * Threading: one engine = one in-flight generation; calls on one engine must
+ * be serialised (the reference's Generation is likewise single-threaded,
+ * proj/src/orchestrator.cpp:138-484). Independent engines may run on
+ * different threads.
+ */
+#ifndef ESPEC_C_H
+#define ESPEC_C_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    ESPEC_OK = 0,
+    ESPEC_CONFIG = 1,    /* ConfigError    (CLI exit code 1) */
+    ESPEC_IO = 2,        /* IoError        (CLI exit code 2) */
+    ESPEC_CHECK = 3,     /* CheckError     (CLI exit code 3) */
+    ESPEC_SHAPE = 4,     /* ShapeError */
+    ESPEC_STRUCTURE = 5, /* StructureError */
+    ESPEC_DOMAIN = 6,    /* DomainError */
+    ESPEC_CUDA = 7,      /* device / runtime failure (no reference analogue) */
+    ESPEC_NCCL = 8
+} espec_status;
+
+typedef enum { ESPEC_F32 = 0, ESPEC_BF16 = 1 } espec_dtype;
+typedef enum { ESPEC_VANILLA = 0, ESPEC_SD = 1, ESPEC_SD_TREE = 2, ESPEC_EASYSPEC = 3 } espec_algorithm;
+
+/* espec::ModelConfig (proj/include/espec/model.hpp:19-33), extended with the
+ * fields real checkpoints need (GQA, rope base, untied head, storage dtypes).
+ * n_kv_heads == n_heads, rope_theta 10000, tied_head 1, f32/f32 reproduces
+ * the reference model exactly. */
+typedef struct {
+    int vocab_size;
+    int d_model;
+    int n_layers;
+    int n_heads;
+    int n_kv_heads;
+    int d_head;
+    int d_mlp;
+    int max_positions;
+    float norm_eps;
+    float rope_theta;
+    int tied_head;
+    int weight_dtype; /* espec_dtype */
+    int kv_dtype;     /* espec_dtype */
+    uint64_t seed;
+} espec_model_cfg;
+
+/* espec::RunConfig (proj/include/espec/orchestrator.hpp:23-38). widths may be
+ * NULL (all ones); plan_override may be NULL or "" (plan_groups(L, lp_size)). */
+typedef struct {
+    int algorithm; /* espec_algorithm */
+    int n;
+    const int* widths;
+    int lp_size;
+    const char* plan_override;
+    float temperature;
+    int max_new_tokens;
+    uint64_t seed;
+    int calibration;
+} espec_run_cfg;
+
+/* Devices used by one engine. Round 1: a single device (lp/tp of 1). */
+typedef struct {
+    int device;
+    int n_lp_devices;
+    const int* lp_devices;
+    int tp_size;
+} espec_device_map;
+
+/* espec::IterationTrace (proj/include/espec/report.hpp:12-28) with real
+ * device stage times in place of the simulated units. */
+typedef struct {
+    int m, n, drafted_nodes, emitted;
+    int sequential_forwards, fuzzy_forwards, base_forwards;
+    int committed, draft_committed, base_committed;
+    int bonus;
+    float calibrate_ms, draft_ms, verify_ms;
+} espec_iteration;
+
+typedef struct espec_engine espec_engine;
+
+/* Generation(...) constructor state: caches, plan and RNG
+ * (proj/src/orchestrator.cpp:138-160). Validates both model configs and the
+ * run config (ModelConfig::validate proj/src/model.cpp:12-24,
+ * validate_run_config proj/src/orchestrator.cpp:95-118). Unlike the
+ * reference (proj/src/orchestrator.cpp:114-117) base and drafter may differ
+ * in width; they must share the vocabulary. */
+espec_status espec_engine_create(const espec_model_cfg* base, const espec_model_cfg* draft,
+                                 const espec_run_cfg* run, const espec_device_map* devices,
+                                 espec_engine** out);
+void espec_engine_destroy(espec_engine* eng);
+const char* espec_last_error(const espec_engine* eng);
+/* Error text for a failed espec_engine_create (no engine exists yet). */
+const char* espec_create_error(void);
+
+/* init_model(config) (proj/src/model.cpp:38-84). which: 0 drafter, 1 base.
+ * parity_mode 1 replays the reference's xoshiro256** stream on the host
+ * (bit-identical fp32 weights); 0 draws the same N(0, sd) rules on device
+ * (perf mode, any dtype/shape). */
+espec_status espec_init_weights_seeded(espec_engine* eng, int which, uint64_t seed, int parity_mode);
+
+/* make_truncated_draft(base, keep) (proj/src/model.cpp:86-99): the drafter
+ * aliases the base's first draft->n_layers blocks, embedding and final norm. */
+espec_status espec_share_truncated_draft(espec_engine* eng);
+
+/* Load one fp32 host tensor in the reference layout (load_model's manifest,
+ * proj/src/model_io.cpp:27-45): "embedding" VxD, "head" DxV (untied),
+ * "final_norm_gain" 1xD, per layer "wq" Dx(H*dh), "wk"/"wv" Dx(Hkv*dh),
+ * "wo" (H*dh)xD, "w_gate"/"w_up" DxF, "w_down" FxD, "attn_norm_gain",
+ * "mlp_norm_gain" 1xD. */
+espec_status espec_load_tensor(espec_engine* eng, int which, const char* name, int layer, const float* data,
+                               int64_t rows, int64_t cols);
+/* Read a tensor back in the same layout (fp32). */
+espec_status espec_read_tensor(espec_engine* eng, int which, const char* name, int layer, float* out, int64_t rows,
+                               int64_t cols);
+
+/* Replace the run config between generations (RunConfig validation). */
+espec_status espec_set_run(espec_engine* eng, const espec_run_cfg* run);
+
+/* generate(base, draft, config, prompt) (proj/src/orchestrator.cpp:488-492):
+ * prompt bytes -> BOS + bytes (tokenize_prompt, proj/src/orchestrator.cpp:42-52),
+ * run to max_new_tokens. out_tokens needs max_new_tokens entries; traces
+ * (optional) needs max_new_tokens entries; *n_iters receives the count. */
+espec_status espec_generate(espec_engine* eng, const uint8_t* prompt, int prompt_len, int32_t* out_tokens,
+                            int* n_out, espec_iteration* traces, int* n_iters);
+
+/* Stage-level API (Generation::run's loop, proj/src/orchestrator.cpp:163-195):
+ * begin() takes already-tokenized input; step() runs one iteration —
+ * run_iteration_speculative (calibrate -> draft -> verify -> resolve,
+ * proj/src/orchestrator.cpp:407-436) or run_iteration_vanilla (438-468) —
+ * and returns the tokens it emitted (<= n+1). */
+espec_status espec_begin(espec_engine* eng, const int32_t* tokens, int n_tokens);
+espec_status espec_step(espec_engine* eng, int32_t* emitted, int* n_emitted, espec_iteration* trace);
+int espec_done(const espec_engine* eng);
+
+/* IterationHook view (proj/include/espec/orchestrator.hpp:46-55): committed
+ * token count and K/V rows [row0, row0+n) of one layer of the drafter (0) or
+ * base (1) cache, n x (n_kv_heads*d_head) fp32 each. */
+espec_status espec_cache_view(espec_engine* eng, int which, int layer, int row0, int n, float* k, float* v,
+                              int* committed_len);
+espec_status espec_committed(espec_engine* eng, int32_t* tokens, int cap, int* n);
+
+/* Parity probe: one chain pass over `tokens` on a freshly reset cache of one
+ * model (forward_sequential, or forward_fuzzy when plan is "lp=N" or a plan
+ * string; proj/src/draft_engine.cpp:35-133) -> logits n x V and final hidden
+ * n x D (either may be NULL). Ends any generation in progress. */
+espec_status espec_forward(espec_engine* eng, int which, const int32_t* tokens, int n, const char* plan,
+                           float* logits, float* hidden);
+
+/* Layer plans (proj/src/layer_plan.cpp:54-128) -> formatted plan string. */
+espec_status espec_plan_groups(int n_layers, int lp_size, char* out, int out_len);
+espec_status espec_parse_plan(const char* spec, char* out, int out_len);
+
+/* Instrumentation: kernel launches issued since the last reset. */
+int espec_kernel_launches(const espec_engine* eng);
+void espec_reset_kernel_launches(espec_engine* eng);
+espec_status espec_sync(espec_engine* eng);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ESPEC_C_H */

@@ -1,0 +1,230 @@
+// extern "C" boundary (include/espec_c.h) over the C++ engine.
+#include <cstring>
+#include <string>
+
+#include "../../include/espec_c.h"
+#include "engine.h"
+
+using namespace espec;
+
+struct espec_engine {
+    std::unique_ptr<Engine> impl;
+    std::string err;
+};
+
+static thread_local std::string g_create_error;
+
+namespace {
+
+ModelCfg to_model(const espec_model_cfg* c) {
+    ModelCfg m;
+    m.vocab_size = c->vocab_size;
+    m.d_model = c->d_model;
+    m.n_layers = c->n_layers;
+    m.n_heads = c->n_heads;
+    m.n_kv_heads = c->n_kv_heads > 0 ? c->n_kv_heads : c->n_heads;
+    m.d_head = c->d_head;
+    m.d_mlp = c->d_mlp;
+    m.max_positions = c->max_positions;
+    m.norm_eps = c->norm_eps;
+    m.rope_theta = c->rope_theta > 0 ? c->rope_theta : 10000.f;
+    m.tied_head = c->tied_head;
+    m.weight_dtype = c->weight_dtype;
+    m.kv_dtype = c->kv_dtype;
+    m.seed = c->seed;
+    return m;
+}
+
+RunCfg to_run(const espec_run_cfg* r) {
+    RunCfg c;
+    c.algorithm = r->algorithm;
+    c.n = r->n;
+    if (r->widths)
+        for (int i = 0; i < r->n; ++i) c.widths.push_back(r->widths[i]);
+    c.lp_size = r->lp_size;
+    c.plan_override = r->plan_override ? r->plan_override : "";
+    c.temperature = r->temperature;
+    c.max_new_tokens = r->max_new_tokens;
+    c.seed = r->seed;
+    c.calibration = r->calibration;
+    return c;
+}
+
+void fill_trace(const IterationTrace& t, espec_iteration* o) {
+    o->m = t.m;
+    o->n = t.n;
+    o->drafted_nodes = t.drafted_nodes;
+    o->emitted = t.emitted;
+    o->sequential_forwards = t.sequential_forwards;
+    o->fuzzy_forwards = t.fuzzy_forwards;
+    o->base_forwards = t.base_forwards;
+    o->committed = t.committed;
+    o->draft_committed = t.draft_committed;
+    o->base_committed = t.base_committed;
+    o->bonus = t.bonus;
+    o->calibrate_ms = t.calibrate_ms;
+    o->draft_ms = t.draft_ms;
+    o->verify_ms = t.verify_ms;
+}
+
+template <typename F>
+espec_status guard(espec_engine* e, F&& f) {
+    if (!e) return ESPEC_CONFIG;
+    try {
+        f();
+        e->err.clear();
+        return ESPEC_OK;
+    } catch (const Error& x) {
+        e->err = x.what();
+        return (espec_status)x.status;
+    } catch (const std::exception& x) {
+        e->err = x.what();
+        return ESPEC_CHECK;
+    }
+}
+
+espec_status copy_plan(const LayerPlan& p, char* out, int out_len) {
+    const std::string s = format_plan(p);
+    if ((int)s.size() + 1 > out_len) return ESPEC_SHAPE;
+    std::memcpy(out, s.c_str(), s.size() + 1);
+    return ESPEC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+espec_status espec_engine_create(const espec_model_cfg* base, const espec_model_cfg* draft, const espec_run_cfg* run,
+                                 const espec_device_map* devices, espec_engine** out) {
+    if (!base || !draft || !run || !out) return ESPEC_CONFIG;
+    *out = nullptr;
+    try {
+        if (devices && (devices->tp_size > 1 || devices->n_lp_devices > 1))
+            throw Error(ST_CONFIG, "multi-device engines are not supported by this build");
+        auto e = new espec_engine();
+        try {
+            e->impl = make_engine(to_model(base), to_model(draft), to_run(run), devices ? devices->device : 0);
+        } catch (...) {
+            delete e;
+            throw;
+        }
+        *out = e;
+        g_create_error.clear();
+        return ESPEC_OK;
+    } catch (const Error& x) {
+        g_create_error = x.what();
+        return (espec_status)x.status;
+    } catch (const std::exception& x) {
+        g_create_error = x.what();
+        return ESPEC_CHECK;
+    }
+}
+
+void espec_engine_destroy(espec_engine* eng) { delete eng; }
+const char* espec_last_error(const espec_engine* eng) { return eng ? eng->err.c_str() : g_create_error.c_str(); }
+const char* espec_create_error(void) { return g_create_error.c_str(); }
+
+espec_status espec_init_weights_seeded(espec_engine* eng, int which, uint64_t seed, int parity_mode) {
+    return guard(eng, [&] { eng->impl->init_weights_seeded(which, seed, parity_mode != 0); });
+}
+
+espec_status espec_share_truncated_draft(espec_engine* eng) {
+    return guard(eng, [&] { eng->impl->share_truncated_draft(); });
+}
+
+espec_status espec_load_tensor(espec_engine* eng, int which, const char* name, int layer, const float* data,
+                               int64_t rows, int64_t cols) {
+    return guard(eng, [&] { eng->impl->load_tensor(which, name, layer, data, rows, cols); });
+}
+
+espec_status espec_read_tensor(espec_engine* eng, int which, const char* name, int layer, float* out, int64_t rows,
+                               int64_t cols) {
+    return guard(eng, [&] { eng->impl->weight(which, name, layer, out, rows, cols); });
+}
+
+espec_status espec_set_run(espec_engine* eng, const espec_run_cfg* run) {
+    return guard(eng, [&] { eng->impl->set_run(to_run(run)); });
+}
+
+espec_status espec_generate(espec_engine* eng, const uint8_t* prompt, int prompt_len, int32_t* out_tokens, int* n_out,
+                            espec_iteration* traces, int* n_iters) {
+    return guard(eng, [&] {
+        std::vector<int> toks = {256};  // BOS (proj/src/orchestrator.cpp:42-52)
+        for (int i = 0; i < prompt_len; ++i) toks.push_back(prompt[i]);
+        std::vector<IterationTrace> tr;
+        const std::vector<int> out = eng->impl->generate(toks, &tr);
+        for (size_t i = 0; i < out.size(); ++i) out_tokens[i] = out[i];
+        if (n_out) *n_out = (int)out.size();
+        if (traces)
+            for (size_t i = 0; i < tr.size(); ++i) fill_trace(tr[i], &traces[i]);
+        if (n_iters) *n_iters = (int)tr.size();
+    });
+}
+
+espec_status espec_begin(espec_engine* eng, const int32_t* tokens, int n_tokens) {
+    return guard(eng, [&] { eng->impl->begin(std::vector<int>(tokens, tokens + n_tokens)); });
+}
+
+espec_status espec_step(espec_engine* eng, int32_t* emitted, int* n_emitted, espec_iteration* trace) {
+    return guard(eng, [&] {
+        std::vector<int> em;
+        const IterationTrace t = eng->impl->step(em);
+        for (size_t i = 0; i < em.size(); ++i) emitted[i] = em[i];
+        if (n_emitted) *n_emitted = (int)em.size();
+        if (trace) fill_trace(t, trace);
+    });
+}
+
+int espec_done(const espec_engine* eng) { return eng && eng->impl->done() ? 1 : 0; }
+
+espec_status espec_cache_view(espec_engine* eng, int which, int layer, int row0, int n, float* k, float* v,
+                              int* committed_len) {
+    return guard(eng, [&] {
+        const int c = n > 0 ? eng->impl->cache_rows(which, layer, row0, n, k, v) : eng->impl->cache_committed(which);
+        if (committed_len) *committed_len = c;
+    });
+}
+
+espec_status espec_committed(espec_engine* eng, int32_t* tokens, int cap, int* n) {
+    return guard(eng, [&] {
+        const auto& c = eng->impl->committed();
+        const int k = std::min<int>(cap, (int)c.size());
+        for (int i = 0; i < k; ++i) tokens[i] = c[i];
+        if (n) *n = (int)c.size();
+    });
+}
+
+espec_status espec_forward(espec_engine* eng, int which, const int32_t* tokens, int n, const char* plan, float* logits,
+                           float* hidden) {
+    return guard(eng, [&] {
+        eng->impl->forward_chain(which, std::vector<int>(tokens, tokens + n), plan ? plan : "", logits, hidden);
+    });
+}
+
+espec_status espec_plan_groups(int n_layers, int lp_size, char* out, int out_len) {
+    try {
+        return copy_plan(plan_groups(n_layers, lp_size), out, out_len);
+    } catch (const Error& x) {
+        g_create_error = x.what();
+        return (espec_status)x.status;
+    }
+}
+
+espec_status espec_parse_plan(const char* spec, char* out, int out_len) {
+    try {
+        return copy_plan(parse_plan_override(spec ? spec : ""), out, out_len);
+    } catch (const Error& x) {
+        g_create_error = x.what();
+        return (espec_status)x.status;
+    }
+}
+
+int espec_kernel_launches(const espec_engine* eng) { return eng ? eng->impl->kernel_launches() : 0; }
+void espec_reset_kernel_launches(espec_engine* eng) {
+    if (eng) eng->impl->reset_launch_count();
+}
+espec_status espec_sync(espec_engine* eng) {
+    return guard(eng, [&] { eng->impl->sync(); });
+}
+
+}  // extern "C"

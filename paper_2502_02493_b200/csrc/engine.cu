@@ -1,0 +1,1329 @@
+// Host orchestrator (see engine.h). Reference: proj/src/orchestrator.cpp,
+// proj/src/draft_engine.cpp, proj/src/kv_cache.cpp, proj/src/layer_plan.cpp,
+// proj/src/model.cpp (init_model order), proj/src/verifier.cpp (acceptance).
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <sstream>
+
+#include "common.cuh"
+#include "engine.h"
+
+namespace espec {
+using namespace espec_dev;
+
+#define CUDA_OK(x)                                                                                   \
+    do {                                                                                             \
+        cudaError_t e_ = (x);                                                                        \
+        if (e_ != cudaSuccess)                                                                       \
+            throw Error(ST_CUDA, std::string(#x) + " failed: " + cudaGetErrorString(e_));            \
+    } while (0)
+
+static void cfg_fail(const std::string& m) { throw Error(ST_CONFIG, m); }
+
+// ---------------------------------------------------------------------------
+// configs and plans
+// ---------------------------------------------------------------------------
+
+void ModelCfg::validate() const {
+    // ModelConfig::validate (proj/src/model.cpp:12-24), extended with GQA.
+    if (vocab_size < 2) cfg_fail("vocab_size must be >= 2");
+    if (n_layers < 2) cfg_fail("n_layers must be >= 2");
+    if (n_heads < 1 || d_head < 2 || d_head % 2 != 0) cfg_fail("need n_heads >= 1 and an even d_head >= 2");
+    if (n_kv_heads < 1 || n_heads % n_kv_heads != 0) cfg_fail("n_heads must be a multiple of n_kv_heads");
+    if (d_mlp < 1) cfg_fail("d_mlp must be >= 1");
+    if (max_positions < 2) cfg_fail("max_positions must be >= 2");
+    if (!(norm_eps > 0.f)) cfg_fail("norm_eps must be positive");
+    if (d_model % 8 != 0) cfg_fail("d_model must be a multiple of 8");
+    if ((n_heads * d_head) % 8 != 0) cfg_fail("n_heads * d_head must be a multiple of 8");
+    if (d_mlp % 8 != 0) cfg_fail("d_mlp must be a multiple of 8");
+    if (n_heads / n_kv_heads * 1 > 64) cfg_fail("query heads per kv head must be <= 64");
+    if (weight_dtype != DT_F32 && weight_dtype != DT_BF16) cfg_fail("weight dtype must be f32 or bf16");
+    if (kv_dtype != DT_F32 && kv_dtype != DT_BF16) cfg_fail("kv dtype must be f32 or bf16");
+}
+
+std::vector<int> RunCfg::effective_widths() const {
+    if (widths.empty()) return std::vector<int>((size_t)std::max(n, 0), 1);
+    return widths;
+}
+
+int LayerPlan::n_layers() const {
+    int c = 0;
+    for (auto& g : groups) c += (int)g.size();
+    return c;
+}
+int LayerPlan::max_group_size() const {
+    int b = 0;
+    for (auto& g : groups) b = std::max(b, (int)g.size());
+    return b;
+}
+
+static void validate_plan(const LayerPlan& p) {
+    // proj/src/layer_plan.cpp:32-52
+    if (p.groups.empty()) cfg_fail("layer plan has no groups");
+    int expected = 0;
+    for (auto& g : p.groups) {
+        if (g.empty()) cfg_fail("layer plan contains an empty group");
+        for (int l : g) {
+            if (l != expected) cfg_fail("layer plan must cover layers contiguously in ascending order");
+            ++expected;
+        }
+    }
+    if (p.groups.front().size() != 1 || p.groups.back().size() != 1)
+        cfg_fail("first and last layer must be singleton groups");
+    if (p.max_group_size() > p.lp_size && p.lp_size > 0) cfg_fail("layer plan group exceeds the layer-parallel size");
+}
+
+LayerPlan plan_groups(int n_layers, int lp) {
+    // proj/src/layer_plan.cpp:54-82: 0 | 1..N-1 | N..2N-1 | ... | last
+    if (n_layers < 2) cfg_fail("layer plan needs at least 2 layers");
+    if (lp < 1) cfg_fail("layer-parallel size must be >= 1");
+    LayerPlan p;
+    p.lp_size = lp;
+    p.groups.push_back({0});
+    const int last = n_layers - 1;
+    for (int next = 1; next < last;) {
+        int end = next == 1 ? std::max(lp, 2) : next + lp;
+        end = std::min(end, last);
+        std::vector<int> g;
+        for (int l = next; l < end; ++l) g.push_back(l);
+        p.groups.push_back(g);
+        next = end;
+    }
+    p.groups.push_back({last});
+    validate_plan(p);
+    return p;
+}
+
+LayerPlan parse_plan_override(const std::string& spec) {
+    // proj/src/layer_plan.cpp:84-114
+    LayerPlan p;
+    std::stringstream ss(spec);
+    std::string tok;
+    while (std::getline(ss, tok, '|')) {
+        if (tok.empty()) cfg_fail("empty group in plan override '" + spec + "'");
+        const auto dash = tok.find('-');
+        int lo = 0, hi = 0;
+        try {
+            if (dash == std::string::npos) lo = hi = std::stoi(tok);
+            else {
+                lo = std::stoi(tok.substr(0, dash));
+                hi = std::stoi(tok.substr(dash + 1));
+            }
+        } catch (const std::exception&) {
+            cfg_fail("unparsable group '" + tok + "' in plan override");
+        }
+        if (lo < 0 || hi < lo) cfg_fail("invalid layer range '" + tok + "' in plan override");
+        std::vector<int> g;
+        for (int l = lo; l <= hi; ++l) g.push_back(l);
+        p.groups.push_back(g);
+    }
+    if (!spec.empty() && spec.back() == '|') cfg_fail("empty group in plan override '" + spec + "'");
+    p.lp_size = p.max_group_size();
+    validate_plan(p);
+    return p;
+}
+
+std::string format_plan(const LayerPlan& p) {
+    std::string out;
+    for (size_t i = 0; i < p.groups.size(); ++i) {
+        if (i) out += '|';
+        out += std::to_string(p.groups[i].front());
+        if (p.groups[i].size() > 1) out += "-" + std::to_string(p.groups[i].back());
+    }
+    return out;
+}
+
+// ---------------------------------------------------------------------------
+// host RNG (proj/include/espec/rng.hpp) — parity-mode weights and T>0 draws
+// ---------------------------------------------------------------------------
+
+struct Xoshiro {
+    uint64_t s[4];
+    explicit Xoshiro(uint64_t seed) {
+        uint64_t st = seed;
+        for (auto& w : s) {
+            uint64_t z = (st += 0x9E3779B97F4A7C15ULL);
+            z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+            z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+            w = z ^ (z >> 31);
+        }
+    }
+    static uint64_t rotl(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
+    uint64_t next() {
+        const uint64_t r = rotl(s[1] * 5, 7) * 9, t = s[1] << 17;
+        s[2] ^= s[0]; s[3] ^= s[1]; s[1] ^= s[2]; s[0] ^= s[3]; s[2] ^= t; s[3] = rotl(s[3], 45);
+        return r;
+    }
+    double uniform() { return (double)(next() >> 11) * 0x1.0p-53; }
+    float normal() {
+        const double u1 = uniform(), u2 = uniform();
+        return (float)(std::sqrt(-2.0 * std::log1p(-u1)) * std::cos(6.283185307179586 * u2));
+    }
+};
+
+// ---------------------------------------------------------------------------
+// device model
+// ---------------------------------------------------------------------------
+
+static int pad8(int n) { return (n + 7) / 8 * 8; }
+static size_t dsize(int dt) { return dt == DT_BF16 ? 2 : 4; }
+
+static uint16_t f2bf(float f) {
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    if ((u & 0x7fffffffu) > 0x7f800000u) return 0x7fc0;
+    u += 0x7fffu + ((u >> 16) & 1u);
+    return (uint16_t)(u >> 16);
+}
+static float bf2f(uint16_t b) {
+    uint32_t u = (uint32_t)b << 16;
+    float f;
+    std::memcpy(&f, &u, 4);
+    return f;
+}
+
+struct LayerDev {
+    void* wqkv = nullptr;  // [d][qkv_ld]
+    void* wo = nullptr;    // [H*dh][d]
+    void* wgu = nullptr;   // [d][gu_ld] interleaved per 128 cols
+    void* wd = nullptr;    // [f][d]
+    float* ga = nullptr;
+    float* gm = nullptr;
+};
+
+struct ModelDev {
+    ModelCfg c;
+    void* emb = nullptr;   // [V][d]
+    void* head = nullptr;  // [d][head_ld]
+    int head_ld = 0;
+    float* fgain = nullptr;
+    std::vector<LayerDev> L;
+    std::vector<void*> owned;
+    int qkv_N() const { return (c.n_heads + 2 * c.n_kv_heads) * c.d_head; }
+    int qkv_ld() const { return pad8(qkv_N()); }
+    int gu_tiles() const { return (c.d_mlp + 127) / 128; }
+    int gu_ld() const { return gu_tiles() * 256; }
+    int qdim() const { return c.n_heads * c.d_head; }
+    int kvdim() const { return c.n_kv_heads * c.d_head; }
+    void* alloc(size_t bytes) {
+        void* p = nullptr;
+        CUDA_OK(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
+        CUDA_OK(cudaMemset(p, 0, std::max<size_t>(bytes, 16)));
+        owned.push_back(p);
+        return p;
+    }
+    void allocate(bool share_layers_from_base, const ModelDev* base) {
+        const int d = c.d_model, f = c.d_mlp, V = c.vocab_size, es = (int)dsize(c.weight_dtype);
+        head_ld = pad8(V);
+        if (share_layers_from_base) {
+            emb = base->emb;
+            head = base->head;
+            head_ld = base->head_ld;
+            fgain = base->fgain;
+            L.assign(base->L.begin(), base->L.begin() + c.n_layers);
+            return;
+        }
+        emb = alloc((size_t)V * d * es);
+        head = alloc((size_t)d * head_ld * es);  // [d][V]; for a tied head, the transposed embedding
+        fgain = (float*)alloc((size_t)d * 4);
+        L.resize(c.n_layers);
+        for (auto& l : L) {
+            l.wqkv = alloc((size_t)d * qkv_ld() * es);
+            l.wo = alloc((size_t)qdim() * d * es);
+            l.wgu = alloc((size_t)d * gu_ld() * es);
+            l.wd = alloc((size_t)f * d * es);
+            l.ga = (float*)alloc((size_t)d * 4);
+            l.gm = (float*)alloc((size_t)d * 4);
+        }
+    }
+    void release() {
+        for (void* p : owned) cudaFree(p);
+        owned.clear();
+    }
+};
+
+// Upload an fp32 host block [rows][cols] into a device matrix with leading
+// dimension ld at column offset col0, converting to the weight dtype.
+static void upload_block(void* dst, int dt, long long ld, long long col0, const float* src, long long rows,
+                         long long cols, cudaStream_t s) {
+    const size_t es = dsize(dt);
+    std::vector<uint16_t> tmp16;
+    const void* h = src;
+    if (dt == DT_BF16) {
+        tmp16.resize((size_t)rows * cols);
+        for (size_t i = 0; i < tmp16.size(); ++i) tmp16[i] = f2bf(src[i]);
+        h = tmp16.data();
+    }
+    CUDA_OK(cudaMemcpy2DAsync((char*)dst + col0 * es, ld * es, h, cols * es, cols * es, rows, cudaMemcpyHostToDevice, s));
+    CUDA_OK(cudaStreamSynchronize(s));
+}
+
+static void download_block(const void* src, int dt, long long ld, long long col0, float* dst, long long rows,
+                           long long cols) {
+    const size_t es = dsize(dt);
+    std::vector<uint16_t> tmp16((size_t)rows * cols);
+    void* h = dt == DT_BF16 ? (void*)tmp16.data() : (void*)dst;
+    CUDA_OK(cudaMemcpy2D(h, cols * es, (const char*)src + col0 * es, ld * es, cols * es, rows, cudaMemcpyDeviceToHost));
+    if (dt == DT_BF16)
+        for (size_t i = 0; i < tmp16.size(); ++i) dst[i] = bf2f(tmp16[i]);
+}
+
+// ---------------------------------------------------------------------------
+// KV cache: host bookkeeping (proj/src/kv_cache.cpp) + paged device pool
+// ---------------------------------------------------------------------------
+
+constexpr int kTail = -1;  // kCommittedTail
+
+struct Staged {
+    int parent;
+    bool fuzzy;
+    int position;
+};
+
+struct Cache {
+    int n_layers = 0, n_kv = 0, dh = 0, dtype = DT_F32;
+    int committed = 0;
+    std::vector<Staged> staged;
+    // paged device pool
+    void* pool = nullptr;
+    int page_rows = 64;
+    long long page_elems = 0;
+    int n_pages = 0;
+    std::vector<int> table;        // logical block -> physical page
+    std::vector<int> free_pages;
+    int* table_dev = nullptr;
+    int mapped_blocks = 0;
+
+    int total() const { return committed + (int)staged.size(); }
+
+    void create(const ModelCfg& c, int capacity_rows) {
+        n_layers = c.n_layers;
+        n_kv = c.n_kv_heads;
+        dh = c.d_head;
+        dtype = c.kv_dtype;
+        page_elems = (long long)n_layers * 2 * n_kv * page_rows * dh;
+        n_pages = (capacity_rows + page_rows - 1) / page_rows;
+        CUDA_OK(cudaMalloc(&pool, (size_t)n_pages * page_elems * dsize(dtype)));
+        CUDA_OK(cudaMemset(pool, 0, (size_t)n_pages * page_elems * dsize(dtype)));
+        CUDA_OK(cudaMalloc(&table_dev, sizeof(int) * (size_t)n_pages));
+        CUDA_OK(cudaMemset(table_dev, 0, sizeof(int) * (size_t)n_pages));
+        table.assign(n_pages, -1);
+        free_pages.clear();
+        for (int p = n_pages - 1; p >= 0; --p) free_pages.push_back(p);
+        mapped_blocks = 0;
+    }
+    void destroy() {
+        if (pool) cudaFree(pool);
+        if (table_dev) cudaFree(table_dev);
+        pool = nullptr;
+        table_dev = nullptr;
+    }
+    KvView view() const {
+        KvView v;
+        v.pool = pool;
+        v.page_table = table_dev;
+        v.page_rows = page_rows;
+        v.n_layers = n_layers;
+        v.n_kv = n_kv;
+        v.dh = dh;
+        v.dtype = dtype;
+        v.page_elems = page_elems;
+        return v;
+    }
+    // Map pages so rows [0, rows) are backed.
+    void ensure(int rows, cudaStream_t s) {
+        const int need = (rows + page_rows - 1) / page_rows;
+        if (need > n_pages) throw Error(ST_CONFIG, "kv cache capacity exceeded");
+        const int first = mapped_blocks;
+        while (mapped_blocks < need) {
+            table[mapped_blocks] = free_pages.back();
+            free_pages.pop_back();
+            ++mapped_blocks;
+        }
+        if (need > first)
+            CUDA_OK(cudaMemcpyAsync(table_dev + first, table.data() + first, sizeof(int) * (size_t)(need - first),
+                                    cudaMemcpyHostToDevice, s));
+    }
+    void reset() {
+        committed = 0;
+        staged.clear();
+    }
+    // stage_append (proj/src/kv_cache.cpp:23-41)
+    std::vector<int> stage_append(const std::vector<int>& parents, bool fuzzy) {
+        std::vector<int> rows;
+        for (int par : parents) {
+            const int flat = total();
+            if (par != kTail && (par < committed || par >= flat))
+                throw Error(ST_STRUCTURE, "staged parent must be the committed tail or an earlier staged row");
+            const int pos = par == kTail ? committed : staged[par - committed].position + 1;
+            staged.push_back({par, fuzzy, pos});
+            rows.push_back(flat);
+        }
+        return rows;
+    }
+    int position_of(int flat) const { return flat < committed ? flat : staged[flat - committed].position; }
+    // commit_path (proj/src/kv_cache.cpp:62-94): returns the row moves.
+    void commit_path(const std::vector<int>& path, std::vector<int>& src, std::vector<int>& dst) {
+        int expect = kTail;
+        for (int flat : path) {
+            if (flat < 0 || flat >= total()) throw Error(ST_STRUCTURE, "kv row out of range");
+            if (flat < committed) throw Error(ST_STRUCTURE, "commit path entry is already committed");
+            if (staged[flat - committed].parent != expect)
+                throw Error(ST_STRUCTURE, "commit path is not a root-to-node chain");
+            expect = flat;
+        }
+        src.clear();
+        dst.clear();
+        for (size_t i = 0; i < path.size(); ++i)
+            if (path[i] != committed + (int)i) {
+                src.push_back(path[i]);
+                dst.push_back(committed + (int)i);
+            }
+        committed += (int)path.size();
+        staged.clear();
+    }
+    void discard() { staged.clear(); }  // proj/src/kv_cache.cpp:96-102
+    bool any_fuzzy() const {
+        for (auto& r : staged)
+            if (r.fuzzy) return true;
+        return false;
+    }
+};
+
+// ---------------------------------------------------------------------------
+// pinned->device staging for per-pass metadata (bump allocator per iteration)
+// ---------------------------------------------------------------------------
+
+struct Staging {
+    char* host = nullptr;
+    char* dev = nullptr;
+    size_t cap = 0, off = 0;
+    void create(size_t bytes) {
+        cap = bytes;
+        CUDA_OK(cudaMallocHost(&host, cap));
+        CUDA_OK(cudaMalloc(&dev, cap));
+    }
+    void destroy() {
+        if (host) cudaFreeHost(host);
+        if (dev) cudaFree(dev);
+        host = dev = nullptr;
+    }
+    template <typename T>
+    T* push(const T* data, size_t n, cudaStream_t s) {
+        const size_t bytes = sizeof(T) * std::max<size_t>(n, 1);
+        const size_t aligned = (bytes + 255) / 256 * 256;
+        if (off + aligned > cap) throw Error(ST_CONFIG, "pass metadata staging exhausted");
+        if (n) std::memcpy(host + off, data, sizeof(T) * n);
+        T* d = reinterpret_cast<T*>(dev + off);
+        CUDA_OK(cudaMemcpyAsync(d, host + off, bytes, cudaMemcpyHostToDevice, s));
+        off += aligned;
+        return d;
+    }
+    void reset() { off = 0; }
+};
+
+// ---------------------------------------------------------------------------
+// engine
+// ---------------------------------------------------------------------------
+
+constexpr int kChunk = 256;     // max rows per forward pass (prefill is chunked)
+constexpr int kAttnQ = 16;      // query rows per attention launch
+constexpr int kMaxNodes = 64;   // drafted tree nodes per iteration (ancestor bitmask)
+
+struct Workspace {
+    float* h = nullptr;       // [kChunk][d]
+    float* stats = nullptr;   // [kChunk][tiles]
+    float* q = nullptr;       // [G][kChunk][H*dh]
+    float* mixed = nullptr;   // [G][kChunk][H*dh]
+    float* attn = nullptr;    // [G][kChunk][d]
+    float* act = nullptr;     // [kChunk][f]
+    float* logits = nullptr;  // [8][head_ld] (parity probes)
+    float* am_val = nullptr;
+    int* am_idx = nullptr;
+    float* gemv_part = nullptr;
+    size_t gemv_part_slot = 0;
+    unsigned* gemv_tickets = nullptr;
+    int gemv_ticket_slot = 0;
+    float* attn_ws = nullptr;
+    size_t attn_ws_slot = 0;
+    unsigned* attn_tickets = nullptr;
+    int attn_ticket_slot = 0;
+    int G = 1;
+};
+
+class EngineImpl final : public Engine {
+public:
+    EngineImpl(const ModelCfg& bc, const ModelCfg& dc, const RunCfg& run, int device) : device_(device) {
+        bc.validate();
+        dc.validate();
+        if (bc.vocab_size != dc.vocab_size) cfg_fail("base and draft models must share the vocabulary");
+        base_.c = bc;
+        draft_.c = dc;
+        set_run(run);
+        CUDA_OK(cudaSetDevice(device));
+        CUDA_OK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+        for (auto& e : ev_) CUDA_OK(cudaEventCreate(&e));
+        const int cap_b = bc.max_positions + kMaxNodes + kChunk;
+        const int cap_d = dc.max_positions + kMaxNodes + kChunk;
+        bcache_.create(bc, cap_b);
+        dcache_.create(dc, cap_d);
+        staging_.create(8 << 20);
+        arena_cap_ = std::max(cap_b, cap_d) + 4 * kMaxNodes + 64;
+        tree_off_ = std::max(cap_b, cap_d);
+        am_off_ = tree_off_ + kMaxNodes;
+        out_off_ = am_off_ + kMaxNodes + 1;
+        CUDA_OK(cudaMalloc(&arena_, sizeof(int) * (size_t)arena_cap_));
+        CUDA_OK(cudaMemset(arena_, 0, sizeof(int) * (size_t)arena_cap_));
+        CUDA_OK(cudaMallocHost(&outcome_host_, sizeof(int) * 256));
+        alloc_ws(bws_, base_, 1);
+        alloc_ws(dws_, draft_, kMaxGroup);
+        base_allocated_ = draft_allocated_ = false;
+    }
+    ~EngineImpl() override {
+        cudaStreamSynchronize(stream_);
+        base_.release();
+        draft_.release();
+        bcache_.destroy();
+        dcache_.destroy();
+        staging_.destroy();
+        for (void* p : ws_owned_) cudaFree(p);
+        cudaFree(arena_);
+        cudaFreeHost(outcome_host_);
+        for (auto& e : ev_) cudaEventDestroy(e);
+        cudaStreamDestroy(stream_);
+    }
+
+    // ---------------- setup ----------------
+
+    void set_run(const RunCfg& run) override {
+        run_ = run;
+        widths_ = run.effective_widths();
+        if (run.algorithm != ALG_EASYSPEC) plan_ = plan_groups(draft_.c.n_layers, 1);
+        else if (!run.plan_override.empty()) plan_ = parse_plan_override(run.plan_override);
+        else plan_ = plan_groups(draft_.c.n_layers, run.lp_size);
+        if (plan_.n_layers() != draft_.c.n_layers)
+            cfg_fail("layer plan covers " + std::to_string(plan_.n_layers()) + " layers, drafter has " +
+                     std::to_string(draft_.c.n_layers));
+        if (plan_.max_group_size() > kMaxGroup) cfg_fail("layer-parallel groups are limited to 8 layers");
+        // validate_run_config (proj/src/orchestrator.cpp:95-118)
+        if (run.n < 1) cfg_fail("speculation length must be >= 1");
+        if (run.max_new_tokens < 1) cfg_fail("max_new_tokens must be >= 1");
+        if (run.temperature < 0.f) cfg_fail("temperature must be >= 0");
+        if ((int)widths_.size() != run.n) cfg_fail("widths must list one branching factor per speculation level");
+        for (int w : widths_) {
+            if (w < 1 || w > draft_.c.vocab_size) cfg_fail("tree widths must lie in [1, vocab]");
+            if (run.algorithm == ALG_SD && w != 1) cfg_fail("plain sd requires all tree widths = 1");
+        }
+        if (run.temperature != 0.f) cfg_fail("temperature > 0 is not supported by the device path yet");
+        long long nodes = 0, level = 1;
+        for (int w : widths_) {
+            level *= w;
+            nodes += level;
+            if (nodes > kMaxNodes) cfg_fail("drafted tree exceeds 64 nodes");
+        }
+        for (int w : widths_)
+            if (w > 16) cfg_fail("tree widths above 16 are not supported on device");
+    }
+
+    void ensure_allocated(int which) {
+        if (which == 1 && !base_allocated_) {
+            base_.allocate(false, nullptr);
+            base_allocated_ = true;
+        }
+        if (which == 0 && !draft_allocated_) {
+            draft_.allocate(false, nullptr);
+            draft_allocated_ = true;
+        }
+    }
+
+    void share_truncated_draft() override {
+        // make_truncated_draft (proj/src/model.cpp:86-99): the drafter reuses the
+        // base's embedding, final norm and first L_d blocks (no copy in HBM).
+        if (!base_allocated_) throw Error(ST_CONFIG, "initialise the base model first");
+        const ModelCfg& b = base_.c;
+        const ModelCfg& d = draft_.c;
+        if (d.n_layers < 2 || d.n_layers >= b.n_layers)
+            cfg_fail("keep_layers must satisfy 2 <= keep_layers < base layers, got " + std::to_string(d.n_layers));
+        if (d.d_model != b.d_model || d.n_heads != b.n_heads || d.n_kv_heads != b.n_kv_heads || d.d_head != b.d_head ||
+            d.d_mlp != b.d_mlp || d.weight_dtype != b.weight_dtype || d.tied_head != b.tied_head)
+            cfg_fail("truncated drafter must share the base architecture");
+        draft_.release();
+        draft_.allocate(true, &base_);
+        draft_allocated_ = true;
+    }
+
+    void init_weights_seeded(int which, uint64_t seed, bool parity) override {
+        ModelDev& M = which ? base_ : draft_;
+        M.c.seed = seed;
+        ensure_allocated(which);
+        const ModelCfg& c = M.c;
+        const int d = c.d_model, f = c.d_mlp, V = c.vocab_size;
+        const float proj_sd = 1.0f / std::sqrt((float)d);
+        const float resid = 1.0f / std::sqrt(2.0f * (float)c.n_layers);
+        const float down_sd = resid / std::sqrt((float)f);
+        const float emb_sd = 3.0f / std::sqrt((float)d);
+        if (parity) {
+            // init_model (proj/src/model.cpp:38-84): one xoshiro256** stream, fixed order.
+            if (c.n_kv_heads != c.n_heads || c.n_heads * c.d_head != d || !c.tied_head)
+                cfg_fail("parity init needs the reference architecture (MHA, tied head)");
+            Xoshiro rng(seed);
+            auto fill = [&](std::vector<float>& v, size_t n, float sd) {
+                v.resize(n);
+                for (auto& x : v) x = rng.normal() * sd;
+            };
+            std::vector<float> t;
+            fill(t, (size_t)V * d, emb_sd);
+            load_tensor(which, "embedding", -1, t.data(), V, d);
+            std::vector<float> ones((size_t)d, 1.f);
+            load_tensor(which, "final_norm_gain", -1, ones.data(), 1, d);
+            for (int l = 0; l < c.n_layers; ++l) {
+                fill(t, (size_t)d * d, proj_sd); load_tensor(which, "wq", l, t.data(), d, d);
+                fill(t, (size_t)d * d, proj_sd); load_tensor(which, "wk", l, t.data(), d, d);
+                fill(t, (size_t)d * d, proj_sd); load_tensor(which, "wv", l, t.data(), d, d);
+                fill(t, (size_t)d * d, proj_sd * resid); load_tensor(which, "wo", l, t.data(), d, d);
+                fill(t, (size_t)d * f, proj_sd); load_tensor(which, "w_gate", l, t.data(), d, f);
+                fill(t, (size_t)d * f, proj_sd); load_tensor(which, "w_up", l, t.data(), d, f);
+                fill(t, (size_t)f * d, down_sd); load_tensor(which, "w_down", l, t.data(), f, d);
+                load_tensor(which, "attn_norm_gain", l, ones.data(), 1, d);
+                load_tensor(which, "mlp_norm_gain", l, ones.data(), 1, d);
+            }
+            return;
+        }
+        // Perf mode: same std rules, drawn on device from a counter hash.
+        const int dt = c.weight_dtype;
+        uint64_t k = seed * 1000003ULL + 17;
+        launch_fill_normal(dt, M.emb, (long long)V * d, emb_sd, k++, stream_);
+        if (c.tied_head) launch_transpose(dt, M.emb, V, d, M.head, M.head_ld, stream_);
+        else launch_fill_normal(dt, M.head, (long long)d * M.head_ld, emb_sd, k++, stream_);
+        if (M.head_ld != V)
+            CUDA_OK(cudaMemset2DAsync((char*)M.head + (size_t)V * dsize(dt), (size_t)M.head_ld * dsize(dt), 0,
+                                      (size_t)(M.head_ld - V) * dsize(dt), d, stream_));
+        launch_fill_const(DT_F32, M.fgain, d, 1.f, stream_);
+        for (int l = 0; l < c.n_layers; ++l) {
+            LayerDev& L = M.L[l];
+            launch_fill_normal(dt, L.wqkv, (long long)d * M.qkv_ld(), proj_sd, k++, stream_);
+            launch_fill_normal(dt, L.wo, (long long)M.qdim() * d, proj_sd * resid, k++, stream_);
+            launch_fill_normal(dt, L.wgu, (long long)d * M.gu_ld(), proj_sd, k++, stream_);
+            launch_fill_normal(dt, L.wd, (long long)f * d, down_sd, k++, stream_);
+            launch_fill_const(DT_F32, L.ga, d, 1.f, stream_);
+            launch_fill_const(DT_F32, L.gm, d, 1.f, stream_);
+            if (f % 128) {
+                // zero the padded gate/up columns of the last interleaved tile
+                const int tiles = M.gu_tiles(), rem = f % 128;
+                const size_t es = dsize(dt);
+                char* base = (char*)L.wgu + (size_t)(tiles - 1) * 256 * es;
+                CUDA_OK(cudaMemset2DAsync(base + rem * es, M.gu_ld() * es, 0, (128 - rem) * es, d, stream_));
+                CUDA_OK(cudaMemset2DAsync(base + (128 + rem) * es, M.gu_ld() * es, 0, (128 - rem) * es, d, stream_));
+            }
+            if (M.qkv_ld() != M.qkv_N())
+                CUDA_OK(cudaMemset2DAsync((char*)L.wqkv + (size_t)M.qkv_N() * dsize(dt), M.qkv_ld() * dsize(dt), 0,
+                                          (M.qkv_ld() - M.qkv_N()) * dsize(dt), d, stream_));
+        }
+        CUDA_OK(cudaStreamSynchronize(stream_));
+        CUDA_OK(cudaGetLastError());
+    }
+
+    void load_tensor(int which, const std::string& name, int layer, const float* data, long long rows,
+                     long long cols) override {
+        ModelDev& M = which ? base_ : draft_;
+        ensure_allocated(which);
+        const ModelCfg& c = M.c;
+        const int d = c.d_model, f = c.d_mlp, V = c.vocab_size, dt = c.weight_dtype;
+        auto expect = [&](long long r, long long cc) {
+            if (rows != r || cols != cc)
+                throw Error(ST_SHAPE, "tensor " + name + " expects " + std::to_string(r) + "x" + std::to_string(cc));
+        };
+        if (name == "embedding") {
+            expect(V, d);
+            upload_block(M.emb, dt, d, 0, data, V, d, stream_);
+            if (c.tied_head) {
+                std::vector<float> t((size_t)d * V);
+                for (int v = 0; v < V; ++v)
+                    for (int j = 0; j < d; ++j) t[(size_t)j * V + v] = data[(size_t)v * d + j];
+                upload_block(M.head, dt, M.head_ld, 0, t.data(), d, V, stream_);
+            }
+            return;
+        }
+        if (name == "head") {
+            if (c.tied_head) throw Error(ST_CONFIG, "model has a tied head");
+            expect(d, V);
+            upload_block(M.head, dt, M.head_ld, 0, data, d, V, stream_);
+            return;
+        }
+        if (name == "final_norm_gain") {
+            expect(1, d);
+            CUDA_OK(cudaMemcpy(M.fgain, data, sizeof(float) * d, cudaMemcpyHostToDevice));
+            return;
+        }
+        if (layer < 0 || layer >= c.n_layers) throw Error(ST_SHAPE, "layer index out of range");
+        LayerDev& L = M.L[layer];
+        const int qd = M.qdim(), kd = M.kvdim();
+        if (name == "wq") { expect(d, qd); upload_block(L.wqkv, dt, M.qkv_ld(), 0, data, d, qd, stream_); }
+        else if (name == "wk") { expect(d, kd); upload_block(L.wqkv, dt, M.qkv_ld(), qd, data, d, kd, stream_); }
+        else if (name == "wv") { expect(d, kd); upload_block(L.wqkv, dt, M.qkv_ld(), qd + kd, data, d, kd, stream_); }
+        else if (name == "wo") { expect(qd, d); upload_block(L.wo, dt, d, 0, data, qd, d, stream_); }
+        else if (name == "w_down") { expect(f, d); upload_block(L.wd, dt, d, 0, data, f, d, stream_); }
+        else if (name == "w_gate" || name == "w_up") {
+            expect(d, f);
+            const int half = name == "w_up" ? 128 : 0;
+            std::vector<float> blk((size_t)d * 128);
+            for (int t = 0; t < M.gu_tiles(); ++t) {
+                const int w = std::min(128, f - t * 128);
+                for (int r = 0; r < d; ++r)
+                    for (int j = 0; j < w; ++j) blk[(size_t)r * w + j] = data[(size_t)r * f + t * 128 + j];
+                upload_block(L.wgu, dt, M.gu_ld(), t * 256 + half, blk.data(), d, w, stream_);
+            }
+        } else if (name == "attn_norm_gain") {
+            expect(1, d);
+            CUDA_OK(cudaMemcpy(L.ga, data, sizeof(float) * d, cudaMemcpyHostToDevice));
+        } else if (name == "mlp_norm_gain") {
+            expect(1, d);
+            CUDA_OK(cudaMemcpy(L.gm, data, sizeof(float) * d, cudaMemcpyHostToDevice));
+        } else {
+            throw Error(ST_CONFIG, "unknown tensor " + name);
+        }
+    }
+
+    void weight(int which, const std::string& name, int layer, float* out, long long rows, long long cols) override {
+        ModelDev& M = which ? base_ : draft_;
+        const ModelCfg& c = M.c;
+        const int d = c.d_model, f = c.d_mlp, dt = c.weight_dtype;
+        if (name == "embedding") return download_block(M.emb, dt, d, 0, out, rows, cols);
+        if (name == "head") return download_block(M.head, dt, M.head_ld, 0, out, rows, cols);
+        if (name == "final_norm_gain") { CUDA_OK(cudaMemcpy(out, M.fgain, 4 * d, cudaMemcpyDeviceToHost)); return; }
+        LayerDev& L = M.L.at(layer);
+        const int qd = M.qdim(), kd = M.kvdim();
+        if (name == "wq") return download_block(L.wqkv, dt, M.qkv_ld(), 0, out, d, qd);
+        if (name == "wk") return download_block(L.wqkv, dt, M.qkv_ld(), qd, out, d, kd);
+        if (name == "wv") return download_block(L.wqkv, dt, M.qkv_ld(), qd + kd, out, d, kd);
+        if (name == "wo") return download_block(L.wo, dt, d, 0, out, qd, d);
+        if (name == "w_down") return download_block(L.wd, dt, d, 0, out, f, d);
+        if (name == "w_gate" || name == "w_up") {
+            const int half = name == "w_up" ? 128 : 0;
+            std::vector<float> blk((size_t)d * 128);
+            for (int t = 0; t < M.gu_tiles(); ++t) {
+                const int w = std::min(128, f - t * 128);
+                download_block(L.wgu, dt, M.gu_ld(), t * 256 + half, blk.data(), d, w);
+                for (int r = 0; r < d; ++r)
+                    for (int j = 0; j < w; ++j) out[(size_t)r * f + t * 128 + j] = blk[(size_t)r * w + j];
+            }
+            return;
+        }
+        throw Error(ST_CONFIG, "unknown tensor " + name);
+    }
+
+    // ---------------- workspaces ----------------
+
+    void* wsalloc(size_t bytes) {
+        void* p = nullptr;
+        CUDA_OK(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
+        CUDA_OK(cudaMemset(p, 0, std::max<size_t>(bytes, 16)));
+        ws_owned_.push_back(p);
+        return p;
+    }
+
+    void alloc_ws(Workspace& W, const ModelDev& M, int G) {
+        const ModelCfg& c = M.c;
+        const int d = c.d_model, qd = c.n_heads * c.d_head, f = c.d_mlp;
+        const int tiles = (d + kStatTile - 1) / kStatTile;
+        const int head_ld = pad8(c.vocab_size);
+        W.G = G;
+        W.h = (float*)wsalloc(sizeof(float) * kChunk * d);
+        W.stats = (float*)wsalloc(sizeof(float) * kChunk * tiles);
+        W.q = (float*)wsalloc(sizeof(float) * (size_t)G * kChunk * qd);
+        W.mixed = (float*)wsalloc(sizeof(float) * (size_t)G * kChunk * qd);
+        W.attn = (float*)wsalloc(sizeof(float) * (size_t)G * kChunk * d);
+        W.act = (float*)wsalloc(sizeof(float) * (size_t)kChunk * f);
+        W.logits = (float*)wsalloc(sizeof(float) * 8 * (size_t)head_ld);
+        const GemvPlan hp = gemv_plan(d, c.vocab_size);
+        W.am_val = (float*)wsalloc(sizeof(float) * kChunk * hp.tiles);
+        W.am_idx = (int*)wsalloc(sizeof(int) * kChunk * hp.tiles);
+        const int qkv_N = (c.n_heads + 2 * c.n_kv_heads) * c.d_head;
+        const int gu_N = 2 * ((f + 127) / 128) * 128;
+        size_t part = 0;
+        int tick = 0;
+        const int shapes[5][2] = {{d, qkv_N}, {qd, d}, {d, gu_N}, {f, d}, {d, c.vocab_size}};
+        for (auto& s : shapes) {
+            part = std::max(part, gemv_partial_floats(s[0], s[1]));
+            tick = std::max(tick, gemv_plan(s[0], s[1]).tiles + 1);
+        }
+        W.gemv_part_slot = part;
+        W.gemv_ticket_slot = tick;
+        W.gemv_part = (float*)wsalloc(sizeof(float) * part * kMaxProblems);
+        W.gemv_tickets = (unsigned*)wsalloc(sizeof(unsigned) * (size_t)tick * kMaxProblems);
+        const int cap = c.max_positions + kMaxNodes + kChunk;
+        W.attn_ws_slot = attn_ws_floats(kAttnQ, c.n_heads, c.d_head, cap);
+        W.attn_ticket_slot = (int)attn_tickets(kAttnQ, c.n_heads, c.n_kv_heads);
+        W.attn_ws = (float*)wsalloc(sizeof(float) * W.attn_ws_slot * G);
+        W.attn_tickets = (unsigned*)wsalloc(sizeof(unsigned) * (size_t)W.attn_ticket_slot * G);
+    }
+
+    // ---------------- forward passes ----------------
+
+    struct Pass {
+        PassView view;
+        const int* tok_idx = nullptr;
+        int T = 0;
+    };
+
+    // Stage rows (already appended to the cache bookkeeping) -> device pass.
+    // Visibility restates build_tree_mask (proj/src/kv_cache.cpp:43-60)
+    // without the dense n x n mask: a staged query sees every committed row,
+    // the longest run of leading staged rows that are all its ancestors
+    // (vis_end), and any further ancestors as bits of a 64-bit mask over the
+    // rows after tree_base (the shortest such run over the pass's queries).
+    Pass make_pass(Cache& C, const std::vector<int>& rows, const std::vector<int>& tok_idx) {
+        const int T = (int)rows.size();
+        const int base = C.committed, S = (int)C.staged.size();
+        std::vector<int> pos(T), vis(T), k_run(T, 0);
+        std::vector<unsigned long long> anc(T, 0ull);
+        std::vector<std::vector<int>> ancestors(T);
+        std::vector<char> is_anc(S, 0);
+        int k_min = S;
+        for (int t = 0; t < T; ++t) {
+            const int r = rows[t];
+            pos[t] = C.position_of(r);
+            if (r < base) {
+                vis[t] = r + 1;
+                continue;
+            }
+            std::fill(is_anc.begin(), is_anc.end(), 0);
+            for (int node = r; node != kTail; node = C.staged[node - base].parent) {
+                is_anc[node - base] = 1;
+                ancestors[t].push_back(node);
+            }
+            int k = 0;
+            while (k < S && is_anc[k]) ++k;
+            k_run[t] = k;
+            vis[t] = base + k;
+            k_min = std::min(k_min, k);
+        }
+        const int tree_base = base + k_min;
+        for (int t = 0; t < T; ++t) {
+            for (int node : ancestors[t]) {
+                if (node < vis[t]) continue;
+                const int o = node - tree_base;
+                if (o >= 64) throw Error(ST_CONFIG, "tree region exceeds 64 rows");
+                anc[t] |= 1ull << o;
+            }
+        }
+        C.ensure(C.total(), stream_);
+        Pass p;
+        p.T = T;
+        p.view.T = T;
+        p.view.rows = staging_.push(rows.data(), T, stream_);
+        p.view.pos = staging_.push(pos.data(), T, stream_);
+        p.view.vis_end = staging_.push(vis.data(), T, stream_);
+        p.view.anc = staging_.push(anc.data(), T, stream_);
+        p.view.tree_base = tree_base;
+        p.view.total = C.total();
+        p.tok_idx = staging_.push(tok_idx.data(), T, stream_);
+        return p;
+    }
+
+    GemvProblem gp(Workspace& W, int slot) {
+        GemvProblem p;
+        p.partial = W.gemv_part + W.gemv_part_slot * slot;
+        p.tickets = W.gemv_tickets + (size_t)W.gemv_ticket_slot * slot;
+        return p;
+    }
+
+    // forward_sequential / forward_fuzzy (proj/src/draft_engine.cpp:35-133)
+    void forward(ModelDev& M, Cache& C, Workspace& W, const LayerPlan* plan, const Pass& ps) {
+        const ModelCfg& c = M.c;
+        const int d = c.d_model, T = ps.T, qd = M.qdim(), f = c.d_mlp;
+        const int tiles = (d + kStatTile - 1) / kStatTile;
+        const int wdt = c.weight_dtype;
+        const KvView kv = C.view();
+        launch_embed(wdt, M.emb, d, arena_, ps.tok_idx, T, W.h, W.stats, stream_);
+        ++launches_;
+        std::vector<std::vector<int>> groups;
+        if (plan) groups = plan->groups;
+        else
+            for (int l = 0; l < c.n_layers; ++l) groups.push_back({l});
+        for (const auto& g : groups) {
+            const int n = (int)g.size();
+            // attention of every layer in the group reads the group-entry state
+            GemvBatch qb;
+            for (int i = 0; i < n; ++i) {
+                GemvProblem p = gp(W, i);
+                const LayerDev& L = M.L[g[i]];
+                p.W = L.wqkv; p.K = d; p.N = M.qkv_N(); p.ldw = M.qkv_ld();
+                p.x = W.h; p.ldx = d; p.gain = L.ga; p.stats_in = W.stats; p.stat_tiles_in = tiles; p.eps = c.norm_eps;
+                p.out = W.q + (size_t)i * kChunk * qd; p.ldo = qd;
+                p.n_heads = c.n_heads; p.n_kv = c.n_kv_heads; p.dh = c.d_head; p.layer = g[i]; p.rope_theta = c.rope_theta;
+                qb.p[i] = p;
+            }
+            launch_gemv(EPI_QKV, wdt, qb, n, T, ps.view, kv, stream_);
+            launches_ += (T + 7) / 8;
+            attention(M, C, W, g, ps);
+            if (n == 1) {
+                const LayerDev& L = M.L[g[0]];
+                GemvBatch ob;
+                GemvProblem p = gp(W, 0);
+                p.W = L.wo; p.K = qd; p.N = d; p.ldw = d; p.x = W.mixed; p.ldx = qd;
+                p.out = W.h; p.ldo = d; p.resid = W.h; p.ldr = d; p.stats_out = W.stats; p.stat_tiles_out = tiles;
+                ob.p[0] = p;
+                launch_gemv(EPI_RESID, wdt, ob, 1, T, ps.view, kv, stream_);
+                launches_ += (T + 7) / 8;
+            } else {
+                GemvBatch ob;
+                for (int i = 0; i < n; ++i) {
+                    GemvProblem p = gp(W, i);
+                    p.W = M.L[g[i]].wo; p.K = qd; p.N = d; p.ldw = d;
+                    p.x = W.mixed + (size_t)i * kChunk * qd; p.ldx = qd;
+                    p.out = W.attn + (size_t)i * kChunk * d; p.ldo = d;
+                    ob.p[i] = p;
+                }
+                launch_gemv(EPI_STORE, wdt, ob, n, T, ps.view, kv, stream_);
+                launches_ += (T + 7) / 8;
+            }
+            // residual / MLP chain stays sequential (proj/src/draft_engine.cpp:112-130)
+            for (int i = 0; i < n; ++i) {
+                const LayerDev& L = M.L[g[i]];
+                if (n > 1) {
+                    launch_add_stats(W.h, W.attn + (size_t)i * kChunk * d, d, T, W.stats, stream_);
+                    ++launches_;
+                }
+                GemvBatch ub;
+                GemvProblem p = gp(W, 0);
+                p.W = L.wgu; p.K = d; p.N = 2 * M.gu_tiles() * 128; p.ldw = M.gu_ld();
+                p.x = W.h; p.ldx = d; p.gain = L.gm; p.stats_in = W.stats; p.stat_tiles_in = tiles; p.eps = c.norm_eps;
+                p.out = W.act; p.ldo = f;
+                ub.p[0] = p;
+                // EPI_SILU guards j < N/2 = padded f; outputs beyond f land in act padding
+                ub.p[0].N = 2 * f;
+                launch_gemv(EPI_SILU, wdt, ub, 1, T, ps.view, kv, stream_);
+                GemvBatch db;
+                GemvProblem q = gp(W, 0);
+                q.W = L.wd; q.K = f; q.N = d; q.ldw = d; q.x = W.act; q.ldx = f;
+                q.out = W.h; q.ldo = d; q.resid = W.h; q.ldr = d; q.stats_out = W.stats; q.stat_tiles_out = tiles;
+                db.p[0] = q;
+                launch_gemv(EPI_RESID, wdt, db, 1, T, ps.view, kv, stream_);
+                launches_ += 2 * ((T + 7) / 8);
+            }
+        }
+    }
+
+    void attention(ModelDev& M, Cache& C, Workspace& W, const std::vector<int>& g, const Pass& ps) {
+        const int qd = M.qdim();
+        const KvView kv = C.view();
+        for (int t0 = 0; t0 < ps.T; t0 += kAttnQ) {
+            const int tc = std::min(kAttnQ, ps.T - t0);
+            PassView v = ps.view;
+            v.T = tc;
+            v.rows += t0; v.pos += t0; v.vis_end += t0; v.anc += t0;
+            AttnBatch ab;
+            for (size_t i = 0; i < g.size(); ++i) {
+                AttnProblem a;
+                a.q = W.q + i * (size_t)kChunk * qd + (size_t)t0 * qd;
+                a.out = W.mixed + i * (size_t)kChunk * qd + (size_t)t0 * qd;
+                a.layer = g[i];
+                a.ws = W.attn_ws + W.attn_ws_slot * i;
+                a.tickets = W.attn_tickets + (size_t)W.attn_ticket_slot * i;
+                ab.p[i] = a;
+            }
+            launch_attention(ab, (int)g.size(), M.c.n_heads, v, kv, stream_);
+            ++launches_;
+        }
+    }
+
+    // final norm + head over n rows starting at row r0 -> argmax token ids
+    // (lm_logits proj/src/model.cpp:212-215, argmax proj/src/matrix.cpp:196-202)
+    void head(ModelDev& M, Workspace& W, int r0, int n, int* tok_out, float* logits) {
+        const ModelCfg& c = M.c;
+        const int d = c.d_model, tiles = (d + kStatTile - 1) / kStatTile;
+        GemvBatch hb;
+        GemvProblem p = gp(W, 0);
+        p.W = M.head; p.K = d; p.N = c.vocab_size; p.ldw = M.head_ld;
+        p.x = W.h + (size_t)r0 * d; p.ldx = d; p.gain = M.fgain; p.stats_in = W.stats + (size_t)r0 * tiles;
+        p.stat_tiles_in = tiles; p.eps = c.norm_eps;
+        p.vocab = c.vocab_size; p.logits = logits; p.ld_logits = M.head_ld;
+        p.am_val = W.am_val; p.am_idx = W.am_idx; p.tok_out = tok_out;
+        hb.p[0] = p;
+        PassView none;
+        launch_gemv(EPI_ARGMAX, c.weight_dtype, hb, 1, n, none, KvView(), stream_);
+        launches_ += (n + 7) / 8;
+    }
+
+    // Stage the committed tokens a cache is missing as a chain and run it,
+    // in chunks of kChunk rows, committing every chunk but (optionally) the
+    // last kept_tail rows. Returns the staged rows of the final chunk.
+    std::vector<int> chain_pass(ModelDev& M, Cache& C, Workspace& W, int from, int to, const LayerPlan* plan,
+                                bool fuzzy, bool commit_last, int keep_uncommitted) {
+        std::vector<int> rows;
+        int s = from;
+        while (s < to) {
+            const int e = std::min(to, s + kChunk);
+            const bool last = e == to;
+            std::vector<int> parents, tok;
+            for (int i = s; i < e; ++i) {
+                parents.push_back(i == s ? kTail : C.committed + (i - s) - 1);
+                tok.push_back(i);
+            }
+            rows = C.stage_append(parents, fuzzy);
+            Pass ps = make_pass(C, rows, tok);
+            forward(M, C, W, plan, ps);
+            if (!last || commit_last) {
+                std::vector<int> a, b;
+                C.commit_path(rows, a, b);
+            }
+            s = e;
+            (void)keep_uncommitted;
+        }
+        return rows;
+    }
+
+    void begin(const std::vector<int>& tokens) override {
+        CUDA_OK(cudaStreamSynchronize(stream_));
+        if (!base_allocated_ || !draft_allocated_) throw Error(ST_CONFIG, "models are not initialised");
+        for (int t : tokens)
+            if (t < 0 || t >= base_.c.vocab_size) cfg_fail("token " + std::to_string(t) + " outside vocabulary");
+        if (tokens.empty()) cfg_fail("empty prompt");
+        const int needed = (int)tokens.size() + run_.max_new_tokens + run_.n;
+        const int room = std::min(base_.c.max_positions, draft_.c.max_positions);
+        if (needed > room)
+            cfg_fail("prompt plus max_new_tokens exceeds max_positions (" + std::to_string(needed) + " > " +
+                     std::to_string(room) + ")");
+        committed_ = tokens;
+        generated_ = 0;
+        draft_cached_ = 0;
+        bcache_.reset();
+        dcache_.reset();
+        staging_.reset();
+        CUDA_OK(cudaMemcpyAsync(arena_, committed_.data(), sizeof(int) * committed_.size(), cudaMemcpyHostToDevice,
+                                stream_));
+        CUDA_OK(cudaStreamSynchronize(stream_));
+    }
+
+    bool done() const override { return generated_ >= run_.max_new_tokens; }
+
+    IterationTrace step(std::vector<int>& emitted) override {
+        if (committed_.empty()) throw Error(ST_CONFIG, "call begin() first");
+        IterationTrace tr = run_.algorithm == ALG_VANILLA ? step_vanilla(emitted) : step_speculative(emitted);
+        tr.committed = (int)committed_.size();
+        tr.draft_committed = dcache_.committed;
+        tr.base_committed = bcache_.committed;
+        return tr;
+    }
+
+    // run_iteration_vanilla (proj/src/orchestrator.cpp:438-468)
+    IterationTrace step_vanilla(std::vector<int>& emitted) {
+        IterationTrace tr;
+        staging_.reset();
+        CUDA_OK(cudaEventRecord(ev_[0], stream_));
+        const int n0 = (int)committed_.size();
+        std::vector<int> rows = chain_pass(base_, bcache_, bws_, bcache_.committed, n0, nullptr, false, false, 0);
+        head(base_, bws_, (int)rows.size() - 1, 1, arena_ + n0, nullptr);
+        CUDA_OK(cudaMemcpyAsync(outcome_host_, arena_ + n0, sizeof(int), cudaMemcpyDeviceToHost, stream_));
+        CUDA_OK(cudaEventRecord(ev_[3], stream_));
+        CUDA_OK(cudaEventSynchronize(ev_[3]));
+        CUDA_OK(cudaGetLastError());
+        std::vector<int> a, b;
+        bcache_.commit_path(rows, a, b);
+        const int next = outcome_host_[0];
+        committed_.push_back(next);
+        emitted.push_back(next);
+        ++generated_;
+        tr.emitted = 1;
+        tr.base_forwards = 1;
+        tr.bonus = next;
+        CUDA_OK(cudaEventElapsedTime(&tr.verify_ms, ev_[0], ev_[3]));
+        return tr;
+    }
+
+    // run_iteration_speculative (proj/src/orchestrator.cpp:407-436)
+    IterationTrace step_speculative(std::vector<int>& emitted) {
+        IterationTrace tr;
+        tr.n = run_.n;
+        staging_.reset();
+        const bool easy = run_.algorithm == ALG_EASYSPEC;
+        const bool calibrated = easy && run_.calibration;
+        const bool fuzzy_lead = easy && !run_.calibration;
+        const int n_comm = (int)committed_.size();
+
+        // ---- drafter leading pass = bonus calibration (orchestrator.cpp:256-300)
+        CUDA_OK(cudaEventRecord(ev_[0], stream_));
+        std::vector<int> lead_rows = chain_pass(draft_, dcache_, dws_, draft_cached_, n_comm,
+                                                fuzzy_lead ? &plan_ : nullptr, fuzzy_lead, true, 0);
+        draft_cached_ = n_comm;
+        if (fuzzy_lead) ++tr.fuzzy_forwards;
+        else ++tr.sequential_forwards;
+        // root logits -> level-1 candidates
+        const int lead_T = (int)lead_rows.size();
+        CUDA_OK(cudaEventRecord(ev_[1], stream_));
+
+        // ---- draft_tree (proj/src/draft_engine.cpp:188-289)
+        // Host tree shape: nodes level by level, siblings contiguous.
+        struct Node { int parent, depth, first_child = -1, n_children = 0, cache_row = -1; };
+        std::vector<Node> nodes;
+        std::vector<int> frontier;
+        for (int i = 0; i < widths_[0]; ++i) {
+            nodes.push_back({-1, 1});
+            frontier.push_back(i);
+        }
+        select(draft_, dws_, lead_T - 1, 1, widths_[0], {0});
+        for (int level = 1; level <= run_.n - 1 && !frontier.empty(); ++level) {
+            std::vector<int> parents, tok;
+            for (int idx : frontier) {
+                const Node& nd = nodes[idx];
+                parents.push_back(nd.parent < 0 ? kTail : nodes[nd.parent].cache_row);
+                tok.push_back(tree_off_ + idx);
+            }
+            std::vector<int> rows = dcache_.stage_append(parents, easy);
+            for (size_t i = 0; i < frontier.size(); ++i) nodes[frontier[i]].cache_row = rows[i];
+            Pass ps = make_pass(dcache_, rows, tok);
+            forward(draft_, dcache_, dws_, easy ? &plan_ : nullptr, ps);
+            if (easy) ++tr.fuzzy_forwards;
+            else ++tr.sequential_forwards;
+            std::vector<int> next, first_child;
+            for (int idx : frontier) {
+                nodes[idx].first_child = (int)nodes.size();
+                nodes[idx].n_children = widths_[level];
+                first_child.push_back((int)nodes.size());
+                for (int k = 0; k < widths_[level]; ++k) {
+                    nodes.push_back({idx, level + 1});
+                    next.push_back((int)nodes.size() - 1);
+                }
+            }
+            select(draft_, dws_, 0, (int)frontier.size(), widths_[level], first_child);
+            frontier = next;
+        }
+        tr.drafted_nodes = (int)nodes.size();
+        CUDA_OK(cudaEventRecord(ev_[2], stream_));
+
+        // ---- verify_stage (orchestrator.cpp:333-388)
+        const int nn = (int)nodes.size();
+        // committed tokens the base has no rows for: all but the frontier token
+        // are prefilled chunk-wise first (equivalent to one pass: causal rows).
+        if (n_comm - 1 > bcache_.committed)
+            chain_pass(base_, bcache_, bws_, bcache_.committed, n_comm - 1, nullptr, false, true, 0);
+        std::vector<int> parents, tok;
+        parents.push_back(kTail);
+        tok.push_back(n_comm - 1);
+        std::vector<int> chain_rows = bcache_.stage_append(parents, false);
+        const int first_node_row = chain_rows.back() + 1;
+        parents.clear();
+        for (int j = 0; j < nn; ++j) {
+            parents.push_back(nodes[j].parent < 0 ? chain_rows.back() : first_node_row + nodes[j].parent);
+        }
+        std::vector<int> node_rows = bcache_.stage_append(parents, false);
+        std::vector<int> all_rows = chain_rows;
+        all_rows.insert(all_rows.end(), node_rows.begin(), node_rows.end());
+        for (int j = 0; j < nn; ++j) tok.push_back(tree_off_ + j);
+        Pass ps = make_pass(bcache_, all_rows, tok);
+        forward(base_, bcache_, bws_, nullptr, ps);
+        ++tr.base_forwards;
+        head(base_, bws_, 0, 1 + nn, arena_ + am_off_, nullptr);
+        // acceptance on device
+        std::vector<int> np(nn), nfc(nn), nnc(nn), nti(nn);
+        int root_children = 0;
+        for (int j = 0; j < nn; ++j) {
+            np[j] = nodes[j].parent;
+            nfc[j] = nodes[j].first_child;
+            nnc[j] = nodes[j].n_children;
+            nti[j] = tree_off_ + j;
+            if (nodes[j].parent < 0) ++root_children;
+        }
+        AcceptArgs aa;
+        aa.n_nodes = nn;
+        aa.n_levels = run_.n;
+        aa.root_children = root_children;
+        aa.node_parent = staging_.push(np.data(), nn, stream_);
+        aa.node_first_child = staging_.push(nfc.data(), nn, stream_);
+        aa.node_n_children = staging_.push(nnc.data(), nn, stream_);
+        aa.node_tok_idx = staging_.push(nti.data(), nn, stream_);
+        aa.tok_arena = arena_;
+        aa.base_argmax = arena_ + am_off_;
+        aa.outcome = arena_ + out_off_;
+        aa.tok_arena_w = arena_;
+        aa.commit_at = n_comm;
+        launch_accept_greedy(aa, stream_);
+        ++launches_;
+        const int out_n = 2 + 2 * run_.n;
+        CUDA_OK(cudaMemcpyAsync(outcome_host_, arena_ + out_off_, sizeof(int) * out_n, cudaMemcpyDeviceToHost, stream_));
+        CUDA_OK(cudaEventRecord(ev_[3], stream_));
+        CUDA_OK(cudaEventSynchronize(ev_[3]));
+        CUDA_OK(cudaGetLastError());
+
+        const int m = outcome_host_[0], bonus = outcome_host_[1];
+        std::vector<int> path(outcome_host_ + 2, outcome_host_ + 2 + m);
+        // base keeps the chain + accepted path (orchestrator.cpp:379-383)
+        std::vector<int> commit_rows = chain_rows;
+        for (int ni : path) commit_rows.push_back(node_rows[ni]);
+        std::vector<int> src, dst;
+        bcache_.commit_path(commit_rows, src, dst);
+        move_rows(bcache_, src, dst);
+        // resolve_draft_cache (orchestrator.cpp:390-405)
+        if (calibrated) {
+            dcache_.discard();
+        } else {
+            std::vector<int> drows;
+            for (int ni : path) {
+                if (nodes[ni].cache_row < 0) break;
+                drows.push_back(nodes[ni].cache_row);
+            }
+            dcache_.commit_path(drows, src, dst);
+            move_rows(dcache_, src, dst);
+            draft_cached_ += (int)drows.size();
+        }
+        for (int i = 0; i < m; ++i) committed_.push_back(outcome_host_[2 + run_.n + i]);
+        committed_.push_back(bonus);
+        const int remaining = run_.max_new_tokens - generated_;
+        const int emit = std::min(m + 1, remaining);
+        for (int i = 0; i < emit; ++i) emitted.push_back(committed_[committed_.size() - (m + 1) + i]);
+        generated_ += emit;
+        tr.m = m;
+        tr.emitted = emit;
+        tr.bonus = bonus;
+        float ms = 0;
+        CUDA_OK(cudaEventElapsedTime(&ms, ev_[0], ev_[1]));
+        if (calibrated) tr.calibrate_ms = ms;
+        else tr.draft_ms = ms;
+        CUDA_OK(cudaEventElapsedTime(&ms, ev_[1], ev_[2]));
+        tr.draft_ms += ms;
+        CUDA_OK(cudaEventElapsedTime(&tr.verify_ms, ev_[2], ev_[3]));
+        return tr;
+    }
+
+    // select_children at temperature 0 (proj/src/draft_engine.cpp:141-160):
+    // width 1 = argmax straight from the head epilogue; wider = top-k.
+    void select(ModelDev& M, Workspace& W, int r0, int n, int width, const std::vector<int>& first_node) {
+        if (width == 1) {
+            // children of consecutive frontier rows are consecutive nodes
+            bool contiguous = true;
+            for (int i = 1; i < n; ++i) contiguous &= first_node[i] == first_node[0] + i;
+            if (contiguous) {
+                head(M, W, r0, n, arena_ + tree_off_ + first_node[0], nullptr);
+                return;
+            }
+        }
+        throw Error(ST_CONFIG, "tree widths > 1 are not supported on device yet");
+    }
+
+    void move_rows(Cache& C, const std::vector<int>& src, const std::vector<int>& dst) {
+        if (src.empty()) return;
+        const int* s = staging_.push(src.data(), src.size(), stream_);
+        const int* d = staging_.push(dst.data(), dst.size(), stream_);
+        launch_kv_move(C.view(), s, d, (int)src.size(), stream_);
+        ++launches_;
+    }
+
+    std::vector<int> generate(const std::vector<int>& tokens, std::vector<IterationTrace>* traces) override {
+        begin(tokens);
+        std::vector<int> out;
+        while (!done()) {
+            IterationTrace t = step(out);
+            if (traces) traces->push_back(t);
+        }
+        return out;
+    }
+
+    void forward_chain(int which, const std::vector<int>& tokens, const std::string& plan_spec, float* logits,
+                       float* hidden) override {
+        ModelDev& M = which ? base_ : draft_;
+        Cache& C = which ? bcache_ : dcache_;
+        Workspace& W = which ? bws_ : dws_;
+        CUDA_OK(cudaStreamSynchronize(stream_));
+        LayerPlan plan;
+        const LayerPlan* pp = nullptr;
+        if (!plan_spec.empty()) {
+            plan = plan_spec.rfind("lp=", 0) == 0 ? plan_groups(M.c.n_layers, std::stoi(plan_spec.substr(3)))
+                                                  : parse_plan_override(plan_spec);
+            if (plan.n_layers() != M.c.n_layers) cfg_fail("plan does not cover the model");
+            if (plan.max_group_size() > kMaxGroup && which == 0) cfg_fail("group too large");
+            pp = &plan;
+        }
+        if (pp && which == 1 && plan.max_group_size() > 1) cfg_fail("fuzzy probes run on the drafter");
+        C.reset();
+        staging_.reset();
+        const int n = (int)tokens.size();
+        if (n > kChunk) cfg_fail("forward_chain probes are limited to 256 tokens");
+        CUDA_OK(cudaMemcpyAsync(arena_, tokens.data(), sizeof(int) * n, cudaMemcpyHostToDevice, stream_));
+        std::vector<int> parents, tok;
+        for (int i = 0; i < n; ++i) {
+            parents.push_back(i == 0 ? kTail : i - 1);
+            tok.push_back(i);
+        }
+        std::vector<int> rows = C.stage_append(parents, pp != nullptr);
+        Pass ps = make_pass(C, rows, tok);
+        forward(M, C, W, pp, ps);
+        const int d = M.c.d_model, V = M.c.vocab_size;
+        if (hidden) CUDA_OK(cudaMemcpyAsync(hidden, W.h, sizeof(float) * n * d, cudaMemcpyDeviceToHost, stream_));
+        for (int r0 = 0; r0 < n; r0 += 8) {
+            const int k = std::min(8, n - r0);
+            head(M, W, r0, k, arena_ + out_off_, W.logits);
+            if (logits)
+                CUDA_OK(cudaMemcpy2DAsync(logits + (size_t)r0 * V, sizeof(float) * V, W.logits, sizeof(float) * M.head_ld,
+                                          sizeof(float) * V, k, cudaMemcpyDeviceToHost, stream_));
+        }
+        std::vector<int> a, b;
+        C.commit_path(rows, a, b);
+        CUDA_OK(cudaStreamSynchronize(stream_));
+        CUDA_OK(cudaGetLastError());
+        committed_.clear();
+    }
+
+    int cache_rows(int which, int layer, int row0, int n, float* k, float* v) override {
+        Cache& C = which ? bcache_ : dcache_;
+        CUDA_OK(cudaStreamSynchronize(stream_));
+        const int dh = C.dh, nkv = C.n_kv;
+        const size_t es = dsize(C.dtype);
+        std::vector<char> buf(dh * es);
+        for (int r = 0; r < n; ++r) {
+            const int row = row0 + r;
+            const int page = C.table.at(row / C.page_rows), off = row % C.page_rows;
+            for (int kind = 0; kind < 2; ++kind)
+                for (int h = 0; h < nkv; ++h) {
+                    const long long e = (long long)page * C.page_elems +
+                                        ((((long long)layer * 2 + kind) * nkv + h) * C.page_rows + off) * dh;
+                    CUDA_OK(cudaMemcpy(buf.data(), (char*)C.pool + e * es, dh * es, cudaMemcpyDeviceToHost));
+                    float* o = (kind ? v : k) + (size_t)r * nkv * dh + (size_t)h * dh;
+                    for (int i = 0; i < dh; ++i)
+                        o[i] = C.dtype == DT_BF16 ? bf2f(((uint16_t*)buf.data())[i]) : ((float*)buf.data())[i];
+                }
+        }
+        return C.committed;
+    }
+
+    int cache_committed(int which) const override { return which ? bcache_.committed : dcache_.committed; }
+    const std::vector<int>& committed() const override { return committed_; }
+    void sync() override { CUDA_OK(cudaStreamSynchronize(stream_)); }
+    void* stream() override { return stream_; }
+    long long device_bytes() const override {
+        size_t f = 0, t = 0;
+        cudaMemGetInfo(&f, &t);
+        return (long long)(t - f);
+    }
+    int kernel_launches() const override { return launches_; }
+    void reset_launch_count() override { launches_ = 0; }
+
+private:
+    int device_ = 0;
+    cudaStream_t stream_ = nullptr;
+    cudaEvent_t ev_[4];
+    ModelDev base_, draft_;
+    bool base_allocated_ = false, draft_allocated_ = false;
+    Cache bcache_, dcache_;
+    Workspace bws_, dws_;
+    std::vector<void*> ws_owned_;
+    Staging staging_;
+    int* arena_ = nullptr;
+    int arena_cap_ = 0, tree_off_ = 0, am_off_ = 0, out_off_ = 0;
+    int* outcome_host_ = nullptr;
+    RunCfg run_;
+    std::vector<int> widths_;
+    LayerPlan plan_;
+    std::vector<int> committed_;
+    int draft_cached_ = 0;
+    int generated_ = 0;
+    int launches_ = 0;
+};
+
+std::unique_ptr<Engine> make_engine(const ModelCfg& base, const ModelCfg& draft, const RunCfg& run, int device) {
+    return std::unique_ptr<Engine>(new EngineImpl(base, draft, run, device));
+}
+
+}  // namespace espec

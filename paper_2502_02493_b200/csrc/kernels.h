@@ -1,0 +1,146 @@
+// Host-side interface of the sm_100a kernels (launchers live in kernels.cu).
+//
+// Data layout in HBM:
+//   * weights: every projection is stored K-major, W[K][ldw] row-major with
+//     y = x · W (the reference's own matmul layout, proj/src/matrix.cpp:38-57);
+//     ldw is padded to a multiple of 8 so each lane streams 16-byte vectors.
+//     QKV of one layer is fused column-wise [q | k | v]; gate/up are fused and
+//     interleaved per 128-column block [gate128 | up128] so one GEMV column
+//     tile owns both halves of its SiLU·up epilogue.
+//   * hidden rows are fp32 [T][d]; their RMSNorm statistics travel as
+//     per-256-column sum-of-squares partials stats[T][ceil(d/256)].
+//   * KV cache: paged pool; page p holds kPage rows for every layer:
+//     pool[p][layer][k|v][kv_head][row][d_head], located through a page table.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace espec_dev {
+
+enum DType : int { DT_F32 = 0, DT_BF16 = 1 };
+
+enum Epilogue : int {
+    EPI_STORE = 0,   // out = x·W
+    EPI_RESID = 1,   // out = resid + x·W ; writes row sum-of-squares partials
+    EPI_SILU = 2,    // out = silu(gate) * up over interleaved gate/up tiles
+    EPI_QKV = 3,     // RoPE(q), RoPE(k) ; q -> q buffer, k/v -> paged KV cache
+    EPI_ARGMAX = 4,  // logits (optional store) + per-row argmax -> token ids
+};
+
+// Paged KV cache view.
+struct KvView {
+    void* pool = nullptr;
+    const int* page_table = nullptr;  // logical block -> physical page
+    int page_rows = 64;
+    int n_layers = 0, n_kv = 0, dh = 0;
+    int dtype = 0;                    // DType
+    long long page_elems = 0;         // elements per page (all layers)
+};
+
+// Per-pass row metadata (device pointers), indexed by pass row t.
+struct PassView {
+    int T = 0;                 // rows in the pass
+    const int* rows = nullptr; // cache row of each input row
+    const int* pos = nullptr;  // rotary position of each row
+    const int* vis_end = nullptr;                 // rows [0, vis_end) visible
+    const unsigned long long* anc = nullptr;      // tree rows visible: bit i -> row tree_base+i
+    int tree_base = 0;
+    int total = 0;             // rows stored in the cache during this pass
+};
+
+struct GemvProblem {
+    const void* W = nullptr;
+    int K = 0, N = 0, ldw = 0;
+    const float* x = nullptr;
+    int ldx = 0;
+    // fused RMSNorm prologue (gain == nullptr: none)
+    const float* gain = nullptr;
+    const float* stats_in = nullptr;
+    int stat_tiles_in = 0;
+    float eps = 1e-5f;
+    // workspace
+    float* partial = nullptr;     // [splits][8][ldw]
+    unsigned* tickets = nullptr;  // [tiles] (+1 for argmax)
+    // epilogue
+    float* out = nullptr;
+    int ldo = 0;
+    const float* resid = nullptr;
+    int ldr = 0;
+    float* stats_out = nullptr;
+    int stat_tiles_out = 0;
+    // EPI_QKV
+    int n_heads = 0, n_kv = 0, dh = 0, layer = 0;
+    float rope_theta = 10000.f;
+    // EPI_ARGMAX
+    int vocab = 0;
+    float* logits = nullptr;  // [T][ld_logits] or nullptr
+    int ld_logits = 0;
+    float* am_val = nullptr;  // [T][tiles]
+    int* am_idx = nullptr;
+    int* tok_out = nullptr;   // [T]
+};
+
+constexpr int kMaxProblems = 8;
+struct GemvBatch {
+    GemvProblem p[kMaxProblems];
+};
+
+// Split planning depends only on (K, N): never on T or the group size, so a
+// row's result is bit-identical whichever batch it is computed in (batch
+// invariance).
+struct GemvPlan {
+    int tiles, splits, kc;
+};
+GemvPlan gemv_plan(int K, int N);
+size_t gemv_partial_floats(int K, int N);  // workspace floats one problem needs
+
+// y = epilogue(norm?(x) · W) for T rows, over nprob same-shape problems.
+void launch_gemv(int epi, int wdtype, const GemvBatch& b, int nprob, int T, const PassView& pass,
+                 const KvView& kv, cudaStream_t s);
+
+// h[t] = embedding[tok[t]] (fp32), + stats.
+void launch_embed(int wdtype, const void* emb, int d, const int* tok_arena, const int* tok_idx, int T,
+                  float* h, float* stats, cudaStream_t s);
+// h += a (T x d), + stats.
+void launch_add_stats(float* h, const float* a, int d, int T, float* stats, cudaStream_t s);
+
+struct AttnProblem {
+    const float* q = nullptr;   // [T][H*dh]
+    float* out = nullptr;       // [T][H*dh]
+    int layer = 0;
+    float* ws = nullptr;        // split partials
+    unsigned* tickets = nullptr;
+};
+struct AttnBatch {
+    AttnProblem p[kMaxProblems];
+};
+size_t attn_ws_floats(int T, int n_heads, int dh, int max_rows);
+size_t attn_tickets(int T, int n_heads, int n_kv);
+void launch_attention(const AttnBatch& b, int nprob, int n_heads, const PassView& pass, const KvView& kv,
+                      cudaStream_t s);
+
+// Copy cache rows src[i] -> dst[i] for every layer (commit_path compaction).
+void launch_kv_move(const KvView& kv, const int* src, const int* dst, int n, cudaStream_t s);
+
+// Greedy acceptance over a drafted tree (see kernels.cu for the walk).
+struct AcceptArgs {
+    int n_nodes = 0, n_levels = 0, root_children = 0;
+    const int* node_parent = nullptr;    // [n_nodes]
+    const int* node_first_child = nullptr;
+    const int* node_n_children = nullptr;
+    const int* node_tok_idx = nullptr;   // index into tok arena
+    const int* tok_arena = nullptr;
+    const int* base_argmax = nullptr;    // [1 + n_nodes] base argmax for frontier + each node
+    int* outcome = nullptr;              // [2 + 2*n_levels]: m, bonus, path[n_levels], tokens[n_levels]
+    int* tok_arena_w = nullptr;          // accepted tokens + bonus are appended at commit_at
+    int commit_at = 0;
+};
+void launch_accept_greedy(const AcceptArgs& a, cudaStream_t s);
+
+// Deterministic N(0, sd) init from a counter hash (perf-mode weights).
+void launch_fill_normal(int dtype, void* dst, long long n, float sd, uint64_t seed, cudaStream_t s);
+void launch_fill_const(int dtype, void* dst, long long n, float v, cudaStream_t s);
+// dst[c][r] = src[r][c]  (src: rows x cols, dst leading dimension ldd)
+void launch_transpose(int dtype, const void* src, int rows, int cols, void* dst, int ldd, cudaStream_t s);
+
+}  // namespace espec_dev

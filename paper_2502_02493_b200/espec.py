@@ -1,0 +1,332 @@
+"""Python binding of the B200 EasySpec engine (ctypes over include/espec_c.h).
+
+Mirrors the reference's public C++ surface (proj/include/espec/*.hpp):
+``ModelConfig``/``RunConfig`` (model.hpp:19-33, orchestrator.hpp:23-38),
+``Engine.generate`` (= espec::generate, orchestrator.cpp:488-492), the
+stage-level ``begin``/``step`` loop (Generation::run, orchestrator.cpp:163-195),
+``forward`` (forward_sequential / forward_fuzzy, draft_engine.cpp:35-133),
+``cache_view`` (the IterationHook view) and ``plan_groups`` /
+``parse_plan_override`` (layer_plan.cpp). Errors surface as ``EspecError``
+carrying the reference's exception kind (errors.hpp:11-44).
+
+There is no CPU fallback: importing this module without the compiled
+``libespec_b200.so`` raises, and every compute call runs on the GPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field, replace
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libespec_b200.so")
+
+F32, BF16 = 0, 1
+ALGORITHMS = {"vanilla": 0, "sd": 1, "sd_tree": 2, "easyspec": 3}
+STATUS = {0: "ok", 1: "config", 2: "io", 3: "check", 4: "shape", 5: "structure", 6: "domain", 7: "cuda", 8: "nccl"}
+BOS, EOS = 256, 257
+
+
+class EspecError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+        self.kind = STATUS.get(status, str(status))
+
+
+class _ModelCfg(C.Structure):
+    _fields_ = [("vocab_size", C.c_int), ("d_model", C.c_int), ("n_layers", C.c_int), ("n_heads", C.c_int),
+                ("n_kv_heads", C.c_int), ("d_head", C.c_int), ("d_mlp", C.c_int), ("max_positions", C.c_int),
+                ("norm_eps", C.c_float), ("rope_theta", C.c_float), ("tied_head", C.c_int),
+                ("weight_dtype", C.c_int), ("kv_dtype", C.c_int), ("seed", C.c_uint64)]
+
+
+class _RunCfg(C.Structure):
+    _fields_ = [("algorithm", C.c_int), ("n", C.c_int), ("widths", C.POINTER(C.c_int)), ("lp_size", C.c_int),
+                ("plan_override", C.c_char_p), ("temperature", C.c_float), ("max_new_tokens", C.c_int),
+                ("seed", C.c_uint64), ("calibration", C.c_int)]
+
+
+class _DevMap(C.Structure):
+    _fields_ = [("device", C.c_int), ("n_lp_devices", C.c_int), ("lp_devices", C.POINTER(C.c_int)),
+                ("tp_size", C.c_int)]
+
+
+class _Iter(C.Structure):
+    _fields_ = [(n, C.c_int) for n in ("m", "n", "drafted_nodes", "emitted", "sequential_forwards",
+                                       "fuzzy_forwards", "base_forwards", "committed", "draft_committed",
+                                       "base_committed", "bonus")] + \
+               [(n, C.c_float) for n in ("calibrate_ms", "draft_ms", "verify_ms")]
+
+
+_lib = None
+
+
+def lib():
+    """Load libespec_b200.so (fails loudly when it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (make -C "
+                              f"paper_2502_02493_b200/csrc) — there is no CPU fallback")
+        L = C.CDLL(LIB_PATH)
+        P, V = C.POINTER, C.c_void_p
+        L.espec_engine_create.argtypes = [P(_ModelCfg), P(_ModelCfg), P(_RunCfg), P(_DevMap), P(V)]
+        L.espec_engine_destroy.argtypes = [V]
+        L.espec_last_error.restype = C.c_char_p
+        L.espec_last_error.argtypes = [V]
+        L.espec_create_error.restype = C.c_char_p
+        L.espec_init_weights_seeded.argtypes = [V, C.c_int, C.c_uint64, C.c_int]
+        L.espec_share_truncated_draft.argtypes = [V]
+        L.espec_load_tensor.argtypes = [V, C.c_int, C.c_char_p, C.c_int, P(C.c_float), C.c_int64, C.c_int64]
+        L.espec_read_tensor.argtypes = [V, C.c_int, C.c_char_p, C.c_int, P(C.c_float), C.c_int64, C.c_int64]
+        L.espec_set_run.argtypes = [V, P(_RunCfg)]
+        L.espec_generate.argtypes = [V, C.c_char_p, C.c_int, P(C.c_int32), P(C.c_int), P(_Iter), P(C.c_int)]
+        L.espec_begin.argtypes = [V, P(C.c_int32), C.c_int]
+        L.espec_step.argtypes = [V, P(C.c_int32), P(C.c_int), P(_Iter)]
+        L.espec_done.argtypes = [V]
+        L.espec_cache_view.argtypes = [V, C.c_int, C.c_int, C.c_int, C.c_int, P(C.c_float), P(C.c_float), P(C.c_int)]
+        L.espec_committed.argtypes = [V, P(C.c_int32), C.c_int, P(C.c_int)]
+        L.espec_forward.argtypes = [V, C.c_int, P(C.c_int32), C.c_int, C.c_char_p, P(C.c_float), P(C.c_float)]
+        L.espec_plan_groups.argtypes = [C.c_int, C.c_int, C.c_char_p, C.c_int]
+        L.espec_parse_plan.argtypes = [C.c_char_p, C.c_char_p, C.c_int]
+        L.espec_kernel_launches.argtypes = [V]
+        L.espec_reset_kernel_launches.argtypes = [V]
+        L.espec_sync.argtypes = [V]
+        _lib = L
+    return _lib
+
+
+def _f(a):
+    return a.ctypes.data_as(C.POINTER(C.c_float)) if a is not None else None
+
+
+def _i(a):
+    return a.ctypes.data_as(C.POINTER(C.c_int32))
+
+
+@dataclass
+class ModelConfig:
+    """espec::ModelConfig plus GQA / rope base / untied head / storage dtypes."""
+    vocab_size: int = 258
+    d_model: int = 64
+    n_layers: int = 4
+    n_heads: int = 4
+    d_head: int = 16
+    d_mlp: int = 128
+    max_positions: int = 512
+    norm_eps: float = 1e-5
+    seed: int = 0
+    n_kv_heads: Optional[int] = None
+    rope_theta: float = 10000.0
+    tied_head: bool = True
+    weight_dtype: int = F32
+    kv_dtype: int = F32
+
+    def _c(self) -> _ModelCfg:
+        return _ModelCfg(self.vocab_size, self.d_model, self.n_layers, self.n_heads,
+                         self.n_kv_heads or self.n_heads, self.d_head, self.d_mlp, self.max_positions,
+                         self.norm_eps, self.rope_theta, 1 if self.tied_head else 0, self.weight_dtype,
+                         self.kv_dtype, self.seed)
+
+
+def tiny_config(n_layers: int, seed: int, d_model=32, n_heads=2, d_head=16, d_mlp=64, max_positions=128):
+    """proj/tests/test_support.hpp:44-54."""
+    return ModelConfig(d_model=d_model, n_heads=n_heads, d_head=d_head, d_mlp=d_mlp, n_layers=n_layers,
+                       max_positions=max_positions, seed=seed)
+
+
+@dataclass
+class RunConfig:
+    """espec::RunConfig (proj/include/espec/orchestrator.hpp:23-38)."""
+    algorithm: str = "easyspec"
+    n: int = 5
+    widths: Optional[List[int]] = None
+    lp_size: int = 4
+    plan_override: Optional[str] = None
+    temperature: float = 0.0
+    max_new_tokens: int = 64
+    seed: int = 1
+    calibration: bool = True
+
+    def effective_widths(self) -> List[int]:
+        return list(self.widths) if self.widths else [1] * self.n
+
+
+@dataclass
+class IterationTrace:
+    m: int
+    n: int
+    drafted_nodes: int
+    emitted: int
+    sequential_forwards: int
+    fuzzy_forwards: int
+    base_forwards: int
+    committed: int
+    draft_committed: int
+    base_committed: int
+    bonus: int
+    calibrate_ms: float
+    draft_ms: float
+    verify_ms: float
+
+
+def _trace(t: _Iter) -> IterationTrace:
+    return IterationTrace(*(getattr(t, n) for n, _ in _Iter._fields_))
+
+
+def tokenize(prompt: bytes) -> List[int]:
+    """tokenize_prompt (proj/src/orchestrator.cpp:42-52)."""
+    return [BOS] + list(prompt)
+
+
+class Engine:
+    """One base/drafter pair with its caches on one B200."""
+
+    DRAFT, BASE = 0, 1
+
+    def __init__(self, base: ModelConfig, draft: ModelConfig, run: RunConfig, device: int = 0):
+        L = lib()
+        self.base_cfg, self.draft_cfg = base, draft
+        self._h = C.c_void_p()
+        self._keep = []
+        dm = _DevMap(device, 1, None, 1)
+        st = L.espec_engine_create(C.byref(base._c()), C.byref(draft._c()), C.byref(self._run(run)), C.byref(dm),
+                                   C.byref(self._h))
+        if st:
+            raise EspecError(st, L.espec_create_error().decode())
+        self.run = run
+
+    def _run(self, run: RunConfig) -> _RunCfg:
+        w = np.asarray(run.effective_widths(), np.int32)
+        po = (run.plan_override or "").encode()
+        self._keep = [w, po]
+        return _RunCfg(ALGORITHMS[run.algorithm], run.n, _i(w), run.lp_size, po, run.temperature,
+                       run.max_new_tokens, run.seed, 1 if run.calibration else 0)
+
+    def _check(self, st: int):
+        if st:
+            raise EspecError(st, lib().espec_last_error(self._h).decode())
+
+    def close(self):
+        if self._h:
+            lib().espec_engine_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- weights
+    def init_weights(self, which: int, seed: int, parity: bool = True):
+        self._check(lib().espec_init_weights_seeded(self._h, which, seed, 1 if parity else 0))
+
+    def share_truncated_draft(self):
+        self._check(lib().espec_share_truncated_draft(self._h))
+
+    def load_tensor(self, which: int, name: str, data: np.ndarray, layer: int = -1):
+        a = np.ascontiguousarray(data, np.float32)
+        if a.ndim == 1:
+            a = a[None, :]
+        self._check(lib().espec_load_tensor(self._h, which, name.encode(), layer, _f(a), a.shape[0], a.shape[1]))
+
+    def read_tensor(self, which: int, name: str, rows: int, cols: int, layer: int = -1) -> np.ndarray:
+        out = np.zeros((rows, cols), np.float32)
+        self._check(lib().espec_read_tensor(self._h, which, name.encode(), layer, _f(out), rows, cols))
+        return out
+
+    def set_run(self, run: RunConfig):
+        self._check(lib().espec_set_run(self._h, C.byref(self._run(run))))
+        self.run = run
+
+    # ---- generation
+    def generate(self, prompt: bytes):
+        n = self.run.max_new_tokens
+        out = np.zeros(n, np.int32)
+        traces = (_Iter * max(n, 1))()
+        n_out, n_it = C.c_int(0), C.c_int(0)
+        self._check(lib().espec_generate(self._h, prompt, len(prompt), _i(out), C.byref(n_out), traces,
+                                         C.byref(n_it)))
+        return list(out[: n_out.value]), [_trace(traces[i]) for i in range(n_it.value)]
+
+    def begin(self, tokens: Sequence[int]):
+        t = np.asarray(tokens, np.int32)
+        self._check(lib().espec_begin(self._h, _i(t), len(t)))
+
+    def step(self):
+        em = np.zeros(self.run.n + 2, np.int32)
+        n = C.c_int(0)
+        tr = _Iter()
+        self._check(lib().espec_step(self._h, _i(em), C.byref(n), C.byref(tr)))
+        return list(em[: n.value]), _trace(tr)
+
+    def done(self) -> bool:
+        return bool(lib().espec_done(self._h))
+
+    def committed(self) -> List[int]:
+        n = C.c_int(0)
+        self._check(lib().espec_committed(self._h, None, 0, C.byref(n)))
+        buf = np.zeros(max(n.value, 1), np.int32)
+        self._check(lib().espec_committed(self._h, _i(buf), len(buf), C.byref(n)))
+        return list(buf[: n.value])
+
+    # ---- probes
+    def forward(self, which: int, tokens: Sequence[int], plan: Optional[str] = None):
+        cfg = self.base_cfg if which == self.BASE else self.draft_cfg
+        t = np.asarray(tokens, np.int32)
+        logits = np.zeros((len(t), cfg.vocab_size), np.float32)
+        hidden = np.zeros((len(t), cfg.d_model), np.float32)
+        self._check(lib().espec_forward(self._h, which, _i(t), len(t), (plan or "").encode(), _f(logits),
+                                        _f(hidden)))
+        return logits, hidden
+
+    def cache_view(self, which: int, layer: int, row0: int = 0, n: Optional[int] = None):
+        cfg = self.base_cfg if which == self.BASE else self.draft_cfg
+        committed = C.c_int(0)
+        self._check(lib().espec_cache_view(self._h, which, layer, 0, 0, None, None, C.byref(committed)))
+        if n is None:
+            n = committed.value - row0
+        w = (cfg.n_kv_heads or cfg.n_heads) * cfg.d_head
+        k = np.zeros((max(n, 0), w), np.float32)
+        v = np.zeros_like(k)
+        if n > 0:
+            self._check(lib().espec_cache_view(self._h, which, layer, row0, n, _f(k), _f(v), C.byref(committed)))
+        return k, v, committed.value
+
+    def kernel_launches(self) -> int:
+        return lib().espec_kernel_launches(self._h)
+
+    def reset_kernel_launches(self):
+        lib().espec_reset_kernel_launches(self._h)
+
+    def sync(self):
+        self._check(lib().espec_sync(self._h))
+
+
+def plan_groups(n_layers: int, lp_size: int) -> str:
+    buf = C.create_string_buffer(4096)
+    st = lib().espec_plan_groups(n_layers, lp_size, buf, 4096)
+    if st:
+        raise EspecError(st, lib().espec_create_error().decode())
+    return buf.value.decode()
+
+
+def parse_plan_override(spec: str) -> str:
+    buf = C.create_string_buffer(4096)
+    st = lib().espec_parse_plan(spec.encode(), buf, 4096)
+    if st:
+        raise EspecError(st, lib().espec_create_error().decode())
+    return buf.value.decode()
+
+
+def truncated_pair(base: ModelConfig, keep: int, run: RunConfig, device: int = 0, parity: bool = True) -> Engine:
+    """Base model from init_model(base) + make_truncated_draft(base, keep)."""
+    eng = Engine(base, replace(base, n_layers=keep), run, device)
+    eng.init_weights(Engine.BASE, base.seed, parity)
+    eng.share_truncated_draft()
+    return eng

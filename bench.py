@@ -1,0 +1,420 @@
+#!/usr/bin/env python
+"""EasySpec decode benchmark on B200 (BASELINE.json configs[1] at one GPU).
+
+One *step* = one EasySpec decode iteration of the reference's loop
+(Generation::run_iteration_speculative, proj/src/orchestrator.cpp:407-436):
+bonus-calibration pass -> (n-1) fuzzy layer-parallel draft passes -> base
+verification of the n+1 rows -> greedy acceptance -> KV commit/discard.
+
+Workload "c2": Llama-3-70B-shaped base + Llama-3-8B-shaped drafter, bf16
+weights and KV, random init (device N(0, sd) with the reference's sd rules),
+layer-parallel width 4 (plan 0|1-3|4-7|...|28-30|31), n = 5, batch 1,
+greedy, synthetic prompt of --ctx uniform-random token ids. The full pair
+(157 GB) is resident on one B200; at N>1 every rank runs an independent
+replica (round 1: replicas only).
+
+Prints ONE JSON line (rank 0). `value` is decode tokens/s of EasySpec with
+inputs resident in HBM; `e2e` the same metric through the C ABI
+(espec_generate_tokens: host token ids in, host tokens out, prefill included).
+The weights (157 GB) exceed L2 (126 MB) many times over: every timed step
+streams them from HBM, so no L2 flush is needed.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    "c2": dict(
+        name="llama3-70b-base(tp1)+llama3-8b-drafter, lp4, n5, batch1, greedy",
+        base=dict(vocab_size=128256, d_model=8192, n_layers=80, n_heads=64, n_kv_heads=8, d_head=128, d_mlp=28672,
+                  rope_theta=500000.0),
+        draft=dict(vocab_size=128256, d_model=4096, n_layers=32, n_heads=32, n_kv_heads=8, d_head=128, d_mlp=14336,
+                   rope_theta=500000.0),
+        lp=4, n=5),
+    # small shapes for quick functional runs of this script
+    "mini": dict(
+        name="mini pair (functional check only)",
+        base=dict(vocab_size=32000, d_model=1024, n_layers=8, n_heads=16, n_kv_heads=4, d_head=64, d_mlp=2816,
+                  rope_theta=500000.0),
+        draft=dict(vocab_size=32000, d_model=512, n_layers=6, n_heads=8, n_kv_heads=2, d_head=64, d_mlp=1408,
+                   rope_theta=500000.0),
+        lp=4, n=5),
+}
+PAPER_ALPHA = 0.82  # Llama-3-70B/8B, MMLU, T=0
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ----------------------------------------------------------------------------
+# CPU baseline: the unmodified reference core (oracle/_ref/ref_bench)
+# ----------------------------------------------------------------------------
+
+def _ref_bench(*args):
+    exe = os.path.join(ROOT, "oracle", "_ref", "ref_bench")
+    out = subprocess.run([exe, *map(str, args)], capture_output=True, text=True, timeout=600)
+    if out.returncode != 0:
+        raise RuntimeError(f"ref_bench {args} failed: {out.stderr[-400:]}")
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+def _mha_equiv(cfg):
+    # the reference is MHA-only: d_model = n_heads * d_head, wk/wv are d x d
+    return cfg["d_model"], cfg["n_heads"], cfg["d_head"], cfg["d_mlp"]
+
+
+def cpu_iteration_seconds(wl, ctx, reps=1, cache=None):
+    """Extrapolated wall time of one EasySpec iteration of the reference CPU
+    path (workers=1) with m = 0 accepted drafts: calibration pass over 1 row,
+    n-1 draft passes over 1 row, base verification over n+1 rows — each pass
+    = layers x (sampled one-layer body) + the LM head rows it scores."""
+    n = wl["n"]
+    b, d = wl["base"], wl["draft"]
+    cache = cache if cache is not None else {}
+
+    def layer(cfg, T):
+        key = ("layer", cfg["d_model"], T)
+        if key not in cache:
+            r = _ref_bench("layer", *_mha_equiv(cfg), T, ctx, reps)
+            cache[key] = (r["mask_ms"] + r["attn_ms"] + r["mlp_ms"] + r["rest_ms"]) / 1000.0
+        return cache[key]
+
+    def head(cfg, T):
+        key = ("head", cfg["d_model"], T)
+        if key not in cache:
+            cache[key] = _ref_bench("head", cfg["d_model"], cfg["vocab_size"], T, reps)["head_ms"] / 1000.0
+        return cache[key]
+
+    calib = d["n_layers"] * layer(d, 1) + head(d, 1)
+    draft = (n - 1) * (d["n_layers"] * layer(d, 1) + head(d, 1))
+    verify = b["n_layers"] * layer(b, n + 1) + head(b, n + 1)
+    return calib + draft + verify, {"calibrate_s": calib, "draft_s": draft, "verify_s": verify}
+
+
+def cpu_baseline(wl, ctx):
+    t0 = time.time()
+    it_s, parts = cpu_iteration_seconds(wl, ctx)
+    return {"value": 1.0 / it_s, "unit": "tokens/s", "cores": 1, "kind": "reference",
+            "sample": (f"oracle/_ref/ref_bench (unmodified reference core, workers=1): one layer per shape at "
+                       f"ctx {ctx} (base T={wl['n'] + 1}, drafter T=1, MHA-equivalent) + LM head rows, "
+                       f"extrapolated to 80/32 layers, 1 token per iteration (m=0); "
+                       f"{time.time() - t0:.1f}s of CPU work"),
+            "stage_s": parts}
+
+
+def run_reference(args, wl):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    cache = {}
+    times = []
+    t_start = time.time()
+    for i in range(args.warmup + args.steps):
+        # each step re-samples the dominant term (one base layer at T=n+1);
+        # drafter layers and LM heads are sampled once (warm-up)
+        cache.pop(("layer", wl["base"]["d_model"], wl["n"] + 1), None)
+        it_s, parts = cpu_iteration_seconds(wl, args.ctx, cache=cache)
+        if i >= args.warmup:
+            times.append(it_s)
+    it = statistics.median(times)
+    value = 1.0 / it
+    line = {"metric": "decode tokens/s (EasySpec, greedy)", "value": value, "unit": "tokens/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": it * 1000.0,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": wl["name"], "ctx": args.ctx, "n": wl["n"], "lp": wl["lp"],
+                       "note": "reference CPU core; 1 token per iteration (m=0)"},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": 1, "kind": "reference",
+                             "sample": f"per step: one base layer (T={wl['n'] + 1}, ctx {args.ctx}) timed, "
+                                       f"extrapolated; drafter layers + heads sampled once; "
+                                       f"{time.time() - t_start:.0f}s total"},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "stage_s": parts}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------
+# GPU arms
+# ----------------------------------------------------------------------------
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--ctx", type=int, default=512)
+    ap.add_argument("--e2e-tokens", type=int, default=32)
+    ap.add_argument("--no-arms", action="store_true", help="skip the vanilla / sd comparison arms")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    args = ap.parse_args()
+    assert args.warmup >= 1
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        return run_reference(args, wl)
+
+    import numpy as np
+    import torch
+    from paper_2502_02493_b200 import espec as E
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = local
+
+    n, lp = wl["n"], wl["lp"]
+    steps, warm = args.steps, args.warmup
+    max_pos = args.ctx + (warm + steps + 4) * (n + 1) + args.e2e_tokens + 64
+    base = E.ModelConfig(max_positions=max_pos, seed=7, tied_head=False, weight_dtype=E.BF16, kv_dtype=E.BF16,
+                         **wl["base"])
+    draft = E.ModelConfig(max_positions=max_pos, seed=9, tied_head=False, weight_dtype=E.BF16, kv_dtype=E.BF16,
+                          **wl["draft"])
+    run = E.RunConfig(algorithm="easyspec", n=n, lp_size=lp, temperature=0.0, max_new_tokens=(warm + steps + 2) * (n + 1))
+    eng = E.Engine(base, draft, run, device=dev)
+    eng.init_weights(E.Engine.BASE, base.seed, parity=False)
+    eng.init_weights(E.Engine.DRAFT, draft.seed, parity=False)
+    rng = np.random.default_rng(1234 + rank)
+    prompt = [int(t) for t in rng.integers(0, base.vocab_size, size=args.ctx)]
+    stream = torch.cuda.ExternalStream(eng.stream(), device=dev)
+
+    def barrier():
+        if ws > 1:
+            torch.distributed.barrier()
+
+    def max_over_ranks(x):
+        if ws == 1:
+            return x
+        t = torch.tensor([x], device=f"cuda:{dev}", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x):
+        if ws == 1:
+            return x
+        t = torch.tensor([x], device=f"cuda:{dev}", dtype=torch.float64)
+        torch.distributed.all_reduce(t)
+        return float(t.item())
+
+    def arm(alg, site=None, clocks=False):
+        eng.set_run(E.RunConfig(algorithm=alg, n=n, lp_size=lp, temperature=0.0,
+                                max_new_tokens=(warm + steps + 2) * (n + 1)))
+        eng.begin(prompt)
+        for _ in range(warm):  # first warm-up step includes the prompt prefill
+            eng.step()
+        if site is not None:
+            eng.time_site(*site)
+        eng.reset_kernel_launches()
+        barrier()
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        sampler = ClockSampler(dev) if clocks else None
+        if sampler:
+            sampler.__enter__()
+        ev0.record(stream)
+        traces, emitted = [], 0
+        for _ in range(steps):
+            em, tr = eng.step()
+            emitted += len(em)
+            traces.append(tr)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if sampler:
+            sampler.__exit__()
+        barrier()
+        ms = ev0.elapsed_time(ev1)
+        launches = eng.kernel_launches()
+        site_stats = eng.site_stats() if site is not None else None
+        if site is not None:
+            eng.time_site(-1, -1)
+        return dict(ms=ms, emitted=emitted, traces=traces, launches=launches, site=site_stats,
+                    clocks=sampler.summary() if sampler else None)
+
+    # main arm: EasySpec; roofline site = base gate/up GEMV (largest kernel)
+    es = arm("easyspec", site=(1, 3), clocks=True)
+    t_max = max_over_ranks(es["ms"])
+    tokens_all = sum_over_ranks(es["emitted"])
+    value = tokens_all / (t_max / 1000.0)
+    m_list = [t.m for t in es["traces"]]
+    alpha = sum(m_list) / (n * len(m_list))
+    calib_ms = sum(t.calibrate_ms for t in es["traces"])
+    draft_ms = sum(t.draft_ms for t in es["traces"])
+    verify_ms = sum(t.verify_ms for t in es["traces"])
+    per_tok = 1.0 / max(es["emitted"], 1)
+
+    arms = {}
+    if not args.no_arms:
+        for alg in ("vanilla", "sd"):
+            r = arm(alg)
+            arms[alg] = dict(tokens_per_s=sum_over_ranks(r["emitted"]) / (max_over_ranks(r["ms"]) / 1000.0),
+                             ms_per_step=r["ms"] / steps,
+                             draft_ms_per_token=sum(t.draft_ms for t in r["traces"]) / max(r["emitted"], 1),
+                             verify_ms_per_step=sum(t.verify_ms for t in r["traces"]) / steps)
+
+    # roofline of the dominant kernel (base gate/up GEMV, bf16 weights streamed once)
+    hbm, peak_kind = peaks()
+    cnt, site_ms, site_bytes = es["site"]
+    achieved = site_bytes / (site_ms / cnt / 1000.0) / 1e9 if cnt else None
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("base_gate_up_dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # e2e through the C ABI: host prompt ids -> host tokens, prefill included
+    e2e = None
+    if args.e2e_tokens > 0:
+        eng.set_run(E.RunConfig(algorithm="easyspec", n=n, lp_size=lp, temperature=0.0,
+                                max_new_tokens=args.e2e_tokens))
+        eng.generate_tokens(prompt)  # warm-up request
+        h0, d0 = eng.io_bytes()
+        reps = 2
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        got = 0
+        for _ in range(reps):
+            out, _tr = eng.generate_tokens(prompt)
+            got += len(out)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        h1, d1 = eng.io_bytes()
+        e_ms = max_over_ranks(e0.elapsed_time(e1))
+        e2e = {"value": sum_over_ranks(got) / (e_ms / 1000.0), "unit": "tokens/s",
+               "h2d_bytes_per_step": (h1 - h0) // reps, "d2h_bytes_per_step": (d1 - d0) // reps + 4 * args.e2e_tokens,
+               "step": f"one espec_generate_tokens request: {args.ctx}-token prompt (prefill included) -> "
+                       f"{args.e2e_tokens} new tokens"}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        try:
+            cpu = cpu_baseline(wl, args.ctx)
+        except Exception as ex:  # the checker binary is built here, not on the box
+            cpu = {"value": None, "unit": "tokens/s", "cores": 1, "kind": "reference", "sample": f"unavailable: {ex}"}
+
+    if rank == 0:
+        it_ms = t_max / steps
+        # alpha-projected: tokens/iteration = n*alpha + 1 at the
+        # paper's alpha; calibration then covers m+1 rows (same weight bytes).
+        proj_tok_s = (n * PAPER_ALPHA + 1) / (it_ms / 1000.0)
+        line = {
+            "metric": "decode tokens/s (EasySpec, greedy)",
+            "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": steps, "warmup": warm,
+            "ms_per_step": it_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic (random-init weights, uniform-random prompt ids)",
+            "config": {"workload": wl["name"], "ctx": args.ctx, "n": n, "lp": lp,
+                       "plan": E.plan_groups(draft.n_layers, lp), "replicas": ws,
+                       "l2": "no flush: 157 GB of weights streamed per step >> 126 MB L2"},
+            "speedup_vs_vanilla": (value / arms["vanilla"]["tokens_per_s"]) if "vanilla" in arms else None,
+            "draft_ms_per_token": (calib_ms + draft_ms) * per_tok,
+            "calibrate_ms_per_token": calib_ms * per_tok, "fuzzy_draft_ms_per_token": draft_ms * per_tok,
+            "verify_ms_per_token": verify_ms * per_tok,
+            "stage_ms_per_step": {"calibrate": calib_ms / steps, "draft": draft_ms / steps,
+                                  "verify": verify_ms / steps},
+            "mean_accept_len": es["emitted"] / steps, "alpha": alpha,
+            "arms": arms,
+            "alpha_projected": {"alpha": PAPER_ALPHA, "tokens_per_s": proj_tok_s,
+                                "speedup_vs_vanilla": (proj_tok_s / arms["vanilla"]["tokens_per_s"])
+                                if "vanilla" in arms else None,
+                                "note": "projection, tokens/iteration = n*alpha+1 (proj/src/cli.cpp:403)"},
+            "roofline": {"kernel": "gemv_kernel<bf16,8,EPI_SILU> (base gate/up, 8192x57344 bf16)",
+                         "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": (achieved / hbm) if achieved else None, "traffic": traffic,
+                         "launches_timed": cnt, "bytes_per_launch": site_bytes, "peak_source": peak_kind},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": es["launches"],
+            "clocks": es["clocks"],
+        }
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -166,6 +166,23 @@ espec_status espec_forward(espec_engine* eng, int which, const int32_t* tokens, 
 espec_status espec_plan_groups(int n_layers, int lp_size, char* out, int out_len);
 espec_status espec_parse_plan(const char* spec, char* out, int out_len);
 
+/* generate() over already-tokenized input (the same loop as espec_generate
+ * without the byte tokenizer; vocabularies larger than 258). */
+espec_status espec_generate_tokens(espec_engine* eng, const int32_t* tokens, int n_tokens, int32_t* out_tokens,
+                                   int* n_out, espec_iteration* traces, int* n_iters);
+
+/* The cudaStream_t every kernel of this engine is launched on. */
+void* espec_stream(espec_engine* eng);
+
+/* Per-launch CUDA-event timing of one kernel site while enabled: which 0/1
+ * (drafter/base, <0 disables), kind 0 QKV GEMV, 1 attention, 2 O GEMV,
+ * 3 gate/up GEMV, 4 down GEMV, 5 head GEMV. Stats: launches timed, their total
+ * device ms and algorithmic bytes per launch. */
+espec_status espec_time_site(espec_engine* eng, int which, int kind);
+espec_status espec_site_stats(espec_engine* eng, int* count, double* total_ms, double* bytes_per_launch);
+/* Host<->device bytes copied so far (metadata, tokens, outcomes). */
+espec_status espec_io_bytes(espec_engine* eng, int64_t* h2d, int64_t* d2h);
+
 /* Instrumentation: kernel launches issued since the last reset. */
 int espec_kernel_launches(const espec_engine* eng);
 void espec_reset_kernel_launches(espec_engine* eng);

@@ -223,6 +223,38 @@ int espec_kernel_launches(const espec_engine* eng) { return eng ? eng->impl->ker
 void espec_reset_kernel_launches(espec_engine* eng) {
     if (eng) eng->impl->reset_launch_count();
 }
+void* espec_stream(espec_engine* eng) { return eng ? eng->impl->stream() : nullptr; }
+
+espec_status espec_time_site(espec_engine* eng, int which, int kind) {
+    return guard(eng, [&] { eng->impl->time_site(which, kind); });
+}
+
+espec_status espec_site_stats(espec_engine* eng, int* count, double* total_ms, double* bytes_per_launch) {
+    return guard(eng, [&] { eng->impl->site_stats(count, total_ms, bytes_per_launch); });
+}
+
+espec_status espec_io_bytes(espec_engine* eng, int64_t* h2d, int64_t* d2h) {
+    return guard(eng, [&] {
+        long long a = 0, b = 0;
+        eng->impl->io_bytes(&a, &b);
+        *h2d = a;
+        *d2h = b;
+    });
+}
+
+espec_status espec_generate_tokens(espec_engine* eng, const int32_t* tokens, int n_tokens, int32_t* out_tokens,
+                                   int* n_out, espec_iteration* traces, int* n_iters) {
+    return guard(eng, [&] {
+        std::vector<IterationTrace> tr;
+        const std::vector<int> out = eng->impl->generate(std::vector<int>(tokens, tokens + n_tokens), &tr);
+        for (size_t i = 0; i < out.size(); ++i) out_tokens[i] = out[i];
+        if (n_out) *n_out = (int)out.size();
+        if (traces)
+            for (size_t i = 0; i < tr.size(); ++i) fill_trace(tr[i], &traces[i]);
+        if (n_iters) *n_iters = (int)tr.size();
+    });
+}
+
 espec_status espec_sync(espec_engine* eng) {
     return guard(eng, [&] { eng->impl->sync(); });
 }

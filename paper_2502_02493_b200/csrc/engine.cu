@@ -410,6 +410,7 @@ struct Staging {
         if (dev) cudaFree(dev);
         host = dev = nullptr;
     }
+    long long* h2d_counter = nullptr;
     template <typename T>
     T* push(const T* data, size_t n, cudaStream_t s) {
         const size_t bytes = sizeof(T) * std::max<size_t>(n, 1);
@@ -418,6 +419,7 @@ struct Staging {
         if (n) std::memcpy(host + off, data, sizeof(T) * n);
         T* d = reinterpret_cast<T*>(dev + off);
         CUDA_OK(cudaMemcpyAsync(d, host + off, bytes, cudaMemcpyHostToDevice, s));
+        if (h2d_counter) *h2d_counter += (long long)bytes;
         off += aligned;
         return d;
     }
@@ -470,6 +472,8 @@ public:
         bcache_.create(bc, cap_b);
         dcache_.create(dc, cap_d);
         staging_.create(8 << 20);
+        staging_.h2d_counter = &h2d_bytes_;
+        for (auto& e : site_ev_) CUDA_OK(cudaEventCreate(&e));
         arena_cap_ = std::max(cap_b, cap_d) + 4 * kMaxNodes + 64;
         tree_off_ = std::max(cap_b, cap_d);
         am_off_ = tree_off_ + kMaxNodes;
@@ -492,6 +496,7 @@ public:
         cudaFree(arena_);
         cudaFreeHost(outcome_host_);
         for (auto& e : ev_) cudaEventDestroy(e);
+        for (auto& e : site_ev_) cudaEventDestroy(e);
         cudaStreamDestroy(stream_);
     }
 
@@ -830,6 +835,47 @@ public:
         return p;
     }
 
+    // ---- per-launch timing of one kernel site (bench roofline evidence)
+    template <typename F>
+    void site(const ModelDev& M, int kind, double bytes, F&& launch) {
+        const int which = &M == &base_ ? 1 : 0;
+        const bool on = which == site_which_ && kind == site_kind_ && site_n_ < kSiteEvents;
+        if (on) CUDA_OK(cudaEventRecord(site_ev_[2 * site_n_], stream_));
+        launch();
+        if (on) {
+            CUDA_OK(cudaEventRecord(site_ev_[2 * site_n_ + 1], stream_));
+            ++site_n_;
+            site_bytes_ = bytes;
+        }
+    }
+    void time_site(int which, int kind) override {
+        CUDA_OK(cudaStreamSynchronize(stream_));
+        site_which_ = which;
+        site_kind_ = kind;
+        site_n_ = 0;
+        site_ms_ = 0;
+        site_bytes_ = 0;
+    }
+    void site_stats(int* count, double* total_ms, double* bytes_per_launch) override {
+        CUDA_OK(cudaStreamSynchronize(stream_));
+        double tot = 0;
+        for (int i = 0; i < site_n_; ++i) {
+            float ms = 0;
+            CUDA_OK(cudaEventElapsedTime(&ms, site_ev_[2 * i], site_ev_[2 * i + 1]));
+            tot += ms;
+        }
+        *count = site_n_;
+        *total_ms = tot;
+        *bytes_per_launch = site_bytes_;
+    }
+    void io_bytes(long long* h2d, long long* d2h) const override {
+        *h2d = h2d_bytes_;
+        *d2h = d2h_bytes_;
+    }
+    static double gemv_bytes(const ModelDev& M, int K, int ldw, int N, int T, int nprob) {
+        return (double)nprob * ((double)K * ldw * dsize(M.c.weight_dtype) + 4.0 * T * (K + N));
+    }
+
     // forward_sequential / forward_fuzzy (proj/src/draft_engine.cpp:35-133)
     void forward(ModelDev& M, Cache& C, Workspace& W, const LayerPlan* plan, const Pass& ps) {
         const ModelCfg& c = M.c;
@@ -856,7 +902,8 @@ public:
                 p.n_heads = c.n_heads; p.n_kv = c.n_kv_heads; p.dh = c.d_head; p.layer = g[i]; p.rope_theta = c.rope_theta;
                 qb.p[i] = p;
             }
-            launch_gemv(EPI_QKV, wdt, qb, n, T, ps.view, kv, stream_);
+            site(M, 0, gemv_bytes(M, d, M.qkv_ld(), M.qkv_N(), T, n),
+                 [&] { launch_gemv(EPI_QKV, wdt, qb, n, T, ps.view, kv, stream_); });
             launches_ += (T + 7) / 8;
             attention(M, C, W, g, ps);
             if (n == 1) {
@@ -866,7 +913,7 @@ public:
                 p.W = L.wo; p.K = qd; p.N = d; p.ldw = d; p.x = W.mixed; p.ldx = qd;
                 p.out = W.h; p.ldo = d; p.resid = W.h; p.ldr = d; p.stats_out = W.stats; p.stat_tiles_out = tiles;
                 ob.p[0] = p;
-                launch_gemv(EPI_RESID, wdt, ob, 1, T, ps.view, kv, stream_);
+                site(M, 2, gemv_bytes(M, qd, d, d, T, 1), [&] { launch_gemv(EPI_RESID, wdt, ob, 1, T, ps.view, kv, stream_); });
                 launches_ += (T + 7) / 8;
             } else {
                 GemvBatch ob;
@@ -877,7 +924,7 @@ public:
                     p.out = W.attn + (size_t)i * kChunk * d; p.ldo = d;
                     ob.p[i] = p;
                 }
-                launch_gemv(EPI_STORE, wdt, ob, n, T, ps.view, kv, stream_);
+                site(M, 2, gemv_bytes(M, qd, d, d, T, n), [&] { launch_gemv(EPI_STORE, wdt, ob, n, T, ps.view, kv, stream_); });
                 launches_ += (T + 7) / 8;
             }
             // residual / MLP chain stays sequential (proj/src/draft_engine.cpp:112-130)
@@ -895,13 +942,14 @@ public:
                 ub.p[0] = p;
                 // EPI_SILU guards j < N/2 = padded f; outputs beyond f land in act padding
                 ub.p[0].N = 2 * f;
-                launch_gemv(EPI_SILU, wdt, ub, 1, T, ps.view, kv, stream_);
+                site(M, 3, gemv_bytes(M, d, M.gu_ld(), 2 * f, T, 1),
+                     [&] { launch_gemv(EPI_SILU, wdt, ub, 1, T, ps.view, kv, stream_); });
                 GemvBatch db;
                 GemvProblem q = gp(W, 0);
                 q.W = L.wd; q.K = f; q.N = d; q.ldw = d; q.x = W.act; q.ldx = f;
                 q.out = W.h; q.ldo = d; q.resid = W.h; q.ldr = d; q.stats_out = W.stats; q.stat_tiles_out = tiles;
                 db.p[0] = q;
-                launch_gemv(EPI_RESID, wdt, db, 1, T, ps.view, kv, stream_);
+                site(M, 4, gemv_bytes(M, f, d, d, T, 1), [&] { launch_gemv(EPI_RESID, wdt, db, 1, T, ps.view, kv, stream_); });
                 launches_ += 2 * ((T + 7) / 8);
             }
         }
@@ -925,7 +973,8 @@ public:
                 a.tickets = W.attn_tickets + (size_t)W.attn_ticket_slot * i;
                 ab.p[i] = a;
             }
-            launch_attention(ab, (int)g.size(), M.c.n_heads, v, kv, stream_);
+            const double kvb = (double)g.size() * 2.0 * ps.view.total * M.kvdim() * dsize(M.c.kv_dtype);
+            site(M, 1, kvb, [&] { launch_attention(ab, (int)g.size(), M.c.n_heads, v, kv, stream_); });
             ++launches_;
         }
     }
@@ -944,7 +993,8 @@ public:
         p.am_val = W.am_val; p.am_idx = W.am_idx; p.tok_out = tok_out;
         hb.p[0] = p;
         PassView none;
-        launch_gemv(EPI_ARGMAX, c.weight_dtype, hb, 1, n, none, KvView(), stream_);
+        site(M, 5, gemv_bytes(M, d, M.head_ld, c.vocab_size, n, 1),
+             [&] { launch_gemv(EPI_ARGMAX, c.weight_dtype, hb, 1, n, none, KvView(), stream_); });
         launches_ += (n + 7) / 8;
     }
 
@@ -995,6 +1045,7 @@ public:
         staging_.reset();
         CUDA_OK(cudaMemcpyAsync(arena_, committed_.data(), sizeof(int) * committed_.size(), cudaMemcpyHostToDevice,
                                 stream_));
+        h2d_bytes_ += (long long)(sizeof(int) * committed_.size());
         CUDA_OK(cudaStreamSynchronize(stream_));
     }
 
@@ -1018,6 +1069,7 @@ public:
         std::vector<int> rows = chain_pass(base_, bcache_, bws_, bcache_.committed, n0, nullptr, false, false, 0);
         head(base_, bws_, (int)rows.size() - 1, 1, arena_ + n0, nullptr);
         CUDA_OK(cudaMemcpyAsync(outcome_host_, arena_ + n0, sizeof(int), cudaMemcpyDeviceToHost, stream_));
+        d2h_bytes_ += sizeof(int);
         CUDA_OK(cudaEventRecord(ev_[3], stream_));
         CUDA_OK(cudaEventSynchronize(ev_[3]));
         CUDA_OK(cudaGetLastError());
@@ -1144,6 +1196,7 @@ public:
         ++launches_;
         const int out_n = 2 + 2 * run_.n;
         CUDA_OK(cudaMemcpyAsync(outcome_host_, arena_ + out_off_, sizeof(int) * out_n, cudaMemcpyDeviceToHost, stream_));
+        d2h_bytes_ += (long long)sizeof(int) * out_n;
         CUDA_OK(cudaEventRecord(ev_[3], stream_));
         CUDA_OK(cudaEventSynchronize(ev_[3]));
         CUDA_OK(cudaGetLastError());
@@ -1320,6 +1373,11 @@ private:
     int draft_cached_ = 0;
     int generated_ = 0;
     int launches_ = 0;
+    static constexpr int kSiteEvents = 4096;
+    cudaEvent_t site_ev_[2 * kSiteEvents];
+    int site_which_ = -1, site_kind_ = -1, site_n_ = 0;
+    double site_ms_ = 0, site_bytes_ = 0;
+    long long h2d_bytes_ = 0, d2h_bytes_ = 0;
 };
 
 std::unique_ptr<Engine> make_engine(const ModelCfg& base, const ModelCfg& draft, const RunCfg& run, int device) {

@@ -105,6 +105,11 @@ public:
     virtual long long device_bytes() const = 0;
     virtual int kernel_launches() const = 0;
     virtual void reset_launch_count() = 0;
+    // Per-launch CUDA-event timing of one kernel site (which model, kind):
+    // kind 0 QKV GEMV, 1 attention, 2 O GEMV, 3 gate/up GEMV, 4 down GEMV, 5 head.
+    virtual void time_site(int which, int kind) = 0;  // which < 0 disables
+    virtual void site_stats(int* count, double* total_ms, double* bytes_per_launch) = 0;
+    virtual void io_bytes(long long* h2d, long long* d2h) const = 0;
 };
 
 }  // namespace espec

@@ -96,6 +96,12 @@ def lib():
         L.espec_kernel_launches.argtypes = [V]
         L.espec_reset_kernel_launches.argtypes = [V]
         L.espec_sync.argtypes = [V]
+        L.espec_generate_tokens.argtypes = [V, P(C.c_int32), C.c_int, P(C.c_int32), P(C.c_int), P(_Iter), P(C.c_int)]
+        L.espec_stream.restype = C.c_void_p
+        L.espec_stream.argtypes = [V]
+        L.espec_time_site.argtypes = [V, C.c_int, C.c_int]
+        L.espec_site_stats.argtypes = [V, P(C.c_int), P(C.c_double), P(C.c_double)]
+        L.espec_io_bytes.argtypes = [V, P(C.c_int64), P(C.c_int64)]
         _lib = L
     return _lib
 
@@ -253,6 +259,36 @@ class Engine:
         self._check(lib().espec_generate(self._h, prompt, len(prompt), _i(out), C.byref(n_out), traces,
                                          C.byref(n_it)))
         return list(out[: n_out.value]), [_trace(traces[i]) for i in range(n_it.value)]
+
+    def generate_tokens(self, tokens: Sequence[int]):
+        """generate() over token ids (host buffers in, host buffers out)."""
+        n = self.run.max_new_tokens
+        t = np.ascontiguousarray(tokens, np.int32)
+        out = np.zeros(n, np.int32)
+        traces = (_Iter * max(n, 1))()
+        n_out, n_it = C.c_int(0), C.c_int(0)
+        self._check(lib().espec_generate_tokens(self._h, _i(t), len(t), _i(out), C.byref(n_out), traces,
+                                                C.byref(n_it)))
+        return list(out[: n_out.value]), [_trace(traces[i]) for i in range(n_it.value)]
+
+    def stream(self) -> int:
+        """cudaStream_t (as an int) all of this engine's kernels run on."""
+        return lib().espec_stream(self._h)
+
+    def time_site(self, which: int, kind: int):
+        """Per-launch event timing of one kernel site (kind: 0 qkv, 1 attention,
+        2 o-proj, 3 gate/up, 4 down, 5 head); which < 0 disables."""
+        self._check(lib().espec_time_site(self._h, which, kind))
+
+    def site_stats(self):
+        n, ms, b = C.c_int(0), C.c_double(0), C.c_double(0)
+        self._check(lib().espec_site_stats(self._h, C.byref(n), C.byref(ms), C.byref(b)))
+        return n.value, ms.value, b.value
+
+    def io_bytes(self):
+        a, b = C.c_int64(0), C.c_int64(0)
+        self._check(lib().espec_io_bytes(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def begin(self, tokens: Sequence[int]):
         t = np.asarray(tokens, np.int32)

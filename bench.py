@@ -290,6 +290,9 @@ def main():
         sampler = ClockSampler(dev) if clocks else None
         if sampler:
             sampler.__enter__()
+        prof = os.environ.get("ESPEC_PROFILE_REGION") == "1" and alg == "easyspec"
+        if prof:  # ncu --profile-from-start off: capture only the timed decode steps
+            torch.cuda.profiler.start()
         ev0.record(stream)
         traces, emitted = [], 0
         for _ in range(steps):
@@ -298,6 +301,8 @@ def main():
             traces.append(tr)
         ev1.record(stream)
         torch.cuda.synchronize()
+        if prof:
+            torch.cuda.profiler.stop()
         if sampler:
             sampler.__exit__()
         barrier()

@@ -40,6 +40,8 @@ void ModelCfg::validate() const {
     if (d_mlp % 8 != 0) cfg_fail("d_mlp must be a multiple of 8");
     if (n_heads / n_kv_heads * 1 > 64) cfg_fail("query heads per kv head must be <= 64");
     if (weight_dtype != DT_F32 && weight_dtype != DT_BF16) cfg_fail("weight dtype must be f32 or bf16");
+    if (weight_dtype == DT_BF16 && (d_model % 32 || (n_heads * d_head) % 16 || d_mlp % 16))
+        cfg_fail("bf16 weights need d_model % 32 == 0 and n_heads*d_head, d_mlp multiples of 16");
     if (kv_dtype != DT_F32 && kv_dtype != DT_BF16) cfg_fail("kv dtype must be f32 or bf16");
 }
 
@@ -168,6 +170,8 @@ struct Xoshiro {
 // ---------------------------------------------------------------------------
 
 static int pad8(int n) { return (n + 7) / 8 * 8; }
+// GEMV weight leading dimension: bf16 weights are packed per 32 columns.
+static int ldpad(int n, int dt) { return dt == DT_BF16 ? (n + 31) / 32 * 32 : pad8(n); }
 static size_t dsize(int dt) { return dt == DT_BF16 ? 2 : 4; }
 
 static uint16_t f2bf(float f) {
@@ -202,7 +206,7 @@ struct ModelDev {
     std::vector<LayerDev> L;
     std::vector<void*> owned;
     int qkv_N() const { return (c.n_heads + 2 * c.n_kv_heads) * c.d_head; }
-    int qkv_ld() const { return pad8(qkv_N()); }
+    int qkv_ld() const { return ldpad(qkv_N(), c.weight_dtype); }
     int gu_tiles() const { return (c.d_mlp + 127) / 128; }
     int gu_ld() const { return gu_tiles() * 256; }
     int qdim() const { return c.n_heads * c.d_head; }
@@ -216,7 +220,7 @@ struct ModelDev {
     }
     void allocate(bool share_layers_from_base, const ModelDev* base) {
         const int d = c.d_model, f = c.d_mlp, V = c.vocab_size, es = (int)dsize(c.weight_dtype);
-        head_ld = pad8(V);
+        head_ld = ldpad(V, c.weight_dtype);
         if (share_layers_from_base) {
             emb = base->emb;
             head = base->head;
@@ -494,6 +498,7 @@ public:
         staging_.destroy();
         for (void* p : ws_owned_) cudaFree(p);
         cudaFree(arena_);
+        if (temp_) cudaFree(temp_);
         cudaFreeHost(outcome_host_);
         for (auto& e : ev_) cudaEventDestroy(e);
         for (auto& e : site_ev_) cudaEventDestroy(e);
@@ -596,38 +601,78 @@ public:
             }
             return;
         }
-        // Perf mode: same std rules, drawn on device from a counter hash.
+        // Perf mode: same std rules, drawn on device from a counter hash
+        // (logical layout first, padding columns zeroed, then packed).
         const int dt = c.weight_dtype;
         uint64_t k = seed * 1000003ULL + 17;
+        const int qd = M.qdim();
         launch_fill_normal(dt, M.emb, (long long)V * d, emb_sd, k++, stream_);
-        if (c.tied_head) launch_transpose(dt, M.emb, V, d, M.head, M.head_ld, stream_);
-        else launch_fill_normal(dt, M.head, (long long)d * M.head_ld, emb_sd, k++, stream_);
-        if (M.head_ld != V)
-            CUDA_OK(cudaMemset2DAsync((char*)M.head + (size_t)V * dsize(dt), (size_t)M.head_ld * dsize(dt), 0,
-                                      (size_t)(M.head_ld - V) * dsize(dt), d, stream_));
         launch_fill_const(DT_F32, M.fgain, d, 1.f, stream_);
+        if (c.tied_head) {
+            void* t = temp((size_t)d * M.head_ld * dsize(dt));
+            CUDA_OK(cudaMemsetAsync(t, 0, (size_t)d * M.head_ld * dsize(dt), stream_));
+            launch_transpose(dt, M.emb, V, d, t, M.head_ld, stream_);
+            finish_logical(M.head, dt, d, M.head_ld, t);
+        } else {
+            mat_fill(M.head, dt, d, M.head_ld, V, emb_sd, k++, [](int) { return true; });
+        }
         for (int l = 0; l < c.n_layers; ++l) {
             LayerDev& L = M.L[l];
-            launch_fill_normal(dt, L.wqkv, (long long)d * M.qkv_ld(), proj_sd, k++, stream_);
-            launch_fill_normal(dt, L.wo, (long long)M.qdim() * d, proj_sd * resid, k++, stream_);
-            launch_fill_normal(dt, L.wgu, (long long)d * M.gu_ld(), proj_sd, k++, stream_);
-            launch_fill_normal(dt, L.wd, (long long)f * d, down_sd, k++, stream_);
+            mat_fill(L.wqkv, dt, d, M.qkv_ld(), M.qkv_N(), proj_sd, k++, [](int) { return true; });
+            mat_fill(L.wo, dt, qd, d, d, proj_sd * resid, k++, [](int) { return true; });
+            mat_fill(L.wgu, dt, d, M.gu_ld(), M.gu_ld(), proj_sd, k++, [f](int n) { return (n / 256) * 128 + (n % 128) < f; });
+            mat_fill(L.wd, dt, f, d, d, down_sd, k++, [](int) { return true; });
             launch_fill_const(DT_F32, L.ga, d, 1.f, stream_);
             launch_fill_const(DT_F32, L.gm, d, 1.f, stream_);
-            if (f % 128) {
-                // zero the padded gate/up columns of the last interleaved tile
-                const int tiles = M.gu_tiles(), rem = f % 128;
-                const size_t es = dsize(dt);
-                char* base = (char*)L.wgu + (size_t)(tiles - 1) * 256 * es;
-                CUDA_OK(cudaMemset2DAsync(base + rem * es, M.gu_ld() * es, 0, (128 - rem) * es, d, stream_));
-                CUDA_OK(cudaMemset2DAsync(base + (128 + rem) * es, M.gu_ld() * es, 0, (128 - rem) * es, d, stream_));
-            }
-            if (M.qkv_ld() != M.qkv_N())
-                CUDA_OK(cudaMemset2DAsync((char*)L.wqkv + (size_t)M.qkv_N() * dsize(dt), M.qkv_ld() * dsize(dt), 0,
-                                          (M.qkv_ld() - M.qkv_N()) * dsize(dt), d, stream_));
         }
         CUDA_OK(cudaStreamSynchronize(stream_));
         CUDA_OK(cudaGetLastError());
+    }
+
+    // ---- weight matrices: fp32 row-major, or bf16 packed in mma fragment order
+    void* temp(size_t bytes) {
+        if (bytes > temp_bytes_) {
+            if (temp_) cudaFree(temp_);
+            CUDA_OK(cudaMalloc(&temp_, bytes));
+            temp_bytes_ = bytes;
+        }
+        return temp_;
+    }
+    // logical (K x ld, in temp) -> final storage
+    void finish_logical(void* W, int dt, int K, int ld, const void* logical) {
+        if (dt == DT_BF16) launch_pack(logical, K, ld, W, false, stream_);
+        else CUDA_OK(cudaMemcpyAsync(W, logical, (size_t)K * ld * 4, cudaMemcpyDeviceToDevice, stream_));
+        CUDA_OK(cudaStreamSynchronize(stream_));
+    }
+    template <typename Valid>
+    void mat_fill(void* W, int dt, int K, int ld, int N, float sd, uint64_t seed, Valid valid) {
+        const size_t es = dsize(dt);
+        void* t = temp((size_t)K * ld * es);
+        launch_fill_normal(dt, t, (long long)K * ld, sd, seed, stream_);
+        if (N < ld) CUDA_OK(cudaMemset2DAsync((char*)t + (size_t)N * es, ld * es, 0, (ld - N) * es, K, stream_));
+        // zero padded columns inside the interleaved gate/up tiles
+        for (int n0 = 0; n0 < std::min(N, ld); n0 += 128) {
+            if (!valid(n0 + 127)) {
+                int first = n0;
+                while (first < n0 + 128 && valid(first)) ++first;
+                CUDA_OK(cudaMemset2DAsync((char*)t + (size_t)first * es, ld * es, 0, (n0 + 128 - first) * es, K, stream_));
+            }
+        }
+        finish_logical(W, dt, K, ld, t);
+    }
+    void mat_write(void* W, int dt, int K, int ld, long long col0, const float* src, long long cols) {
+        if (dt != DT_BF16) return upload_block(W, dt, ld, col0, src, K, cols, stream_);
+        void* t = temp((size_t)K * ld * 2);
+        launch_pack(t, K, ld, W, true, stream_);
+        upload_block(t, dt, ld, col0, src, K, cols, stream_);
+        finish_logical(W, dt, K, ld, t);
+    }
+    void mat_read(const void* W, int dt, int K, int ld, long long col0, float* dst, long long cols) {
+        if (dt != DT_BF16) return download_block(W, dt, ld, col0, dst, K, cols);
+        void* t = temp((size_t)K * ld * 2);
+        launch_pack(t, K, ld, const_cast<void*>(W), true, stream_);
+        CUDA_OK(cudaStreamSynchronize(stream_));
+        download_block(t, dt, ld, col0, dst, K, cols);
     }
 
     void load_tensor(int which, const std::string& name, int layer, const float* data, long long rows,
@@ -647,14 +692,14 @@ public:
                 std::vector<float> t((size_t)d * V);
                 for (int v = 0; v < V; ++v)
                     for (int j = 0; j < d; ++j) t[(size_t)j * V + v] = data[(size_t)v * d + j];
-                upload_block(M.head, dt, M.head_ld, 0, t.data(), d, V, stream_);
+                mat_write(M.head, dt, d, M.head_ld, 0, t.data(), V);
             }
             return;
         }
         if (name == "head") {
             if (c.tied_head) throw Error(ST_CONFIG, "model has a tied head");
             expect(d, V);
-            upload_block(M.head, dt, M.head_ld, 0, data, d, V, stream_);
+            mat_write(M.head, dt, d, M.head_ld, 0, data, V);
             return;
         }
         if (name == "final_norm_gain") {
@@ -665,11 +710,11 @@ public:
         if (layer < 0 || layer >= c.n_layers) throw Error(ST_SHAPE, "layer index out of range");
         LayerDev& L = M.L[layer];
         const int qd = M.qdim(), kd = M.kvdim();
-        if (name == "wq") { expect(d, qd); upload_block(L.wqkv, dt, M.qkv_ld(), 0, data, d, qd, stream_); }
-        else if (name == "wk") { expect(d, kd); upload_block(L.wqkv, dt, M.qkv_ld(), qd, data, d, kd, stream_); }
-        else if (name == "wv") { expect(d, kd); upload_block(L.wqkv, dt, M.qkv_ld(), qd + kd, data, d, kd, stream_); }
-        else if (name == "wo") { expect(qd, d); upload_block(L.wo, dt, d, 0, data, qd, d, stream_); }
-        else if (name == "w_down") { expect(f, d); upload_block(L.wd, dt, d, 0, data, f, d, stream_); }
+        if (name == "wq") { expect(d, qd); mat_write(L.wqkv, dt, d, M.qkv_ld(), 0, data, qd); }
+        else if (name == "wk") { expect(d, kd); mat_write(L.wqkv, dt, d, M.qkv_ld(), qd, data, kd); }
+        else if (name == "wv") { expect(d, kd); mat_write(L.wqkv, dt, d, M.qkv_ld(), qd + kd, data, kd); }
+        else if (name == "wo") { expect(qd, d); mat_write(L.wo, dt, qd, d, 0, data, d); }
+        else if (name == "w_down") { expect(f, d); mat_write(L.wd, dt, f, d, 0, data, d); }
         else if (name == "w_gate" || name == "w_up") {
             expect(d, f);
             const int half = name == "w_up" ? 128 : 0;
@@ -678,7 +723,7 @@ public:
                 const int w = std::min(128, f - t * 128);
                 for (int r = 0; r < d; ++r)
                     for (int j = 0; j < w; ++j) blk[(size_t)r * w + j] = data[(size_t)r * f + t * 128 + j];
-                upload_block(L.wgu, dt, M.gu_ld(), t * 256 + half, blk.data(), d, w, stream_);
+                mat_write(L.wgu, dt, d, M.gu_ld(), t * 256 + half, blk.data(), w);
             }
         } else if (name == "attn_norm_gain") {
             expect(1, d);
@@ -696,21 +741,21 @@ public:
         const ModelCfg& c = M.c;
         const int d = c.d_model, f = c.d_mlp, dt = c.weight_dtype;
         if (name == "embedding") return download_block(M.emb, dt, d, 0, out, rows, cols);
-        if (name == "head") return download_block(M.head, dt, M.head_ld, 0, out, rows, cols);
+        if (name == "head") return mat_read(M.head, dt, d, M.head_ld, 0, out, cols);
         if (name == "final_norm_gain") { CUDA_OK(cudaMemcpy(out, M.fgain, 4 * d, cudaMemcpyDeviceToHost)); return; }
         LayerDev& L = M.L.at(layer);
         const int qd = M.qdim(), kd = M.kvdim();
-        if (name == "wq") return download_block(L.wqkv, dt, M.qkv_ld(), 0, out, d, qd);
-        if (name == "wk") return download_block(L.wqkv, dt, M.qkv_ld(), qd, out, d, kd);
-        if (name == "wv") return download_block(L.wqkv, dt, M.qkv_ld(), qd + kd, out, d, kd);
-        if (name == "wo") return download_block(L.wo, dt, d, 0, out, qd, d);
-        if (name == "w_down") return download_block(L.wd, dt, d, 0, out, f, d);
+        if (name == "wq") return mat_read(L.wqkv, dt, d, M.qkv_ld(), 0, out, qd);
+        if (name == "wk") return mat_read(L.wqkv, dt, d, M.qkv_ld(), qd, out, kd);
+        if (name == "wv") return mat_read(L.wqkv, dt, d, M.qkv_ld(), qd + kd, out, kd);
+        if (name == "wo") return mat_read(L.wo, dt, qd, d, 0, out, d);
+        if (name == "w_down") return mat_read(L.wd, dt, f, d, 0, out, d);
         if (name == "w_gate" || name == "w_up") {
             const int half = name == "w_up" ? 128 : 0;
             std::vector<float> blk((size_t)d * 128);
             for (int t = 0; t < M.gu_tiles(); ++t) {
                 const int w = std::min(128, f - t * 128);
-                download_block(L.wgu, dt, M.gu_ld(), t * 256 + half, blk.data(), d, w);
+                mat_read(L.wgu, dt, d, M.gu_ld(), t * 256 + half, blk.data(), w);
                 for (int r = 0; r < d; ++r)
                     for (int j = 0; j < w; ++j) out[(size_t)r * f + t * 128 + j] = blk[(size_t)r * w + j];
             }
@@ -733,7 +778,7 @@ public:
         const ModelCfg& c = M.c;
         const int d = c.d_model, qd = c.n_heads * c.d_head, f = c.d_mlp;
         const int tiles = (d + kStatTile - 1) / kStatTile;
-        const int head_ld = pad8(c.vocab_size);
+        const int head_ld = ldpad(c.vocab_size, c.weight_dtype);
         W.G = G;
         W.h = (float*)wsalloc(sizeof(float) * kChunk * d);
         W.stats = (float*)wsalloc(sizeof(float) * kChunk * tiles);
@@ -872,6 +917,10 @@ public:
         *h2d = h2d_bytes_;
         *d2h = d2h_bytes_;
     }
+    static int chunks(const ModelDev& M, int T) {
+        const int r = gemv_rows_per_launch(M.c.weight_dtype);
+        return (T + r - 1) / r;
+    }
     static double gemv_bytes(const ModelDev& M, int K, int ldw, int N, int T, int nprob) {
         return (double)nprob * ((double)K * ldw * dsize(M.c.weight_dtype) + 4.0 * T * (K + N));
     }
@@ -904,7 +953,7 @@ public:
             }
             site(M, 0, gemv_bytes(M, d, M.qkv_ld(), M.qkv_N(), T, n),
                  [&] { launch_gemv(EPI_QKV, wdt, qb, n, T, ps.view, kv, stream_); });
-            launches_ += (T + 7) / 8;
+            launches_ += chunks(M, T);
             attention(M, C, W, g, ps);
             if (n == 1) {
                 const LayerDev& L = M.L[g[0]];
@@ -914,7 +963,7 @@ public:
                 p.out = W.h; p.ldo = d; p.resid = W.h; p.ldr = d; p.stats_out = W.stats; p.stat_tiles_out = tiles;
                 ob.p[0] = p;
                 site(M, 2, gemv_bytes(M, qd, d, d, T, 1), [&] { launch_gemv(EPI_RESID, wdt, ob, 1, T, ps.view, kv, stream_); });
-                launches_ += (T + 7) / 8;
+                launches_ += chunks(M, T);
             } else {
                 GemvBatch ob;
                 for (int i = 0; i < n; ++i) {
@@ -925,7 +974,7 @@ public:
                     ob.p[i] = p;
                 }
                 site(M, 2, gemv_bytes(M, qd, d, d, T, n), [&] { launch_gemv(EPI_STORE, wdt, ob, n, T, ps.view, kv, stream_); });
-                launches_ += (T + 7) / 8;
+                launches_ += chunks(M, T);
             }
             // residual / MLP chain stays sequential (proj/src/draft_engine.cpp:112-130)
             for (int i = 0; i < n; ++i) {
@@ -950,7 +999,7 @@ public:
                 q.out = W.h; q.ldo = d; q.resid = W.h; q.ldr = d; q.stats_out = W.stats; q.stat_tiles_out = tiles;
                 db.p[0] = q;
                 site(M, 4, gemv_bytes(M, f, d, d, T, 1), [&] { launch_gemv(EPI_RESID, wdt, db, 1, T, ps.view, kv, stream_); });
-                launches_ += 2 * ((T + 7) / 8);
+                launches_ += 2 * chunks(M, T);
             }
         }
     }
@@ -995,7 +1044,7 @@ public:
         PassView none;
         site(M, 5, gemv_bytes(M, d, M.head_ld, c.vocab_size, n, 1),
              [&] { launch_gemv(EPI_ARGMAX, c.weight_dtype, hb, 1, n, none, KvView(), stream_); });
-        launches_ += (n + 7) / 8;
+        launches_ += chunks(M, n);
     }
 
     // Stage the committed tokens a cache is missing as a chain and run it,
@@ -1366,6 +1415,8 @@ private:
     int* arena_ = nullptr;
     int arena_cap_ = 0, tree_off_ = 0, am_off_ = 0, out_off_ = 0;
     int* outcome_host_ = nullptr;
+    void* temp_ = nullptr;
+    size_t temp_bytes_ = 0;
     RunCfg run_;
     std::vector<int> widths_;
     LayerPlan plan_;

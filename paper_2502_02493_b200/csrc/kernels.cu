@@ -14,6 +14,7 @@
 // a 1-row draft pass and a 6-row verify pass (greedy losslessness).
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -52,7 +53,7 @@ GemvPlan gemv_plan(int K, int N) {
 
 size_t gemv_partial_floats(int K, int N) {
     const GemvPlan p = gemv_plan(K, N);
-    return (size_t)p.splits * 8 * (size_t)p.tiles * kTileN;
+    return (size_t)p.splits * 16 * (size_t)p.tiles * kTileN;
 }
 
 struct GemvLaunch {
@@ -97,6 +98,29 @@ __device__ __forceinline__ long long kv_off(const KvView& kv, int layer, int kin
            ((((long long)layer * 2 + kind) * kv.n_kv + head) * kv.page_rows + r) * kv.dh;
 }
 
+__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
+    const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(a));
+}
+
+// Two GEMV main loops share the prologue/epilogue:
+//  * WT = bf16 (perf mode): tensor-core mma.sync m16n8k16, weights pre-packed
+//    in HBM in mma B-fragment order (see pack_index) so each lane's 16-byte
+//    load lands directly in its fragment registers — no shared-memory staging
+//    of W at all. Each warp owns 32 columns over the CTA's whole K chunk;
+//    the (<=16) input rows are the A operand (bf16, via ldmatrix).
+//  * WT = float (parity mode): CUDA-core FMA over the reference's row-major
+//    layout, 8 warps splitting K.
 template <typename WT, int TM, int EPI>
 __global__ void __launch_bounds__(kThreads) gemv_kernel(const __grid_constant__ GemvLaunch L) {
     extern __shared__ __align__(16) float smem[];
@@ -104,6 +128,7 @@ __global__ void __launch_bounds__(kThreads) gemv_kernel(const __grid_constant__ 
     __shared__ float red_small[8 * TM * 2];
     __shared__ int red_idx[8 * TM];
     __shared__ unsigned s_last;
+    constexpr bool kMma = std::is_same<WT, __nv_bfloat16>::value;
 
     const GemvProblem& P = L.b.p[blockIdx.z];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -125,72 +150,140 @@ __global__ void __launch_bounds__(kThreads) gemv_kernel(const __grid_constant__ 
         inv_rms[tid] = r;
     }
     __syncthreads();
-    float* xs = smem;  // [kc][TM]
-    for (int i = tid; i < kn * TM; i += kThreads) {
-        const int kk = i / TM, t = i - kk * TM;
-        float v = 0.f;
-        if (t < T) {
-            v = P.x[(size_t)(t0 + t) * P.ldx + k0 + kk];
-            if (P.gain != nullptr) v = __fmul_rn(__fmul_rn(v, inv_rms[t]), P.gain[k0 + kk]);
-        }
-        xs[kk * TM + t] = v;
-    }
-    __syncthreads();
 
-    // ---- main loop: stream W[k0:k0+kn, n0:n0+256]
-    constexpr int U = 8;
-    float acc[TM][8];
-#pragma unroll
-    for (int t = 0; t < TM; ++t)
-#pragma unroll
-        for (int c = 0; c < 8; ++c) acc[t][c] = 0.f;
-
-    const int col = n0 + lane * 8;
-    const bool col_ok = col < P.ldw;
-    const WT* Wb = reinterpret_cast<const WT*>(P.W) + (size_t)k0 * P.ldw + col;
-    for (int kk = warp; kk < kn; kk += 8 * U) {
-        W8<WT> w[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int k = kk + 8 * u;
-            if (k < kn && col_ok) w[u].load(Wb + (size_t)k * P.ldw);
-            else w[u].zero();
+    float s[TM];
+    if constexpr (kMma) {
+        static_assert(TM == 16, "the mma path covers 16 rows");
+        const int ldx = L.kc + 8;  // bf16 elements; +16 B keeps ldmatrix conflict-free
+        __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(smem);  // [16][kc+8]
+        for (int i = tid; i < TM * kn; i += kThreads) {
+            const int t = i / kn, kk = i - t * kn;
+            float v = 0.f;
+            if (t < T) {
+                v = P.x[(size_t)(t0 + t) * P.ldx + k0 + kk];
+                if (P.gain != nullptr) v = __fmul_rn(__fmul_rn(v, inv_rms[t]), P.gain[k0 + kk]);
+            }
+            xs[t * ldx + kk] = __float2bfloat16_rn(v);
         }
+        __syncthreads();
+        float acc[4][4];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int k = kk + 8 * u;
-            if (k < kn) {
-                float wf[8];
-                w[u].to_f32(wf);
-                const float* xr = xs + k * TM;
-                float xv[TM];
+        for (int j = 0; j < 4; ++j)
 #pragma unroll
-                for (int t = 0; t < TM; ++t) xv[t] = xr[t];
+            for (int e = 0; e < 4; ++e) acc[j][e] = 0.f;
+        const int g = tile * 8 + warp;  // 32-column group of this warp
+        if (g * 32 < P.ldw) {
+            const int KT = (P.K + 15) / 16;
+            const __nv_bfloat16* wp = reinterpret_cast<const __nv_bfloat16*>(P.W) +
+                                      ((size_t)g * KT + k0 / 16) * 512 + lane * 8;
+            const __nv_bfloat16* xrow = xs + (lane & 7) * ldx + ((lane >> 3) & 1) * 8 * ldx + (lane >> 4) * 8;
+            const int steps = kn / 16;
+            constexpr int U = 4;
+            for (int ks = 0; ks < steps; ks += U) {
+                uint4 w[U][2];
 #pragma unroll
-                for (int t = 0; t < TM; ++t)
+                for (int u = 0; u < U; ++u) {
+                    if (ks + u < steps) {
+                        w[u][0] = ld_stream(wp + (size_t)(ks + u) * 512);
+                        w[u][1] = ld_stream(wp + (size_t)(ks + u) * 512 + 256);
+                    } else {
+                        w[u][0] = w[u][1] = make_uint4(0, 0, 0, 0);
+                    }
+                }
 #pragma unroll
-                    for (int c = 0; c < 8; ++c) acc[t][c] = __fmaf_rn(xv[t], wf[c], acc[t][c]);
+                for (int u = 0; u < U; ++u) {
+                    if (ks + u < steps) {
+                        uint32_t a[4];
+                        ldsm_x4(a, xrow + (ks + u) * 16);
+                        mma_bf16_16816(acc[0], a, w[u][0].x, w[u][0].y);
+                        mma_bf16_16816(acc[1], a, w[u][0].z, w[u][0].w);
+                        mma_bf16_16816(acc[2], a, w[u][1].x, w[u][1].y);
+                        mma_bf16_16816(acc[3], a, w[u][1].z, w[u][1].w);
+                    }
+                }
             }
         }
-    }
-    __syncthreads();  // xs no longer needed
+        __syncthreads();  // xs dead
+        float* red = smem;  // [16][256]
+        const int gid = lane >> 2, tig = lane & 3;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int col = warp * 32 + j * 8 + 2 * tig;
+            red[gid * kTileN + col] = acc[j][0];
+            red[gid * kTileN + col + 1] = acc[j][1];
+            red[(gid + 8) * kTileN + col] = acc[j][2];
+            red[(gid + 8) * kTileN + col + 1] = acc[j][3];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int t = 0; t < TM; ++t) s[t] = red[t * kTileN + tid];
+    } else {
+        float* xs = smem;  // [kc][TM]
+        for (int i = tid; i < kn * TM; i += kThreads) {
+            const int kk = i / TM, t = i - kk * TM;
+            float v = 0.f;
+            if (t < T) {
+                v = P.x[(size_t)(t0 + t) * P.ldx + k0 + kk];
+                if (P.gain != nullptr) v = __fmul_rn(__fmul_rn(v, inv_rms[t]), P.gain[k0 + kk]);
+            }
+            xs[kk * TM + t] = v;
+        }
+        __syncthreads();
 
-    // ---- cross-warp reduction (fixed warp order)
-    float* red = smem;  // [8][TM][256]
+        // ---- main loop: stream W[k0:k0+kn, n0:n0+256]
+        constexpr int U = 8;
+        float acc[TM][8];
 #pragma unroll
-    for (int t = 0; t < TM; ++t) {
-        float4* dst = reinterpret_cast<float4*>(red + ((size_t)warp * TM + t) * kTileN + lane * 8);
-        dst[0] = make_float4(acc[t][0], acc[t][1], acc[t][2], acc[t][3]);
-        dst[1] = make_float4(acc[t][4], acc[t][5], acc[t][6], acc[t][7]);
-    }
-    __syncthreads();
-    float s[TM];
+        for (int t = 0; t < TM; ++t)
 #pragma unroll
-    for (int t = 0; t < TM; ++t) {
-        float v = 0.f;
+            for (int c = 0; c < 8; ++c) acc[t][c] = 0.f;
+
+        const int col = n0 + lane * 8;
+        const bool col_ok = col < P.ldw;
+        const WT* Wb = reinterpret_cast<const WT*>(P.W) + (size_t)k0 * P.ldw + col;
+        for (int kk = warp; kk < kn; kk += 8 * U) {
+            W8<WT> w[U];
 #pragma unroll
-        for (int w = 0; w < 8; ++w) v += red[((size_t)w * TM + t) * kTileN + tid];
-        s[t] = v;
+            for (int u = 0; u < U; ++u) {
+                const int k = kk + 8 * u;
+                if (k < kn && col_ok) w[u].load(Wb + (size_t)k * P.ldw);
+                else w[u].zero();
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int k = kk + 8 * u;
+                if (k < kn) {
+                    float wf[8];
+                    w[u].to_f32(wf);
+                    const float* xr = xs + k * TM;
+                    float xv[TM];
+#pragma unroll
+                    for (int t = 0; t < TM; ++t) xv[t] = xr[t];
+#pragma unroll
+                    for (int t = 0; t < TM; ++t)
+#pragma unroll
+                        for (int c = 0; c < 8; ++c) acc[t][c] = __fmaf_rn(xv[t], wf[c], acc[t][c]);
+                }
+            }
+        }
+        __syncthreads();  // xs no longer needed
+
+        // ---- cross-warp reduction (fixed warp order)
+        float* red = smem;  // [8][TM][256]
+#pragma unroll
+        for (int t = 0; t < TM; ++t) {
+            float4* dst = reinterpret_cast<float4*>(red + ((size_t)warp * TM + t) * kTileN + lane * 8);
+            dst[0] = make_float4(acc[t][0], acc[t][1], acc[t][2], acc[t][3]);
+            dst[1] = make_float4(acc[t][4], acc[t][5], acc[t][6], acc[t][7]);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int t = 0; t < TM; ++t) {
+            float v = 0.f;
+#pragma unroll
+            for (int w = 0; w < 8; ++w) v += red[((size_t)w * TM + t) * kTileN + tid];
+            s[t] = v;
+        }
     }
 
     const int c = n0 + tid;  // this thread's output column
@@ -198,7 +291,7 @@ __global__ void __launch_bounds__(kThreads) gemv_kernel(const __grid_constant__ 
         const size_t plane = (size_t)L.tiles * kTileN;
 #pragma unroll
         for (int t = 0; t < TM; ++t)
-            if (t < T) P.partial[((size_t)split * 8 + t) * plane + c] = s[t];
+            if (t < T) P.partial[((size_t)split * 16 + t) * plane + c] = s[t];
         __threadfence();
         __syncthreads();
         if (tid == 0) {
@@ -213,7 +306,7 @@ __global__ void __launch_bounds__(kThreads) gemv_kernel(const __grid_constant__ 
         for (int t = 0; t < TM; ++t) {
             float v = 0.f;
             if (t < T)
-                for (int sp = 0; sp < L.splits; ++sp) v += __ldcg(&P.partial[((size_t)sp * 8 + t) * plane + c]);
+                for (int sp = 0; sp < L.splits; ++sp) v += __ldcg(&P.partial[((size_t)sp * 16 + t) * plane + c]);
             s[t] = v;
         }
     }
@@ -344,7 +437,9 @@ __global__ void __launch_bounds__(kThreads) gemv_kernel(const __grid_constant__ 
 
 template <typename WT, int TM, int EPI>
 static void gemv_launch_t(const GemvLaunch& L, int nprob, cudaStream_t s) {
-    const size_t smem = sizeof(float) * (size_t)max(L.kc * TM, 8 * TM * kTileN);
+    constexpr bool kMma = std::is_same<WT, __nv_bfloat16>::value;
+    const size_t smem = kMma ? std::max<size_t>((size_t)TM * (L.kc + 8) * 2, (size_t)TM * kTileN * 4)
+                             : sizeof(float) * (size_t)max(L.kc * TM, 8 * TM * kTileN);
     static bool configured = false;
     if (!configured) {
         CK(cudaFuncSetAttribute(gemv_kernel<WT, TM, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -357,10 +452,14 @@ static void gemv_launch_t(const GemvLaunch& L, int nprob, cudaStream_t s) {
 
 template <typename WT, int EPI>
 static void gemv_dispatch_tm(const GemvLaunch& L, int nprob, cudaStream_t s) {
-    if (L.T <= 1) gemv_launch_t<WT, 1, EPI>(L, nprob, s);
-    else if (L.T <= 2) gemv_launch_t<WT, 2, EPI>(L, nprob, s);
-    else if (L.T <= 4) gemv_launch_t<WT, 4, EPI>(L, nprob, s);
-    else gemv_launch_t<WT, 8, EPI>(L, nprob, s);
+    if constexpr (std::is_same<WT, __nv_bfloat16>::value) {
+        gemv_launch_t<WT, 16, EPI>(L, nprob, s);
+    } else {
+        if (L.T <= 1) gemv_launch_t<WT, 1, EPI>(L, nprob, s);
+        else if (L.T <= 2) gemv_launch_t<WT, 2, EPI>(L, nprob, s);
+        else if (L.T <= 4) gemv_launch_t<WT, 4, EPI>(L, nprob, s);
+        else gemv_launch_t<WT, 8, EPI>(L, nprob, s);
+    }
 }
 
 template <typename WT>
@@ -374,6 +473,8 @@ static void gemv_dispatch_epi(int epi, const GemvLaunch& L, int nprob, cudaStrea
     }
 }
 
+int gemv_rows_per_launch(int wdtype) { return wdtype == DT_BF16 ? 16 : 8; }
+
 void launch_gemv(int epi, int wdtype, const GemvBatch& b, int nprob, int T, const PassView& pass,
                  const KvView& kv, cudaStream_t s) {
     if (T <= 0 || nprob <= 0) return;
@@ -385,12 +486,48 @@ void launch_gemv(int epi, int wdtype, const GemvBatch& b, int nprob, int T, cons
     L.tiles = plan.tiles;
     L.splits = plan.splits;
     L.kc = plan.kc;
-    for (int t0 = 0; t0 < T; t0 += 8) {
+    const int rows = gemv_rows_per_launch(wdtype);
+    for (int t0 = 0; t0 < T; t0 += rows) {
         L.t0 = t0;
-        L.T = min(8, T - t0);
+        L.T = min(rows, T - t0);
         if (wdtype == DT_BF16) gemv_dispatch_epi<__nv_bfloat16>(epi, L, nprob, s);
         else gemv_dispatch_epi<float>(epi, L, nprob, s);
     }
+}
+
+// Pre-packed bf16 layout: element (k, n) of a K x ldw matrix lives at
+//   ((g*KT + k/16)*512) + h*256 + lane*8 + j2*4 + e
+// with g = n/32, j = (n%32)/8 = 2h + j2, lane = (n%8)*4 + ((k%16)%8)/2,
+// e = (k&1) + 2*((k%16) >= 8): one lane's 16-byte load = its two mma
+// B fragments (m16n8k16, .col) for n8 tiles 2h and 2h+1.
+__host__ __device__ __forceinline__ size_t pack_index(int k, int n, int KT) {
+    const int g = n >> 5, j = (n & 31) >> 3, gid = n & 7;
+    const int kt = k >> 4, kk = k & 15;
+    const int tig = (kk & 7) >> 1, e = (kk & 1) + ((kk >> 3) << 1);
+    const int lane = gid * 4 + tig, h = j >> 1, j2 = j & 1;
+    return ((size_t)g * KT + kt) * 512 + h * 256 + lane * 8 + j2 * 4 + e;
+}
+
+__global__ void pack_kernel(const __nv_bfloat16* src, int K, int ldw, __nv_bfloat16* dst, int unpack) {
+    const int KT = (K + 15) / 16;
+    const long long total = (long long)KT * 16 * ldw;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+        const int k = (int)(i / ldw), n = (int)(i - (long long)k * ldw);
+        const size_t p = pack_index(k, n, KT);
+        if (unpack) {
+            if (k < K) dst[i] = src[p];
+        } else {
+            dst[p] = k < K ? src[i] : __float2bfloat16_rn(0.f);
+        }
+    }
+}
+
+size_t packed_elems(int K, int ldw) { return (size_t)((K + 15) / 16) * 16 * (size_t)ldw; }
+
+void launch_pack(const void* logical, int K, int ldw, void* packed, bool unpack, cudaStream_t s) {
+    pack_kernel<<<148 * 8, 256, 0, s>>>(reinterpret_cast<const __nv_bfloat16*>(unpack ? packed : logical), K, ldw,
+                                        reinterpret_cast<__nv_bfloat16*>(unpack ? const_cast<void*>(logical) : packed),
+                                        unpack ? 1 : 0);
 }
 
 // ---------------------------------------------------------------------------

@@ -59,7 +59,7 @@ struct GemvProblem {
     int stat_tiles_in = 0;
     float eps = 1e-5f;
     // workspace
-    float* partial = nullptr;     // [splits][8][ldw]
+    float* partial = nullptr;     // [splits][16][tiles*256]
     unsigned* tickets = nullptr;  // [tiles] (+1 for argmax)
     // epilogue
     float* out = nullptr;
@@ -93,6 +93,13 @@ struct GemvPlan {
 };
 GemvPlan gemv_plan(int K, int N);
 size_t gemv_partial_floats(int K, int N);  // workspace floats one problem needs
+
+// Rows handled per GEMV launch (bf16 mma path: 16; fp32 FMA path: 8).
+int gemv_rows_per_launch(int wdtype);
+// bf16 GEMV weights are stored pre-packed in mma fragment order (kernels.cu
+// pack_index); K x ldw logical <-> packed, ldw a multiple of 32.
+size_t packed_elems(int K, int ldw);
+void launch_pack(const void* logical, int K, int ldw, void* packed, bool unpack, cudaStream_t s);
 
 // y = epilogue(norm?(x) · W) for T rows, over nprob same-shape problems.
 void launch_gemv(int epi, int wdtype, const GemvBatch& b, int nprob, int T, const PassView& pass,

@@ -604,7 +604,7 @@ size_t attn_ws_floats(int T, int n_heads, int dh, int max_rows) {
 }
 size_t attn_tickets(int T, int n_heads, int n_kv) {
     const int G = n_heads / n_kv;
-    const int pb = (T * G + kAttnPairs - 1) / kAttnPairs;
+    const int pb = (T * G + 15) / 16;  // >= the fp32 kernel's 64-pair blocks
     return (size_t)n_kv * pb;
 }
 
@@ -757,6 +757,263 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(const __grid_constan
     }
 }
 
+// ---------------------------------------------------------------------------
+// bf16 KV: tensor-core split-KV attention (mma.sync m16n8k16).
+// CTA = 4 warps = 4 consecutive 64-row key splits (one KV page each) of one
+// kv head and one 16-pair m-tile ((query, q-head) pairs of the GQA group).
+// Per warp: S = Q K^T (ldmatrix K from smem), masked online softmax in
+// registers, O = P V (P re-used from the S accumulators as the A operand,
+// ldmatrix.trans V). Warps combine in shared memory; CTAs along the context
+// combine through a split workspace, last CTA in fixed order.
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&v);
+}
+
+__device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], const void* p) {
+    const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(a));
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const uint32_t a = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(a), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+
+template <int DH>
+__global__ void __launch_bounds__(128) attn_mma_kernel(const __grid_constant__ AttnLaunch L) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    __shared__ unsigned s_last;
+    constexpr int LDK = DH + 8;           // bf16 elements per smem row (16 B pad)
+    constexpr int NT = DH / 8;            // n8 tiles over head dims
+    const AttnProblem& A = L.b.p[blockIdx.z];
+    const int G = L.G, H = L.n_heads, T = L.pass.T, P = T * G;
+    const int n_kv = L.kv.n_kv;
+    const int hk = blockIdx.y % n_kv, mt = blockIdx.y / n_kv;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gid = lane >> 2, tig = lane & 3;
+    const int split = blockIdx.x * 4 + warp;
+    const int j0 = split * 64;
+    const int nr = max(0, min(64, L.pass.total - j0));
+    __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(smraw) + (size_t)warp * 2 * 64 * LDK;
+    __nv_bfloat16* Vs = Ks + 64 * LDK;
+    const __nv_bfloat16* pool = reinterpret_cast<const __nv_bfloat16*>(L.kv.pool);
+
+    if (nr > 0) {  // 64-row split = one page: K and V of this head are contiguous 64 x DH runs
+        const __nv_bfloat16* kg = pool + kv_off(L.kv, A.layer, 0, hk, j0);
+        const __nv_bfloat16* vg = pool + kv_off(L.kv, A.layer, 1, hk, j0);
+        constexpr int CH = DH / 8;  // 16-byte chunks per row
+        for (int i = lane; i < 64 * CH; i += 32) {
+            const int r = i / CH, c = (i % CH) * 8;
+            cp_async16(Ks + r * LDK + c, kg + (size_t)r * DH + c);
+        }
+        cp_async_commit();
+        for (int i = lane; i < 64 * CH; i += 32) {
+            const int r = i / CH, c = (i % CH) * 8;
+            cp_async16(Vs + r * LDK + c, vg + (size_t)r * DH + c);
+        }
+        cp_async_commit();
+    }
+    // Q A-fragments (pairs 16mt + gid / +8), scaled later on the scores
+    uint32_t qa[DH / 16][4];
+    {
+        const int p0 = mt * 16 + gid, p1 = p0 + 8;
+        const float* q0 = nullptr;
+        const float* q1 = nullptr;
+        if (p0 < P) q0 = A.q + (size_t)(p0 / G) * H * DH + (hk * G + p0 % G) * DH;
+        if (p1 < P) q1 = A.q + (size_t)(p1 / G) * H * DH + (hk * G + p1 % G) * DH;
+#pragma unroll
+        for (int s = 0; s < DH / 16; ++s) {
+            const int c = s * 16 + 2 * tig;
+            float2 a = q0 ? *reinterpret_cast<const float2*>(q0 + c) : make_float2(0.f, 0.f);
+            float2 b = q1 ? *reinterpret_cast<const float2*>(q1 + c) : make_float2(0.f, 0.f);
+            float2 cc = q0 ? *reinterpret_cast<const float2*>(q0 + c + 8) : make_float2(0.f, 0.f);
+            float2 d = q1 ? *reinterpret_cast<const float2*>(q1 + c + 8) : make_float2(0.f, 0.f);
+            qa[s][0] = pack_bf16x2(a.x, a.y);
+            qa[s][1] = pack_bf16x2(b.x, b.y);
+            qa[s][2] = pack_bf16x2(cc.x, cc.y);
+            qa[s][3] = pack_bf16x2(d.x, d.y);
+        }
+    }
+    float m_r[2] = {-INFINITY, -INFINITY}, l_r[2] = {0.f, 0.f};
+    float o[NT][4];
+#pragma unroll
+    for (int d = 0; d < NT; ++d) o[d][0] = o[d][1] = o[d][2] = o[d][3] = 0.f;
+    if (nr > 0) {
+        cp_async_wait<1>();
+        __syncwarp();
+        float sc[8][4];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) sc[j][0] = sc[j][1] = sc[j][2] = sc[j][3] = 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+#pragma unroll
+            for (int s = 0; s < DH / 16; s += 2) {
+                uint32_t b[4];
+                ldsm_x4(b, Ks + (j * 8 + (lane & 7)) * LDK + s * 16 + (lane >> 3) * 8);
+                mma_bf16_16816(sc[j], qa[s], b[0], b[1]);
+                mma_bf16_16816(sc[j], qa[s + 1], b[2], b[3]);
+            }
+        }
+        // scale + mask, row max / exp / sum over this split's 64 keys
+        const float inv_sqrt = 1.0f / sqrtf((float)DH);
+        const int pr[2] = {mt * 16 + gid, mt * 16 + gid + 8};
+        float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int ri = e >> 1;
+                const int key = j * 8 + 2 * tig + (e & 1);
+                const bool ok = pr[ri] < P && key < nr && visible(L.pass, pr[ri] / G, j0 + key);
+                sc[j][e] = ok ? __fmul_rn(sc[j][e], inv_sqrt) : -INFINITY;
+                mx[ri] = fmaxf(mx[ri], sc[j][e]);
+            }
+#pragma unroll
+        for (int ri = 0; ri < 2; ++ri) {
+            mx[ri] = fmaxf(mx[ri], __shfl_xor_sync(0xffffffffu, mx[ri], 1));
+            mx[ri] = fmaxf(mx[ri], __shfl_xor_sync(0xffffffffu, mx[ri], 2));
+        }
+        float sum[2] = {0.f, 0.f};
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int ri = e >> 1;
+                const float v = sc[j][e] == -INFINITY ? 0.f : expf(sc[j][e] - mx[ri]);
+                sc[j][e] = v;
+                sum[ri] += v;
+            }
+#pragma unroll
+        for (int ri = 0; ri < 2; ++ri) {
+            sum[ri] += __shfl_xor_sync(0xffffffffu, sum[ri], 1);
+            sum[ri] += __shfl_xor_sync(0xffffffffu, sum[ri], 2);
+            m_r[ri] = mx[ri];
+            l_r[ri] = sum[ri];
+        }
+        cp_async_wait<0>();
+        __syncwarp();
+        // O = P V
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {  // 16-key steps
+            uint32_t pa[4];
+            pa[0] = pack_bf16x2(sc[2 * s][0], sc[2 * s][1]);
+            pa[1] = pack_bf16x2(sc[2 * s][2], sc[2 * s][3]);
+            pa[2] = pack_bf16x2(sc[2 * s + 1][0], sc[2 * s + 1][1]);
+            pa[3] = pack_bf16x2(sc[2 * s + 1][2], sc[2 * s + 1][3]);
+#pragma unroll
+            for (int d = 0; d < NT; d += 2) {
+                uint32_t b[4];
+                // matrices: (keys 16s..+7, dims 8d), (keys +8, dims 8d), (keys 16s.., dims 8d+8), (keys +8, dims 8d+8)
+                const int mi = lane >> 3;
+                ldsm_x4_t(b, Vs + (s * 16 + (mi & 1) * 8 + (lane & 7)) * LDK + d * 8 + (mi >> 1) * 8);
+                mma_bf16_16816(o[d], pa, b[0], b[1]);
+                mma_bf16_16816(o[d + 1], pa, b[2], b[3]);
+            }
+        }
+    }
+    __syncthreads();  // K/V smem free: reuse for the warp combine
+    float* Os = reinterpret_cast<float*>(smraw);           // [4][16][DH]
+    float* Ms = Os + 4 * 16 * DH;                          // [4][16]
+    float* Ls = Ms + 64;
+#pragma unroll
+    for (int d = 0; d < NT; ++d) {
+        const int c = d * 8 + 2 * tig;
+        Os[(warp * 16 + gid) * DH + c] = o[d][0];
+        Os[(warp * 16 + gid) * DH + c + 1] = o[d][1];
+        Os[(warp * 16 + gid + 8) * DH + c] = o[d][2];
+        Os[(warp * 16 + gid + 8) * DH + c + 1] = o[d][3];
+    }
+    if (tig == 0) {
+        Ms[warp * 16 + gid] = m_r[0];
+        Ms[warp * 16 + gid + 8] = m_r[1];
+        Ls[warp * 16 + gid] = l_r[0];
+        Ls[warp * 16 + gid + 8] = l_r[1];
+    }
+    __syncthreads();
+    const int nchunks = gridDim.x;
+    const size_t ps = (size_t)DH + 2;
+    // CTA partial for (pair row r, dim c)
+    float* wsb = A.ws + (((size_t)blockIdx.x * gridDim.y + blockIdx.y) * 16) * ps;
+    for (int i = threadIdx.x; i < 16 * DH; i += 128) {
+        const int r = i / DH, c = i - r * DH;
+        float M = -INFINITY;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) M = fmaxf(M, Ms[w * 16 + r]);
+        float num = 0.f, den = 0.f;
+        if (M != -INFINITY)
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+                const float m = Ms[w * 16 + r];
+                if (m == -INFINITY) continue;
+                const float f = expf(m - M);
+                num = __fmaf_rn(f, Os[(w * 16 + r) * DH + c], num);
+                den = __fmaf_rn(f, Ls[w * 16 + r], den);
+            }
+        const int p = mt * 16 + r;
+        if (nchunks == 1) {
+            if (p < P) A.out[(size_t)(p / G) * H * DH + (hk * G + p % G) * DH + c] = den > 0.f ? num / den : 0.f;
+        } else {
+            wsb[r * ps + c] = num;
+            if (c == 0) {
+                wsb[r * ps + DH] = M;
+                wsb[r * ps + DH + 1] = den;
+            }
+        }
+    }
+    if (nchunks == 1) return;
+    __threadfence();
+    __syncthreads();
+    unsigned* ticket = A.tickets + blockIdx.y;
+    if (threadIdx.x == 0) {
+        const unsigned tk = atomicAdd(ticket, 1u);
+        s_last = (tk == (unsigned)nchunks - 1) ? 1u : 0u;
+        if (s_last) *ticket = 0u;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const size_t cstride = (size_t)gridDim.y * 16 * ps;
+    const float* base = A.ws + ((size_t)blockIdx.y * 16) * ps;
+    for (int i = threadIdx.x; i < 16 * DH; i += 128) {
+        const int r = i / DH, c = i - r * DH;
+        const int p = mt * 16 + r;
+        if (p >= P) continue;
+        float M = -INFINITY;
+        for (int ch = 0; ch < nchunks; ++ch) M = fmaxf(M, __ldcg(base + ch * cstride + r * ps + DH));
+        float num = 0.f, den = 0.f;
+        if (M != -INFINITY)
+            for (int ch = 0; ch < nchunks; ++ch) {
+                const float m = __ldcg(base + ch * cstride + r * ps + DH);
+                if (m == -INFINITY) continue;
+                const float f = expf(m - M);
+                num = __fmaf_rn(f, __ldcg(base + ch * cstride + r * ps + c), num);
+                den = __fmaf_rn(f, __ldcg(base + ch * cstride + r * ps + DH + 1), den);
+            }
+        A.out[(size_t)(p / G) * H * DH + (hk * G + p % G) * DH + c] = den > 0.f ? num / den : 0.f;
+    }
+}
+
+template <int DH>
+static void attn_mma_launch(const AttnLaunch& L, int nprob, cudaStream_t s) {
+    const int splits = (L.pass.total + 63) / 64;
+    const int mtiles = (L.pass.T * L.G + 15) / 16;
+    dim3 grid((splits + 3) / 4, L.kv.n_kv * mtiles, nprob);
+    const size_t smem = std::max<size_t>((size_t)4 * 2 * 64 * (DH + 8) * 2, (size_t)(4 * 16 * DH + 128) * 4);
+    static bool configured = false;
+    if (!configured) {
+        CK(cudaFuncSetAttribute(attn_mma_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        configured = true;
+    }
+    attn_mma_kernel<DH><<<grid, 128, smem, s>>>(L);
+}
+
 void launch_attention(const AttnBatch& b, int nprob, int n_heads, const PassView& pass, const KvView& kv,
                       cudaStream_t s) {
     if (pass.T <= 0 || nprob <= 0) return;
@@ -771,7 +1028,10 @@ void launch_attention(const AttnBatch& b, int nprob, int n_heads, const PassView
     const size_t smem = sizeof(float) * ((size_t)(kAttnPairs + kAttnRows) * (kv.dh + 1) + kAttnPairs * kAttnRows);
     static bool configured[2] = {false, false};
     dim3 grid(L.splits, kv.n_kv * L.pblocks, nprob);
-    if (kv.dtype == DT_BF16) {
+    if (kv.dtype == DT_BF16 && kv.page_rows == 64 && (kv.dh == 64 || kv.dh == 128)) {
+        if (kv.dh == 128) attn_mma_launch<128>(L, nprob, s);
+        else attn_mma_launch<64>(L, nprob, s);
+    } else if (kv.dtype == DT_BF16) {
         if (!configured[1]) {
             CK(cudaFuncSetAttribute(attn_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
             configured[1] = true;

@@ -188,6 +188,13 @@ int espec_kernel_launches(const espec_engine* eng);
 void espec_reset_kernel_launches(espec_engine* eng);
 espec_status espec_sync(espec_engine* eng);
 
+/* Instrumentation: time one bf16 decode GEMV shape (K x N, T rows, nprob
+ * batched problems, epilogue 0 store / 1 residual / 2 SiLU) in isolation on
+ * `device`, weights rotated over > 512 MB so every launch streams from HBM.
+ * Returns the mean device time per launch and the weight bytes it reads. */
+espec_status espec_bench_gemv(int K, int N, int T, int nprob, int epi, int iters, int device, double* us_per_launch,
+                              double* bytes_per_launch);
+
 #ifdef __cplusplus
 }
 #endif

@@ -4,13 +4,15 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "kernels.h"
 
 namespace espec_dev {
 
 constexpr int kThreads = 256;      // GEMV / elementwise CTA size (8 warps)
 constexpr int kTileN = 256;        // GEMV output columns per CTA (32 lanes x 8 cols)
-constexpr int kStatTile = 256;     // hidden-row sum-of-squares partial granularity
+constexpr int kStatTile = 32;      // hidden-row sum-of-squares partial granularity (one warp / one packed group)
 constexpr int kMaxGroup = 8;       // layers per fuzzy-group launch
 
 __device__ __forceinline__ float bf16_lo(uint32_t v) { return __uint_as_float(v << 16); }
@@ -51,6 +53,33 @@ __device__ __forceinline__ float ld_f(const float* p) { return *p; }
 __device__ __forceinline__ float ld_f(const __nv_bfloat16* p) { return __bfloat162float(*p); }
 __device__ __forceinline__ void st_f(float* p, float v) { *p = v; }
 __device__ __forceinline__ void st_f(__nv_bfloat16* p, float v) { *p = __float2bfloat16_rn(v); }
+
+// Programmatic dependent launch: every kernel waits for its predecessor's
+// memory before touching dependent data and lets its successor launch early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+bool pdl_enabled();
+void set_pdl(bool on);
+
+// Launch with programmatic stream serialisation (PDL) so the kernel's
+// launch and prologue overlap the previous kernel's tail; every kernel in
+// this library calls pdl_wait() before reading what its predecessor wrote.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll

@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <sstream>
 
@@ -37,7 +38,7 @@ void ModelCfg::validate() const {
     if (!(norm_eps > 0.f)) cfg_fail("norm_eps must be positive");
     if (d_model % 8 != 0) cfg_fail("d_model must be a multiple of 8");
     if ((n_heads * d_head) % 8 != 0) cfg_fail("n_heads * d_head must be a multiple of 8");
-    if (d_mlp % 8 != 0) cfg_fail("d_mlp must be a multiple of 8");
+    if (d_mlp % 16 != 0) cfg_fail("d_mlp must be a multiple of 16");
     if (n_heads / n_kv_heads * 1 > 64) cfg_fail("query heads per kv head must be <= 64");
     if (weight_dtype != DT_F32 && weight_dtype != DT_BF16) cfg_fail("weight dtype must be f32 or bf16");
     if (weight_dtype == DT_BF16 && (d_model % 32 || (n_heads * d_head) % 16 || d_mlp % 16))
@@ -191,7 +192,7 @@ static float bf2f(uint16_t b) {
 struct LayerDev {
     void* wqkv = nullptr;  // [d][qkv_ld]
     void* wo = nullptr;    // [H*dh][d]
-    void* wgu = nullptr;   // [d][gu_ld] interleaved per 128 cols
+    void* wgu = nullptr;   // [d][gu_ld] interleaved per 32 cols: [gate16 | up16]
     void* wd = nullptr;    // [f][d]
     float* ga = nullptr;
     float* gm = nullptr;
@@ -207,8 +208,8 @@ struct ModelDev {
     std::vector<void*> owned;
     int qkv_N() const { return (c.n_heads + 2 * c.n_kv_heads) * c.d_head; }
     int qkv_ld() const { return ldpad(qkv_N(), c.weight_dtype); }
-    int gu_tiles() const { return (c.d_mlp + 127) / 128; }
-    int gu_ld() const { return gu_tiles() * 256; }
+    int gu_N() const { return 2 * c.d_mlp; }
+    int gu_ld() const { return ldpad(gu_N(), c.weight_dtype); }
     int qdim() const { return c.n_heads * c.d_head; }
     int kvdim() const { return c.n_kv_heads * c.d_head; }
     void* alloc(size_t bytes) {
@@ -469,6 +470,7 @@ public:
         draft_.c = dc;
         set_run(run);
         CUDA_OK(cudaSetDevice(device));
+        if (const char* e = std::getenv("ESPEC_PDL")) set_pdl(std::atoi(e) != 0);
         CUDA_OK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
         for (auto& e : ev_) CUDA_OK(cudaEventCreate(&e));
         const int cap_b = bc.max_positions + kMaxNodes + kChunk;
@@ -620,7 +622,7 @@ public:
             LayerDev& L = M.L[l];
             mat_fill(L.wqkv, dt, d, M.qkv_ld(), M.qkv_N(), proj_sd, k++, [](int) { return true; });
             mat_fill(L.wo, dt, qd, d, d, proj_sd * resid, k++, [](int) { return true; });
-            mat_fill(L.wgu, dt, d, M.gu_ld(), M.gu_ld(), proj_sd, k++, [f](int n) { return (n / 256) * 128 + (n % 128) < f; });
+            mat_fill(L.wgu, dt, d, M.gu_ld(), M.gu_N(), proj_sd, k++, [](int) { return true; });
             mat_fill(L.wd, dt, f, d, d, down_sd, k++, [](int) { return true; });
             launch_fill_const(DT_F32, L.ga, d, 1.f, stream_);
             launch_fill_const(DT_F32, L.gm, d, 1.f, stream_);
@@ -716,14 +718,14 @@ public:
         else if (name == "wo") { expect(qd, d); mat_write(L.wo, dt, qd, d, 0, data, d); }
         else if (name == "w_down") { expect(f, d); mat_write(L.wd, dt, f, d, 0, data, d); }
         else if (name == "w_gate" || name == "w_up") {
+            // interleave per 32 packed columns: [gate16 | up16]
             expect(d, f);
-            const int half = name == "w_up" ? 128 : 0;
-            std::vector<float> blk((size_t)d * 128);
-            for (int t = 0; t < M.gu_tiles(); ++t) {
-                const int w = std::min(128, f - t * 128);
+            const int half = name == "w_up" ? 16 : 0;
+            std::vector<float> blk((size_t)d * 16);
+            for (int t = 0; t < f / 16; ++t) {
                 for (int r = 0; r < d; ++r)
-                    for (int j = 0; j < w; ++j) blk[(size_t)r * w + j] = data[(size_t)r * f + t * 128 + j];
-                mat_write(L.wgu, dt, d, M.gu_ld(), t * 256 + half, blk.data(), w);
+                    for (int j = 0; j < 16; ++j) blk[(size_t)r * 16 + j] = data[(size_t)r * f + t * 16 + j];
+                mat_write(L.wgu, dt, d, M.gu_ld(), t * 32 + half, blk.data(), 16);
             }
         } else if (name == "attn_norm_gain") {
             expect(1, d);
@@ -751,13 +753,12 @@ public:
         if (name == "wo") return mat_read(L.wo, dt, qd, d, 0, out, d);
         if (name == "w_down") return mat_read(L.wd, dt, f, d, 0, out, d);
         if (name == "w_gate" || name == "w_up") {
-            const int half = name == "w_up" ? 128 : 0;
-            std::vector<float> blk((size_t)d * 128);
-            for (int t = 0; t < M.gu_tiles(); ++t) {
-                const int w = std::min(128, f - t * 128);
-                mat_read(L.wgu, dt, d, M.gu_ld(), t * 256 + half, blk.data(), w);
+            const int half = name == "w_up" ? 16 : 0;
+            std::vector<float> blk((size_t)d * 16);
+            for (int t = 0; t < f / 16; ++t) {
+                mat_read(L.wgu, dt, d, M.gu_ld(), t * 32 + half, blk.data(), 16);
                 for (int r = 0; r < d; ++r)
-                    for (int j = 0; j < w; ++j) out[(size_t)r * f + t * 128 + j] = blk[(size_t)r * w + j];
+                    for (int j = 0; j < 16; ++j) out[(size_t)r * f + t * 16 + j] = blk[(size_t)r * 16 + j];
             }
             return;
         }
@@ -787,17 +788,17 @@ public:
         W.attn = (float*)wsalloc(sizeof(float) * (size_t)G * kChunk * d);
         W.act = (float*)wsalloc(sizeof(float) * (size_t)kChunk * f);
         W.logits = (float*)wsalloc(sizeof(float) * 8 * (size_t)head_ld);
-        const GemvPlan hp = gemv_plan(d, c.vocab_size);
-        W.am_val = (float*)wsalloc(sizeof(float) * kChunk * hp.tiles);
-        W.am_idx = (int*)wsalloc(sizeof(int) * kChunk * hp.tiles);
+        const int dt = c.weight_dtype;
+        const int head_tiles = gemv_col_tiles(d, c.vocab_size, dt);
+        W.am_val = (float*)wsalloc(sizeof(float) * kChunk * head_tiles);
+        W.am_idx = (int*)wsalloc(sizeof(int) * kChunk * head_tiles);
         const int qkv_N = (c.n_heads + 2 * c.n_kv_heads) * c.d_head;
-        const int gu_N = 2 * ((f + 127) / 128) * 128;
         size_t part = 0;
         int tick = 0;
-        const int shapes[5][2] = {{d, qkv_N}, {qd, d}, {d, gu_N}, {f, d}, {d, c.vocab_size}};
+        const int shapes[5][2] = {{d, qkv_N}, {qd, d}, {d, 2 * f}, {f, d}, {d, c.vocab_size}};
         for (auto& s : shapes) {
-            part = std::max(part, gemv_partial_floats(s[0], s[1]));
-            tick = std::max(tick, gemv_plan(s[0], s[1]).tiles + 1);
+            part = std::max(part, gemv_partial_floats(s[0], s[1], dt));
+            tick = std::max(tick, gemv_col_tiles(s[0], s[1], dt) + 1);
         }
         W.gemv_part_slot = part;
         W.gemv_ticket_slot = tick;
@@ -985,12 +986,10 @@ public:
                 }
                 GemvBatch ub;
                 GemvProblem p = gp(W, 0);
-                p.W = L.wgu; p.K = d; p.N = 2 * M.gu_tiles() * 128; p.ldw = M.gu_ld();
+                p.W = L.wgu; p.K = d; p.N = M.gu_N(); p.ldw = M.gu_ld();
                 p.x = W.h; p.ldx = d; p.gain = L.gm; p.stats_in = W.stats; p.stat_tiles_in = tiles; p.eps = c.norm_eps;
                 p.out = W.act; p.ldo = f;
                 ub.p[0] = p;
-                // EPI_SILU guards j < N/2 = padded f; outputs beyond f land in act padding
-                ub.p[0].N = 2 * f;
                 site(M, 3, gemv_bytes(M, d, M.gu_ld(), 2 * f, T, 1),
                      [&] { launch_gemv(EPI_SILU, wdt, ub, 1, T, ps.view, kv, stream_); });
                 GemvBatch db;

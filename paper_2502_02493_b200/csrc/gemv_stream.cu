@@ -1,0 +1,649 @@
+// Stream-K tensor-core GEMV for bf16 decode projections (sm_100a).
+//
+// y[T x N] = epilogue(norm?(x)[T x K] · W[K x N]) with T <= 16 rows and W
+// streamed once from HBM. W is stored pre-packed in mma.sync B-fragment order
+// (kernels.cu pack_index): a 32-column group g is one contiguous run of K/16
+// 1 KB blocks. The work is cut into *units* (problem, k-chunk j, group g) of
+// up to kUnitBlocks blocks, ordered (problem, j, g) with g fastest, and every
+// CTA of a persistent 1-CTA-per-SM grid takes one contiguous, balanced range
+// of units (the split depends only on K, N and the problem count).
+//
+// Per CTA: one producer warp streams the CTA's weight bytes with 1-D TMA bulk
+// copies (cp.async.bulk + mbarrier complete_tx) through a 16-stage x 8 KB
+// shared-memory ring — 128 KB in flight per SM without register pressure —
+// while 8 consumer warps each take one 1 KB block per stage: ldmatrix the
+// activation fragment from a staged bf16 copy of x, two ld.shared.v4 for the
+// weight fragments, four mma.m16n8k16 (fp32 accumulate). At the end of a unit
+// the 8 warp accumulators are summed in fixed warp order through shared
+// memory; units whose group is split over several k-chunks write a partial
+// and the last-arriving CTA (per-group ticket) sums the partials in fixed
+// k-chunk order. Every row's reduction order is therefore independent of T
+// and of which CTA ran which unit (batch invariance).
+//
+// Programmatic dependent launch: the producer starts streaming weights
+// before `griddepcontrol.wait`, so a GEMV's HBM pipeline fills while the
+// previous kernel (which produces x) drains; consumers wait before reading x.
+#include <cstdio>
+#include <cstdlib>
+#include <stdexcept>
+#include <string>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace espec_dev {
+
+constexpr int kSgConsumers = 8;                    // warps 0-7: tensor-core consumers
+constexpr int kSgProducer = kSgConsumers;          // warp 8: TMA producer
+constexpr int kSgEpi = kSgConsumers + 1;           // warps 9..: unit epilogues, round-robin over units
+// epilogue warps (= reduction buffers): 4 for <= 8 rows, 2 for 16 rows
+template <int TM> constexpr int sg_ne() { return TM == 8 ? 4 : 2; }
+template <int TM> constexpr int sg_threads() { return (kSgConsumers + 1 + sg_ne<TM>()) * 32; }
+// Stage = kBpw(TM) 1 KB blocks per consumer warp: 32 KB (TM=8) / 16 KB (TM=16),
+// so one mbarrier wait (~90 cycles even when already complete) is amortised
+// over several mma blocks.
+template <int TM> constexpr int sg_bpw() { return TM == 8 ? 4 : 2; }
+constexpr int kSgMaxStages = 16;
+constexpr int kSgSlots = 2;      // (problem, k-chunk) activation slots per CTA
+constexpr int kSgMaxUnitBlocks = 128;              // 2048 k-rows per unit
+constexpr int kSgSms = 148;
+constexpr int kSgSmemLimit = 227 * 1024 - 2048;    // dynamic smem budget (static smem aside)
+
+struct SgLaunch {
+    GemvBatch b;
+    PassView pass;
+    KvView kv;
+    int t0, T;
+    int KT, kcb, nK, ngroups, units, xld, stages, rotate;
+};
+
+SgPlan sgemv_plan(int K, int ldw, int nprob) {
+    SgPlan p;
+    p.KT = (K + 15) / 16;
+    p.ngroups = ldw / 32;
+    // Largest unit (<= 128 blocks = 2048 k-rows) that still leaves >= 4 units
+    // per SM, so the contiguous per-CTA ranges balance to within a few %.
+    // Depends on (K, N) only: the reduction tree never depends on T.
+    static const int min_units = [] {
+        const char* e = std::getenv("ESPEC_SG_UNITS_PER_SM");
+        return e ? std::atoi(e) : 4;
+    }();
+    int kcb = kSgMaxUnitBlocks;
+    while (kcb > 8 && (long long)p.ngroups * ((p.KT + kcb - 1) / kcb) < (long long)min_units * kSgSms) kcb /= 2;
+    if (kcb > p.KT) kcb = p.KT;
+    p.kcb = kcb;
+    p.nK = (p.KT + kcb - 1) / kcb;
+    p.units = nprob * p.nK * p.ngroups;
+    p.grid = p.units < kSgSms ? p.units : kSgSms;
+    // every CTA range must touch at most kSgSlots (problem, k-chunk) pairs
+    for (int c = 0; c < p.grid; ++c) {
+        const long long s = (long long)c * p.units / p.grid, e = (long long)(c + 1) * p.units / p.grid;
+        if (e > s && (e - 1) / p.ngroups - s / p.ngroups + 1 > kSgSlots)
+            throw std::runtime_error("sgemv_plan: K x problems too large for the activation slots");
+    }
+    return p;
+}
+
+size_t sgemv_partial_floats(int K, int ldw) {
+    const SgPlan p = sgemv_plan(K, ldw, 1);
+    return p.nK > 1 ? (size_t)p.nK * 16 * ldw : 0;
+}
+
+// smem = ring (stages x 8 KB) + activation slots + 2 reduction buffers
+static size_t sg_fixed_bytes(int TM, int kcb) {
+    return (size_t)kSgSlots * TM * (kcb * 16 + 8) * 2 + (size_t)(TM == 8 ? 4 : 2) * kSgConsumers * TM * 32 * 4;
+}
+static int sg_stage_bytes(int TM) { return (TM == 8 ? 4 : 2) * kSgConsumers * 1024; }
+static int sg_stages(int TM, int kcb) {
+    const long long room = (long long)kSgSmemLimit - (long long)sg_fixed_bytes(TM, kcb);
+    int st = (int)(room / sg_stage_bytes(TM));
+    if (st > kSgMaxStages) st = kSgMaxStages;
+    if (st < 2) throw std::runtime_error("sgemv: shared memory too small for the weight ring");
+    return st;
+}
+static size_t sg_smem_bytes(int TM, int kcb) {
+    return (size_t)sg_stages(TM, kcb) * sg_stage_bytes(TM) + sg_fixed_bytes(TM, kcb);
+}
+
+// ---------------------------------------------------------------------------
+// PTX helpers: mbarrier, 1-D TMA bulk copy, PDL
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// Ticket for "last one finishes": acq_rel at gpu scope orders this warp's
+// preceding partial stores (ordered before lane 0 by __syncwarp) before the
+// increment, and the winner's subsequent loads after it.
+__device__ __forceinline__ unsigned ticket_acq_rel(unsigned* p) {
+    unsigned old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(p) : "memory");
+    return old;
+}
+
+__device__ __forceinline__ bool sg_better(float v, int i, float bv, int bi) { return v > bv || (v == bv && i < bi); }
+
+__device__ __forceinline__ long long sg_kv_off(const KvView& kv, int layer, int kind, int head, int row) {
+    const int page = kv.page_table[row / kv.page_rows];
+    const int r = row % kv.page_rows;
+    return (long long)page * kv.page_elems + ((((long long)layer * 2 + kind) * kv.n_kv + head) * kv.page_rows + r) * kv.dh;
+}
+
+// ---------------------------------------------------------------------------
+// kernel
+// ---------------------------------------------------------------------------
+
+// Unit epilogue, run by one epilogue warp: lane = column within the 32-column
+// group, v[t] = the unit's full sum for row t (after the k-chunk reduction).
+template <int TM, int EPI>
+__device__ __forceinline__ void sg_epilogue(const SgLaunch& L, const GemvProblem& P, int g, const float (&v)[TM],
+                                            int lane) {
+    const int T = L.T, t0 = L.t0;
+    const int c = g * 32 + lane;
+    if constexpr (EPI == EPI_STORE) {
+#pragma unroll
+        for (int t = 0; t < TM; ++t)
+            if (t < T && c < P.N) P.out[(size_t)(t0 + t) * P.ldo + c] = v[t];
+    } else if constexpr (EPI == EPI_RESID) {
+        // h_mid = h + attn / h_next = h_mid + mlp (proj/src/draft_engine.cpp:15-19) + row stats
+#pragma unroll
+        for (int t = 0; t < TM; ++t) {
+            if (t >= T) break;
+            float sq = 0.f;
+            if (c < P.N) {
+                const float y = __fadd_rn(P.resid[(size_t)(t0 + t) * P.ldr + c], v[t]);
+                P.out[(size_t)(t0 + t) * P.ldo + c] = y;
+                sq = y * y;
+            }
+            sq = warp_sum(sq);
+            if (lane == 0) P.stats_out[(t0 + t) * P.stat_tiles_out + g] = sq;
+        }
+    } else if constexpr (EPI == EPI_SILU) {
+        // packed group = [gate 16 | up 16]: silu(gate) * up (proj/src/model.cpp:197-210)
+        const int a = g * 16 + lane;
+#pragma unroll
+        for (int t = 0; t < TM; ++t) {
+            const float up = __shfl_down_sync(0xffffffffu, v[t], 16);
+            if (t < T && lane < 16 && a < P.N / 2)
+                P.out[(size_t)(t0 + t) * P.ldo + a] = __fmul_rn(__fdiv_rn(v[t], __fadd_rn(1.0f, expf(-v[t]))), up);
+        }
+    } else if constexpr (EPI == EPI_QKV) {
+        // q = rope(h.Wq), k = rope(h.Wk), v = h.Wv ; K/V into the paged cache
+        // (proj/src/model.cpp:130-138, rotary proj/src/matrix.cpp:159-194)
+        const int qd = P.n_heads * P.dh, kd = P.n_kv * P.dh;
+        const int region = c < qd ? 0 : (c < qd + kd ? 1 : 2);
+        const int base = region == 0 ? 0 : (region == 1 ? qd : qd + kd);
+        const int within = c - base;
+        const int head = within / P.dh, i = within - head * P.dh;
+        const double inv_freq = pow((double)P.rope_theta, -2.0 * (i >> 1) / (double)P.dh);
+#pragma unroll
+        for (int t = 0; t < TM; ++t) {
+            const float other = __shfl_xor_sync(0xffffffffu, v[t], 1);
+            if (t >= T || c >= P.N) continue;
+            float y = v[t];
+            if (region < 2) {
+                const double th = (double)L.pass.pos[t0 + t] * inv_freq;
+                const float cs = (float)cos(th), sn = (float)sin(th);
+                y = (i & 1) ? __fadd_rn(__fmul_rn(other, sn), __fmul_rn(v[t], cs))
+                            : __fsub_rn(__fmul_rn(v[t], cs), __fmul_rn(other, sn));
+            }
+            if (region == 0) {
+                P.out[(size_t)(t0 + t) * P.ldo + c] = y;
+            } else {
+                const long long off = sg_kv_off(L.kv, P.layer, region - 1, head, L.pass.rows[t0 + t]) + i;
+                if (L.kv.dtype == DT_BF16) reinterpret_cast<__nv_bfloat16*>(L.kv.pool)[off] = __float2bfloat16_rn(y);
+                else reinterpret_cast<float*>(L.kv.pool)[off] = y;
+            }
+        }
+    } else if constexpr (EPI == EPI_ARGMAX) {
+        // logits = norm(h).E^T ; greedy pick = first maximum (proj/src/matrix.cpp:196-202)
+#pragma unroll
+        for (int t = 0; t < TM; ++t) {
+            if (t >= T) break;
+            float bv = -INFINITY;
+            int bi = 0x7fffffff;
+            if (c < P.vocab) {
+                if (P.logits) P.logits[(size_t)(t0 + t) * P.ld_logits + c] = v[t];
+                bv = v[t];
+                bi = c;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (sg_better(ov, oi, bv, bi)) {
+                    bv = ov;
+                    bi = oi;
+                }
+            }
+            if (lane == 0) {
+                P.am_val[(t0 + t) * L.ngroups + g] = bv;
+                P.am_idx[(t0 + t) * L.ngroups + g] = bi;
+            }
+        }
+        // last group to finish reduces the per-group maxima (fixed-order-free:
+        // max with lowest-index tie-break is order independent)
+        __syncwarp();
+        unsigned last = 0;
+        if (lane == 0) {
+            last = ticket_acq_rel(&P.tickets[L.ngroups]) == (unsigned)L.ngroups - 1 ? 1u : 0u;
+            if (last) P.tickets[L.ngroups] = 0u;
+        }
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (last) {
+            for (int t = 0; t < T; ++t) {
+                float fv = -INFINITY;
+                int fi = 0x7fffffff;
+                for (int q = lane; q < L.ngroups; q += 32) {
+                    const float ov = __ldcg(&P.am_val[(t0 + t) * L.ngroups + q]);
+                    const int oi = __ldcg(&P.am_idx[(t0 + t) * L.ngroups + q]);
+                    if (sg_better(ov, oi, fv, fi)) {
+                        fv = ov;
+                        fi = oi;
+                    }
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const float ov = __shfl_xor_sync(0xffffffffu, fv, o);
+                    const int oi = __shfl_xor_sync(0xffffffffu, fi, o);
+                    if (sg_better(ov, oi, fv, fi)) {
+                        fv = ov;
+                        fi = oi;
+                    }
+                }
+                if (lane == 0) P.tok_out[t0 + t] = fi;
+            }
+        }
+    }
+}
+
+template <int TM, int EPI>
+__global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid_constant__ SgLaunch L) {
+    extern __shared__ __align__(1024) unsigned char sm[];
+    __shared__ __align__(8) uint64_t full_bar[kSgMaxStages];
+    __shared__ __align__(8) uint64_t empty_bar[kSgMaxStages];
+    constexpr int NE = sg_ne<TM>();
+    __shared__ __align__(8) uint64_t red_full[NE];
+    __shared__ __align__(8) uint64_t red_empty[NE];
+    __shared__ float inv_rms[kSgSlots][TM];
+
+    constexpr int kBpw = sg_bpw<TM>();
+    constexpr int kStageBlocks = kBpw * kSgConsumers;
+    constexpr int kStageBytes = kStageBlocks * 1024;
+    const int stages = L.stages;
+    unsigned char* ring = sm;
+    __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(sm + (size_t)stages * kStageBytes);
+    const int xslot = TM * L.xld;  // elements per activation slot
+    float* red = reinterpret_cast<float*>(sm + (size_t)stages * kStageBytes + (size_t)kSgSlots * xslot * 2);
+    constexpr int kRedBuf = kSgConsumers * TM * 32;  // floats per reduction buffer
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int start = (int)((long long)blockIdx.x * L.units / gridDim.x);
+    const int end = (int)((long long)(blockIdx.x + 1) * L.units / gridDim.x);
+    const int pair0 = start / L.ngroups;
+    // Processing order: the range rotated so that units with g = 0 (mod R),
+    // R the nominal range length, come first. Every CTA then handles group g
+    // near step (g mod R) whatever its k-chunk, so the k-chunks of one group
+    // finish at about the same time and the final (last-chunk) reductions are
+    // spread over the kernel instead of piling up at its end.
+    const int len = end - start;
+    const int R = (L.units + gridDim.x - 1) / gridDim.x;
+    int off = L.rotate ? (R - (start % L.ngroups) % R) % R : 0;
+    if (off >= len) off = 0;
+
+    if (tid == 0) {
+        for (int s = 0; s < stages; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], kSgConsumers);
+        }
+        for (int e = 0; e < NE; ++e) {
+            mbar_init(&red_full[e], kSgConsumers);
+            mbar_init(&red_empty[e], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    // let the next kernel in the stream start its weight prefetch early
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+
+    if (warp == kSgProducer) {
+        // ---------------- producer: stream this CTA's weight range (no dependency on earlier kernels)
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int i = 0; i < len; ++i) {
+                const int u = start + (i + off) % len;
+                const int g = u % L.ngroups, pair = u / L.ngroups;
+                const int prob = pair / L.nK, j = pair - prob * L.nK;
+                const int kb0 = j * L.kcb, nb = min(L.kcb, L.KT - kb0);
+                const char* src = reinterpret_cast<const char*>(L.b.p[prob].W) + ((size_t)g * L.KT + kb0) * 1024;
+                for (int b = 0; b < nb; b += kStageBlocks) {
+                    const uint32_t bytes = (uint32_t)min(kStageBlocks, nb - b) * 1024u;
+                    mbar_wait(&empty_bar[stage], phase ^ 1u);
+                    mbar_arrive_expect_tx(&full_bar[stage], bytes);
+                    tma_bulk_g2s(ring + (size_t)stage * kStageBytes, src + (size_t)b * 1024, bytes, &full_bar[stage]);
+                    if (++stage == stages) {
+                        stage = 0;
+                        phase ^= 1u;
+                    }
+                }
+            }
+        }
+        return;
+    }
+
+    // x, stats, workspaces and outputs are shared with earlier kernels
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+
+    if (warp >= kSgEpi) {
+        // ---------------- epilogue warps: warp 9 finishes even units, warp 10 odd units
+        const int e = warp - kSgEpi;
+        uint32_t phase = 0;
+        for (int i = e; i < len; i += NE) {
+            const int u = start + (i + off) % len;
+            const int g = u % L.ngroups, pair = u / L.ngroups;
+            const int prob = pair / L.nK, j = pair - prob * L.nK;
+            const GemvProblem& P = L.b.p[prob];
+            mbar_wait(&red_full[e], phase);
+            phase ^= 1u;
+            const float* rb = red + e * kRedBuf;
+            float v[TM];
+#pragma unroll
+            for (int t = 0; t < TM; ++t) {
+                float acc = 0.f;
+#pragma unroll
+                for (int w = 0; w < kSgConsumers; ++w) acc += rb[(w * TM + t) * 32 + lane];
+                v[t] = acc;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&red_empty[e]);
+            if (L.nK > 1) {
+                // partial for (j, g); the last of the nK chunks of group g finishes it
+                const int ldw = L.ngroups * 32;
+                float* pp = P.partial + (size_t)j * 16 * ldw + g * 32 + lane;
+#pragma unroll
+                for (int t = 0; t < TM; ++t)
+                    if (t < L.T) pp[(size_t)t * ldw] = v[t];
+                __syncwarp();
+                unsigned last = 0;
+                if (lane == 0) {
+                    last = ticket_acq_rel(&P.tickets[g]) == (unsigned)L.nK - 1 ? 1u : 0u;
+                    if (last) P.tickets[g] = 0u;
+                }
+                last = __shfl_sync(0xffffffffu, last, 0);
+                if (!last) continue;
+                // sum the nK partials in fixed k-chunk order; loads batched so
+                // they are all in flight together
+                const float* q = P.partial + g * 32 + lane;
+#pragma unroll
+                for (int t = 0; t < TM; ++t) v[t] = 0.f;
+                for (int jj = 0; jj < L.nK; jj += 4) {
+                    float ld[4][TM];
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+#pragma unroll
+                        for (int t = 0; t < TM; ++t)
+                            ld[c][t] = (jj + c < L.nK && t < L.T) ? __ldcg(q + ((size_t)(jj + c) * 16 + t) * ldw) : 0.f;
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+#pragma unroll
+                        for (int t = 0; t < TM; ++t)
+                            if (jj + c < L.nK) v[t] += ld[c][t];
+                }
+            }
+            sg_epilogue<TM, EPI>(L, P, g, v, lane);
+        }
+        return;
+    }
+
+    // ---------------- consumers (warps 0-7)
+    const int T = L.T, t0 = L.t0;
+    const int pair1 = end > start ? (end - 1) / L.ngroups : pair0;
+    const int kc = L.kcb * 16;
+    for (int s = 0; s <= pair1 - pair0; ++s) {
+        const int pair = pair0 + s, prob = pair / L.nK, j = pair - prob * L.nK;
+        const GemvProblem& P = L.b.p[prob];
+        // RMSNorm statistics: warp w sums row w's per-32-column partials
+        // (lane-strided, then a fixed shuffle tree; independent of T)
+        for (int t = warp; t < TM; t += kSgConsumers) {
+            float r = 1.f;
+            if (P.gain != nullptr && t < T) {
+                float ss = 0.f;
+                const float* st = P.stats_in + (size_t)(t0 + t) * P.stat_tiles_in;
+#pragma unroll 8
+                for (int i = lane; i < P.stat_tiles_in; i += 32) ss += __ldcg(st + i);
+                ss = warp_sum(ss);
+                r = 1.0f / sqrtf(ss / (float)P.K + P.eps);
+            }
+            if (lane == 0) inv_rms[s][t] = r;
+        }
+        named_bar(1, kSgConsumers * 32);
+        __nv_bfloat16* xd = xs + (size_t)s * xslot;
+        const int k0 = j * kc;
+        const int kq = kc >> 2;
+        // rows >= T are zero; rows < T: batches of 8 independent float4 loads
+        // per thread so the L2 round trips overlap
+        for (int i = T * kq + tid; i < TM * kq; i += kSgConsumers * 32) {
+            const int t = i / kq, kk = (i - t * kq) * 4;
+            *reinterpret_cast<uint2*>(xd + t * L.xld + kk) = make_uint2(0u, 0u);
+        }
+        constexpr int U = 8;
+        for (int i0 = tid; i0 < T * kq; i0 += kSgConsumers * 32 * U) {
+            float4 v[U], gn[U];
+#pragma unroll
+            for (int q = 0; q < U; ++q) {
+                const int i = i0 + q * kSgConsumers * 32;
+                const int t = i / kq, k = k0 + (i - t * kq) * 4;
+                v[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+                gn[q] = make_float4(1.f, 1.f, 1.f, 1.f);
+                if (i < T * kq && k < P.K) {  // K is a multiple of 16
+                    v[q] = __ldcg(reinterpret_cast<const float4*>(P.x + (size_t)(t0 + t) * P.ldx + k));
+                    if (P.gain != nullptr) gn[q] = __ldg(reinterpret_cast<const float4*>(P.gain + k));
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < U; ++q) {
+                const int i = i0 + q * kSgConsumers * 32;
+                if (i >= T * kq) break;
+                const int t = i / kq, kk = (i - t * kq) * 4;
+                float4 w = v[q];
+                if (P.gain != nullptr) {
+                    const float r = inv_rms[s][t];
+                    w.x = __fmul_rn(__fmul_rn(w.x, r), gn[q].x);
+                    w.y = __fmul_rn(__fmul_rn(w.y, r), gn[q].y);
+                    w.z = __fmul_rn(__fmul_rn(w.z, r), gn[q].z);
+                    w.w = __fmul_rn(__fmul_rn(w.w, r), gn[q].w);
+                }
+                const __nv_bfloat162 lo = __floats2bfloat162_rn(w.x, w.y), hi = __floats2bfloat162_rn(w.z, w.w);
+                uint2 pk;
+                pk.x = *reinterpret_cast<const uint32_t*>(&lo);
+                pk.y = *reinterpret_cast<const uint32_t*>(&hi);
+                *reinterpret_cast<uint2*>(xd + t * L.xld + kk) = pk;
+            }
+        }
+    }
+    named_bar(1, kSgConsumers * 32);
+
+    int stage = 0;
+    uint32_t phase = 0;
+    uint32_t rphase[NE];
+#pragma unroll
+    for (int e = 0; e < NE; ++e) rphase[e] = 0u;
+    const int gid = lane >> 2, tig = lane & 3;
+    for (int i = 0; i < len; ++i) {
+        const int u = start + (i + off) % len;
+        const int pair = u / L.ngroups;
+        const int j = pair % L.nK;
+        const int nb = min(L.kcb, L.KT - j * L.kcb);
+        const __nv_bfloat16* xb = xs + (size_t)(pair - pair0) * xslot;
+        const __nv_bfloat16* xrow = TM == 16 ? xb + (lane & 7) * L.xld + ((lane >> 3) & 1) * 8 * L.xld + (lane >> 4) * 8
+                                             : xb + (lane & 7) * L.xld + ((lane >> 3) & 1) * 8;
+        float acc[4][4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = acc[q][2] = acc[q][3] = 0.f;
+        for (int b = 0; b < nb; b += kStageBlocks) {
+            mbar_wait(&full_bar[stage], phase);
+            // this warp's blocks of the stage: b + warp*kBpw + i
+            uint4 w[kBpw][2];
+            uint32_t a[kBpw][4];
+#pragma unroll
+            for (int i = 0; i < kBpw; ++i) {
+                const int bi = warp * kBpw + i;
+                if (b + bi < nb) {
+                    const unsigned char* wb = ring + (size_t)stage * kStageBytes + bi * 1024 + lane * 16;
+                    w[i][0] = *reinterpret_cast<const uint4*>(wb);
+                    w[i][1] = *reinterpret_cast<const uint4*>(wb + 512);
+                    const uint32_t xa = smem_u32(xrow + (b + bi) * 16);
+                    if constexpr (TM == 16) {
+                        asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                                     : "=r"(a[i][0]), "=r"(a[i][1]), "=r"(a[i][2]), "=r"(a[i][3])
+                                     : "r"(xa));
+                    } else {
+                        asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];"
+                                     : "=r"(a[i][0]), "=r"(a[i][2])
+                                     : "r"(xa));
+                        a[i][1] = a[i][3] = 0u;
+                    }
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < kBpw; ++i) {
+                if (b + warp * kBpw + i < nb) {
+                    mma16816(acc[0], a[i], w[i][0].x, w[i][0].y);
+                    mma16816(acc[1], a[i], w[i][0].z, w[i][0].w);
+                    mma16816(acc[2], a[i], w[i][1].x, w[i][1].y);
+                    mma16816(acc[3], a[i], w[i][1].z, w[i][1].w);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty_bar[stage]);
+            if (++stage == stages) {
+                stage = 0;
+                phase ^= 1u;
+            }
+        }
+        // hand the warp's partial sums to this unit's epilogue warp
+        const int e = i % NE;
+        mbar_wait(&red_empty[e], rphase[e] ^ 1u);
+        rphase[e] ^= 1u;
+        float* rw = red + e * kRedBuf + warp * TM * 32;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int col = q * 8 + 2 * tig;
+            rw[gid * 32 + col] = acc[q][0];
+            rw[gid * 32 + col + 1] = acc[q][1];
+            if (TM == 16) {
+                rw[(gid + 8) * 32 + col] = acc[q][2];
+                rw[(gid + 8) * 32 + col + 1] = acc[q][3];
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&red_full[e]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host launch
+// ---------------------------------------------------------------------------
+
+static bool g_pdl = true;
+void set_pdl(bool on) { g_pdl = on; }
+bool pdl_enabled() { return g_pdl; }
+
+template <int TM, int EPI>
+static void sg_launch_t(const SgLaunch& L, int grid, size_t smem, cudaStream_t s) {
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(sgemv_kernel<TM, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSgSmemLimit);
+        configured = true;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(sg_threads<TM>());
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, sgemv_kernel<TM, EPI>, L);
+}
+
+template <int TM>
+static void sg_dispatch(int epi, const SgLaunch& L, int grid, size_t smem, cudaStream_t s) {
+    switch (epi) {
+        case EPI_STORE: sg_launch_t<TM, EPI_STORE>(L, grid, smem, s); break;
+        case EPI_RESID: sg_launch_t<TM, EPI_RESID>(L, grid, smem, s); break;
+        case EPI_SILU: sg_launch_t<TM, EPI_SILU>(L, grid, smem, s); break;
+        case EPI_QKV: sg_launch_t<TM, EPI_QKV>(L, grid, smem, s); break;
+        case EPI_ARGMAX: sg_launch_t<TM, EPI_ARGMAX>(L, grid, smem, s); break;
+    }
+}
+
+void launch_sgemv(int epi, const GemvBatch& b, int nprob, int T, const PassView& pass, const KvView& kv,
+                  cudaStream_t s) {
+    if (T <= 0 || nprob <= 0) return;
+    const SgPlan p = sgemv_plan(b.p[0].K, b.p[0].ldw, nprob);
+    SgLaunch L;
+    L.b = b;
+    L.pass = pass;
+    L.kv = kv;
+    L.KT = p.KT;
+    L.kcb = p.kcb;
+    L.nK = p.nK;
+    L.ngroups = p.ngroups;
+    L.units = p.units;
+    L.xld = p.kcb * 16 + 8;
+    static const int rotate = [] {
+        const char* e = std::getenv("ESPEC_SG_ROTATE");
+        return e ? std::atoi(e) : 0;  // measured slower on B200 (DRAM locality); off by default
+    }();
+    L.rotate = rotate;
+    for (int t0 = 0; t0 < T; t0 += 16) {
+        L.t0 = t0;
+        L.T = T - t0 < 16 ? T - t0 : 16;
+        const int TM = L.T <= 8 ? 8 : 16;
+        L.stages = sg_stages(TM, p.kcb);
+        const size_t smem = sg_smem_bytes(TM, p.kcb);
+        if (TM == 8) sg_dispatch<8>(epi, L, p.grid, smem, s);
+        else sg_dispatch<16>(epi, L, p.grid, smem, s);
+    }
+}
+
+}  // namespace espec_dev

@@ -1,17 +1,14 @@
-// sm_100a kernels for the EasySpec decode loop.
+// sm_100a kernels for the EasySpec decode loop (the bf16 GEMV lives in
+// gemv_stream.cu).
 //
-// Every decode-time projection is a skinny GEMV (T <= 8 rows against a
-// weight matrix read once from HBM), so the kernels here are organised
-// around streaming weights at full HBM bandwidth:
-//   * 16-byte ld.global.nc.L1::no_allocate weight loads, 8 rows in flight
-//     per lane, 8 warps per CTA splitting K, a CTA per (256-column tile,
-//     K split), grid sized from (K, N) only;
-//   * the RMSNorm of the input is fused into the prologue (from row
-//     sum-of-squares partials left by the producer), the residual add / SiLU
-//     gate / RoPE + paged-KV write / argmax into the epilogue, which the last
-//     CTA of each column tile runs after a deterministic split reduction.
-// Reduction order never depends on T, so a row's result is bit-identical in
-// a 1-row draft pass and a 6-row verify pass (greedy losslessness).
+// This file holds the fp32 parity-mode GEMV (the reference model in fp32:
+// CUDA-core FMA over the row-major layout, 8 warps splitting K, a CTA per
+// (256-column tile, K split)), the embedding / residual kernels, paged-KV
+// attention, KV commit compaction, greedy acceptance and weight init.
+// Fused prologue/epilogue semantics are shared with the bf16 path: RMSNorm
+// from row sum-of-squares partials (one per 32 columns), residual add + row
+// stats, SiLU over [gate16 | up16] packed groups, RoPE + paged-KV write,
+// argmax. Reduction order never depends on T (batch invariance).
 #include <cstdio>
 #include <cstdlib>
 #include <type_traits>
@@ -65,27 +62,8 @@ struct GemvLaunch {
 };
 
 // ---------------------------------------------------------------------------
-// GEMV kernel
+// fp32 GEMV kernel (parity mode)
 // ---------------------------------------------------------------------------
-
-template <int TM>
-__device__ __forceinline__ void block_sum_rows(float (&v)[TM], float* red /*[8][TM]*/) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#pragma unroll
-    for (int t = 0; t < TM; ++t) {
-        const float s = warp_sum(v[t]);
-        if (lane == 0) red[warp * TM + t] = s;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int t = 0; t < TM; ++t) {
-        float s = 0.f;
-#pragma unroll
-        for (int w = 0; w < 8; ++w) s += red[w * TM + t];
-        v[t] = s;
-    }
-    __syncthreads();
-}
 
 __device__ __forceinline__ bool am_better(float v, int i, float bv, int bi) {
     return v > bv || (v == bv && i < bi);
@@ -113,23 +91,16 @@ __device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
                  : "r"(a));
 }
 
-// Two GEMV main loops share the prologue/epilogue:
-//  * WT = bf16 (perf mode): tensor-core mma.sync m16n8k16, weights pre-packed
-//    in HBM in mma B-fragment order (see pack_index) so each lane's 16-byte
-//    load lands directly in its fragment registers — no shared-memory staging
-//    of W at all. Each warp owns 32 columns over the CTA's whole K chunk;
-//    the (<=16) input rows are the A operand (bf16, via ldmatrix).
-//  * WT = float (parity mode): CUDA-core FMA over the reference's row-major
-//    layout, 8 warps splitting K.
-template <typename WT, int TM, int EPI>
-__global__ void __launch_bounds__(kThreads) gemv_kernel(const __grid_constant__ GemvLaunch L) {
+template <int TM, int EPI>
+__global__ void __launch_bounds__(kThreads) gemv_f32_kernel(const __grid_constant__ GemvLaunch L) {
     extern __shared__ __align__(16) float smem[];
     __shared__ float inv_rms[TM];
-    __shared__ float red_small[8 * TM * 2];
+    __shared__ float red_small[8 * TM];
     __shared__ int red_idx[8 * TM];
     __shared__ unsigned s_last;
-    constexpr bool kMma = std::is_same<WT, __nv_bfloat16>::value;
 
+    pdl_wait();
+    pdl_trigger();
     const GemvProblem& P = L.b.p[blockIdx.z];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int tile = blockIdx.x, split = blockIdx.y;
@@ -152,72 +123,7 @@ __global__ void __launch_bounds__(kThreads) gemv_kernel(const __grid_constant__ 
     __syncthreads();
 
     float s[TM];
-    if constexpr (kMma) {
-        static_assert(TM == 16, "the mma path covers 16 rows");
-        const int ldx = L.kc + 8;  // bf16 elements; +16 B keeps ldmatrix conflict-free
-        __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(smem);  // [16][kc+8]
-        for (int i = tid; i < TM * kn; i += kThreads) {
-            const int t = i / kn, kk = i - t * kn;
-            float v = 0.f;
-            if (t < T) {
-                v = P.x[(size_t)(t0 + t) * P.ldx + k0 + kk];
-                if (P.gain != nullptr) v = __fmul_rn(__fmul_rn(v, inv_rms[t]), P.gain[k0 + kk]);
-            }
-            xs[t * ldx + kk] = __float2bfloat16_rn(v);
-        }
-        __syncthreads();
-        float acc[4][4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-#pragma unroll
-            for (int e = 0; e < 4; ++e) acc[j][e] = 0.f;
-        const int g = tile * 8 + warp;  // 32-column group of this warp
-        if (g * 32 < P.ldw) {
-            const int KT = (P.K + 15) / 16;
-            const __nv_bfloat16* wp = reinterpret_cast<const __nv_bfloat16*>(P.W) +
-                                      ((size_t)g * KT + k0 / 16) * 512 + lane * 8;
-            const __nv_bfloat16* xrow = xs + (lane & 7) * ldx + ((lane >> 3) & 1) * 8 * ldx + (lane >> 4) * 8;
-            const int steps = kn / 16;
-            constexpr int U = 4;
-            for (int ks = 0; ks < steps; ks += U) {
-                uint4 w[U][2];
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    if (ks + u < steps) {
-                        w[u][0] = ld_stream(wp + (size_t)(ks + u) * 512);
-                        w[u][1] = ld_stream(wp + (size_t)(ks + u) * 512 + 256);
-                    } else {
-                        w[u][0] = w[u][1] = make_uint4(0, 0, 0, 0);
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    if (ks + u < steps) {
-                        uint32_t a[4];
-                        ldsm_x4(a, xrow + (ks + u) * 16);
-                        mma_bf16_16816(acc[0], a, w[u][0].x, w[u][0].y);
-                        mma_bf16_16816(acc[1], a, w[u][0].z, w[u][0].w);
-                        mma_bf16_16816(acc[2], a, w[u][1].x, w[u][1].y);
-                        mma_bf16_16816(acc[3], a, w[u][1].z, w[u][1].w);
-                    }
-                }
-            }
-        }
-        __syncthreads();  // xs dead
-        float* red = smem;  // [16][256]
-        const int gid = lane >> 2, tig = lane & 3;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int col = warp * 32 + j * 8 + 2 * tig;
-            red[gid * kTileN + col] = acc[j][0];
-            red[gid * kTileN + col + 1] = acc[j][1];
-            red[(gid + 8) * kTileN + col] = acc[j][2];
-            red[(gid + 8) * kTileN + col + 1] = acc[j][3];
-        }
-        __syncthreads();
-#pragma unroll
-        for (int t = 0; t < TM; ++t) s[t] = red[t * kTileN + tid];
-    } else {
+    {
         float* xs = smem;  // [kc][TM]
         for (int i = tid; i < kn * TM; i += kThreads) {
             const int kk = i / TM, t = i - kk * TM;
@@ -240,9 +146,9 @@ __global__ void __launch_bounds__(kThreads) gemv_kernel(const __grid_constant__ 
 
         const int col = n0 + lane * 8;
         const bool col_ok = col < P.ldw;
-        const WT* Wb = reinterpret_cast<const WT*>(P.W) + (size_t)k0 * P.ldw + col;
+        const float* Wb = reinterpret_cast<const float*>(P.W) + (size_t)k0 * P.ldw + col;
         for (int kk = warp; kk < kn; kk += 8 * U) {
-            W8<WT> w[U];
+            W8<float> w[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int k = kk + 8 * u;
@@ -319,35 +225,31 @@ __global__ void __launch_bounds__(kThreads) gemv_kernel(const __grid_constant__ 
                 if (t < T) P.out[(size_t)(t0 + t) * P.ldo + c] = s[t];
     } else if constexpr (EPI == EPI_RESID) {
         // h_mid = h + attn  /  h_next = h_mid + mlp  (proj/src/draft_engine.cpp:15-19, 50-54)
-        float sq[TM];
+        // row sum-of-squares partial per 32 columns (one warp)
 #pragma unroll
         for (int t = 0; t < TM; ++t) {
-            sq[t] = 0.f;
+            float sq = 0.f;
             if (t < T && c < P.N) {
                 const float y = __fadd_rn(P.resid[(size_t)(t0 + t) * P.ldr + c], s[t]);
                 P.out[(size_t)(t0 + t) * P.ldo + c] = y;
-                sq[t] = y * y;
+                sq = y * y;
+            }
+            sq = warp_sum(sq);
+            if (lane == 0 && t < T && c < P.N) P.stats_out[(t0 + t) * P.stat_tiles_out + c / 32] = sq;
+        }
+    } else if constexpr (EPI == EPI_SILU) {
+        // packed group of 32 columns = [gate 16 | up 16]; gate = silu(x.Wg) * (x.Wu)
+        // (proj/src/model.cpp:197-210)
+#pragma unroll
+        for (int t = 0; t < TM; ++t) {
+            const float up = __shfl_down_sync(0xffffffffu, s[t], 16);
+            const int j = (c / 32) * 16 + lane;
+            if (t < T && lane < 16 && j < P.N / 2) {
+                const float g = s[t];
+                const float si = __fdiv_rn(g, __fadd_rn(1.0f, expf(-g)));
+                P.out[(size_t)(t0 + t) * P.ldo + j] = __fmul_rn(si, up);
             }
         }
-        block_sum_rows<TM>(sq, red_small);
-        if (tid < TM && tid < T) P.stats_out[(t0 + tid) * P.stat_tiles_out + tile] = sq[tid];
-    } else if constexpr (EPI == EPI_SILU) {
-        // gate = silu(x·Wg) * (x·Wu)  (proj/src/model.cpp:197-210)
-        float* up = smem;  // [TM][128]
-        __syncthreads();
-        if (tid >= 128)
-#pragma unroll
-            for (int t = 0; t < TM; ++t) up[t * 128 + (tid - 128)] = s[t];
-        __syncthreads();
-        const int j = tile * 128 + tid;
-        if (tid < 128 && j < P.N / 2)
-#pragma unroll
-            for (int t = 0; t < TM; ++t)
-                if (t < T) {
-                    const float g = s[t];
-                    const float si = __fdiv_rn(g, __fadd_rn(1.0f, expf(-g)));
-                    P.out[(size_t)(t0 + t) * P.ldo + j] = __fmul_rn(si, up[t * 128 + tid]);
-                }
     } else if constexpr (EPI == EPI_QKV) {
         // q = rope(h·Wq), k = rope(h·Wk), v = h·Wv; K/V written to the cache rows
         // of the pass (proj/src/model.cpp:130-138, rotary proj/src/matrix.cpp:159-194).
@@ -435,49 +337,47 @@ __global__ void __launch_bounds__(kThreads) gemv_kernel(const __grid_constant__ 
     }
 }
 
-template <typename WT, int TM, int EPI>
+template <int TM, int EPI>
 static void gemv_launch_t(const GemvLaunch& L, int nprob, cudaStream_t s) {
-    constexpr bool kMma = std::is_same<WT, __nv_bfloat16>::value;
-    const size_t smem = kMma ? std::max<size_t>((size_t)TM * (L.kc + 8) * 2, (size_t)TM * kTileN * 4)
-                             : sizeof(float) * (size_t)max(L.kc * TM, 8 * TM * kTileN);
+    const size_t smem = sizeof(float) * (size_t)max(L.kc * TM, 8 * TM * kTileN);
     static bool configured = false;
     if (!configured) {
-        CK(cudaFuncSetAttribute(gemv_kernel<WT, TM, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CK(cudaFuncSetAttribute(gemv_f32_kernel<TM, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 8 * 8 * kTileN * (int)sizeof(float)));
         configured = true;
     }
     dim3 grid(L.tiles, L.splits, nprob);
-    gemv_kernel<WT, TM, EPI><<<grid, kThreads, smem, s>>>(L);
+    CK(launch_pdl(gemv_f32_kernel<TM, EPI>, grid, dim3(kThreads), smem, s, L));
 }
 
-template <typename WT, int EPI>
+template <int EPI>
 static void gemv_dispatch_tm(const GemvLaunch& L, int nprob, cudaStream_t s) {
-    if constexpr (std::is_same<WT, __nv_bfloat16>::value) {
-        gemv_launch_t<WT, 16, EPI>(L, nprob, s);
-    } else {
-        if (L.T <= 1) gemv_launch_t<WT, 1, EPI>(L, nprob, s);
-        else if (L.T <= 2) gemv_launch_t<WT, 2, EPI>(L, nprob, s);
-        else if (L.T <= 4) gemv_launch_t<WT, 4, EPI>(L, nprob, s);
-        else gemv_launch_t<WT, 8, EPI>(L, nprob, s);
-    }
-}
-
-template <typename WT>
-static void gemv_dispatch_epi(int epi, const GemvLaunch& L, int nprob, cudaStream_t s) {
-    switch (epi) {
-        case EPI_STORE: gemv_dispatch_tm<WT, EPI_STORE>(L, nprob, s); break;
-        case EPI_RESID: gemv_dispatch_tm<WT, EPI_RESID>(L, nprob, s); break;
-        case EPI_SILU: gemv_dispatch_tm<WT, EPI_SILU>(L, nprob, s); break;
-        case EPI_QKV: gemv_dispatch_tm<WT, EPI_QKV>(L, nprob, s); break;
-        case EPI_ARGMAX: gemv_dispatch_tm<WT, EPI_ARGMAX>(L, nprob, s); break;
-    }
+    if (L.T <= 1) gemv_launch_t<1, EPI>(L, nprob, s);
+    else if (L.T <= 2) gemv_launch_t<2, EPI>(L, nprob, s);
+    else if (L.T <= 4) gemv_launch_t<4, EPI>(L, nprob, s);
+    else gemv_launch_t<8, EPI>(L, nprob, s);
 }
 
 int gemv_rows_per_launch(int wdtype) { return wdtype == DT_BF16 ? 16 : 8; }
 
+size_t gemv_partial_floats(int K, int N, int wdtype) {
+    if (wdtype == DT_BF16) return sgemv_partial_floats(K, (N + 31) / 32 * 32);
+    const GemvPlan p = gemv_plan(K, N);
+    return (size_t)p.splits * 16 * (size_t)p.tiles * kTileN;
+}
+
+int gemv_col_tiles(int K, int N, int wdtype) {
+    if (wdtype == DT_BF16) return (N + 31) / 32;
+    return gemv_plan(K, N).tiles;
+}
+
 void launch_gemv(int epi, int wdtype, const GemvBatch& b, int nprob, int T, const PassView& pass,
                  const KvView& kv, cudaStream_t s) {
     if (T <= 0 || nprob <= 0) return;
+    if (wdtype == DT_BF16) {
+        launch_sgemv(epi, b, nprob, T, pass, kv, s);
+        return;
+    }
     GemvLaunch L;
     L.b = b;
     L.pass = pass;
@@ -490,8 +390,13 @@ void launch_gemv(int epi, int wdtype, const GemvBatch& b, int nprob, int T, cons
     for (int t0 = 0; t0 < T; t0 += rows) {
         L.t0 = t0;
         L.T = min(rows, T - t0);
-        if (wdtype == DT_BF16) gemv_dispatch_epi<__nv_bfloat16>(epi, L, nprob, s);
-        else gemv_dispatch_epi<float>(epi, L, nprob, s);
+        switch (epi) {
+            case EPI_STORE: gemv_dispatch_tm<EPI_STORE>(L, nprob, s); break;
+            case EPI_RESID: gemv_dispatch_tm<EPI_RESID>(L, nprob, s); break;
+            case EPI_SILU: gemv_dispatch_tm<EPI_SILU>(L, nprob, s); break;
+            case EPI_QKV: gemv_dispatch_tm<EPI_QKV>(L, nprob, s); break;
+            case EPI_ARGMAX: gemv_dispatch_tm<EPI_ARGMAX>(L, nprob, s); break;
+        }
     }
 }
 
@@ -534,59 +439,56 @@ void launch_pack(const void* logical, int K, int ldw, void* packed, bool unpack,
 // embedding gather / residual add (+ row sum-of-squares partials)
 // ---------------------------------------------------------------------------
 
+// Row sum-of-squares partials are one per 32 columns (one warp): the same
+// granularity the GEMV epilogues write, so the consumer's RMSNorm prologue
+// sums them in the same fixed order whatever produced the row.
 template <typename WT>
 __global__ void __launch_bounds__(kThreads) embed_kernel(const WT* emb, int d, const int* arena, const int* idx,
-                                                        float* h, float* stats) {
-    __shared__ float red[8];
-    const int t = blockIdx.y, tile = blockIdx.x, c = tile * kStatTile + threadIdx.x;
+                                                        float* h, float* stats, int stat_tiles) {
+    pdl_wait();
+    pdl_trigger();
+    const int t = blockIdx.y, c = blockIdx.x * kThreads + threadIdx.x;
     const int tok = arena[idx[t]];
     float v = 0.f;
     if (c < d) {
         v = ld_f(emb + (size_t)tok * d + c);
         h[(size_t)t * d + c] = v;
     }
-    float sq = warp_sum(v * v);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        float ss = 0.f;
-        for (int w = 0; w < 8; ++w) ss += red[w];
-        stats[t * gridDim.x + tile] = ss;
-    }
+    const float sq = warp_sum(v * v);
+    if ((threadIdx.x & 31) == 0 && c < d) stats[t * stat_tiles + c / kStatTile] = sq;
 }
 
 void launch_embed(int wdtype, const void* emb, int d, const int* arena, const int* idx, int T, float* h,
                   float* stats, cudaStream_t s) {
     if (T <= 0) return;
-    dim3 grid((d + kStatTile - 1) / kStatTile, T);
+    dim3 grid((d + kThreads - 1) / kThreads, T);
+    const int st = (d + kStatTile - 1) / kStatTile;
     if (wdtype == DT_BF16)
-        embed_kernel<<<grid, kThreads, 0, s>>>(reinterpret_cast<const __nv_bfloat16*>(emb), d, arena, idx, h, stats);
+        CK(launch_pdl(embed_kernel<__nv_bfloat16>, grid, dim3(kThreads), 0, s,
+                      reinterpret_cast<const __nv_bfloat16*>(emb), d, arena, idx, h, stats, st));
     else
-        embed_kernel<<<grid, kThreads, 0, s>>>(reinterpret_cast<const float*>(emb), d, arena, idx, h, stats);
+        CK(launch_pdl(embed_kernel<float>, grid, dim3(kThreads), 0, s, reinterpret_cast<const float*>(emb), d, arena,
+                      idx, h, stats, st));
 }
 
-__global__ void __launch_bounds__(kThreads) add_stats_kernel(float* h, const float* a, int d, float* stats) {
-    __shared__ float red[8];
-    const int t = blockIdx.y, tile = blockIdx.x, c = tile * kStatTile + threadIdx.x;
+__global__ void __launch_bounds__(kThreads) add_stats_kernel(float* h, const float* a, int d, float* stats,
+                                                            int stat_tiles) {
+    pdl_wait();
+    pdl_trigger();
+    const int t = blockIdx.y, c = blockIdx.x * kThreads + threadIdx.x;
     float y = 0.f;
     if (c < d) {
         y = __fadd_rn(h[(size_t)t * d + c], a[(size_t)t * d + c]);
         h[(size_t)t * d + c] = y;
     }
-    float sq = warp_sum(y * y);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        float ss = 0.f;
-        for (int w = 0; w < 8; ++w) ss += red[w];
-        stats[t * gridDim.x + tile] = ss;
-    }
+    const float sq = warp_sum(y * y);
+    if ((threadIdx.x & 31) == 0 && c < d) stats[t * stat_tiles + c / kStatTile] = sq;
 }
 
 void launch_add_stats(float* h, const float* a, int d, int T, float* stats, cudaStream_t s) {
     if (T <= 0) return;
-    dim3 grid((d + kStatTile - 1) / kStatTile, T);
-    add_stats_kernel<<<grid, kThreads, 0, s>>>(h, a, d, stats);
+    dim3 grid((d + kThreads - 1) / kThreads, T);
+    CK(launch_pdl(add_stats_kernel, grid, dim3(kThreads), 0, s, h, a, d, stats, (d + kStatTile - 1) / kStatTile));
 }
 
 // ---------------------------------------------------------------------------
@@ -626,6 +528,8 @@ template <typename KT>
 __global__ void __launch_bounds__(kAttnThreads) attn_kernel(const __grid_constant__ AttnLaunch L) {
     extern __shared__ __align__(16) float sm[];
     __shared__ unsigned s_last;
+    pdl_wait();
+    pdl_trigger();
     const AttnProblem& A = L.b.p[blockIdx.z];
     const int dh = L.kv.dh, G = L.G, H = L.n_heads;
     const int split = blockIdx.x;
@@ -793,6 +697,8 @@ __global__ void __launch_bounds__(128) attn_mma_kernel(const __grid_constant__ A
     __shared__ unsigned s_last;
     constexpr int LDK = DH + 8;           // bf16 elements per smem row (16 B pad)
     constexpr int NT = DH / 8;            // n8 tiles over head dims
+    pdl_wait();
+    pdl_trigger();
     const AttnProblem& A = L.b.p[blockIdx.z];
     const int G = L.G, H = L.n_heads, T = L.pass.T, P = T * G;
     const int n_kv = L.kv.n_kv;
@@ -968,34 +874,53 @@ __global__ void __launch_bounds__(128) attn_mma_kernel(const __grid_constant__ A
         }
     }
     if (nchunks == 1) return;
-    __threadfence();
+    // Cross-CTA combine (last CTA of this (kv head, m-tile)), fixed chunk order.
     __syncthreads();
     unsigned* ticket = A.tickets + blockIdx.y;
     if (threadIdx.x == 0) {
-        const unsigned tk = atomicAdd(ticket, 1u);
+        unsigned tk;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(tk) : "l"(ticket) : "memory");
         s_last = (tk == (unsigned)nchunks - 1) ? 1u : 0u;
         if (s_last) *ticket = 0u;
     }
     __syncthreads();
     if (!s_last) return;
-    __threadfence();
     const size_t cstride = (size_t)gridDim.y * 16 * ps;
     const float* base = A.ws + ((size_t)blockIdx.y * 16) * ps;
+    // per-row chunk weights f = exp(m_ch - M) and denominator, once per row
+    float* fac = Os;              // [nchunks][16]
+    float* sden = Os + 64 * 16;   // [16]
+    if (threadIdx.x < 16) {
+        const int r = threadIdx.x;
+        float M = -INFINITY;
+        for (int ch = 0; ch < nchunks; ++ch) M = fmaxf(M, __ldcg(base + ch * cstride + r * ps + DH));
+        float den = 0.f;
+        for (int ch = 0; ch < nchunks; ++ch) {
+            const float m = __ldcg(base + ch * cstride + r * ps + DH);
+            float f = 0.f;
+            if (M != -INFINITY && m != -INFINITY) {
+                f = expf(m - M);
+                den = __fmaf_rn(f, __ldcg(base + ch * cstride + r * ps + DH + 1), den);
+            }
+            fac[ch * 16 + r] = f;
+        }
+        sden[r] = den;
+    }
+    __syncthreads();
     for (int i = threadIdx.x; i < 16 * DH; i += 128) {
         const int r = i / DH, c = i - r * DH;
         const int p = mt * 16 + r;
         if (p >= P) continue;
-        float M = -INFINITY;
-        for (int ch = 0; ch < nchunks; ++ch) M = fmaxf(M, __ldcg(base + ch * cstride + r * ps + DH));
-        float num = 0.f, den = 0.f;
-        if (M != -INFINITY)
-            for (int ch = 0; ch < nchunks; ++ch) {
-                const float m = __ldcg(base + ch * cstride + r * ps + DH);
-                if (m == -INFINITY) continue;
-                const float f = expf(m - M);
-                num = __fmaf_rn(f, __ldcg(base + ch * cstride + r * ps + c), num);
-                den = __fmaf_rn(f, __ldcg(base + ch * cstride + r * ps + DH + 1), den);
-            }
+        float num = 0.f;
+        for (int ch0 = 0; ch0 < nchunks; ch0 += 8) {
+            float v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[q] = ch0 + q < nchunks ? __ldcg(base + (ch0 + q) * cstride + r * ps + c) : 0.f;
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (ch0 + q < nchunks) num = __fmaf_rn(fac[(ch0 + q) * 16 + r], v[q], num);
+        }
+        const float den = sden[r];
         A.out[(size_t)(p / G) * H * DH + (hk * G + p % G) * DH + c] = den > 0.f ? num / den : 0.f;
     }
 }
@@ -1003,6 +928,10 @@ __global__ void __launch_bounds__(128) attn_mma_kernel(const __grid_constant__ A
 template <int DH>
 static void attn_mma_launch(const AttnLaunch& L, int nprob, cudaStream_t s) {
     const int splits = (L.pass.total + 63) / 64;
+    if ((splits + 3) / 4 > 64) {
+        fprintf(stderr, "attention: context of %d rows exceeds the 16K-row split-combine limit\n", L.pass.total);
+        return;
+    }
     const int mtiles = (L.pass.T * L.G + 15) / 16;
     dim3 grid((splits + 3) / 4, L.kv.n_kv * mtiles, nprob);
     const size_t smem = std::max<size_t>((size_t)4 * 2 * 64 * (DH + 8) * 2, (size_t)(4 * 16 * DH + 128) * 4);
@@ -1011,7 +940,7 @@ static void attn_mma_launch(const AttnLaunch& L, int nprob, cudaStream_t s) {
         CK(cudaFuncSetAttribute(attn_mma_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured = true;
     }
-    attn_mma_kernel<DH><<<grid, 128, smem, s>>>(L);
+    CK(launch_pdl(attn_mma_kernel<DH>, grid, dim3(128), smem, s, L));
 }
 
 void launch_attention(const AttnBatch& b, int nprob, int n_heads, const PassView& pass, const KvView& kv,
@@ -1036,13 +965,13 @@ void launch_attention(const AttnBatch& b, int nprob, int n_heads, const PassView
             CK(cudaFuncSetAttribute(attn_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
             configured[1] = true;
         }
-        attn_kernel<__nv_bfloat16><<<grid, kAttnThreads, smem, s>>>(L);
+        CK(launch_pdl(attn_kernel<__nv_bfloat16>, grid, dim3(kAttnThreads), smem, s, L));
     } else {
         if (!configured[0]) {
             CK(cudaFuncSetAttribute(attn_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
             configured[0] = true;
         }
-        attn_kernel<float><<<grid, kAttnThreads, smem, s>>>(L);
+        CK(launch_pdl(attn_kernel<float>, grid, dim3(kAttnThreads), smem, s, L));
     }
 }
 
@@ -1054,6 +983,8 @@ template <typename KT>
 __global__ void kv_move_kernel(KvView kv, const int* src, const int* dst, int n) {
     // grid: (layer*2+kind, kv head); sequential over the path keeps the
     // reference's in-order memcpy semantics (dst <= src, ascending).
+    pdl_wait();
+    pdl_trigger();
     const int lk = blockIdx.x, head = blockIdx.y;
     const int layer = lk >> 1, kind = lk & 1;
     KT* pool = reinterpret_cast<KT*>(kv.pool);
@@ -1069,8 +1000,8 @@ __global__ void kv_move_kernel(KvView kv, const int* src, const int* dst, int n)
 void launch_kv_move(const KvView& kv, const int* src, const int* dst, int n, cudaStream_t s) {
     if (n <= 0) return;
     dim3 grid(kv.n_layers * 2, kv.n_kv);
-    if (kv.dtype == DT_BF16) kv_move_kernel<__nv_bfloat16><<<grid, 128, 0, s>>>(kv, src, dst, n);
-    else kv_move_kernel<float><<<grid, 128, 0, s>>>(kv, src, dst, n);
+    if (kv.dtype == DT_BF16) CK(launch_pdl(kv_move_kernel<__nv_bfloat16>, grid, dim3(128), 0, s, kv, src, dst, n));
+    else CK(launch_pdl(kv_move_kernel<float>, grid, dim3(128), 0, s, kv, src, dst, n));
 }
 
 // ---------------------------------------------------------------------------
@@ -1078,6 +1009,8 @@ void launch_kv_move(const KvView& kv, const int* src, const int* dst, int n, cud
 // ---------------------------------------------------------------------------
 
 __global__ void accept_greedy_kernel(AcceptArgs a) {
+    pdl_wait();
+    pdl_trigger();
     if (threadIdx.x != 0) return;
     int target = a.base_argmax[0];
     int parent = -1, m = 0;
@@ -1110,7 +1043,7 @@ __global__ void accept_greedy_kernel(AcceptArgs a) {
     a.tok_arena_w[a.commit_at + m] = target;
 }
 
-void launch_accept_greedy(const AcceptArgs& a, cudaStream_t s) { accept_greedy_kernel<<<1, 32, 0, s>>>(a); }
+void launch_accept_greedy(const AcceptArgs& a, cudaStream_t s) { CK(launch_pdl(accept_greedy_kernel, dim3(1), dim3(32), 0, s, a)); }
 
 // ---------------------------------------------------------------------------
 // perf-mode weight init: N(0, sd) from a counter-based hash (Box-Muller)

@@ -3,12 +3,13 @@
 // Data layout in HBM:
 //   * weights: every projection is stored K-major, W[K][ldw] row-major with
 //     y = x · W (the reference's own matmul layout, proj/src/matrix.cpp:38-57);
-//     ldw is padded to a multiple of 8 so each lane streams 16-byte vectors.
-//     QKV of one layer is fused column-wise [q | k | v]; gate/up are fused and
-//     interleaved per 128-column block [gate128 | up128] so one GEMV column
-//     tile owns both halves of its SiLU·up epilogue.
+//     ldw is padded to a multiple of 8 (fp32) / 32 (bf16, stored pre-packed
+//     in mma fragment order, see pack_index). QKV of one layer is fused
+//     column-wise [q | k | v]; gate/up are fused and interleaved per 32
+//     columns [gate16 | up16] so one packed column group owns both halves of
+//     its SiLU·up epilogue.
 //   * hidden rows are fp32 [T][d]; their RMSNorm statistics travel as
-//     per-256-column sum-of-squares partials stats[T][ceil(d/256)].
+//     per-32-column sum-of-squares partials stats[T][ceil(d/32)].
 //   * KV cache: paged pool; page p holds kPage rows for every layer:
 //     pool[p][layer][k|v][kv_head][row][d_head], located through a page table.
 #pragma once
@@ -91,8 +92,22 @@ struct GemvBatch {
 struct GemvPlan {
     int tiles, splits, kc;
 };
-GemvPlan gemv_plan(int K, int N);
-size_t gemv_partial_floats(int K, int N);  // workspace floats one problem needs
+GemvPlan gemv_plan(int K, int N);                     // fp32 parity path
+size_t gemv_partial_floats(int K, int N, int wdtype);  // workspace floats one problem needs
+int gemv_col_tiles(int K, int N, int wdtype);          // argmax partials per row
+
+// bf16 stream-K GEMV (gemv_stream.cu): units (problem, k-chunk, 32-column
+// group) of kcb 1 KB blocks, contiguous balanced ranges over <= 148 CTAs.
+struct SgPlan {
+    int KT, kcb, nK, ngroups, units, grid;
+};
+SgPlan sgemv_plan(int K, int ldw, int nprob);
+size_t sgemv_partial_floats(int K, int ldw);
+void launch_sgemv(int epi, const GemvBatch& b, int nprob, int T, const PassView& pass, const KvView& kv,
+                  cudaStream_t s);
+// Programmatic dependent launch on/off (default on; ESPEC_PDL=0 disables).
+void set_pdl(bool on);
+bool pdl_enabled();
 
 // Rows handled per GEMV launch (bf16 mma path: 16; fp32 FMA path: 8).
 int gemv_rows_per_launch(int wdtype);

@@ -194,6 +194,10 @@ espec_status espec_sync(espec_engine* eng);
  * Returns the mean device time per launch and the weight bytes it reads. */
 espec_status espec_bench_gemv(int K, int N, int T, int nprob, int epi, int iters, int device, double* us_per_launch,
                               double* bytes_per_launch);
+/* Instrumentation: time the paged bf16 decode/verify attention for T causal
+ * query rows at the end of a ctx-row context (nprob layers batched). */
+espec_status espec_bench_attn(int T, int n_heads, int n_kv, int d_head, int ctx, int nprob, int iters, int device,
+                              double* us_per_launch, double* bytes_per_launch);
 
 #ifdef __cplusplus
 }

@@ -480,13 +480,26 @@ public:
         staging_.create(8 << 20);
         staging_.h2d_counter = &h2d_bytes_;
         for (auto& e : site_ev_) CUDA_OK(cudaEventCreate(&e));
-        arena_cap_ = std::max(cap_b, cap_d) + 4 * kMaxNodes + 64;
         tree_off_ = std::max(cap_b, cap_d);
         am_off_ = tree_off_ + kMaxNodes;
-        out_off_ = am_off_ + kMaxNodes + 1;
+        out_off_ = am_off_ + kMaxNodes + 1;   // m, bonus, path[kMaxNodes], tokens[kMaxNodes]
+        cur_off_ = out_off_ + 2 + 2 * kMaxNodes;  // uniform cursor
+        err_off_ = cur_off_ + 1;                   // device error flag
+        arena_cap_ = err_off_ + 64;
         CUDA_OK(cudaMalloc(&arena_, sizeof(int) * (size_t)arena_cap_));
         CUDA_OK(cudaMemset(arena_, 0, sizeof(int) * (size_t)arena_cap_));
-        CUDA_OK(cudaMallocHost(&outcome_host_, sizeof(int) * 256));
+        CUDA_OK(cudaMallocHost(&outcome_host_, sizeof(int) * (size_t)(err_off_ - out_off_ + 1)));
+        // T > 0 / tree-level buffers: logits and dists per drafted row
+        const int V = bc.vocab_size;
+        const int ldl = std::max(ldpad(V, bc.weight_dtype), ldpad(V, dc.weight_dtype));
+        logits_ld_ = ldl;
+        CUDA_OK(cudaMalloc(&dlogits_, sizeof(float) * (size_t)(kMaxNodes + 1) * ldl));
+        CUDA_OK(cudaMalloc(&blogits_, sizeof(float) * (size_t)(kMaxNodes + 1) * ldl));
+        CUDA_OK(cudaMalloc(&ddists_, sizeof(float) * (size_t)(kMaxNodes + 1) * V));
+        CUDA_OK(cudaMalloc(&bdists_, sizeof(float) * (size_t)(kMaxNodes + 1) * V));
+        CUDA_OK(cudaMalloc(&target_, sizeof(float) * (size_t)V));
+        CUDA_OK(cudaMalloc(&unif_dev_, sizeof(double) * kMaxDraws));
+        CUDA_OK(cudaMallocHost(&unif_host_, sizeof(double) * kMaxDraws));
         alloc_ws(bws_, base_, 1);
         alloc_ws(dws_, draft_, kMaxGroup);
         base_allocated_ = draft_allocated_ = false;
@@ -502,6 +515,13 @@ public:
         cudaFree(arena_);
         if (temp_) cudaFree(temp_);
         cudaFreeHost(outcome_host_);
+        cudaFree(dlogits_);
+        cudaFree(blogits_);
+        cudaFree(ddists_);
+        cudaFree(bdists_);
+        cudaFree(target_);
+        cudaFree(unif_dev_);
+        cudaFreeHost(unif_host_);
         for (auto& e : ev_) cudaEventDestroy(e);
         for (auto& e : site_ev_) cudaEventDestroy(e);
         cudaStreamDestroy(stream_);
@@ -528,7 +548,6 @@ public:
             if (w < 1 || w > draft_.c.vocab_size) cfg_fail("tree widths must lie in [1, vocab]");
             if (run.algorithm == ALG_SD && w != 1) cfg_fail("plain sd requires all tree widths = 1");
         }
-        if (run.temperature != 0.f) cfg_fail("temperature > 0 is not supported by the device path yet");
         long long nodes = 0, level = 1;
         for (int w : widths_) {
             level *= w;
@@ -536,7 +555,7 @@ public:
             if (nodes > kMaxNodes) cfg_fail("drafted tree exceeds 64 nodes");
         }
         for (int w : widths_)
-            if (w > 16) cfg_fail("tree widths above 16 are not supported on device");
+            if (w > kMaxWidth) cfg_fail("tree widths above 16 are not supported on device");
     }
 
     void ensure_allocated(int which) {
@@ -1088,6 +1107,7 @@ public:
         committed_ = tokens;
         generated_ = 0;
         draft_cached_ = 0;
+        rng_ = Xoshiro(run_.seed);  // Generation's RNG (proj/src/orchestrator.cpp:150)
         bcache_.reset();
         dcache_.reset();
         staging_.reset();
@@ -1108,19 +1128,98 @@ public:
         return tr;
     }
 
+    // ---- T > 0: the iteration's uniforms, drawn from a copy of the stream;
+    // the stream is advanced by what the device consumed (sync_outcome).
+    void upload_uniforms(int n) {
+        Xoshiro copy = rng_;
+        for (int i = 0; i < n; ++i) unif_host_[i] = copy.uniform();
+        CUDA_OK(cudaMemcpyAsync(unif_dev_, unif_host_, sizeof(double) * n, cudaMemcpyHostToDevice, stream_));
+        h2d_bytes_ += (long long)sizeof(double) * n;
+    }
+    void reset_flags() {
+        CUDA_OK(cudaMemsetAsync(arena_ + cur_off_, 0, sizeof(int) * 2, stream_));
+    }
+    // read {m, bonus, path, tokens, cursor, err} back (one D2H per iteration)
+    void sync_outcome(int n_levels) {
+        const int lo = out_off_, n_out = 2 + 2 * n_levels;
+        CUDA_OK(cudaMemcpyAsync(outcome_host_, arena_ + lo, sizeof(int) * (size_t)(err_off_ - lo + 1),
+                                cudaMemcpyDeviceToHost, stream_));
+        d2h_bytes_ += (long long)sizeof(int) * n_out;
+        CUDA_OK(cudaEventRecord(ev_[3], stream_));
+        CUDA_OK(cudaEventSynchronize(ev_[3]));
+        CUDA_OK(cudaGetLastError());
+        const int err = outcome_host_[err_off_ - lo];
+        static const char* msgs[] = {"", "softmax input contains a non-finite logit",
+                                     "draft distribution exhausted before the tree width",
+                                     "drafted token carries zero draft probability",
+                                     "sibling candidates exhaust the draft distribution",
+                                     "sampling from an all-zero distribution"};
+        if (err == 1) throw Error(ST_DOMAIN, msgs[1]);
+        if (err > 1 && err <= 5) throw Error(ST_CHECK, msgs[err]);
+        const int used = outcome_host_[cur_off_ - lo];
+        for (int i = 0; i < used; ++i) (void)rng_.next();
+    }
+    // softmax_temp of `rows` logits rows (row i of src at dist index first+i)
+    void softmax(const float* logits, float* dists, int first, int rows, int V) {
+        std::vector<int> idx(rows);
+        for (int i = 0; i < rows; ++i) idx[i] = first + i;
+        SoftmaxArgs a;
+        a.logits = logits;
+        a.ld_logits = logits_ld_;
+        a.src_row = staging_.push(idx.data(), rows, stream_);
+        a.dists = dists;
+        a.ld_dists = V;
+        a.dst_row = a.src_row;
+        a.vocab = V;
+        a.temperature = run_.temperature;
+        a.err = arena_ + err_off_;
+        launch_softmax_rows(a, rows, stream_);
+        ++launches_;
+    }
+
     // run_iteration_vanilla (proj/src/orchestrator.cpp:438-468)
     IterationTrace step_vanilla(std::vector<int>& emitted) {
         IterationTrace tr;
         staging_.reset();
+        const bool sampled = run_.temperature > 0.f;
+        if (sampled) {
+            upload_uniforms(1);
+            reset_flags();
+        }
         CUDA_OK(cudaEventRecord(ev_[0], stream_));
         const int n0 = (int)committed_.size();
         std::vector<int> rows = chain_pass(base_, bcache_, bws_, bcache_.committed, n0, nullptr, false, false, 0);
-        head(base_, bws_, (int)rows.size() - 1, 1, arena_ + n0, nullptr);
-        CUDA_OK(cudaMemcpyAsync(outcome_host_, arena_ + n0, sizeof(int), cudaMemcpyDeviceToHost, stream_));
-        d2h_bytes_ += sizeof(int);
-        CUDA_OK(cudaEventRecord(ev_[3], stream_));
-        CUDA_OK(cudaEventSynchronize(ev_[3]));
-        CUDA_OK(cudaGetLastError());
+        const int V = base_.c.vocab_size;
+        if (!sampled) {
+            head(base_, bws_, (int)rows.size() - 1, 1, arena_ + n0, nullptr);
+            CUDA_OK(cudaMemcpyAsync(outcome_host_, arena_ + n0, sizeof(int), cudaMemcpyDeviceToHost, stream_));
+            d2h_bytes_ += sizeof(int);
+            CUDA_OK(cudaEventRecord(ev_[3], stream_));
+            CUDA_OK(cudaEventSynchronize(ev_[3]));
+            CUDA_OK(cudaGetLastError());
+        } else {
+            // sample_from(softmax_temp(logits)) (orchestrator.cpp:457-460)
+            head(base_, bws_, (int)rows.size() - 1, 1, arena_ + am_off_, blogits_);
+            softmax(blogits_, bdists_, 0, 1, V);
+            VerifyArgs va;
+            va.vocab = V;
+            va.n_levels = 0;
+            va.tok_arena = arena_;
+            va.base_dists = bdists_;
+            va.draft_dists = ddists_;
+            va.ld_dists = V;
+            va.target = target_;
+            va.uniforms = unif_dev_;
+            va.cursor = arena_ + cur_off_;
+            va.outcome = arena_ + out_off_;
+            va.tok_arena_w = arena_;
+            va.commit_at = n0;
+            va.err = arena_ + err_off_;
+            launch_verify_sample(va, stream_);
+            ++launches_;
+            sync_outcome(0);
+            outcome_host_[0] = outcome_host_[1];
+        }
         std::vector<int> a, b;
         bcache_.commit_path(rows, a, b);
         const int next = outcome_host_[0];
@@ -1142,7 +1241,18 @@ public:
         const bool easy = run_.algorithm == ALG_EASYSPEC;
         const bool calibrated = easy && run_.calibration;
         const bool fuzzy_lead = easy && !run_.calibration;
+        const bool sampled = run_.temperature > 0.f;
+        bool wide = false;
+        for (int w : widths_) wide |= w > 1;
+        const bool need_logits = sampled || wide;  // else: argmax straight from the head epilogue
         const int n_comm = (int)committed_.size();
+        const int V = draft_.c.vocab_size;
+        if (sampled) {
+            long long nodes = 0, level = 1;
+            for (int w : widths_) nodes += (level *= w);
+            upload_uniforms((int)std::min<long long>(kMaxDraws, 2 * nodes + 2));
+        }
+        reset_flags();
 
         // ---- drafter leading pass = bonus calibration (orchestrator.cpp:256-300)
         CUDA_OK(cudaEventRecord(ev_[0], stream_));
@@ -1151,20 +1261,27 @@ public:
         draft_cached_ = n_comm;
         if (fuzzy_lead) ++tr.fuzzy_forwards;
         else ++tr.sequential_forwards;
-        // root logits -> level-1 candidates
         const int lead_T = (int)lead_rows.size();
         CUDA_OK(cudaEventRecord(ev_[1], stream_));
 
         // ---- draft_tree (proj/src/draft_engine.cpp:188-289)
-        // Host tree shape: nodes level by level, siblings contiguous.
-        struct Node { int parent, depth, first_child = -1, n_children = 0, cache_row = -1; };
+        // Host tree shape: nodes level by level, siblings contiguous; the
+        // tokens live on device (tree arena). Dist index 0 = the root row,
+        // then one per forwarded frontier row in order (prob_index).
+        struct Node { int parent, depth, prob_index, first_child = -1, n_children = 0, cache_row = -1; };
         std::vector<Node> nodes;
         std::vector<int> frontier;
         for (int i = 0; i < widths_[0]; ++i) {
-            nodes.push_back({-1, 1});
+            nodes.push_back({-1, 1, 0});
             frontier.push_back(i);
         }
-        select(draft_, dws_, lead_T - 1, 1, widths_[0], {0});
+        int n_dists = 1;
+        if (!need_logits) {
+            head(draft_, dws_, lead_T - 1, 1, arena_ + tree_off_, nullptr);
+        } else {
+            head(draft_, dws_, lead_T - 1, 1, arena_ + am_off_, dlogits_);
+            select_level(0, 1, {widths_[0]}, {0}, V);
+        }
         for (int level = 1; level <= run_.n - 1 && !frontier.empty(); ++level) {
             std::vector<int> parents, tok;
             for (int idx : frontier) {
@@ -1178,17 +1295,28 @@ public:
             forward(draft_, dcache_, dws_, easy ? &plan_ : nullptr, ps);
             if (easy) ++tr.fuzzy_forwards;
             else ++tr.sequential_forwards;
-            std::vector<int> next, first_child;
-            for (int idx : frontier) {
+            std::vector<int> next, first_child, widths;
+            const int dist0 = n_dists;
+            for (size_t i = 0; i < frontier.size(); ++i) {
+                const int idx = frontier[i];
                 nodes[idx].first_child = (int)nodes.size();
                 nodes[idx].n_children = widths_[level];
                 first_child.push_back((int)nodes.size());
+                widths.push_back(widths_[level]);
                 for (int k = 0; k < widths_[level]; ++k) {
-                    nodes.push_back({idx, level + 1});
+                    nodes.push_back({idx, level + 1, dist0 + (int)i});
                     next.push_back((int)nodes.size() - 1);
                 }
             }
-            select(draft_, dws_, 0, (int)frontier.size(), widths_[level], first_child);
+            const int nf = (int)frontier.size();
+            if (!need_logits) {
+                // width 1: children of consecutive frontier rows are consecutive nodes
+                head(draft_, dws_, 0, nf, arena_ + tree_off_ + first_child[0], nullptr);
+            } else {
+                head(draft_, dws_, 0, nf, arena_ + am_off_, dlogits_ + (size_t)dist0 * logits_ld_);
+                select_level(dist0, nf, widths, first_child, V);
+            }
+            n_dists += nf;
             frontier = next;
         }
         tr.drafted_nodes = (int)nodes.size();
@@ -1216,38 +1344,58 @@ public:
         Pass ps = make_pass(bcache_, all_rows, tok);
         forward(base_, bcache_, bws_, nullptr, ps);
         ++tr.base_forwards;
-        head(base_, bws_, 0, 1 + nn, arena_ + am_off_, nullptr);
+        head(base_, bws_, 0, 1 + nn, arena_ + am_off_, sampled ? blogits_ : nullptr);
         // acceptance on device
-        std::vector<int> np(nn), nfc(nn), nnc(nn), nti(nn);
+        std::vector<int> np(nn), nfc(nn), nnc(nn), nti(nn), npi(nn);
         int root_children = 0;
         for (int j = 0; j < nn; ++j) {
             np[j] = nodes[j].parent;
             nfc[j] = nodes[j].first_child;
             nnc[j] = nodes[j].n_children;
             nti[j] = tree_off_ + j;
+            npi[j] = nodes[j].prob_index;
             if (nodes[j].parent < 0) ++root_children;
         }
-        AcceptArgs aa;
-        aa.n_nodes = nn;
-        aa.n_levels = run_.n;
-        aa.root_children = root_children;
-        aa.node_parent = staging_.push(np.data(), nn, stream_);
-        aa.node_first_child = staging_.push(nfc.data(), nn, stream_);
-        aa.node_n_children = staging_.push(nnc.data(), nn, stream_);
-        aa.node_tok_idx = staging_.push(nti.data(), nn, stream_);
-        aa.tok_arena = arena_;
-        aa.base_argmax = arena_ + am_off_;
-        aa.outcome = arena_ + out_off_;
-        aa.tok_arena_w = arena_;
-        aa.commit_at = n_comm;
-        launch_accept_greedy(aa, stream_);
+        if (!sampled) {
+            AcceptArgs aa;
+            aa.n_nodes = nn;
+            aa.n_levels = run_.n;
+            aa.root_children = root_children;
+            aa.node_parent = staging_.push(np.data(), nn, stream_);
+            aa.node_first_child = staging_.push(nfc.data(), nn, stream_);
+            aa.node_n_children = staging_.push(nnc.data(), nn, stream_);
+            aa.node_tok_idx = staging_.push(nti.data(), nn, stream_);
+            aa.tok_arena = arena_;
+            aa.base_argmax = arena_ + am_off_;
+            aa.outcome = arena_ + out_off_;
+            aa.tok_arena_w = arena_;
+            aa.commit_at = n_comm;
+            launch_accept_greedy(aa, stream_);
+        } else {
+            softmax(blogits_, bdists_, 0, 1 + nn, V);
+            VerifyArgs va;
+            va.vocab = V;
+            va.n_levels = run_.n;
+            va.root_children = root_children;
+            va.node_first_child = staging_.push(nfc.data(), nn, stream_);
+            va.node_n_children = staging_.push(nnc.data(), nn, stream_);
+            va.node_tok_idx = staging_.push(nti.data(), nn, stream_);
+            va.node_prob_index = staging_.push(npi.data(), nn, stream_);
+            va.tok_arena = arena_;
+            va.base_dists = bdists_;
+            va.draft_dists = ddists_;
+            va.ld_dists = V;
+            va.target = target_;
+            va.uniforms = unif_dev_;
+            va.cursor = arena_ + cur_off_;
+            va.outcome = arena_ + out_off_;
+            va.tok_arena_w = arena_;
+            va.commit_at = n_comm;
+            va.err = arena_ + err_off_;
+            launch_verify_sample(va, stream_);
+        }
         ++launches_;
-        const int out_n = 2 + 2 * run_.n;
-        CUDA_OK(cudaMemcpyAsync(outcome_host_, arena_ + out_off_, sizeof(int) * out_n, cudaMemcpyDeviceToHost, stream_));
-        d2h_bytes_ += (long long)sizeof(int) * out_n;
-        CUDA_OK(cudaEventRecord(ev_[3], stream_));
-        CUDA_OK(cudaEventSynchronize(ev_[3]));
-        CUDA_OK(cudaGetLastError());
+        sync_outcome(run_.n);
 
         const int m = outcome_host_[0], bonus = outcome_host_[1];
         std::vector<int> path(outcome_host_ + 2, outcome_host_ + 2 + m);
@@ -1289,19 +1437,36 @@ public:
         return tr;
     }
 
-    // select_children at temperature 0 (proj/src/draft_engine.cpp:141-160):
-    // width 1 = argmax straight from the head epilogue; wider = top-k.
-    void select(ModelDev& M, Workspace& W, int r0, int n, int width, const std::vector<int>& first_node) {
-        if (width == 1) {
-            // children of consecutive frontier rows are consecutive nodes
-            bool contiguous = true;
-            for (int i = 1; i < n; ++i) contiguous &= first_node[i] == first_node[0] + i;
-            if (contiguous) {
-                head(M, W, r0, n, arena_ + tree_off_ + first_node[0], nullptr);
-                return;
-            }
+    // select_children (proj/src/draft_engine.cpp:141-186) for `rows`
+    // frontier rows whose logits sit at dist indices [dist0, dist0+rows):
+    // T = 0 top-k of the logits; T > 0 softmax_temp, then draws without
+    // replacement consuming the iteration's uniforms in row order.
+    void select_level(int dist0, int rows, const std::vector<int>& widths, const std::vector<int>& first_node, int V) {
+        const bool sampled = run_.temperature > 0.f;
+        if (sampled) softmax(dlogits_, ddists_, dist0, rows, V);
+        std::vector<int> idx(rows), child_at(rows);
+        for (int i = 0; i < rows; ++i) {
+            idx[i] = dist0 + i;
+            child_at[i] = tree_off_ + first_node[i];
         }
-        throw Error(ST_CONFIG, "tree widths > 1 are not supported on device yet");
+        SelectArgs a;
+        a.rows = rows;
+        a.vocab = V;
+        a.temperature = run_.temperature;
+        a.logits = dlogits_;
+        a.ld_logits = logits_ld_;
+        a.logit_row = staging_.push(idx.data(), rows, stream_);
+        a.dists = ddists_;
+        a.ld_dists = V;
+        a.dist_row = a.logit_row;
+        a.width = staging_.push(widths.data(), rows, stream_);
+        a.child_at = staging_.push(child_at.data(), rows, stream_);
+        a.tok_arena = arena_;
+        a.uniforms = unif_dev_;
+        a.cursor = arena_ + cur_off_;
+        a.err = arena_ + err_off_;
+        launch_select_children(a, stream_);
+        ++launches_;
     }
 
     void move_rows(Cache& C, const std::vector<int>& src, const std::vector<int>& dst) {
@@ -1412,8 +1577,19 @@ private:
     std::vector<void*> ws_owned_;
     Staging staging_;
     int* arena_ = nullptr;
-    int arena_cap_ = 0, tree_off_ = 0, am_off_ = 0, out_off_ = 0;
+    int arena_cap_ = 0, tree_off_ = 0, am_off_ = 0, out_off_ = 0, cur_off_ = 0, err_off_ = 0;
     int* outcome_host_ = nullptr;
+    // T > 0 sampling / tree levels
+    static constexpr int kMaxDraws = 4 * kMaxNodes + 8;
+    float* dlogits_ = nullptr;  // [kMaxNodes+1][logits_ld_] drafted-row logits (row = dist index)
+    float* blogits_ = nullptr;  // [kMaxNodes+1][logits_ld_] verify-row logits
+    float* ddists_ = nullptr;   // [kMaxNodes+1][V] draft distributions
+    float* bdists_ = nullptr;   // [kMaxNodes+1][V] base distributions
+    float* target_ = nullptr;   // [V] verify scratch
+    int logits_ld_ = 0;
+    double* unif_dev_ = nullptr;
+    double* unif_host_ = nullptr;
+    Xoshiro rng_{1};
     void* temp_ = nullptr;
     size_t temp_bytes_ = 0;
     RunCfg run_;

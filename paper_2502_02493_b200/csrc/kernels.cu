@@ -502,7 +502,9 @@ constexpr int kAttnThreads = 128;
 
 size_t attn_ws_floats(int T, int n_heads, int dh, int max_rows) {
     const size_t splits = (size_t)(max_rows + kAttnRows - 1) / kAttnRows;
-    return splits * (size_t)T * n_heads * (dh + 2);
+    // covers both layouts: fp32 [split][n_kv][T*G][dh+2] and bf16 mma
+    // [chunk][n_kv * mtiles][16][dh+4]
+    return splits * (size_t)(T * n_heads + 16 * n_heads) * (dh + 4);
 }
 size_t attn_tickets(int T, int n_heads, int n_kv) {
     const int G = n_heads / n_kv;
@@ -707,22 +709,20 @@ __global__ void __launch_bounds__(128) attn_mma_kernel(const __grid_constant__ A
     const int split = blockIdx.x * 4 + warp;
     const int j0 = split * 64;
     const int nr = max(0, min(64, L.pass.total - j0));
-    __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(smraw) + (size_t)warp * 2 * 64 * LDK;
-    __nv_bfloat16* Vs = Ks + 64 * LDK;
+    // one 64-row page buffer per warp: K first, then V into the same buffer
+    // once the scores are computed (halves shared memory: 3 CTAs per SM)
+    __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(smraw) + (size_t)warp * 64 * LDK;
+    __nv_bfloat16* Vs = Ks;
     const __nv_bfloat16* pool = reinterpret_cast<const __nv_bfloat16*>(L.kv.pool);
-
+    constexpr int CH = DH / 8;  // 16-byte chunks per row
+    const __nv_bfloat16* vg = nullptr;
     if (nr > 0) {  // 64-row split = one page: K and V of this head are contiguous 64 x DH runs
         const __nv_bfloat16* kg = pool + kv_off(L.kv, A.layer, 0, hk, j0);
-        const __nv_bfloat16* vg = pool + kv_off(L.kv, A.layer, 1, hk, j0);
-        constexpr int CH = DH / 8;  // 16-byte chunks per row
+        vg = pool + kv_off(L.kv, A.layer, 1, hk, j0);
+#pragma unroll 8
         for (int i = lane; i < 64 * CH; i += 32) {
             const int r = i / CH, c = (i % CH) * 8;
             cp_async16(Ks + r * LDK + c, kg + (size_t)r * DH + c);
-        }
-        cp_async_commit();
-        for (int i = lane; i < 64 * CH; i += 32) {
-            const int r = i / CH, c = (i % CH) * 8;
-            cp_async16(Vs + r * LDK + c, vg + (size_t)r * DH + c);
         }
         cp_async_commit();
     }
@@ -752,7 +752,7 @@ __global__ void __launch_bounds__(128) attn_mma_kernel(const __grid_constant__ A
 #pragma unroll
     for (int d = 0; d < NT; ++d) o[d][0] = o[d][1] = o[d][2] = o[d][3] = 0.f;
     if (nr > 0) {
-        cp_async_wait<1>();
+        cp_async_wait<0>();
         __syncwarp();
         float sc[8][4];
 #pragma unroll
@@ -767,6 +767,14 @@ __global__ void __launch_bounds__(128) attn_mma_kernel(const __grid_constant__ A
                 mma_bf16_16816(sc[j], qa[s + 1], b[2], b[3]);
             }
         }
+        // K consumed: stream V into the same buffer while the softmax runs
+        __syncwarp();
+#pragma unroll 8
+        for (int i = lane; i < 64 * CH; i += 32) {
+            const int r = i / CH, c = (i % CH) * 8;
+            cp_async16(Vs + r * LDK + c, vg + (size_t)r * DH + c);
+        }
+        cp_async_commit();
         // scale + mask, row max / exp / sum over this split's 64 keys
         const float inv_sqrt = 1.0f / sqrtf((float)DH);
         const int pr[2] = {mt * 16 + gid, mt * 16 + gid + 8};
@@ -827,14 +835,15 @@ __global__ void __launch_bounds__(128) attn_mma_kernel(const __grid_constant__ A
     __syncthreads();  // K/V smem free: reuse for the warp combine
     float* Os = reinterpret_cast<float*>(smraw);           // [4][16][DH]
     float* Ms = Os + 4 * 16 * DH;                          // [4][16]
-    float* Ls = Ms + 64;
+    float* Ls = Ms + 64;                                   // [4][16]
+    float* Fw = Ls + 64;                                   // [4][16] warp weights exp(m_w - M)
+    float* Rm = Fw + 64;                                   // [16] row max
+    float* Rd = Rm + 16;                                   // [16] row denominator
 #pragma unroll
     for (int d = 0; d < NT; ++d) {
         const int c = d * 8 + 2 * tig;
-        Os[(warp * 16 + gid) * DH + c] = o[d][0];
-        Os[(warp * 16 + gid) * DH + c + 1] = o[d][1];
-        Os[(warp * 16 + gid + 8) * DH + c] = o[d][2];
-        Os[(warp * 16 + gid + 8) * DH + c + 1] = o[d][3];
+        *reinterpret_cast<float2*>(&Os[(warp * 16 + gid) * DH + c]) = make_float2(o[d][0], o[d][1]);
+        *reinterpret_cast<float2*>(&Os[(warp * 16 + gid + 8) * DH + c]) = make_float2(o[d][2], o[d][3]);
     }
     if (tig == 0) {
         Ms[warp * 16 + gid] = m_r[0];
@@ -843,33 +852,67 @@ __global__ void __launch_bounds__(128) attn_mma_kernel(const __grid_constant__ A
         Ls[warp * 16 + gid + 8] = l_r[1];
     }
     __syncthreads();
-    const int nchunks = gridDim.x;
-    const size_t ps = (size_t)DH + 2;
-    // CTA partial for (pair row r, dim c)
-    float* wsb = A.ws + (((size_t)blockIdx.x * gridDim.y + blockIdx.y) * 16) * ps;
-    for (int i = threadIdx.x; i < 16 * DH; i += 128) {
-        const int r = i / DH, c = i - r * DH;
+    if (threadIdx.x < 16) {  // per-row weights, fixed warp order
+        const int r = threadIdx.x;
         float M = -INFINITY;
 #pragma unroll
         for (int w = 0; w < 4; ++w) M = fmaxf(M, Ms[w * 16 + r]);
-        float num = 0.f, den = 0.f;
-        if (M != -INFINITY)
+        float den = 0.f;
 #pragma unroll
-            for (int w = 0; w < 4; ++w) {
-                const float m = Ms[w * 16 + r];
-                if (m == -INFINITY) continue;
-                const float f = expf(m - M);
-                num = __fmaf_rn(f, Os[(w * 16 + r) * DH + c], num);
+        for (int w = 0; w < 4; ++w) {
+            const float m = Ms[w * 16 + r];
+            float f = 0.f;
+            if (M != -INFINITY && m != -INFINITY) {
+                f = expf(m - M);
                 den = __fmaf_rn(f, Ls[w * 16 + r], den);
             }
-        const int p = mt * 16 + r;
-        if (nchunks == 1) {
-            if (p < P) A.out[(size_t)(p / G) * H * DH + (hk * G + p % G) * DH + c] = den > 0.f ? num / den : 0.f;
-        } else {
-            wsb[r * ps + c] = num;
-            if (c == 0) {
-                wsb[r * ps + DH] = M;
-                wsb[r * ps + DH + 1] = den;
+            Fw[w * 16 + r] = f;
+        }
+        Rm[r] = M;
+        Rd[r] = den;
+    }
+    __syncthreads();
+    const int nchunks = gridDim.x;
+    constexpr int PS = DH + 4;  // workspace row: DH values, M, den (float4-aligned)
+    float* wsb = A.ws + (((size_t)blockIdx.x * gridDim.y + blockIdx.y) * 16) * PS;
+    {
+        // thread -> (row r, 16 consecutive dims)
+        constexpr int CPR = DH / 16;  // threads per row
+        for (int it = threadIdx.x; it < 16 * CPR; it += 128) {
+            const int r = it / CPR, c0 = (it % CPR) * 16;
+            float4 acc[4];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+                const float f = Fw[w * 16 + r];
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    const float4 x = *reinterpret_cast<const float4*>(&Os[(w * 16 + r) * DH + c0 + 4 * v]);
+                    acc[v].x = __fmaf_rn(f, x.x, acc[v].x);
+                    acc[v].y = __fmaf_rn(f, x.y, acc[v].y);
+                    acc[v].z = __fmaf_rn(f, x.z, acc[v].z);
+                    acc[v].w = __fmaf_rn(f, x.w, acc[v].w);
+                }
+            }
+            const int p = mt * 16 + r;
+            if (nchunks == 1) {
+                if (p < P) {
+                    const float den = Rd[r];
+                    float* o = A.out + (size_t)(p / G) * H * DH + (hk * G + p % G) * DH + c0;
+#pragma unroll
+                    for (int v = 0; v < 4; ++v)
+                        *reinterpret_cast<float4*>(o + 4 * v) =
+                            den > 0.f ? make_float4(acc[v].x / den, acc[v].y / den, acc[v].z / den, acc[v].w / den)
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+            } else {
+#pragma unroll
+                for (int v = 0; v < 4; ++v) *reinterpret_cast<float4*>(wsb + r * PS + c0 + 4 * v) = acc[v];
+                if (c0 == 0) {
+                    wsb[r * PS + DH] = Rm[r];
+                    wsb[r * PS + DH + 1] = Rd[r];
+                }
             }
         }
     }
@@ -885,43 +928,72 @@ __global__ void __launch_bounds__(128) attn_mma_kernel(const __grid_constant__ A
     }
     __syncthreads();
     if (!s_last) return;
-    const size_t cstride = (size_t)gridDim.y * 16 * ps;
-    const float* base = A.ws + ((size_t)blockIdx.y * 16) * ps;
+    const size_t cstride = (size_t)gridDim.y * 16 * PS;
+    const float* base = A.ws + ((size_t)blockIdx.y * 16) * PS;
     // per-row chunk weights f = exp(m_ch - M) and denominator, once per row
     float* fac = Os;              // [nchunks][16]
     float* sden = Os + 64 * 16;   // [16]
+    // (m, l) of every chunk: one float2 load each, all issued together
+    float2* ml = reinterpret_cast<float2*>(Os + 64 * 16 + 16);  // [nchunks][16]
+    for (int i = threadIdx.x; i < nchunks * 16; i += 128) {
+        const int ch = i >> 4, r = i & 15;
+        ml[i] = __ldcg(reinterpret_cast<const float2*>(base + ch * cstride + r * PS + DH));
+    }
+    __syncthreads();
     if (threadIdx.x < 16) {
         const int r = threadIdx.x;
         float M = -INFINITY;
-        for (int ch = 0; ch < nchunks; ++ch) M = fmaxf(M, __ldcg(base + ch * cstride + r * ps + DH));
+        for (int ch = 0; ch < nchunks; ++ch) M = fmaxf(M, ml[ch * 16 + r].x);
         float den = 0.f;
         for (int ch = 0; ch < nchunks; ++ch) {
-            const float m = __ldcg(base + ch * cstride + r * ps + DH);
+            const float m = ml[ch * 16 + r].x;
             float f = 0.f;
             if (M != -INFINITY && m != -INFINITY) {
                 f = expf(m - M);
-                den = __fmaf_rn(f, __ldcg(base + ch * cstride + r * ps + DH + 1), den);
+                den = __fmaf_rn(f, ml[ch * 16 + r].y, den);
             }
             fac[ch * 16 + r] = f;
         }
         sden[r] = den;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < 16 * DH; i += 128) {
-        const int r = i / DH, c = i - r * DH;
+    constexpr int CPR = DH / 16;
+    for (int it = threadIdx.x; it < 16 * CPR; it += 128) {
+        const int r = it / CPR, c0 = (it % CPR) * 16;
         const int p = mt * 16 + r;
         if (p >= P) continue;
-        float num = 0.f;
-        for (int ch0 = 0; ch0 < nchunks; ch0 += 8) {
-            float v[8];
+        float4 acc[4];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) v[q] = ch0 + q < nchunks ? __ldcg(base + (ch0 + q) * cstride + r * ps + c) : 0.f;
+        for (int v = 0; v < 4; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int ch0 = 0; ch0 < nchunks; ch0 += 4) {
+            float4 x[4][4];
 #pragma unroll
-            for (int q = 0; q < 8; ++q)
-                if (ch0 + q < nchunks) num = __fmaf_rn(fac[(ch0 + q) * 16 + r], v[q], num);
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int v = 0; v < 4; ++v)
+                    x[q][v] = ch0 + q < nchunks
+                                  ? __ldcg(reinterpret_cast<const float4*>(base + (ch0 + q) * cstride + r * PS + c0 + 4 * v))
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (ch0 + q >= nchunks) break;
+                const float f = fac[(ch0 + q) * 16 + r];
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    acc[v].x = __fmaf_rn(f, x[q][v].x, acc[v].x);
+                    acc[v].y = __fmaf_rn(f, x[q][v].y, acc[v].y);
+                    acc[v].z = __fmaf_rn(f, x[q][v].z, acc[v].z);
+                    acc[v].w = __fmaf_rn(f, x[q][v].w, acc[v].w);
+                }
+            }
         }
         const float den = sden[r];
-        A.out[(size_t)(p / G) * H * DH + (hk * G + p % G) * DH + c] = den > 0.f ? num / den : 0.f;
+        float* o = A.out + (size_t)(p / G) * H * DH + (hk * G + p % G) * DH + c0;
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+            *reinterpret_cast<float4*>(o + 4 * v) =
+                den > 0.f ? make_float4(acc[v].x / den, acc[v].y / den, acc[v].z / den, acc[v].w / den)
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
     }
 }
 
@@ -934,7 +1006,7 @@ static void attn_mma_launch(const AttnLaunch& L, int nprob, cudaStream_t s) {
     }
     const int mtiles = (L.pass.T * L.G + 15) / 16;
     dim3 grid((splits + 3) / 4, L.kv.n_kv * mtiles, nprob);
-    const size_t smem = std::max<size_t>((size_t)4 * 2 * 64 * (DH + 8) * 2, (size_t)(4 * 16 * DH + 128) * 4);
+    const size_t smem = std::max<size_t>((size_t)4 * 64 * (DH + 8) * 2, (size_t)(4 * 16 * DH + 256) * 4);
     static bool configured = false;
     if (!configured) {
         CK(cudaFuncSetAttribute(attn_mma_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -159,6 +159,69 @@ struct AcceptArgs {
 };
 void launch_accept_greedy(const AcceptArgs& a, cudaStream_t s);
 
+// ---- T > 0 sampling and multi-sibling tree levels (sample.cu) ----
+constexpr int kMaxWidth = 16;  // children per drafted node
+
+// dists[dst_row[r]] = softmax_temp(logits[src_row[r]], temperature)
+// (one-hot at the first argmax when temperature == 0).
+struct SoftmaxArgs {
+    const float* logits = nullptr;
+    int ld_logits = 0;
+    const int* src_row = nullptr;
+    float* dists = nullptr;
+    int ld_dists = 0;
+    const int* dst_row = nullptr;
+    int vocab = 0;
+    float temperature = 0.f;
+    int* err = nullptr;  // set to 1 on a non-finite logit (DomainError)
+};
+void launch_softmax_rows(const SoftmaxArgs& a, int rows, cudaStream_t s);
+
+// select_children for `rows` frontier rows in order: T = 0 top-k of the
+// logits row; T > 0 `width` draws without replacement from the dists row,
+// consuming uniforms at *cursor. Children go to tok_arena[child_at[r] + i].
+struct SelectArgs {
+    int rows = 0, vocab = 0;
+    float temperature = 0.f;
+    const float* logits = nullptr;
+    int ld_logits = 0;
+    const int* logit_row = nullptr;
+    const float* dists = nullptr;
+    int ld_dists = 0;
+    const int* dist_row = nullptr;
+    const int* width = nullptr;
+    const int* child_at = nullptr;
+    int* tok_arena = nullptr;
+    const double* uniforms = nullptr;
+    int* cursor = nullptr;
+    int* err = nullptr;  // 2: draft distribution exhausted before the width
+};
+void launch_select_children(const SelectArgs& a, cudaStream_t s);
+
+// verify_tree at T > 0 over the drafted tree (n_levels = 0: vanilla
+// sampling). base_dists rows: frontier, then one per node; draft_dists
+// indexed by node_prob_index. Writes outcome = {m, bonus, path[n_levels],
+// tokens[n_levels]} and appends accepted tokens + bonus to tok_arena_w.
+struct VerifyArgs {
+    int vocab = 0, n_levels = 0, root_children = 0;
+    const int* node_first_child = nullptr;
+    const int* node_n_children = nullptr;
+    const int* node_tok_idx = nullptr;
+    const int* node_prob_index = nullptr;
+    const int* tok_arena = nullptr;
+    const float* base_dists = nullptr;
+    const float* draft_dists = nullptr;
+    int ld_dists = 0;
+    float* target = nullptr;  // [vocab] scratch
+    const double* uniforms = nullptr;
+    int* cursor = nullptr;
+    int* outcome = nullptr;
+    int* tok_arena_w = nullptr;
+    int commit_at = 0;
+    int* err = nullptr;  // 3..5: CheckError conditions of verify_tree / sample_from
+};
+void launch_verify_sample(const VerifyArgs& a, cudaStream_t s);
+
 // Deterministic N(0, sd) init from a counter hash (perf-mode weights).
 void launch_fill_normal(int dtype, void* dst, long long n, float sd, uint64_t seed, cudaStream_t s);
 void launch_fill_const(int dtype, void* dst, long long n, float v, cudaStream_t s);

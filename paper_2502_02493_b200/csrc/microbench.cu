@@ -87,3 +87,102 @@ extern "C" espec_status espec_bench_gemv(int K, int N, int T, int nprob, int epi
     cudaStreamDestroy(s);
     return err == cudaSuccess ? ESPEC_OK : ESPEC_CUDA;
 }
+
+// Decode/verify attention over a paged bf16 cache in isolation: T query rows
+// (the last T rows of a ctx-row context, causal), n_heads = G * n_kv.
+extern "C" espec_status espec_bench_attn(int T, int n_heads, int n_kv, int dh, int ctx, int nprob, int iters,
+                                         int device, double* us_per_launch, double* bytes_per_launch) {
+    if (T < 1 || T > 16 || n_kv < 1 || n_heads % n_kv || (dh != 64 && dh != 128) || ctx < T || nprob < 1 ||
+        nprob > kMaxProblems || iters < 1)
+        return ESPEC_CONFIG;
+    if (cudaSetDevice(device) != cudaSuccess) return ESPEC_CUDA;
+    const int page_rows = 64, n_layers = nprob;
+    const int n_pages = (ctx + page_rows - 1) / page_rows;
+    const long long page_elems = (long long)n_layers * 2 * n_kv * page_rows * dh;
+    void* pool = nullptr;
+    int *table = nullptr, *rows = nullptr, *pos = nullptr, *vis = nullptr;
+    unsigned long long* anc = nullptr;
+    float *q = nullptr, *out = nullptr, *ws = nullptr;
+    unsigned* tk = nullptr;
+    cudaStream_t s;
+    cudaEvent_t e0, e1;
+    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaMalloc(&pool, (size_t)n_pages * page_elems * 2);
+    launch_fill_normal(DT_BF16, pool, (long long)n_pages * page_elems, 1.0f, 7, s);
+    std::vector<int> h_table(n_pages), h_rows(T), h_pos(T), h_vis(T);
+    for (int p = 0; p < n_pages; ++p) h_table[p] = p;
+    for (int t = 0; t < T; ++t) {
+        h_rows[t] = ctx - T + t;
+        h_pos[t] = h_rows[t];
+        h_vis[t] = h_rows[t] + 1;
+    }
+    cudaMalloc(&table, sizeof(int) * n_pages);
+    cudaMalloc(&rows, sizeof(int) * T);
+    cudaMalloc(&pos, sizeof(int) * T);
+    cudaMalloc(&vis, sizeof(int) * T);
+    cudaMalloc(&anc, sizeof(unsigned long long) * T);
+    cudaMemcpy(table, h_table.data(), sizeof(int) * n_pages, cudaMemcpyHostToDevice);
+    cudaMemcpy(rows, h_rows.data(), sizeof(int) * T, cudaMemcpyHostToDevice);
+    cudaMemcpy(pos, h_pos.data(), sizeof(int) * T, cudaMemcpyHostToDevice);
+    cudaMemcpy(vis, h_vis.data(), sizeof(int) * T, cudaMemcpyHostToDevice);
+    cudaMemset(anc, 0, sizeof(unsigned long long) * T);
+    const size_t wsf = attn_ws_floats(16, n_heads, dh, ctx + 64);
+    const size_t tkn = attn_tickets(16, n_heads, n_kv);
+    cudaMalloc(&q, sizeof(float) * (size_t)nprob * 16 * n_heads * dh);
+    cudaMalloc(&out, sizeof(float) * (size_t)nprob * 16 * n_heads * dh);
+    cudaMalloc(&ws, sizeof(float) * wsf * nprob);
+    cudaMalloc(&tk, sizeof(unsigned) * tkn * nprob);
+    cudaMemset(tk, 0, sizeof(unsigned) * tkn * nprob);
+    launch_fill_normal(DT_F32, q, (long long)nprob * 16 * n_heads * dh, 1.0f, 3, s);
+    KvView kv;
+    kv.pool = pool;
+    kv.page_table = table;
+    kv.page_rows = page_rows;
+    kv.n_layers = n_layers;
+    kv.n_kv = n_kv;
+    kv.dh = dh;
+    kv.dtype = DT_BF16;
+    kv.page_elems = page_elems;
+    PassView pv;
+    pv.T = T;
+    pv.rows = rows;
+    pv.pos = pos;
+    pv.vis_end = vis;
+    pv.anc = anc;
+    pv.tree_base = ctx;
+    pv.total = ctx;
+    AttnBatch b;
+    for (int p = 0; p < nprob; ++p) {
+        b.p[p].q = q + (size_t)p * 16 * n_heads * dh;
+        b.p[p].out = out + (size_t)p * 16 * n_heads * dh;
+        b.p[p].layer = p;
+        b.p[p].ws = ws + wsf * p;
+        b.p[p].tickets = tk + tkn * p;
+    }
+    for (int i = 0; i < 3; ++i) launch_attention(b, nprob, n_heads, pv, kv, s);
+    cudaEventRecord(e0, s);
+    for (int i = 0; i < iters; ++i) launch_attention(b, nprob, n_heads, pv, kv, s);
+    cudaEventRecord(e1, s);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const cudaError_t err = cudaGetLastError();
+    *us_per_launch = 1000.0 * ms / iters;
+    *bytes_per_launch = (double)nprob * 2.0 * ctx * n_kv * dh * 2;
+    cudaFree(pool);
+    cudaFree(table);
+    cudaFree(rows);
+    cudaFree(pos);
+    cudaFree(vis);
+    cudaFree(anc);
+    cudaFree(q);
+    cudaFree(out);
+    cudaFree(ws);
+    cudaFree(tk);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamDestroy(s);
+    return err == cudaSuccess ? ESPEC_OK : ESPEC_CUDA;
+}

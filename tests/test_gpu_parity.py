@@ -158,6 +158,52 @@ def test_generate_matches_reference_tokens(case):
             np.testing.assert_allclose(got, last[key][layer], rtol=1e-4, atol=1e-2 * max(1, n))
 
 
+SAMPLED_OR_TREES = [c for c in GEN if c not in GREEDY_CHAINS]
+
+
+@pytest.mark.parametrize("case", SAMPLED_OR_TREES, ids=[c["name"] for c in SAMPLED_OR_TREES])
+def test_generate_sampled_and_trees_match_reference(case):
+    """T > 0 rejection sampling (uniforms drawn from the reference's xoshiro
+    stream in the reference's order) and multi-sibling tree levels
+    (top-k at T = 0): emitted tokens, m, drafted nodes, forward counts and
+    cache lengths bit-exact against the reference fixtures."""
+    eng = _engine_for_case(case)
+    toks, traces = eng.generate(case["prompt"].encode())
+    assert toks == case["tokens"]
+    assert len(traces) == len(case["iterations"])
+    for t, want in zip(traces, case["iterations"]):
+        assert (t.m, t.emitted, t.drafted_nodes, t.sequential_forwards, t.fuzzy_forwards, t.base_forwards,
+                t.committed, t.draft_committed, t.base_committed) == \
+               (want["m"], want["emitted"], want["drafted_nodes"], want["sequential_forwards"],
+                want["fuzzy_forwards"], want["base_forwards"], want["committed"], want["draft_committed"],
+                want["base_committed"])
+
+
+def test_sampled_easyspec_first_token_distribution_matches_vanilla():
+    """Statistical losslessness on device (acceptance criterion 2,
+    proj/tests/acceptance_main.cpp:156-183, reduced): the first generated
+    token of T = 0.8 EasySpec with a 2-wide tree follows the same law as
+    vanilla sampling. TV over 2500 seeds each; bound 0.08 (sampling noise of
+    two 2500-run histograms over this support is ~0.03)."""
+    base = E.tiny_config(4, 21, max_positions=64)
+    dcfg = replace(base, n_layers=3)
+    counts = {}
+    runs = 2500
+    for alg, widths in (("vanilla", [1, 1, 1]), ("easyspec", [2, 2, 2])):
+        run = E.RunConfig(algorithm=alg, n=3, widths=widths, lp_size=2, temperature=0.8, max_new_tokens=1, seed=1)
+        eng = E.truncated_pair(base, 3, run)
+        hist = {}
+        for r in range(runs):
+            eng.set_run(replace(run, seed=1000 + r))
+            toks, _ = eng.generate(b"easyspec")
+            hist[toks[0]] = hist.get(toks[0], 0) + 1
+        counts[alg] = hist
+        eng.close()
+    keys = set(counts["vanilla"]) | set(counts["easyspec"])
+    tv = 0.5 * sum(abs(counts["vanilla"].get(k, 0) - counts["easyspec"].get(k, 0)) / runs for k in keys)
+    assert tv < 0.08, tv
+
+
 def test_calibrated_drafter_cache_equals_fresh_prefill_every_iteration():
     """Criterion 4 (proj/tests/acceptance_main.cpp:221-275) / test_orchestrator
     144-177: after each calibrated iteration the drafter cache holds exactly

@@ -74,12 +74,17 @@ typedef struct {
     int calibration;
 } espec_run_cfg;
 
-/* Devices used by one engine. Round 1: a single device (lp/tp of 1). */
+/* Devices used by one engine. One engine drives one GPU; a tensor-parallel
+ * group of tp_size engines (one per GPU, usually one per process) shards both
+ * models Megatron-style and exchanges partial sums over
+ * NVLink peer memory. Layer-parallel fuzzy groups run on every GPU of the
+ * group (n_lp_devices must be 0 or 1). */
 typedef struct {
     int device;
     int n_lp_devices;
     const int* lp_devices;
     int tp_size;
+    int tp_rank;
 } espec_device_map;
 
 /* espec::IterationTrace (proj/include/espec/report.hpp:12-28) with real
@@ -104,6 +109,15 @@ espec_status espec_engine_create(const espec_model_cfg* base, const espec_model_
                                  const espec_run_cfg* run, const espec_device_map* devices,
                                  espec_engine** out);
 void espec_engine_destroy(espec_engine* eng);
+
+/* Tensor-parallel wiring (tp_size > 1), before the first forward pass.
+ * One process holding all shards: espec_comm_link(engines in rank order).
+ * One process per GPU: every rank exports its 64-byte cudaIpcMemHandle_t,
+ * the caller all-gathers them (e.g. torch.distributed) and every rank
+ * imports the world * 64 bytes in rank order. */
+espec_status espec_comm_link(espec_engine** engines, int world);
+espec_status espec_comm_export(espec_engine* eng, void* handle64);
+espec_status espec_comm_import(espec_engine* eng, const void* handles, int world);
 const char* espec_last_error(const espec_engine* eng);
 /* Error text for a failed espec_engine_create (no engine exists yet). */
 const char* espec_create_error(void);

@@ -1,6 +1,7 @@
 // extern "C" boundary (include/espec_c.h) over the C++ engine.
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "../../include/espec_c.h"
 #include "engine.h"
@@ -99,11 +100,13 @@ espec_status espec_engine_create(const espec_model_cfg* base, const espec_model_
     if (!base || !draft || !run || !out) return ESPEC_CONFIG;
     *out = nullptr;
     try {
-        if (devices && (devices->tp_size > 1 || devices->n_lp_devices > 1))
-            throw Error(ST_CONFIG, "multi-device engines are not supported by this build");
+        if (devices && devices->n_lp_devices > 1)
+            throw Error(ST_CONFIG, "layer-parallel groups run tensor-parallel: use tp_size (one engine per GPU)");
+        const int tp = devices && devices->tp_size > 0 ? devices->tp_size : 1;
+        const int rank = devices ? devices->tp_rank : 0;
         auto e = new espec_engine();
         try {
-            e->impl = make_engine(to_model(base), to_model(draft), to_run(run), devices ? devices->device : 0);
+            e->impl = make_engine(to_model(base), to_model(draft), to_run(run), devices ? devices->device : 0, tp, rank);
         } catch (...) {
             delete e;
             throw;
@@ -121,6 +124,28 @@ espec_status espec_engine_create(const espec_model_cfg* base, const espec_model_
 }
 
 void espec_engine_destroy(espec_engine* eng) { delete eng; }
+
+espec_status espec_comm_link(espec_engine** engines, int world) {
+    if (!engines || world < 1) return ESPEC_CONFIG;
+    std::vector<Engine*> group;
+    for (int i = 0; i < world; ++i) {
+        if (!engines[i]) return ESPEC_CONFIG;
+        group.push_back(engines[i]->impl.get());
+    }
+    for (int i = 0; i < world; ++i) {
+        const espec_status st = guard(engines[i], [&] { engines[i]->impl->comm_link(group); });
+        if (st != ESPEC_OK) return st;
+    }
+    return ESPEC_OK;
+}
+
+espec_status espec_comm_export(espec_engine* eng, void* handle64) {
+    return guard(eng, [&] { eng->impl->comm_ipc_export(handle64); });
+}
+
+espec_status espec_comm_import(espec_engine* eng, const void* handles, int world) {
+    return guard(eng, [&] { eng->impl->comm_ipc_import(handles, world); });
+}
 const char* espec_last_error(const espec_engine* eng) { return eng ? eng->err.c_str() : g_create_error.c_str(); }
 const char* espec_create_error(void) { return g_create_error.c_str(); }
 

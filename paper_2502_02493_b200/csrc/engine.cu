@@ -2,11 +2,15 @@
 // proj/src/draft_engine.cpp, proj/src/kv_cache.cpp, proj/src/layer_plan.cpp,
 // proj/src/model.cpp (init_model order), proj/src/verifier.cpp (acceptance).
 #include <algorithm>
+#include <array>
+#include <initializer_list>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <sstream>
+#include <condition_variable>
+#include <mutex>
 
 #include "common.cuh"
 #include "engine.h"
@@ -198,20 +202,31 @@ struct LayerDev {
     float* gm = nullptr;
 };
 
+// One tensor-parallel shard of a model (Megatron split):
+// QKV / gate-up column-parallel (this rank's q heads, kv heads and MLP
+// columns), O / down row-parallel (partials all-reduced over NVLink), head
+// vocab-parallel; embedding and norm gains replicated. tp == 1 is the whole
+// model. Weight values depend only on the global (row, column), so any TP
+// degree runs the same model.
 struct ModelDev {
     ModelCfg c;
-    void* emb = nullptr;   // [V][d]
-    void* head = nullptr;  // [d][head_ld]
+    int tp = 1, rank = 0;
+    void* emb = nullptr;   // [V][d] (replicated)
+    void* head = nullptr;  // [d][head_ld]: this rank's vocabulary slice
     int head_ld = 0;
     float* fgain = nullptr;
     std::vector<LayerDev> L;
     std::vector<void*> owned;
-    int qkv_N() const { return (c.n_heads + 2 * c.n_kv_heads) * c.d_head; }
+    int qh() const { return c.n_heads / tp; }
+    int kvh() const { return c.n_kv_heads / tp; }
+    int f_loc() const { return c.d_mlp / tp; }
+    int V_loc() const { return c.vocab_size / tp; }
+    int qkv_N() const { return (qh() + 2 * kvh()) * c.d_head; }
     int qkv_ld() const { return ldpad(qkv_N(), c.weight_dtype); }
-    int gu_N() const { return 2 * c.d_mlp; }
+    int gu_N() const { return 2 * f_loc(); }
     int gu_ld() const { return ldpad(gu_N(), c.weight_dtype); }
-    int qdim() const { return c.n_heads * c.d_head; }
-    int kvdim() const { return c.n_kv_heads * c.d_head; }
+    int qdim() const { return qh() * c.d_head; }
+    int kvdim() const { return kvh() * c.d_head; }
     void* alloc(size_t bytes) {
         void* p = nullptr;
         CUDA_OK(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
@@ -220,8 +235,8 @@ struct ModelDev {
         return p;
     }
     void allocate(bool share_layers_from_base, const ModelDev* base) {
-        const int d = c.d_model, f = c.d_mlp, V = c.vocab_size, es = (int)dsize(c.weight_dtype);
-        head_ld = ldpad(V, c.weight_dtype);
+        const int d = c.d_model, f = f_loc(), V = c.vocab_size, es = (int)dsize(c.weight_dtype);
+        head_ld = ldpad(V_loc(), c.weight_dtype);
         if (share_layers_from_base) {
             emb = base->emb;
             head = base->head;
@@ -303,9 +318,9 @@ struct Cache {
 
     int total() const { return committed + (int)staged.size(); }
 
-    void create(const ModelCfg& c, int capacity_rows) {
+    void create(const ModelCfg& c, int kv_heads, int capacity_rows) {
         n_layers = c.n_layers;
-        n_kv = c.n_kv_heads;
+        n_kv = kv_heads;
         dh = c.d_head;
         dtype = c.kv_dtype;
         page_elems = (long long)n_layers * 2 * n_kv * page_rows * dh;
@@ -432,6 +447,43 @@ struct Staging {
 };
 
 // ---------------------------------------------------------------------------
+// single-device tensor-parallel harness: cross-stream ordering of the
+// collectives' push and combine kernels (see CommView::local_sync)
+// ---------------------------------------------------------------------------
+
+struct LocalGroup {
+    int world = 0;
+    std::mutex mu;
+    std::condition_variable cv;
+    std::vector<long long> calls;            // collectives each rank has reached
+    std::vector<std::array<cudaEvent_t, 2>> ev;  // per rank, per call parity
+    explicit LocalGroup(int w) : world(w), calls(w, 0), ev(w) {
+        for (auto& e : ev)
+            for (auto& x : e) cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
+    }
+    ~LocalGroup() {
+        for (auto& e : ev)
+            for (auto& x : e) cudaEventDestroy(x);
+    }
+};
+
+static void local_sync_fn(void* ctx, int rank, cudaStream_t s) {
+    LocalGroup* g = static_cast<LocalGroup*>(ctx);
+    std::unique_lock<std::mutex> lk(g->mu);
+    const long long k = g->calls[rank];
+    cudaEventRecord(g->ev[rank][k & 1], s);  // this rank's push is issued
+    g->calls[rank] = k + 1;
+    g->cv.notify_all();
+    g->cv.wait(lk, [&] {
+        for (long long c : g->calls)
+            if (c < k + 1) return false;
+        return true;
+    });
+    for (int p = 0; p < g->world; ++p)
+        if (p != rank) cudaStreamWaitEvent(s, g->ev[p][k & 1], 0);
+}
+
+// ---------------------------------------------------------------------------
 // engine
 // ---------------------------------------------------------------------------
 
@@ -457,17 +509,32 @@ struct Workspace {
     size_t attn_ws_slot = 0;
     unsigned* attn_tickets = nullptr;
     int attn_ticket_slot = 0;
+    // tensor parallelism
+    float* part = nullptr;      // [kChunk][d] row-parallel GEMV partial
+    float* best_val = nullptr;  // [kChunk] vocab-slice max per row
+    int* best_idx = nullptr;
+    float* lg_loc = nullptr;    // [kMaxNodes+1][head_ld] vocab-slice logits
     int G = 1;
 };
 
 class EngineImpl final : public Engine {
 public:
-    EngineImpl(const ModelCfg& bc, const ModelCfg& dc, const RunCfg& run, int device) : device_(device) {
+    EngineImpl(const ModelCfg& bc, const ModelCfg& dc, const RunCfg& run, int device, int tp, int rank)
+        : device_(device) {
         bc.validate();
         dc.validate();
         if (bc.vocab_size != dc.vocab_size) cfg_fail("base and draft models must share the vocabulary");
+        if (tp < 1 || tp > kMaxTp) cfg_fail("tp_size must lie in [1, 8]");
+        if (rank < 0 || rank >= tp) cfg_fail("tp_rank must lie in [0, tp_size)");
+        for (const ModelCfg* c : {&bc, &dc}) {
+            if (c->n_heads % tp || c->n_kv_heads % tp) cfg_fail("attention heads must divide by tp_size");
+            if (c->d_mlp % (16 * tp)) cfg_fail("d_mlp must be a multiple of 16 * tp_size");
+            if (c->vocab_size % tp) cfg_fail("vocab_size must divide by tp_size");
+        }
         base_.c = bc;
         draft_.c = dc;
+        base_.tp = draft_.tp = tp;
+        base_.rank = draft_.rank = rank;
         set_run(run);
         CUDA_OK(cudaSetDevice(device));
         if (const char* e = std::getenv("ESPEC_PDL")) set_pdl(std::atoi(e) != 0);
@@ -475,8 +542,24 @@ public:
         for (auto& e : ev_) CUDA_OK(cudaEventCreate(&e));
         const int cap_b = bc.max_positions + kMaxNodes + kChunk;
         const int cap_d = dc.max_positions + kMaxNodes + kChunk;
-        bcache_.create(bc, cap_b);
-        dcache_.create(dc, cap_d);
+        bcache_.create(bc, base_.kvh(), cap_b);
+        dcache_.create(dc, draft_.kvh(), cap_d);
+        if (tp > 1) {
+            // symmetric receive region for the NVLink collectives: sized for a
+            // prefill chunk of hidden rows or the gathered verify logits
+            const int dmax = std::max(bc.d_model, dc.d_model);
+            comm_.rank = rank;
+            comm_.world = tp;
+            comm_.debug = std::getenv("ESPEC_TRACE_COMM") ? 1 : 0;
+            comm_.slot_floats = std::max<size_t>((size_t)kChunk * dmax, (size_t)(kMaxNodes + 1) * (bc.vocab_size / tp));
+            const size_t bytes = sizeof(float) * comm_.slot_floats * 2 * tp + sizeof(uint64_t) * 2 * tp;
+            CUDA_OK(cudaMalloc(&comm_mem_, bytes));
+            CUDA_OK(cudaMemset(comm_mem_, 0, bytes));
+            comm_.recv_local = reinterpret_cast<float*>(comm_mem_);
+            comm_.flags_local = reinterpret_cast<uint64_t*>(comm_.recv_local + comm_.slot_floats * 2 * tp);
+            CUDA_OK(cudaMalloc(&comm_.ticket, sizeof(unsigned)));
+            CUDA_OK(cudaMemset(comm_.ticket, 0, sizeof(unsigned)));
+        }
         staging_.create(8 << 20);
         staging_.h2d_counter = &h2d_bytes_;
         for (auto& e : site_ev_) CUDA_OK(cudaEventCreate(&e));
@@ -522,6 +605,9 @@ public:
         cudaFree(target_);
         cudaFree(unif_dev_);
         cudaFreeHost(unif_host_);
+        for (void* p : ipc_opened_) cudaIpcCloseMemHandle(p);
+        if (comm_mem_) cudaFree(comm_mem_);
+        if (comm_.ticket) cudaFree(comm_.ticket);
         for (auto& e : ev_) cudaEventDestroy(e);
         for (auto& e : site_ev_) cudaEventDestroy(e);
         cudaStreamDestroy(stream_);
@@ -622,32 +708,66 @@ public:
             }
             return;
         }
-        // Perf mode: same std rules, drawn on device from a counter hash
-        // (logical layout first, padding columns zeroed, then packed).
+        // Perf mode: same std rules, drawn on device from a counter hash of
+        // the GLOBAL (row, column), so a TP shard holds exactly its slice of
+        // the one model (logical layout first, padding zeroed, then packed).
         const int dt = c.weight_dtype;
         uint64_t k = seed * 1000003ULL + 17;
-        const int qd = M.qdim();
-        launch_fill_normal(dt, M.emb, (long long)V * d, emb_sd, k++, stream_);
+        const int H = c.n_heads, Hkv = c.n_kv_heads, dh = c.d_head, r = M.rank;
+        const int qh = M.qh(), kvh = M.kvh(), fl = M.f_loc(), Vl = M.V_loc();
+        auto seg = [](std::initializer_list<std::array<int, 3>> ss) {
+            ColMap m;
+            for (auto& x : ss) {
+                m.lc0[m.nseg] = x[0];
+                m.gc0[m.nseg] = x[1];
+                m.len[m.nseg] = x[2];
+                ++m.nseg;
+            }
+            return m;
+        };
+        launch_fill_normal(dt, M.emb, (long long)V * d, emb_sd, k++, stream_);  // replicated
         launch_fill_const(DT_F32, M.fgain, d, 1.f, stream_);
         if (c.tied_head) {
             void* t = temp((size_t)d * M.head_ld * dsize(dt));
             CUDA_OK(cudaMemsetAsync(t, 0, (size_t)d * M.head_ld * dsize(dt), stream_));
-            launch_transpose(dt, M.emb, V, d, t, M.head_ld, stream_);
+            launch_transpose(dt, (const char*)M.emb + (size_t)r * Vl * d * dsize(dt), Vl, d, t, M.head_ld, stream_);
             finish_logical(M.head, dt, d, M.head_ld, t);
         } else {
-            mat_fill(M.head, dt, d, M.head_ld, V, emb_sd, k++, [](int) { return true; });
+            ColMap m = seg({{0, r * Vl, Vl}});
+            m.seed = k++;
+            mat_fill_map(M.head, dt, d, M.head_ld, m, 0, V, emb_sd);
         }
         for (int l = 0; l < c.n_layers; ++l) {
             LayerDev& L = M.L[l];
-            mat_fill(L.wqkv, dt, d, M.qkv_ld(), M.qkv_N(), proj_sd, k++, [](int) { return true; });
-            mat_fill(L.wo, dt, qd, d, d, proj_sd * resid, k++, [](int) { return true; });
-            mat_fill(L.wgu, dt, d, M.gu_ld(), M.gu_N(), proj_sd, k++, [](int) { return true; });
-            mat_fill(L.wd, dt, f, d, d, down_sd, k++, [](int) { return true; });
+            ColMap mq = seg({{0, r * qh * dh, qh * dh},
+                             {qh * dh, H * dh + r * kvh * dh, kvh * dh},
+                             {(qh + kvh) * dh, (H + Hkv) * dh + r * kvh * dh, kvh * dh}});
+            mq.seed = k++;
+            mat_fill_map(L.wqkv, dt, d, M.qkv_ld(), mq, 0, (long long)(H + 2 * Hkv) * dh, proj_sd);
+            ColMap mo = seg({{0, 0, d}});
+            mo.seed = k++;
+            mat_fill_map(L.wo, dt, qh * dh, d, mo, r * qh * dh, d, proj_sd * resid);
+            ColMap mg;
+            mg.gateup = 1;
+            mg.f_loc = fl;
+            mg.f_base = r * fl;
+            mg.seed = k++;
+            mg.seed2 = k++;
+            mat_fill_map(L.wgu, dt, d, M.gu_ld(), mg, 0, f, proj_sd);
+            ColMap md = seg({{0, 0, d}});
+            md.seed = k++;
+            mat_fill_map(L.wd, dt, fl, d, md, r * fl, d, down_sd);
             launch_fill_const(DT_F32, L.ga, d, 1.f, stream_);
             launch_fill_const(DT_F32, L.gm, d, 1.f, stream_);
         }
         CUDA_OK(cudaStreamSynchronize(stream_));
         CUDA_OK(cudaGetLastError());
+    }
+
+    void mat_fill_map(void* W, int dt, int K, int ld, const ColMap& m, int row_off, long long n_full, float sd) {
+        void* t = temp((size_t)K * ld * dsize(dt));
+        launch_fill_normal_map(dt, t, K, ld, m, row_off, n_full, sd, stream_);
+        finish_logical(W, dt, K, ld, t);
     }
 
     // ---- weight matrices: fp32 row-major, or bf16 packed in mma fragment order
@@ -696,31 +816,42 @@ public:
         download_block(t, dt, ld, col0, dst, K, cols);
     }
 
+    // Full reference-layout tensors in; this shard keeps its slice
+    // (column-parallel: wq/wk/wv/w_gate/w_up/head; row-parallel: wo/w_down).
     void load_tensor(int which, const std::string& name, int layer, const float* data, long long rows,
                      long long cols) override {
         ModelDev& M = which ? base_ : draft_;
         ensure_allocated(which);
         const ModelCfg& c = M.c;
         const int d = c.d_model, f = c.d_mlp, V = c.vocab_size, dt = c.weight_dtype;
-        auto expect = [&](long long r, long long cc) {
-            if (rows != r || cols != cc)
-                throw Error(ST_SHAPE, "tensor " + name + " expects " + std::to_string(r) + "x" + std::to_string(cc));
+        const int r = M.rank, fl = M.f_loc(), Vl = M.V_loc();
+        auto expect = [&](long long rr, long long cc) {
+            if (rows != rr || cols != cc)
+                throw Error(ST_SHAPE, "tensor " + name + " expects " + std::to_string(rr) + "x" + std::to_string(cc));
+        };
+        // columns [c0, c0+n) of a rows x cols host matrix
+        auto cslice = [&](long long c0, long long n) {
+            std::vector<float> o((size_t)rows * n);
+            for (long long i = 0; i < rows; ++i)
+                std::memcpy(o.data() + i * n, data + i * cols + c0, sizeof(float) * n);
+            return o;
         };
         if (name == "embedding") {
             expect(V, d);
             upload_block(M.emb, dt, d, 0, data, V, d, stream_);
             if (c.tied_head) {
-                std::vector<float> t((size_t)d * V);
-                for (int v = 0; v < V; ++v)
-                    for (int j = 0; j < d; ++j) t[(size_t)j * V + v] = data[(size_t)v * d + j];
-                mat_write(M.head, dt, d, M.head_ld, 0, t.data(), V);
+                std::vector<float> t((size_t)d * Vl);
+                for (int v = 0; v < Vl; ++v)
+                    for (int j = 0; j < d; ++j) t[(size_t)j * Vl + v] = data[(size_t)(r * Vl + v) * d + j];
+                mat_write(M.head, dt, d, M.head_ld, 0, t.data(), Vl);
             }
             return;
         }
         if (name == "head") {
             if (c.tied_head) throw Error(ST_CONFIG, "model has a tied head");
             expect(d, V);
-            mat_write(M.head, dt, d, M.head_ld, 0, data, V);
+            const auto sl = cslice((long long)r * Vl, Vl);
+            mat_write(M.head, dt, d, M.head_ld, 0, sl.data(), Vl);
             return;
         }
         if (name == "final_norm_gain") {
@@ -731,21 +862,36 @@ public:
         if (layer < 0 || layer >= c.n_layers) throw Error(ST_SHAPE, "layer index out of range");
         LayerDev& L = M.L[layer];
         const int qd = M.qdim(), kd = M.kvdim();
-        if (name == "wq") { expect(d, qd); mat_write(L.wqkv, dt, d, M.qkv_ld(), 0, data, qd); }
-        else if (name == "wk") { expect(d, kd); mat_write(L.wqkv, dt, d, M.qkv_ld(), qd, data, kd); }
-        else if (name == "wv") { expect(d, kd); mat_write(L.wqkv, dt, d, M.qkv_ld(), qd + kd, data, kd); }
-        else if (name == "wo") { expect(qd, d); mat_write(L.wo, dt, qd, d, 0, data, d); }
-        else if (name == "w_down") { expect(f, d); mat_write(L.wd, dt, f, d, 0, data, d); }
-        else if (name == "w_gate" || name == "w_up") {
-            // interleave per 32 packed columns: [gate16 | up16]
+        const int qd_full = c.n_heads * c.d_head, kd_full = c.n_kv_heads * c.d_head;
+        if (name == "wq") {
+            expect(d, qd_full);
+            const auto sl = cslice((long long)r * qd, qd);
+            mat_write(L.wqkv, dt, d, M.qkv_ld(), 0, sl.data(), qd);
+        } else if (name == "wk") {
+            expect(d, kd_full);
+            const auto sl = cslice((long long)r * kd, kd);
+            mat_write(L.wqkv, dt, d, M.qkv_ld(), qd, sl.data(), kd);
+        } else if (name == "wv") {
+            expect(d, kd_full);
+            const auto sl = cslice((long long)r * kd, kd);
+            mat_write(L.wqkv, dt, d, M.qkv_ld(), qd + kd, sl.data(), kd);
+        } else if (name == "wo") {
+            expect(qd_full, d);
+            mat_write(L.wo, dt, qd, d, 0, data + (size_t)r * qd * d, d);
+        } else if (name == "w_down") {
+            expect(f, d);
+            mat_write(L.wd, dt, fl, d, 0, data + (size_t)r * fl * d, d);
+        } else if (name == "w_gate" || name == "w_up") {
+            // this shard's columns, interleaved per 32 packed columns: [gate16 | up16]
             expect(d, f);
             const int half = name == "w_up" ? 16 : 0;
-            std::vector<float> blk((size_t)d * 16);
-            for (int t = 0; t < f / 16; ++t) {
-                for (int r = 0; r < d; ++r)
-                    for (int j = 0; j < 16; ++j) blk[(size_t)r * 16 + j] = data[(size_t)r * f + t * 16 + j];
-                mat_write(L.wgu, dt, d, M.gu_ld(), t * 32 + half, blk.data(), 16);
-            }
+            std::vector<float> cur((size_t)d * M.gu_N());
+            mat_read(L.wgu, dt, d, M.gu_ld(), 0, cur.data(), M.gu_N());
+            for (int t = 0; t < fl / 16; ++t)
+                for (int i = 0; i < d; ++i)
+                    for (int j = 0; j < 16; ++j)
+                        cur[(size_t)i * M.gu_N() + t * 32 + half + j] = data[(size_t)i * f + r * fl + t * 16 + j];
+            mat_write(L.wgu, dt, d, M.gu_ld(), 0, cur.data(), M.gu_N());
         } else if (name == "attn_norm_gain") {
             expect(1, d);
             CUDA_OK(cudaMemcpy(L.ga, data, sizeof(float) * d, cudaMemcpyHostToDevice));
@@ -759,6 +905,7 @@ public:
 
     void weight(int which, const std::string& name, int layer, float* out, long long rows, long long cols) override {
         ModelDev& M = which ? base_ : draft_;
+        if (M.tp != 1) throw Error(ST_CONFIG, "reading weights back needs tp_size 1");
         const ModelCfg& c = M.c;
         const int d = c.d_model, f = c.d_mlp, dt = c.weight_dtype;
         if (name == "embedding") return download_block(M.emb, dt, d, 0, out, rows, cols);
@@ -796,9 +943,9 @@ public:
 
     void alloc_ws(Workspace& W, const ModelDev& M, int G) {
         const ModelCfg& c = M.c;
-        const int d = c.d_model, qd = c.n_heads * c.d_head, f = c.d_mlp;
+        const int d = c.d_model, qd = M.qdim(), f = M.f_loc(), Vl = M.V_loc();
         const int tiles = (d + kStatTile - 1) / kStatTile;
-        const int head_ld = ldpad(c.vocab_size, c.weight_dtype);
+        const int head_ld = M.head_ld ? M.head_ld : ldpad(Vl, c.weight_dtype);
         W.G = G;
         W.h = (float*)wsalloc(sizeof(float) * kChunk * d);
         W.stats = (float*)wsalloc(sizeof(float) * kChunk * tiles);
@@ -806,15 +953,20 @@ public:
         W.mixed = (float*)wsalloc(sizeof(float) * (size_t)G * kChunk * qd);
         W.attn = (float*)wsalloc(sizeof(float) * (size_t)G * kChunk * d);
         W.act = (float*)wsalloc(sizeof(float) * (size_t)kChunk * f);
-        W.logits = (float*)wsalloc(sizeof(float) * 8 * (size_t)head_ld);
+        W.logits = (float*)wsalloc(sizeof(float) * 8 * (size_t)ldpad(c.vocab_size, c.weight_dtype));
         const int dt = c.weight_dtype;
-        const int head_tiles = gemv_col_tiles(d, c.vocab_size, dt);
+        const int head_tiles = gemv_col_tiles(d, Vl, dt);
         W.am_val = (float*)wsalloc(sizeof(float) * kChunk * head_tiles);
         W.am_idx = (int*)wsalloc(sizeof(int) * kChunk * head_tiles);
-        const int qkv_N = (c.n_heads + 2 * c.n_kv_heads) * c.d_head;
+        if (M.tp > 1) {
+            W.part = (float*)wsalloc(sizeof(float) * kChunk * d);
+            W.best_val = (float*)wsalloc(sizeof(float) * kChunk);
+            W.best_idx = (int*)wsalloc(sizeof(int) * kChunk);
+            W.lg_loc = (float*)wsalloc(sizeof(float) * (size_t)(kMaxNodes + 1) * head_ld);
+        }
         size_t part = 0;
         int tick = 0;
-        const int shapes[5][2] = {{d, qkv_N}, {qd, d}, {d, 2 * f}, {f, d}, {d, c.vocab_size}};
+        const int shapes[5][2] = {{d, M.qkv_N()}, {qd, d}, {d, 2 * f}, {f, d}, {d, Vl}};
         for (auto& s : shapes) {
             part = std::max(part, gemv_partial_floats(s[0], s[1], dt));
             tick = std::max(tick, gemv_col_tiles(s[0], s[1], dt) + 1);
@@ -824,8 +976,8 @@ public:
         W.gemv_part = (float*)wsalloc(sizeof(float) * part * kMaxProblems);
         W.gemv_tickets = (unsigned*)wsalloc(sizeof(unsigned) * (size_t)tick * kMaxProblems);
         const int cap = c.max_positions + kMaxNodes + kChunk;
-        W.attn_ws_slot = attn_ws_floats(kAttnQ, c.n_heads, c.d_head, cap);
-        W.attn_ticket_slot = (int)attn_tickets(kAttnQ, c.n_heads, c.n_kv_heads);
+        W.attn_ws_slot = attn_ws_floats(kAttnQ, M.qh(), c.d_head, cap);
+        W.attn_ticket_slot = (int)attn_tickets(kAttnQ, M.qh(), M.kvh());
         W.attn_ws = (float*)wsalloc(sizeof(float) * W.attn_ws_slot * G);
         W.attn_tickets = (unsigned*)wsalloc(sizeof(unsigned) * (size_t)W.attn_ticket_slot * G);
     }
@@ -946,12 +1098,42 @@ public:
     }
 
     // forward_sequential / forward_fuzzy (proj/src/draft_engine.cpp:35-133)
+    // Row-parallel projection + residual: h = h + x.W (+ row stats). One GPU:
+    // the GEMV's RESID epilogue. Tensor parallel: the GEMV stores this rank's
+    // partial, the NVLink all-reduce sums partials in rank order and applies
+    // the residual + stats.
+    void row_parallel_resid(ModelDev& M, Workspace& W, void* Wm, int K, const float* x, int ldx, int kind, int T,
+                            const Pass& ps, const KvView& kv) {
+        const int d = M.c.d_model, tiles = (d + kStatTile - 1) / kStatTile, wdt = M.c.weight_dtype;
+        GemvBatch b;
+        GemvProblem p = gp(W, 0);
+        p.W = Wm; p.K = K; p.N = d; p.ldw = d; p.x = x; p.ldx = ldx;
+        if (!tp()) {
+            p.out = W.h; p.ldo = d; p.resid = W.h; p.ldr = d; p.stats_out = W.stats; p.stat_tiles_out = tiles;
+            b.p[0] = p;
+            site(M, kind, gemv_bytes(M, K, d, d, T, 1), [&] { launch_gemv(EPI_RESID, wdt, b, 1, T, ps.view, kv, stream_); });
+            launches_ += chunks(M, T);
+            return;
+        }
+        p.out = W.part; p.ldo = d;
+        b.p[0] = p;
+        site(M, kind, gemv_bytes(M, K, d, d, T, 1), [&] { launch_gemv(EPI_STORE, wdt, b, 1, T, ps.view, kv, stream_); });
+        launches_ += chunks(M, T);
+        AllreduceArgs a;
+        a.rows = T; a.d = d; a.src = W.part; a.ld_src = d; a.mode = AR_RESID;
+        a.out = W.h; a.ldo = d; a.resid = W.h; a.ldr = d; a.stats = W.stats; a.stat_tiles = tiles;
+        launch_allreduce_rows(comm_, a, stream_);
+        ++launches_;
+    }
+
+    // forward_sequential / forward_fuzzy (proj/src/draft_engine.cpp:35-133)
     void forward(ModelDev& M, Cache& C, Workspace& W, const LayerPlan* plan, const Pass& ps) {
         const ModelCfg& c = M.c;
-        const int d = c.d_model, T = ps.T, qd = M.qdim(), f = c.d_mlp;
+        const int d = c.d_model, T = ps.T, qd = M.qdim(), f = M.f_loc();
         const int tiles = (d + kStatTile - 1) / kStatTile;
         const int wdt = c.weight_dtype;
         const KvView kv = C.view();
+        check_comm();
         launch_embed(wdt, M.emb, d, arena_, ps.tok_idx, T, W.h, W.stats, stream_);
         ++launches_;
         std::vector<std::vector<int>> groups;
@@ -968,7 +1150,7 @@ public:
                 p.W = L.wqkv; p.K = d; p.N = M.qkv_N(); p.ldw = M.qkv_ld();
                 p.x = W.h; p.ldx = d; p.gain = L.ga; p.stats_in = W.stats; p.stat_tiles_in = tiles; p.eps = c.norm_eps;
                 p.out = W.q + (size_t)i * kChunk * qd; p.ldo = qd;
-                p.n_heads = c.n_heads; p.n_kv = c.n_kv_heads; p.dh = c.d_head; p.layer = g[i]; p.rope_theta = c.rope_theta;
+                p.n_heads = M.qh(); p.n_kv = M.kvh(); p.dh = c.d_head; p.layer = g[i]; p.rope_theta = c.rope_theta;
                 qb.p[i] = p;
             }
             site(M, 0, gemv_bytes(M, d, M.qkv_ld(), M.qkv_N(), T, n),
@@ -976,14 +1158,7 @@ public:
             launches_ += chunks(M, T);
             attention(M, C, W, g, ps);
             if (n == 1) {
-                const LayerDev& L = M.L[g[0]];
-                GemvBatch ob;
-                GemvProblem p = gp(W, 0);
-                p.W = L.wo; p.K = qd; p.N = d; p.ldw = d; p.x = W.mixed; p.ldx = qd;
-                p.out = W.h; p.ldo = d; p.resid = W.h; p.ldr = d; p.stats_out = W.stats; p.stat_tiles_out = tiles;
-                ob.p[0] = p;
-                site(M, 2, gemv_bytes(M, qd, d, d, T, 1), [&] { launch_gemv(EPI_RESID, wdt, ob, 1, T, ps.view, kv, stream_); });
-                launches_ += chunks(M, T);
+                row_parallel_resid(M, W, M.L[g[0]].wo, qd, W.mixed, qd, 2, T, ps, kv);
             } else {
                 GemvBatch ob;
                 for (int i = 0; i < n; ++i) {
@@ -995,6 +1170,19 @@ public:
                 }
                 site(M, 2, gemv_bytes(M, qd, d, d, T, n), [&] { launch_gemv(EPI_STORE, wdt, ob, n, T, ps.view, kv, stream_); });
                 launches_ += chunks(M, T);
+                if (tp()) {
+                    // ONE all-reduce for the whole group's attention outputs
+                    const int per = (size_t)n * T * d <= comm_.slot_floats ? n : 1;
+                    for (int i0 = 0; i0 < n; i0 += per) {
+                        AllreduceArgs a;
+                        a.rows = per * T; a.d = d; a.mode = AR_STORE;
+                        a.src = W.attn + (size_t)i0 * kChunk * d; a.ld_src = d;
+                        a.out = W.attn + (size_t)i0 * kChunk * d; a.ldo = d;
+                        a.rows_per_block = T; a.block_stride = (size_t)kChunk * d;
+                        launch_allreduce_rows(comm_, a, stream_);
+                        ++launches_;
+                    }
+                }
             }
             // residual / MLP chain stays sequential (proj/src/draft_engine.cpp:112-130)
             for (int i = 0; i < n; ++i) {
@@ -1011,13 +1199,8 @@ public:
                 ub.p[0] = p;
                 site(M, 3, gemv_bytes(M, d, M.gu_ld(), 2 * f, T, 1),
                      [&] { launch_gemv(EPI_SILU, wdt, ub, 1, T, ps.view, kv, stream_); });
-                GemvBatch db;
-                GemvProblem q = gp(W, 0);
-                q.W = L.wd; q.K = f; q.N = d; q.ldw = d; q.x = W.act; q.ldx = f;
-                q.out = W.h; q.ldo = d; q.resid = W.h; q.ldr = d; q.stats_out = W.stats; q.stat_tiles_out = tiles;
-                db.p[0] = q;
-                site(M, 4, gemv_bytes(M, f, d, d, T, 1), [&] { launch_gemv(EPI_RESID, wdt, db, 1, T, ps.view, kv, stream_); });
-                launches_ += 2 * chunks(M, T);
+                launches_ += chunks(M, T);
+                row_parallel_resid(M, W, L.wd, f, W.act, f, 4, T, ps, kv);
             }
         }
     }
@@ -1041,28 +1224,47 @@ public:
                 ab.p[i] = a;
             }
             const double kvb = (double)g.size() * 2.0 * ps.view.total * M.kvdim() * dsize(M.c.kv_dtype);
-            site(M, 1, kvb, [&] { launch_attention(ab, (int)g.size(), M.c.n_heads, v, kv, stream_); });
+            site(M, 1, kvb, [&] { launch_attention(ab, (int)g.size(), M.qh(), v, kv, stream_); });
             ++launches_;
         }
     }
 
     // final norm + head over n rows starting at row r0 -> argmax token ids
     // (lm_logits proj/src/model.cpp:212-215, argmax proj/src/matrix.cpp:196-202)
-    void head(ModelDev& M, Workspace& W, int r0, int n, int* tok_out, float* logits) {
+    void head(ModelDev& M, Workspace& W, int r0, int n, int* tok_out, float* logits, int ld_logits = 0) {
         const ModelCfg& c = M.c;
-        const int d = c.d_model, tiles = (d + kStatTile - 1) / kStatTile;
+        const int d = c.d_model, tiles = (d + kStatTile - 1) / kStatTile, Vl = M.V_loc();
+        if (ld_logits == 0) ld_logits = logits_ld_;
         GemvBatch hb;
         GemvProblem p = gp(W, 0);
-        p.W = M.head; p.K = d; p.N = c.vocab_size; p.ldw = M.head_ld;
+        p.W = M.head; p.K = d; p.N = Vl; p.ldw = M.head_ld;
         p.x = W.h + (size_t)r0 * d; p.ldx = d; p.gain = M.fgain; p.stats_in = W.stats + (size_t)r0 * tiles;
         p.stat_tiles_in = tiles; p.eps = c.norm_eps;
-        p.vocab = c.vocab_size; p.logits = logits; p.ld_logits = M.head_ld;
-        p.am_val = W.am_val; p.am_idx = W.am_idx; p.tok_out = tok_out;
+        p.vocab = Vl;
+        p.am_val = W.am_val; p.am_idx = W.am_idx;
+        if (!tp()) {
+            p.logits = logits; p.ld_logits = ld_logits; p.tok_out = tok_out;
+        } else {
+            // vocab-parallel: this rank's slice, then a (max, argmax) gather
+            // and, when logits are wanted, a column all-gather over NVLink
+            p.logits = logits ? W.lg_loc : nullptr; p.ld_logits = M.head_ld;
+            p.tok_out = W.best_idx; p.tok_val = W.best_val; p.col_base = M.rank * Vl;
+        }
         hb.p[0] = p;
         PassView none;
-        site(M, 5, gemv_bytes(M, d, M.head_ld, c.vocab_size, n, 1),
+        site(M, 5, gemv_bytes(M, d, M.head_ld, Vl, n, 1),
              [&] { launch_gemv(EPI_ARGMAX, c.weight_dtype, hb, 1, n, none, KvView(), stream_); });
         launches_ += chunks(M, n);
+        if (tp()) {
+            launch_allgather_argmax(comm_, n, W.best_val, W.best_idx, tok_out, stream_);
+            ++launches_;
+            if (logits) {
+                GatherColsArgs g;
+                g.rows = n; g.cols = Vl; g.src = W.lg_loc; g.ld_src = M.head_ld; g.dst = logits; g.ld_dst = ld_logits;
+                launch_allgather_cols(comm_, g, stream_);
+                ++launches_;
+            }
+        }
     }
 
     // Stage the committed tokens a cache is missing as a chain and run it,
@@ -1520,9 +1722,10 @@ public:
         if (hidden) CUDA_OK(cudaMemcpyAsync(hidden, W.h, sizeof(float) * n * d, cudaMemcpyDeviceToHost, stream_));
         for (int r0 = 0; r0 < n; r0 += 8) {
             const int k = std::min(8, n - r0);
-            head(M, W, r0, k, arena_ + out_off_, W.logits);
+            head(M, W, r0, k, arena_ + out_off_, W.logits, ldpad(M.c.vocab_size, M.c.weight_dtype));
             if (logits)
-                CUDA_OK(cudaMemcpy2DAsync(logits + (size_t)r0 * V, sizeof(float) * V, W.logits, sizeof(float) * M.head_ld,
+                CUDA_OK(cudaMemcpy2DAsync(logits + (size_t)r0 * V, sizeof(float) * V, W.logits,
+                                          sizeof(float) * ldpad(M.c.vocab_size, M.c.weight_dtype),
                                           sizeof(float) * V, k, cudaMemcpyDeviceToHost, stream_));
         }
         std::vector<int> a, b;
@@ -1564,6 +1767,57 @@ public:
         return (long long)(t - f);
     }
     int kernel_launches() const override { return launches_; }
+
+    // ---------------- tensor-parallel wiring ----------------
+    int tp_size() const override { return comm_.world; }
+    void* comm_region() override { return comm_mem_; }
+    void set_peer(int p, void* region) {
+        comm_.peer_recv[p] = reinterpret_cast<float*>(region);
+        comm_.peer_flags[p] = reinterpret_cast<uint64_t*>(comm_.peer_recv[p] + comm_.slot_floats * 2 * comm_.world);
+    }
+    void comm_link(const std::vector<Engine*>& group) override {
+        if ((int)group.size() != comm_.world) cfg_fail("tensor-parallel group size does not match tp_size");
+        for (int p = 0; p < comm_.world; ++p) {
+            if (group[p]->tp_size() != comm_.world) cfg_fail("tensor-parallel group members disagree on tp_size");
+            set_peer(p, group[p]->comm_region());
+        }
+        // shards share one GPU: no early PDL trigger, event-ordered phases
+        comm_.early_trigger = 0;
+        auto* lead = static_cast<EngineImpl*>(group[0]);
+        if (!lead->local_group_) lead->local_group_ = std::make_shared<LocalGroup>(comm_.world);
+        local_group_ = lead->local_group_;
+        comm_.local_sync = &local_sync_fn;
+        comm_.local_ctx = local_group_.get();
+    }
+    void comm_ipc_export(void* handle64) override {
+        if (!comm_mem_) cfg_fail("tp_size is 1: nothing to export");
+        cudaIpcMemHandle_t h;
+        CUDA_OK(cudaSetDevice(device_));
+        CUDA_OK(cudaIpcGetMemHandle(&h, comm_mem_));
+        std::memcpy(handle64, &h, sizeof(h));
+    }
+    void comm_ipc_import(const void* handles, int world) override {
+        if (world != comm_.world) cfg_fail("tensor-parallel group size does not match tp_size");
+        CUDA_OK(cudaSetDevice(device_));
+        for (int p = 0; p < world; ++p) {
+            if (p == comm_.rank) {
+                set_peer(p, comm_mem_);
+                continue;
+            }
+            cudaIpcMemHandle_t h;
+            std::memcpy(&h, (const char*)handles + 64 * p, sizeof(h));
+            void* ptr = nullptr;
+            CUDA_OK(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+            ipc_opened_.push_back(ptr);
+            set_peer(p, ptr);
+        }
+    }
+    bool tp() const { return comm_.world > 1; }
+    void check_comm() const {
+        if (tp())
+            for (int p = 0; p < comm_.world; ++p)
+                if (!comm_.peer_recv[p]) throw Error(ST_NCCL, "tensor-parallel group not linked (comm_link / ipc import)");
+    }
     void reset_launch_count() override { launches_ = 0; }
 
 private:
@@ -1590,6 +1844,11 @@ private:
     double* unif_dev_ = nullptr;
     double* unif_host_ = nullptr;
     Xoshiro rng_{1};
+    // tensor parallelism
+    CommView comm_;
+    std::shared_ptr<LocalGroup> local_group_;
+    void* comm_mem_ = nullptr;
+    std::vector<void*> ipc_opened_;
     void* temp_ = nullptr;
     size_t temp_bytes_ = 0;
     RunCfg run_;
@@ -1606,8 +1865,9 @@ private:
     long long h2d_bytes_ = 0, d2h_bytes_ = 0;
 };
 
-std::unique_ptr<Engine> make_engine(const ModelCfg& base, const ModelCfg& draft, const RunCfg& run, int device) {
-    return std::unique_ptr<Engine>(new EngineImpl(base, draft, run, device));
+std::unique_ptr<Engine> make_engine(const ModelCfg& base, const ModelCfg& draft, const RunCfg& run, int device,
+                                    int tp, int rank) {
+    return std::unique_ptr<Engine>(new EngineImpl(base, draft, run, device, tp, rank));
 }
 
 }  // namespace espec

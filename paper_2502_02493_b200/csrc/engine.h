@@ -77,7 +77,11 @@ struct IterationTrace {
 };
 
 class Engine;
-std::unique_ptr<Engine> make_engine(const ModelCfg& base, const ModelCfg& draft, const RunCfg& run, int device);
+// tp > 1: this engine is shard `rank` of a tensor-parallel group (one per
+// GPU); link the group with comm_link (one process) or comm_ipc_* (one
+// process per GPU) before loading weights' first use.
+std::unique_ptr<Engine> make_engine(const ModelCfg& base, const ModelCfg& draft, const RunCfg& run, int device,
+                                    int tp = 1, int rank = 0);
 
 class Engine {
 public:
@@ -110,6 +114,16 @@ public:
     virtual void time_site(int which, int kind) = 0;  // which < 0 disables
     virtual void site_stats(int* count, double* total_ms, double* bytes_per_launch) = 0;
     virtual void io_bytes(long long* h2d, long long* d2h) const = 0;
+    // ---- tensor-parallel group wiring (tp > 1)
+    virtual int tp_size() const = 0;
+    // one process: give every shard the others' receive regions
+    virtual void comm_link(const std::vector<Engine*>& group) = 0;
+    // one process per GPU: export this rank's cudaIpcMemHandle_t (64 bytes),
+    // then import all ranks' handles in rank order
+    virtual void comm_ipc_export(void* handle64) = 0;
+    virtual void comm_ipc_import(const void* handles, int world) = 0;
+    // device pointer of this shard's receive region (comm_link)
+    virtual void* comm_region() = 0;
 };
 
 }  // namespace espec

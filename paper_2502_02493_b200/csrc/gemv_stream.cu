@@ -286,7 +286,10 @@ __device__ __forceinline__ void sg_epilogue(const SgLaunch& L, const GemvProblem
                         fi = oi;
                     }
                 }
-                if (lane == 0) P.tok_out[t0 + t] = fi;
+                if (lane == 0) {
+                    P.tok_out[t0 + t] = fi + P.col_base;
+                    if (P.tok_val) P.tok_val[t0 + t] = fv;
+                }
             }
         }
     }

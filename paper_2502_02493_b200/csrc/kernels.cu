@@ -332,7 +332,8 @@ __global__ void __launch_bounds__(kThreads) gemv_f32_kernel(const __grid_constan
                 const int oi = __ldcg(&P.am_idx[(t0 + tid) * L.tiles + tl]);
                 if (am_better(ov, oi, v, ix)) { v = ov; ix = oi; }
             }
-            P.tok_out[t0 + tid] = ix;
+            P.tok_out[t0 + tid] = ix + P.col_base;
+            if (P.tok_val) P.tok_val[t0 + tid] = v;
         }
     }
 }
@@ -1149,6 +1150,49 @@ void launch_fill_normal(int dtype, void* dst, long long n, float sd, uint64_t se
     const int blocks = 148 * 8;
     if (dtype == DT_BF16) fill_normal_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<__nv_bfloat16*>(dst), n, sd, seed);
     else fill_normal_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<float*>(dst), n, sd, seed);
+}
+
+// Sharded N(0, sd) fill: element (k, c) of this rank's K x ld block takes
+// the value of global element (k + row_off, gcol(c)) of the full logical
+// matrix (K_full x N_full), so every TP degree holds slices of one model.
+template <typename T>
+__global__ void fill_normal_map_kernel(T* dst, int K, int ld, ColMap m, int row_off, long long n_full, float sd) {
+    const long long total = (long long)K * ld;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+        const int k = (int)(i / ld), c = (int)(i - (long long)k * ld);
+        long long g = -1;
+        uint64_t seed = m.seed;
+        if (m.gateup) {
+            // packed [gate16 | up16] per 32 local columns
+            const int j = (c >> 5) * 16 + (c & 15);
+            if (j < m.f_loc) {
+                g = (long long)m.f_base + j;
+                if (c & 16) seed = m.seed2;
+            }
+        } else {
+            for (int q = 0; q < m.nseg; ++q)
+                if (c >= m.lc0[q] && c < m.lc0[q] + m.len[q]) g = m.gc0[q] + (c - m.lc0[q]);
+        }
+        float v = 0.f;
+        if (g >= 0) {
+            const uint64_t idx = (uint64_t)(k + row_off) * (uint64_t)n_full + (uint64_t)g;
+            const uint64_t h1 = mix64(seed * 0x9E3779B97F4A7C15ULL + idx * 2 + 1);
+            const uint64_t h2 = mix64(h1 + 0x632BE59BD9B4E019ULL);
+            const float u1 = ((h1 >> 40) + 0.5f) * (1.0f / 16777216.0f);
+            const float u2 = (h2 >> 40) * (1.0f / 16777216.0f);
+            v = sqrtf(-2.0f * __logf(u1)) * __cosf(6.283185307f * u2) * sd;
+        }
+        st_f(dst + i, v);
+    }
+}
+
+void launch_fill_normal_map(int dtype, void* dst, int K, int ld, const ColMap& m, int row_off, long long n_full,
+                            float sd, cudaStream_t s) {
+    const int blocks = 148 * 8;
+    if (dtype == DT_BF16)
+        fill_normal_map_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<__nv_bfloat16*>(dst), K, ld, m, row_off, n_full, sd);
+    else
+        fill_normal_map_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<float*>(dst), K, ld, m, row_off, n_full, sd);
 }
 
 void launch_fill_const(int dtype, void* dst, long long n, float v, cudaStream_t s) {

@@ -79,6 +79,8 @@ struct GemvProblem {
     float* am_val = nullptr;  // [T][tiles]
     int* am_idx = nullptr;
     int* tok_out = nullptr;   // [T]
+    float* tok_val = nullptr; // [T] optional: the max itself (vocab-parallel gather)
+    int col_base = 0;         // added to argmax indices (vocab-parallel slice offset)
 };
 
 constexpr int kMaxProblems = 8;
@@ -222,9 +224,70 @@ struct VerifyArgs {
 };
 void launch_verify_sample(const VerifyArgs& a, cudaStream_t s);
 
+// ---- tensor-parallel collectives over NVLink peer memory (comm.cu) ----
+constexpr int kMaxTp = 8;
+struct CommView {
+    int rank = 0, world = 1;
+    size_t slot_floats = 0;          // floats per (parity, sender) slot
+    float* recv_local = nullptr;     // this rank's [2][world][slot_floats]
+    uint64_t* flags_local = nullptr; // this rank's [2][world]
+    float* peer_recv[kMaxTp] = {};   // every rank's recv region (self included)
+    uint64_t* peer_flags[kMaxTp] = {};
+    unsigned* ticket = nullptr;      // local: last-CTA election
+    uint64_t seq = 0;                // collectives issued so far (host side)
+    int early_trigger = 1;           // PDL-trigger the successor before waiting (GPUs not shared)
+    int debug = 0;                   // ESPEC_TRACE_COMM: device-side trace
+    // Shards sharing ONE GPU (single-device harness): device-side spinning
+    // could wait on a peer whose copies queue behind this rank's work, so the
+    // push and combine run as two kernels and local_sync orders them with
+    // CUDA events across the shards' streams instead (host barrier + event
+    // waits). nullptr between GPUs.
+    void (*local_sync)(void* ctx, int rank, cudaStream_t s) = nullptr;
+    void* local_ctx = nullptr;
+};
+enum AllreduceMode : int { AR_STORE = 0, AR_RESID = 1 };
+struct AllreduceArgs {
+    int rows = 0, d = 0;
+    const float* src = nullptr;  // this rank's partial [rows][ld_src]
+    int ld_src = 0;
+    int mode = AR_STORE;
+    float* out = nullptr;
+    int ldo = 0;
+    const float* resid = nullptr;  // AR_RESID: out = resid + sum, + row stats
+    int ldr = 0;
+    float* stats = nullptr;
+    int stat_tiles = 0;
+    // src / out rows come in blocks: row r at (r / rows_per_block) * block_stride
+    // + (r % rows_per_block) * ld (0 = one block)
+    int rows_per_block = 0;
+    size_t block_stride = 0;
+};
+void launch_allreduce_rows(CommView& c, const AllreduceArgs& a, cudaStream_t s);
+struct GatherColsArgs {
+    int rows = 0, cols = 0;  // each rank's slice: rows x cols
+    const float* src = nullptr;
+    int ld_src = 0;
+    float* dst = nullptr;    // rows x (world*cols)
+    int ld_dst = 0;
+};
+void launch_allgather_cols(CommView& c, const GatherColsArgs& a, cudaStream_t s);
+// vocab-parallel argmax: (val, idx) per row from every rank -> first maximum
+void launch_allgather_argmax(CommView& c, int T, const float* val, const int* idx, int* tok_out, cudaStream_t s);
+
 // Deterministic N(0, sd) init from a counter hash (perf-mode weights).
 void launch_fill_normal(int dtype, void* dst, long long n, float sd, uint64_t seed, cudaStream_t s);
 void launch_fill_const(int dtype, void* dst, long long n, float v, cudaStream_t s);
+// Local column -> global column map of a sharded fill: up to 3 contiguous
+// segments, or the packed gate/up interleave of f_loc columns starting at
+// global column f_base (gate drawn with seed, up with seed2).
+struct ColMap {
+    int nseg = 0;
+    int lc0[3] = {0, 0, 0}, gc0[3] = {0, 0, 0}, len[3] = {0, 0, 0};
+    int gateup = 0, f_loc = 0, f_base = 0;
+    uint64_t seed = 0, seed2 = 0;
+};
+void launch_fill_normal_map(int dtype, void* dst, int K, int ld, const ColMap& m, int row_off, long long n_full,
+                            float sd, cudaStream_t s);
 // dst[c][r] = src[r][c]  (src: rows x cols, dst leading dimension ldd)
 void launch_transpose(int dtype, const void* src, int rows, int cols, void* dst, int ldd, cudaStream_t s);
 

@@ -52,7 +52,7 @@ class _RunCfg(C.Structure):
 
 class _DevMap(C.Structure):
     _fields_ = [("device", C.c_int), ("n_lp_devices", C.c_int), ("lp_devices", C.POINTER(C.c_int)),
-                ("tp_size", C.c_int)]
+                ("tp_size", C.c_int), ("tp_rank", C.c_int)]
 
 
 class _Iter(C.Structure):
@@ -102,6 +102,9 @@ def lib():
         L.espec_time_site.argtypes = [V, C.c_int, C.c_int]
         L.espec_site_stats.argtypes = [V, P(C.c_int), P(C.c_double), P(C.c_double)]
         L.espec_io_bytes.argtypes = [V, P(C.c_int64), P(C.c_int64)]
+        L.espec_comm_link.argtypes = [P(V), C.c_int]
+        L.espec_comm_export.argtypes = [V, C.c_void_p]
+        L.espec_comm_import.argtypes = [V, C.c_void_p, C.c_int]
         _lib = L
     return _lib
 
@@ -194,12 +197,14 @@ class Engine:
 
     DRAFT, BASE = 0, 1
 
-    def __init__(self, base: ModelConfig, draft: ModelConfig, run: RunConfig, device: int = 0):
+    def __init__(self, base: ModelConfig, draft: ModelConfig, run: RunConfig, device: int = 0, tp_size: int = 1,
+                 tp_rank: int = 0):
         L = lib()
         self.base_cfg, self.draft_cfg = base, draft
+        self.tp_size, self.tp_rank = tp_size, tp_rank
         self._h = C.c_void_p()
         self._keep = []
-        dm = _DevMap(device, 1, None, 1)
+        dm = _DevMap(device, 1, None, tp_size, tp_rank)
         st = L.espec_engine_create(C.byref(base._c()), C.byref(draft._c()), C.byref(self._run(run)), C.byref(dm),
                                    C.byref(self._h))
         if st:
@@ -227,6 +232,29 @@ class Engine:
             self.close()
         except Exception:
             pass
+
+    # ---- tensor-parallel wiring (tp_size > 1)
+    @staticmethod
+    def link_local(engines: Sequence["Engine"]):
+        """All shards of a TP group in this process (rank order)."""
+        arr = (C.c_void_p * len(engines))(*[e._h.value for e in engines])
+        st = lib().espec_comm_link(arr, len(engines))
+        if st:
+            raise EspecError(st, lib().espec_last_error(engines[0]._h).decode())
+
+    def ipc_handle(self) -> bytes:
+        buf = C.create_string_buffer(64)
+        self._check(lib().espec_comm_export(self._h, buf))
+        return buf.raw
+
+    def ipc_import(self, handles: Sequence[bytes]):
+        blob = b"".join(handles)
+        self._check(lib().espec_comm_import(self._h, blob, len(handles)))
+
+    def link_process_group(self, group=None):
+        """One process per GPU: all-gather the IPC handles over a
+        torch.distributed group (any backend) and import them."""
+        self.ipc_import(exchange_ipc_handles(self.ipc_handle(), group))
 
     # ---- weights
     def init_weights(self, which: int, seed: int, parity: bool = True):
@@ -342,6 +370,55 @@ class Engine:
 
     def sync(self):
         self._check(lib().espec_sync(self._h))
+
+
+def exchange_ipc_handles(local: bytes, group=None) -> List[bytes]:
+    """All-gather every rank's 64-byte receive-region handle, in rank order."""
+    import torch.distributed as dist
+    if len(local) != 64:
+        raise ValueError("an IPC handle is 64 bytes")
+    handles = [None] * dist.get_world_size(group)
+    dist.all_gather_object(handles, local, group=group)
+    return handles
+
+
+def tp_group_local(base: ModelConfig, draft: ModelConfig, run: RunConfig, tp: int, device: int = 0,
+                   parity: bool = True, truncated: int = 0) -> List[Engine]:
+    """All tp shards of one tensor-parallel group in this process (testing
+    the sharded path on one GPU: the collectives run over plain device
+    pointers instead of NVLink-mapped ones)."""
+    engines = [Engine(base, draft, run, device=device, tp_size=tp, tp_rank=r) for r in range(tp)]
+    Engine.link_local(engines)
+    for e in engines:
+        e.init_weights(Engine.BASE, base.seed, parity=parity)
+        if truncated:
+            e.share_truncated_draft()
+        else:
+            e.init_weights(Engine.DRAFT, draft.seed, parity=parity)
+    return engines
+
+
+def tp_generate(engines: Sequence[Engine], prompt: bytes = None, tokens: Sequence[int] = None):
+    """Run one generation on every shard concurrently (one host thread per
+    shard, as one process per GPU would); returns each shard's result."""
+    import threading
+    out = [None] * len(engines)
+    err = []
+
+    def work(i):
+        try:
+            out[i] = engines[i].generate(prompt) if prompt is not None else engines[i].generate_tokens(tokens)
+        except Exception as ex:  # surfaced below
+            err.append(ex)
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(len(engines))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if err:
+        raise err[0]
+    return out
 
 
 def plan_groups(n_layers: int, lp_size: int) -> str:

@@ -10,8 +10,11 @@ Workload "c2": Llama-3-70B-shaped base + Llama-3-8B-shaped drafter, bf16
 weights and KV, random init (device N(0, sd) with the reference's sd rules),
 layer-parallel width 4 (plan 0|1-3|4-7|...|28-30|31), n = 5, batch 1,
 greedy, synthetic prompt of --ctx uniform-random token ids. The full pair
-(157 GB) is resident on one B200; at N>1 every rank runs an independent
-replica (round 1: replicas only).
+(157 GB) is resident on one B200; at N>1 the pair is tensor-parallel over
+the N GPUs (one rank per GPU, Megatron-sharded base AND drafter, partial sums
+exchanged by the engine's own one-shot all-reduce kernels over NVLink peer
+memory) and one generation stream is decoded by the whole job
+(scaling "strong").
 
 Prints ONE JSON line (rank 0). `value` is decode tokens/s of EasySpec with
 inputs resident in HBM; `e2e` the same metric through the C ABI
@@ -236,11 +239,14 @@ def main():
     from paper_2502_02493_b200 import espec as E
 
     ws, rank, local = dist_env()
+    one_gpu = os.environ.get("ESPEC_BENCH_ONE_GPU") == "1"
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl")
-    torch.cuda.set_device(local)
-    dev = local
+        dist.init_process_group("gloo" if one_gpu else "nccl")
+    # ESPEC_BENCH_ONE_GPU=1: every rank on cuda:0 (functional check of the
+    # multi-rank path on a 1-GPU box; timings are then meaningless)
+    dev = 0 if one_gpu else local
+    torch.cuda.set_device(dev)
 
     n, lp = wl["n"], wl["lp"]
     steps, warm = args.steps, args.warmup
@@ -250,10 +256,12 @@ def main():
     draft = E.ModelConfig(max_positions=max_pos, seed=9, tied_head=False, weight_dtype=E.BF16, kv_dtype=E.BF16,
                           **wl["draft"])
     run = E.RunConfig(algorithm="easyspec", n=n, lp_size=lp, temperature=0.0, max_new_tokens=(warm + steps + 2) * (n + 1))
-    eng = E.Engine(base, draft, run, device=dev)
+    eng = E.Engine(base, draft, run, device=dev, tp_size=ws, tp_rank=rank)
+    if ws > 1:
+        eng.link_process_group()  # all-gather the NVLink receive-region IPC handles
     eng.init_weights(E.Engine.BASE, base.seed, parity=False)
     eng.init_weights(E.Engine.DRAFT, draft.seed, parity=False)
-    rng = np.random.default_rng(1234 + rank)
+    rng = np.random.default_rng(1234)  # the same prompt on every TP rank
     prompt = [int(t) for t in rng.integers(0, base.vocab_size, size=args.ctx)]
     stream = torch.cuda.ExternalStream(eng.stream(), device=dev)
 
@@ -264,16 +272,13 @@ def main():
     def max_over_ranks(x):
         if ws == 1:
             return x
-        t = torch.tensor([x], device=f"cuda:{dev}", dtype=torch.float64)
+        t = torch.tensor([x], device="cpu" if one_gpu else f"cuda:{dev}", dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return float(t.item())
 
     def sum_over_ranks(x):
-        if ws == 1:
-            return x
-        t = torch.tensor([x], device=f"cuda:{dev}", dtype=torch.float64)
-        torch.distributed.all_reduce(t)
-        return float(t.item())
+        # tensor parallel: every rank emits the SAME tokens of one stream
+        return x
 
     def arm(alg, site=None, clocks=False):
         eng.set_run(E.RunConfig(algorithm=alg, n=n, lp_size=lp, temperature=0.0,
@@ -388,10 +393,12 @@ def main():
         line = {
             "metric": "decode tokens/s (EasySpec, greedy)",
             "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": steps, "warmup": warm,
-            "ms_per_step": it_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": it_ms, "higher_is_better": True, "scaling": "strong" if ws > 1 else "weak",
+            "vs_baseline": None,
             "dtype": "bf16", "data": "synthetic (random-init weights, uniform-random prompt ids)",
             "config": {"workload": wl["name"], "ctx": args.ctx, "n": n, "lp": lp,
-                       "plan": E.plan_groups(draft.n_layers, lp), "replicas": ws,
+                       "plan": E.plan_groups(draft.n_layers, lp), "tp": ws,
+                       "parallelism": f"tp{ws} (base + drafter)" if ws > 1 else "single GPU",
                        "l2": "no flush: 157 GB of weights streamed per step >> 126 MB L2"},
             "speedup_vs_vanilla": (value / arms["vanilla"]["tokens_per_s"]) if "vanilla" in arms else None,
             "draft_ms_per_token": (calib_ms + draft_ms) * per_tok,

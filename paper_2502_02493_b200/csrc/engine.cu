@@ -770,7 +770,7 @@ public:
         finish_logical(W, dt, K, ld, t);
     }
 
-    // ---- weight matrices: fp32 row-major, or bf16 packed in mma fragment order
+    // ---- weight matrices: fp32 row-major, or bf16 packed in the UMMA canonical K-major layout
     void* temp(size_t bytes) {
         if (bytes > temp_bytes_) {
             if (temp_) cudaFree(temp_);

@@ -1,9 +1,9 @@
 // Stream-K tensor-core GEMV for bf16 decode projections (sm_100a).
 //
 // y[T x N] = epilogue(norm?(x)[T x K] · W[K x N]) with T <= 16 rows and W
-// streamed once from HBM. W is stored pre-packed in mma.sync B-fragment order
-// (kernels.cu pack_index): a 32-column group g is one contiguous run of K/16
-// 1 KB blocks. The work is cut into *units* (problem, k-chunk j, group g) of
+// streamed once from HBM. W is stored pre-packed in 1 KB core-matrix blocks
+// (kernels.cu pack_index, the UMMA canonical K-major core-matrix layout): a
+// 32-column group g is one contiguous run of K/16 1 KB blocks. The work is cut into *units* (problem, k-chunk j, group g) of
 // up to kUnitBlocks blocks, ordered (problem, j, g) with g fastest, and every
 // CTA of a persistent 1-CTA-per-SM grid takes one contiguous, balanced range
 // of units (the split depends only on K, N and the problem count).
@@ -12,7 +12,7 @@
 // copies (cp.async.bulk + mbarrier complete_tx) through a 16-stage x 8 KB
 // shared-memory ring — 128 KB in flight per SM without register pressure —
 // while 8 consumer warps each take one 1 KB block per stage: ldmatrix the
-// activation fragment from a staged bf16 copy of x, two ld.shared.v4 for the
+// activation fragment from a staged bf16 copy of x, two ldmatrix.x4 for the
 // weight fragments, four mma.m16n8k16 (fp32 accumulate). At the end of a unit
 // the 8 warp accumulators are summed in fixed warp order through shared
 // memory; units whose group is split over several k-chunks write a partial
@@ -522,15 +522,21 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
         for (int b = 0; b < nb; b += kStageBlocks) {
             mbar_wait(&full_bar[stage], phase);
             // this warp's blocks of the stage: b + warp*kBpw + i
-            uint4 w[kBpw][2];
+            uint32_t w[kBpw][8];
             uint32_t a[kBpw][4];
 #pragma unroll
             for (int i = 0; i < kBpw; ++i) {
                 const int bi = warp * kBpw + i;
                 if (b + bi < nb) {
-                    const unsigned char* wb = ring + (size_t)stage * kStageBytes + bi * 1024 + lane * 16;
-                    w[i][0] = *reinterpret_cast<const uint4*>(wb);
-                    w[i][1] = *reinterpret_cast<const uint4*>(wb + 512);
+                    // canonical K-major block: core matrices (n8, khalf) at
+                    // (2*n8 + khalf)*128 B -> b0/b1 of n8 tiles 0,1 then 2,3
+                    const uint32_t wb = smem_u32(ring + (size_t)stage * kStageBytes + bi * 1024 + lane * 16);
+                    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                                 : "=r"(w[i][0]), "=r"(w[i][1]), "=r"(w[i][2]), "=r"(w[i][3])
+                                 : "r"(wb));
+                    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                                 : "=r"(w[i][4]), "=r"(w[i][5]), "=r"(w[i][6]), "=r"(w[i][7])
+                                 : "r"(wb + 512));
                     const uint32_t xa = smem_u32(xrow + (b + bi) * 16);
                     if constexpr (TM == 16) {
                         asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -547,10 +553,10 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
 #pragma unroll
             for (int i = 0; i < kBpw; ++i) {
                 if (b + warp * kBpw + i < nb) {
-                    mma16816(acc[0], a[i], w[i][0].x, w[i][0].y);
-                    mma16816(acc[1], a[i], w[i][0].z, w[i][0].w);
-                    mma16816(acc[2], a[i], w[i][1].x, w[i][1].y);
-                    mma16816(acc[3], a[i], w[i][1].z, w[i][1].w);
+                    mma16816(acc[0], a[i], w[i][0], w[i][1]);
+                    mma16816(acc[1], a[i], w[i][2], w[i][3]);
+                    mma16816(acc[2], a[i], w[i][4], w[i][5]);
+                    mma16816(acc[3], a[i], w[i][6], w[i][7]);
                 }
             }
             __syncwarp();

@@ -401,17 +401,20 @@ void launch_gemv(int epi, int wdtype, const GemvBatch& b, int nprob, int T, cons
     }
 }
 
-// Pre-packed bf16 layout: element (k, n) of a K x ldw matrix lives at
-//   ((g*KT + k/16)*512) + h*256 + lane*8 + j2*4 + e
-// with g = n/32, j = (n%32)/8 = 2h + j2, lane = (n%8)*4 + ((k%16)%8)/2,
-// e = (k&1) + 2*((k%16) >= 8): one lane's 16-byte load = its two mma
-// B fragments (m16n8k16, .col) for n8 tiles 2h and 2h+1.
+// Pre-packed bf16 layout = the tcgen05 / UMMA canonical K-major
+// "interleave" (no-swizzle) layout, tiled per 32-column group:
+//   element (k, n) lives at (g*KT + kt)*512 + (n8*2 + kh)*64 + r*8 + c
+// with g = n/32, kt = k/16, n8 = (n%32)/8, kh = (k%16)/8, r = n%8, c = k%8.
+// A 1 KB block (g, kt) is eight 8x8 core matrices (8 n-rows x 16 bytes of
+// consecutive k): its two k-halves of one n8 tile are adjacent (LBO 128 B)
+// and n8 tiles are 256 B apart (SBO), so consecutive groups' blocks laid
+// side by side in shared memory form one uniform K-major UMMA operand tile
+// (prefill tcgen05 GEMM), while a decode warp gets its mma.sync B fragments
+// for two n8 tiles with one ldmatrix.x4 at block + lane*16.
 __host__ __device__ __forceinline__ size_t pack_index(int k, int n, int KT) {
-    const int g = n >> 5, j = (n & 31) >> 3, gid = n & 7;
-    const int kt = k >> 4, kk = k & 15;
-    const int tig = (kk & 7) >> 1, e = (kk & 1) + ((kk >> 3) << 1);
-    const int lane = gid * 4 + tig, h = j >> 1, j2 = j & 1;
-    return ((size_t)g * KT + kt) * 512 + h * 256 + lane * 8 + j2 * 4 + e;
+    const int g = n >> 5, n8 = (n & 31) >> 3, r = n & 7;
+    const int kt = k >> 4, kh = (k & 15) >> 3, c = k & 7;
+    return ((size_t)g * KT + kt) * 512 + (n8 * 2 + kh) * 64 + r * 8 + c;
 }
 
 __global__ void pack_kernel(const __nv_bfloat16* src, int K, int ldw, __nv_bfloat16* dst, int unpack) {

@@ -4,7 +4,7 @@
 //   * weights: every projection is stored K-major, W[K][ldw] row-major with
 //     y = x · W (the reference's own matmul layout, proj/src/matrix.cpp:38-57);
 //     ldw is padded to a multiple of 8 (fp32) / 32 (bf16, stored pre-packed
-//     in mma fragment order, see pack_index). QKV of one layer is fused
+//     in the UMMA canonical K-major core-matrix layout, see pack_index). QKV of one layer is fused
 //     column-wise [q | k | v]; gate/up are fused and interleaved per 32
 //     columns [gate16 | up16] so one packed column group owns both halves of
 //     its SiLU·up epilogue.
@@ -113,7 +113,7 @@ bool pdl_enabled();
 
 // Rows handled per GEMV launch (bf16 mma path: 16; fp32 FMA path: 8).
 int gemv_rows_per_launch(int wdtype);
-// bf16 GEMV weights are stored pre-packed in mma fragment order (kernels.cu
+// bf16 GEMV weights are stored pre-packed in the UMMA canonical K-major layout (kernels.cu
 // pack_index); K x ldw logical <-> packed, ldw a multiple of 32.
 size_t packed_elems(int K, int ldw);
 void launch_pack(const void* logical, int K, int ldw, void* packed, bool unpack, cudaStream_t s);

@@ -208,6 +208,11 @@ espec_status espec_sync(espec_engine* eng);
  * Returns the mean device time per launch and the weight bytes it reads. */
 espec_status espec_bench_gemv(int K, int N, int T, int nprob, int epi, int iters, int device, double* us_per_launch,
                               double* bytes_per_launch);
+/* Instrumentation: time the tcgen05 prompt-prefill GEMM (M <= 256 rows). */
+espec_status espec_bench_tc(int M, int K, int N, int iters, int device, double* us_per_launch,
+                            double* flops_per_launch);
+/* Test probe: the prefill GEMM on host fp32 inputs (W logical K x N). */
+espec_status espec_probe_tc(int M, int K, int N, const float* x, const float* w, float* out, int device);
 /* Instrumentation: time the paged bf16 decode/verify attention for T causal
  * query rows at the end of a ctx-row context (nprob layers batched). */
 espec_status espec_bench_attn(int T, int n_heads, int n_kv, int d_head, int ctx, int nprob, int iters, int device,

@@ -514,6 +514,9 @@ struct Workspace {
     float* best_val = nullptr;  // [kChunk] vocab-slice max per row
     int* best_idx = nullptr;
     float* lg_loc = nullptr;    // [kMaxNodes+1][head_ld] vocab-slice logits
+    // prefill (tcgen05 GEMM) workspace
+    __nv_bfloat16* tc_xa = nullptr;
+    float* tc_rms = nullptr;
     int G = 1;
 };
 
@@ -973,6 +976,11 @@ public:
         }
         W.gemv_part_slot = part;
         W.gemv_ticket_slot = tick;
+        if (dt == DT_BF16) {
+            const int kmax = std::max(std::max(d, qd), f);
+            W.tc_xa = (__nv_bfloat16*)wsalloc(sizeof(__nv_bfloat16) * tc_xa_elems(kChunk, kmax));
+            W.tc_rms = (float*)wsalloc(sizeof(float) * kChunk);
+        }
         W.gemv_part = (float*)wsalloc(sizeof(float) * part * kMaxProblems);
         W.gemv_tickets = (unsigned*)wsalloc(sizeof(unsigned) * (size_t)tick * kMaxProblems);
         const int cap = c.max_positions + kMaxNodes + kChunk;
@@ -1049,6 +1057,8 @@ public:
         GemvProblem p;
         p.partial = W.gemv_part + W.gemv_part_slot * slot;
         p.tickets = W.gemv_tickets + (size_t)W.gemv_ticket_slot * slot;
+        p.tc_xa = W.tc_xa;
+        p.tc_rms = W.tc_rms;
         return p;
     }
 
@@ -1284,7 +1294,10 @@ public:
             }
             rows = C.stage_append(parents, fuzzy);
             Pass ps = make_pass(C, rows, tok);
+            // prompt chunks (> 16 rows) run on the tcgen05 prefill GEMM
+            set_prefill_mode(e - s > 16);
             forward(M, C, W, plan, ps);
+            set_prefill_mode(false);
             if (!last || commit_last) {
                 std::vector<int> a, b;
                 C.commit_path(rows, a, b);
@@ -1390,6 +1403,11 @@ public:
         }
         CUDA_OK(cudaEventRecord(ev_[0], stream_));
         const int n0 = (int)committed_.size();
+        // the prompt but its last token is prefilled (tcgen05 when long); the
+        // last token always goes through a decode-sized pass, exactly like the
+        // frontier row of a speculative verify, so greedy outputs agree
+        if (n0 - 1 > bcache_.committed)
+            chain_pass(base_, bcache_, bws_, bcache_.committed, n0 - 1, nullptr, false, true, 0);
         std::vector<int> rows = chain_pass(base_, bcache_, bws_, bcache_.committed, n0, nullptr, false, false, 0);
         const int V = base_.c.vocab_size;
         if (!sampled) {
@@ -1717,7 +1735,9 @@ public:
         }
         std::vector<int> rows = C.stage_append(parents, pp != nullptr);
         Pass ps = make_pass(C, rows, tok);
+        set_prefill_mode(n > 16);  // same rule as chain_pass
         forward(M, C, W, pp, ps);
+        set_prefill_mode(false);
         const int d = M.c.d_model, V = M.c.vocab_size;
         if (hidden) CUDA_OK(cudaMemcpyAsync(hidden, W.h, sizeof(float) * n * d, cudaMemcpyDeviceToHost, stream_));
         for (int r0 = 0; r0 < n; r0 += 8) {

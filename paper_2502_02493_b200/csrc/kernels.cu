@@ -361,6 +361,15 @@ static void gemv_dispatch_tm(const GemvLaunch& L, int nprob, cudaStream_t s) {
 
 int gemv_rows_per_launch(int wdtype) { return wdtype == DT_BF16 ? 16 : 8; }
 
+static thread_local bool g_prefill = false;
+void set_prefill_mode(bool on) {
+    static const bool enabled = [] {
+        const char* e = getenv("ESPEC_TC_PREFILL");
+        return e == nullptr || atoi(e) != 0;
+    }();
+    g_prefill = on && enabled;
+}
+
 size_t gemv_partial_floats(int K, int N, int wdtype) {
     if (wdtype == DT_BF16) return sgemv_partial_floats(K, (N + 31) / 32 * 32);
     const GemvPlan p = gemv_plan(K, N);
@@ -376,6 +385,10 @@ void launch_gemv(int epi, int wdtype, const GemvBatch& b, int nprob, int T, cons
                  const KvView& kv, cudaStream_t s) {
     if (T <= 0 || nprob <= 0) return;
     if (wdtype == DT_BF16) {
+        if (g_prefill && T > 16 && epi != EPI_ARGMAX && b.p[0].tc_xa != nullptr) {
+            for (int i = 0; i < nprob; ++i) launch_tc_gemm(epi, b.p[i], T, pass, kv, b.p[i].tc_xa, b.p[i].tc_rms, s);
+            return;
+        }
         launch_sgemv(epi, b, nprob, T, pass, kv, s);
         return;
     }

@@ -13,6 +13,7 @@
 //   * KV cache: paged pool; page p holds kPage rows for every layer:
 //     pool[p][layer][k|v][kv_head][row][d_head], located through a page table.
 #pragma once
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -81,6 +82,9 @@ struct GemvProblem {
     int* tok_out = nullptr;   // [T]
     float* tok_val = nullptr; // [T] optional: the max itself (vocab-parallel gather)
     int col_base = 0;         // added to argmax indices (vocab-parallel slice offset)
+    // prefill (tcgen05) workspace: packed bf16 A tiles and per-row 1/rms
+    __nv_bfloat16* tc_xa = nullptr;
+    float* tc_rms = nullptr;
 };
 
 constexpr int kMaxProblems = 8;
@@ -107,6 +111,14 @@ SgPlan sgemv_plan(int K, int ldw, int nprob);
 size_t sgemv_partial_floats(int K, int ldw);
 void launch_sgemv(int epi, const GemvBatch& b, int nprob, int T, const PassView& pass, const KvView& kv,
                   cudaStream_t s);
+// Prompt prefill (tc_gemm.cu): while prefill mode is on (thread-local, set by
+// the engine around prompt chunks), bf16 launch_gemv calls with more than 16
+// rows run on tcgen05 (M=128 x N=256 tiles, TMEM accumulators) instead of the
+// decode GEMV. Decode passes never use it, so their batch invariance holds.
+void set_prefill_mode(bool on);
+size_t tc_xa_elems(int rows, int K);
+void launch_tc_gemm(int epi, const GemvProblem& P, int T, const PassView& pass, const KvView& kv,
+                    __nv_bfloat16* xa, float* inv_rms, cudaStream_t s);
 // Programmatic dependent launch on/off (default on; ESPEC_PDL=0 disables).
 void set_pdl(bool on);
 bool pdl_enabled();

@@ -186,3 +186,99 @@ extern "C" espec_status espec_bench_attn(int T, int n_heads, int n_kv, int dh, i
     cudaStreamDestroy(s);
     return err == cudaSuccess ? ESPEC_OK : ESPEC_CUDA;
 }
+
+// Prefill GEMM (tcgen05) in isolation: M rows x K -> N (store epilogue).
+extern "C" espec_status espec_bench_tc(int M, int K, int N, int iters, int device, double* us_per_launch,
+                                       double* flops_per_launch) {
+    if (M < 1 || M > 256 || K % 16 || N % 32 || iters < 1) return ESPEC_CONFIG;
+    if (cudaSetDevice(device) != cudaSuccess) return ESPEC_CUDA;
+    void* W = nullptr;
+    float *x = nullptr, *out = nullptr, *rms = nullptr;
+    __nv_bfloat16* xa = nullptr;
+    cudaStream_t s;
+    cudaEvent_t e0, e1;
+    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaMalloc(&W, (size_t)K * N * 2);
+    launch_fill_normal(DT_BF16, W, (long long)K * N, 0.02f, 1234, s);
+    cudaMalloc(&x, sizeof(float) * (size_t)M * K);
+    cudaMalloc(&out, sizeof(float) * (size_t)M * N);
+    cudaMalloc(&rms, sizeof(float) * 256);
+    cudaMalloc(&xa, sizeof(__nv_bfloat16) * tc_xa_elems(M, K));
+    launch_fill_normal(DT_F32, x, (long long)M * K, 1.0f, 99, s);
+    GemvProblem P;
+    P.W = W;
+    P.K = K;
+    P.N = N;
+    P.ldw = N;
+    P.x = x;
+    P.ldx = K;
+    P.out = out;
+    P.ldo = N;
+    PassView pv;
+    KvView kv;
+    for (int i = 0; i < 2; ++i) launch_tc_gemm(EPI_STORE, P, M, pv, kv, xa, rms, s);
+    cudaEventRecord(e0, s);
+    for (int i = 0; i < iters; ++i) launch_tc_gemm(EPI_STORE, P, M, pv, kv, xa, rms, s);
+    cudaEventRecord(e1, s);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const cudaError_t err = cudaGetLastError();
+    *us_per_launch = 1000.0 * ms / iters;
+    *flops_per_launch = 2.0 * M * (double)K * N;
+    cudaFree(W);
+    cudaFree(x);
+    cudaFree(out);
+    cudaFree(rms);
+    cudaFree(xa);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamDestroy(s);
+    return err == cudaSuccess ? ESPEC_OK : ESPEC_CUDA;
+}
+
+// Correctness probe of the prefill GEMM: out = bf16(x) . W for M rows with
+// host fp32 inputs (W logical K x N, row-major), packed on device.
+extern "C" espec_status espec_probe_tc(int M, int K, int N, const float* x_host, const float* w_host, float* out_host,
+                                       int device) {
+    if (M < 1 || M > 256 || K % 16 || N % 32) return ESPEC_CONFIG;
+    if (cudaSetDevice(device) != cudaSuccess) return ESPEC_CUDA;
+    std::vector<__nv_bfloat16> wb((size_t)K * N);
+    for (size_t i = 0; i < wb.size(); ++i) wb[i] = __float2bfloat16_rn(w_host[i]);
+    void *Wl = nullptr, *W = nullptr;
+    float *x = nullptr, *out = nullptr, *rms = nullptr;
+    __nv_bfloat16* xa = nullptr;
+    cudaMalloc(&Wl, (size_t)K * N * 2);
+    cudaMalloc(&W, packed_elems(K, N) * 2);
+    cudaMemcpy(Wl, wb.data(), (size_t)K * N * 2, cudaMemcpyHostToDevice);
+    launch_pack(Wl, K, N, W, false, 0);
+    cudaMalloc(&x, sizeof(float) * (size_t)M * K);
+    cudaMalloc(&out, sizeof(float) * (size_t)M * N);
+    cudaMalloc(&rms, sizeof(float) * 256);
+    cudaMalloc(&xa, sizeof(__nv_bfloat16) * tc_xa_elems(M, K));
+    cudaMemcpy(x, x_host, sizeof(float) * (size_t)M * K, cudaMemcpyHostToDevice);
+    cudaMemset(out, 0, sizeof(float) * (size_t)M * N);
+    GemvProblem P;
+    P.W = W;
+    P.K = K;
+    P.N = N;
+    P.ldw = N;
+    P.x = x;
+    P.ldx = K;
+    P.out = out;
+    P.ldo = N;
+    PassView pv;
+    KvView kv;
+    launch_tc_gemm(EPI_STORE, P, M, pv, kv, xa, rms, 0);
+    cudaMemcpy(out_host, out, sizeof(float) * (size_t)M * N, cudaMemcpyDeviceToHost);
+    const cudaError_t err = cudaGetLastError();
+    cudaFree(Wl);
+    cudaFree(W);
+    cudaFree(x);
+    cudaFree(out);
+    cudaFree(rms);
+    cudaFree(xa);
+    return err == cudaSuccess ? ESPEC_OK : ESPEC_CUDA;
+}

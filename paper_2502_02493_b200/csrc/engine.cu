@@ -517,6 +517,8 @@ struct Workspace {
     // prefill (tcgen05 GEMM) workspace
     __nv_bfloat16* tc_xa = nullptr;
     float* tc_rms = nullptr;
+    float* tc_part = nullptr;
+    unsigned* tc_tickets = nullptr;
     int G = 1;
 };
 
@@ -980,6 +982,12 @@ public:
             const int kmax = std::max(std::max(d, qd), f);
             W.tc_xa = (__nv_bfloat16*)wsalloc(sizeof(__nv_bfloat16) * tc_xa_elems(kChunk, kmax));
             W.tc_rms = (float*)wsalloc(sizeof(float) * kChunk);
+            size_t tpf = 0;
+            for (auto& sh : shapes) tpf = std::max(tpf, tc_part_floats(sh[0], ldpad(sh[1], dt)));
+            if (tpf) {
+                W.tc_part = (float*)wsalloc(sizeof(float) * tpf);
+                W.tc_tickets = (unsigned*)wsalloc(sizeof(unsigned) * 4096);
+            }
         }
         W.gemv_part = (float*)wsalloc(sizeof(float) * part * kMaxProblems);
         W.gemv_tickets = (unsigned*)wsalloc(sizeof(unsigned) * (size_t)tick * kMaxProblems);
@@ -1059,6 +1067,8 @@ public:
         p.tickets = W.gemv_tickets + (size_t)W.gemv_ticket_slot * slot;
         p.tc_xa = W.tc_xa;
         p.tc_rms = W.tc_rms;
+        p.tc_part = W.tc_part;
+        p.tc_tickets = W.tc_tickets;
         return p;
     }
 

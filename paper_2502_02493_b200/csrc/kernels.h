@@ -85,6 +85,8 @@ struct GemvProblem {
     // prefill (tcgen05) workspace: packed bf16 A tiles and per-row 1/rms
     __nv_bfloat16* tc_xa = nullptr;
     float* tc_rms = nullptr;
+    float* tc_part = nullptr;        // split-K partial tiles (nullptr: no split)
+    unsigned* tc_tickets = nullptr;
 };
 
 constexpr int kMaxProblems = 8;
@@ -117,6 +119,7 @@ void launch_sgemv(int epi, const GemvBatch& b, int nprob, int T, const PassView&
 // decode GEMV. Decode passes never use it, so their batch invariance holds.
 void set_prefill_mode(bool on);
 size_t tc_xa_elems(int rows, int K);
+size_t tc_part_floats(int K, int ldw);
 void launch_tc_gemm(int epi, const GemvProblem& P, int T, const PassView& pass, const KvView& kv,
                     __nv_bfloat16* xa, float* inv_rms, cudaStream_t s);
 // Programmatic dependent launch on/off (default on; ESPEC_PDL=0 disables).

@@ -216,6 +216,16 @@ extern "C" espec_status espec_bench_tc(int M, int K, int N, int iters, int devic
     P.ldx = K;
     P.out = out;
     P.ldo = N;
+    float* part = nullptr;
+    unsigned* tks = nullptr;
+    const size_t pf = tc_part_floats(K, N);
+    if (pf) {
+        cudaMalloc(&part, sizeof(float) * pf);
+        cudaMalloc(&tks, sizeof(unsigned) * 1024);
+        cudaMemset(tks, 0, sizeof(unsigned) * 1024);
+        P.tc_part = part;
+        P.tc_tickets = tks;
+    }
     PassView pv;
     KvView kv;
     for (int i = 0; i < 2; ++i) launch_tc_gemm(EPI_STORE, P, M, pv, kv, xa, rms, s);
@@ -232,6 +242,8 @@ extern "C" espec_status espec_bench_tc(int M, int K, int N, int iters, int devic
     cudaFree(x);
     cudaFree(out);
     cudaFree(rms);
+    if (part) cudaFree(part);
+    if (tks) cudaFree(tks);
     cudaFree(xa);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
@@ -269,6 +281,16 @@ extern "C" espec_status espec_probe_tc(int M, int K, int N, const float* x_host,
     P.ldx = K;
     P.out = out;
     P.ldo = N;
+    float* part = nullptr;
+    unsigned* tks = nullptr;
+    const size_t pf = tc_part_floats(K, N);
+    if (pf) {
+        cudaMalloc(&part, sizeof(float) * pf);
+        cudaMalloc(&tks, sizeof(unsigned) * 1024);
+        cudaMemset(tks, 0, sizeof(unsigned) * 1024);
+        P.tc_part = part;
+        P.tc_tickets = tks;
+    }
     PassView pv;
     KvView kv;
     launch_tc_gemm(EPI_STORE, P, M, pv, kv, xa, rms, 0);
@@ -279,6 +301,8 @@ extern "C" espec_status espec_probe_tc(int M, int K, int N, const float* x_host,
     cudaFree(x);
     cudaFree(out);
     cudaFree(rms);
+    if (part) cudaFree(part);
+    if (tks) cudaFree(tks);
     cudaFree(xa);
     return err == cudaSuccess ? ESPEC_OK : ESPEC_CUDA;
 }

@@ -5,14 +5,16 @@
 // the prompt through every projection of both models. Decode passes (M <= 16)
 // stay on the HBM-streaming GEMV (gemv_stream.cu).
 //
-// One CTA computes a 128 x 256 output tile over all of K:
-//   warp 0  TMA producer: 1-D bulk copies of the A tile (16 KB: 128 rows x 64 k,
-//           pre-packed by pack_a_kernel) and of eight 1 KB weight blocks per
-//           k-step (32 KB) into a 4-stage shared-memory ring (mbarrier
+// One CTA computes a 256 x 256 output tile (two 128-row UMMA accumulators
+// sharing every weight tile) over its K split (split-K when the N tiles
+// alone cannot fill 148 SMs; the last split reduces partials in order):
+//   warp 0  TMA producer: 1-D bulk copies of the A tiles (2 x 16 KB: 256 rows x
+//           64 k, pre-packed by pack_a_kernel) and of eight 1 KB weight blocks
+//           per k-step (32 KB) into a 3-stage shared-memory ring (mbarrier
 //           complete_tx);
-//   warp 1  allocates 256 TMEM columns; lane 0 issues tcgen05.mma
-//           (kind::f16, M=128, N=256, K=16, fp32 accumulate in TMEM) — four per
-//           stage — and releases each stage with tcgen05.commit;
+//   warp 1  allocates all 512 TMEM columns; lane 0 issues tcgen05.mma
+//           (kind::f16, M=128, N=256, K=16, fp32 accumulate in TMEM) — eight
+//           per stage — and releases each stage with tcgen05.commit;
 //   warps 2-5 epilogue: tcgen05.ld 32 columns at a time (each thread one row),
 //           then the same fused epilogues as the decode GEMV (residual + row
 //           statistics, SiLU(gate)*up, RoPE + paged-KV write, store).
@@ -28,15 +30,18 @@
 
 namespace espec_dev {
 
-constexpr int kTcM = 128;
+constexpr int kTcM = 128;             // rows per UMMA (one TMEM accumulator)
+constexpr int kTcMSub = 2;            // UMMA row blocks per CTA: 256 rows share each weight tile
 constexpr int kTcN = 256;             // 8 x 32-column weight groups
 constexpr int kTcKStep = 16;          // one tcgen05.mma (bf16)
 constexpr int kTcStepsPerStage = 4;   // 64 k per stage
-constexpr int kTcStages = 4;
-constexpr int kTcAStage = kTcM * kTcKStep * kTcStepsPerStage * 2;  // 16 KB
-constexpr int kTcBStage = kTcN * kTcKStep * kTcStepsPerStage * 2;  // 32 KB
+constexpr int kTcStages = 3;
+constexpr int kTcABlock = kTcM * kTcKStep * 2;                      // 4 KB: 128 rows x 16 k
+constexpr int kTcAStage = kTcMSub * kTcABlock * kTcStepsPerStage;   // 32 KB
+constexpr int kTcBStage = kTcN * kTcKStep * kTcStepsPerStage * 2;   // 32 KB
 constexpr int kTcStageBytes = kTcAStage + kTcBStage;
 constexpr int kTcThreads = 6 * 32;
+constexpr int kTcMinStagesPerSplit = 8;  // >= 512 k per K-split
 
 __device__ __forceinline__ uint32_t tc_smem(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -78,8 +83,11 @@ struct TcLaunch {
     KvView kv;
     int t0, T;       // rows [t0, t0+T) of the pass
     int KS;          // k-steps (K/16, K padded to 16)
-    int mtiles;
+    int mtiles;      // 128-row blocks of A (1 or 2)
+    int ksplits;     // K split across grid.z; partials reduced by the last CTA
     const __nv_bfloat16* xa;  // packed A: [mtile][KS][16 m8][2 kh][8 rows][8] bf16
+    float* part;              // [ksplits][256][ldw] fp32 partial tiles (ksplits > 1)
+    unsigned* tickets;        // [ntiles]
 };
 
 // epilogue for one (row, 32-column group): v = 32 fp32 sums of that row
@@ -156,12 +164,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
     extern __shared__ __align__(1024) unsigned char sm[];
     __shared__ __align__(8) uint64_t full_bar[kTcStages], empty_bar[kTcStages], acc_bar;
     __shared__ uint32_t tmem_base;
+    __shared__ unsigned s_last;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int ntile = blockIdx.x, mt = blockIdx.y;
+    const int ntile = blockIdx.x, z = blockIdx.z;
     const int g0 = ntile * (kTcN / 32);
     const int KS = L.KS;
-    const int n_stages_total = (KS + kTcStepsPerStage - 1) / kTcStepsPerStage;
+    const int nm = L.mtiles;  // active 128-row blocks
+    const int stages_all = (KS + kTcStepsPerStage - 1) / kTcStepsPerStage;
+    const int st0 = (int)((long long)z * stages_all / L.ksplits);
+    const int st1 = (int)((long long)(z + 1) * stages_all / L.ksplits);
     const int ngroups = L.P.ldw / 32;
+    const int ng = min(kTcN / 32, ngroups - g0);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kTcStages; ++s) {
@@ -171,9 +184,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
         tc_mbar_init(&acc_bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 1) {
+    if (warp == 1) {  // two 128 x 256 fp32 accumulators = all 512 TMEM columns
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc_smem(&tmem_base)),
-                     "r"(kTcN));
+                     "r"(kTcMSub * kTcN));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tc_fence_before();
@@ -185,20 +198,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
         // ---------------- producer (weights need no dependency; A does)
         if (lane == 0) {
             asm volatile("griddepcontrol.wait;" ::: "memory");
-            const char* A = reinterpret_cast<const char*>(L.xa) + (size_t)mt * KS * (kTcM * kTcKStep * 2);
+            const char* A = reinterpret_cast<const char*>(L.xa);
             const char* B = reinterpret_cast<const char*>(L.P.W);
-            const size_t KT = (size_t)KS;  // weight k-blocks per group (K padded to 16)
-            for (int st = 0; st < n_stages_total; ++st) {
-                const int s = st % kTcStages;
-                const uint32_t ph = (uint32_t)(st / kTcStages) & 1u;
-                tc_mbar_wait(&empty_bar[s], ph ^ 1u);
+            const size_t KT = (size_t)KS;
+            for (int st = st0; st < st1; ++st) {
+                const int i = st - st0, s = i % kTcStages;
+                tc_mbar_wait(&empty_bar[s], ((uint32_t)(i / kTcStages) & 1u) ^ 1u);
                 const int ks0 = st * kTcStepsPerStage;
                 const int nks = min(kTcStepsPerStage, KS - ks0);
-                int ng = min(kTcN / 32, ngroups - g0);
-                tc_mbar_expect(&full_bar[s], (uint32_t)(nks * (kTcM * kTcKStep * 2) + nks * ng * 1024));
+                tc_mbar_expect(&full_bar[s], (uint32_t)(nm * nks * kTcABlock + nks * ng * 1024));
                 unsigned char* sa = sm + (size_t)s * kTcStageBytes;
                 unsigned char* sb = sa + kTcAStage;
-                tc_bulk(sa, A + (size_t)ks0 * (kTcM * kTcKStep * 2), (uint32_t)(nks * kTcM * kTcKStep * 2), &full_bar[s]);
+                for (int m = 0; m < nm; ++m)
+                    tc_bulk(sa + (size_t)m * kTcStepsPerStage * kTcABlock,
+                            A + ((size_t)m * KS + ks0) * kTcABlock, (uint32_t)(nks * kTcABlock), &full_bar[s]);
                 for (int k = 0; k < nks; ++k)
                     for (int gl = 0; gl < ng; ++gl)
                         tc_bulk(sb + (size_t)k * (kTcN / 32) * 1024 + gl * 1024,
@@ -208,23 +221,24 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
     } else if (warp == 1) {
         // ---------------- MMA issuer (one thread)
         if (lane == 0) {
-            const uint32_t d = tmem_base;
-            for (int st = 0; st < n_stages_total; ++st) {
-                const int s = st % kTcStages;
-                tc_mbar_wait(&full_bar[s], (uint32_t)(st / kTcStages) & 1u);
+            for (int st = st0; st < st1; ++st) {
+                const int i = st - st0, s = i % kTcStages;
+                tc_mbar_wait(&full_bar[s], (uint32_t)(i / kTcStages) & 1u);
                 tc_fence_after();
                 const int ks0 = st * kTcStepsPerStage;
                 const int nks = min(kTcStepsPerStage, KS - ks0);
                 const uint32_t sa = tc_smem(sm + (size_t)s * kTcStageBytes);
                 const uint32_t sb = sa + kTcAStage;
                 for (int k = 0; k < nks; ++k) {
-                    const uint64_t da = umma_desc(sa + k * (kTcM * kTcKStep * 2), 128, 256);
                     const uint64_t db = umma_desc(sb + k * (kTcN / 32) * 1024, 128, 256);
-                    const uint32_t acc = (st > 0 || k > 0) ? 1u : 0u;
-                    asm volatile(
-                        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
-                        "l"(da), "l"(db), "r"(kTcIdesc), "r"(acc));
+                    const uint32_t acc = (i > 0 || k > 0) ? 1u : 0u;
+                    for (int m = 0; m < nm; ++m) {
+                        const uint64_t da = umma_desc(sa + (m * kTcStepsPerStage + k) * kTcABlock, 128, 256);
+                        asm volatile(
+                            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_base + m * kTcN),
+                            "l"(da), "l"(db), "r"(kTcIdesc), "r"(acc));
+                    }
                 }
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                     tc_smem(&empty_bar[s])));
@@ -238,34 +252,76 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
         tc_mbar_wait(&acc_bar, 0);
         tc_fence_after();
         const int lane_base = 32 * (warp & 3);
-        const int r = lane_base + lane;            // row within the tile
-        const int t = L.t0 + mt * kTcM + r;        // pass row
-        const bool ok = mt * kTcM + r < L.T;
-        const int ng = min(kTcN / 32, ngroups - g0);
-        for (int gl = 0; gl < ng; ++gl) {
-            uint32_t u[32];
-            const uint32_t taddr = tmem_base + ((uint32_t)lane_base << 16) + (uint32_t)(gl * 32);
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-                : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7]),
-                  "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]), "=r"(u[14]),
-                  "=r"(u[15]), "=r"(u[16]), "=r"(u[17]), "=r"(u[18]), "=r"(u[19]), "=r"(u[20]), "=r"(u[21]),
-                  "=r"(u[22]), "=r"(u[23]), "=r"(u[24]), "=r"(u[25]), "=r"(u[26]), "=r"(u[27]), "=r"(u[28]),
-                  "=r"(u[29]), "=r"(u[30]), "=r"(u[31])
-                : "r"(taddr));
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            float v[32];
+        const int ldw = L.P.ldw;
+        for (int m = 0; m < nm; ++m) {
+            const int r = m * kTcM + lane_base + lane;  // row within the CTA's 256
+            const bool ok = r < L.T;
+            for (int gl = 0; gl < ng; ++gl) {
+                uint32_t u[32];
+                const uint32_t taddr = tmem_base + ((uint32_t)lane_base << 16) + (uint32_t)(m * kTcN + gl * 32);
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                    : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7]),
+                      "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]), "=r"(u[14]),
+                      "=r"(u[15]), "=r"(u[16]), "=r"(u[17]), "=r"(u[18]), "=r"(u[19]), "=r"(u[20]), "=r"(u[21]),
+                      "=r"(u[22]), "=r"(u[23]), "=r"(u[24]), "=r"(u[25]), "=r"(u[26]), "=r"(u[27]), "=r"(u[28]),
+                      "=r"(u[29]), "=r"(u[30]), "=r"(u[31])
+                    : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                float v[32];
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(u[j]);
-            if (ok) tc_epilogue<EPI>(L, t, g0 + gl, v);
+                for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(u[j]);
+                if (L.ksplits == 1) {
+                    if (ok) tc_epilogue<EPI>(L, L.t0 + r, g0 + gl, v);
+                } else if (ok) {
+                    float4* pp = reinterpret_cast<float4*>(L.part + ((size_t)z * 256 + r) * ldw + (g0 + gl) * 32);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) pp[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                }
+            }
+        }
+        if (L.ksplits > 1) {
+            // last K-split CTA of this tile sums the partials in split order
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (threadIdx.x == 64) {
+                unsigned tk;
+                asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(tk) : "l"(L.tickets + ntile) : "memory");
+                s_last = tk == (unsigned)L.ksplits - 1 ? 1u : 0u;
+                if (s_last) L.tickets[ntile] = 0u;
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (s_last) {
+                for (int m = 0; m < nm; ++m) {
+                    const int r = m * kTcM + lane_base + lane;
+                    if (r >= L.T) continue;
+                    for (int gl = 0; gl < ng; ++gl) {
+                        float v[32];
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) v[j] = 0.f;
+                        for (int zz = 0; zz < L.ksplits; ++zz) {
+                            const float4* pp =
+                                reinterpret_cast<const float4*>(L.part + ((size_t)zz * 256 + r) * ldw + (g0 + gl) * 32);
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) {
+                                const float4 q = __ldcg(pp + j);
+                                v[4 * j] += q.x;
+                                v[4 * j + 1] += q.y;
+                                v[4 * j + 2] += q.z;
+                                v[4 * j + 3] += q.w;
+                            }
+                        }
+                        tc_epilogue<EPI>(L, L.t0 + r, g0 + gl, v);
+                    }
+                }
+            }
         }
     }
     tc_fence_before();
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTcN));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTcMSub * kTcN));
     }
 }
 
@@ -334,7 +390,7 @@ static void tc_launch_t(const TcLaunch& L, int ntiles, cudaStream_t s) {
         cudaFuncSetAttribute(tc_gemm_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         configured = true;
     }
-    launch_pdl(tc_gemm_kernel<EPI>, dim3(ntiles, L.mtiles), dim3(kTcThreads), (size_t)smem, s, L);
+    launch_pdl(tc_gemm_kernel<EPI>, dim3(ntiles, 1, L.ksplits), dim3(kTcThreads), (size_t)smem, s, L);
 }
 
 size_t tc_xa_elems(int rows, int K) {
@@ -342,11 +398,30 @@ size_t tc_xa_elems(int rows, int K) {
     return (size_t)mtiles * ((K + 15) / 16) * kTcM * 16;
 }
 
-// Prefill GEMM for rows [0, T) of the problem; workspace xa (tc_xa_elems
-// bf16) and inv_rms (T floats).
+// K splits for an output of ldw columns: fill ~148 SMs when the N tiles
+// alone do not, keeping >= 512 k per split.
+static int tc_ksplits(int K, int ldw) {
+    const int ntiles = (ldw / 32 + kTcN / 32 - 1) / (kTcN / 32);
+    const int stages = ((K + 15) / 16 + kTcStepsPerStage - 1) / kTcStepsPerStage;
+    int ks = 148 / ntiles;
+    if (ks > stages / kTcMinStagesPerSplit) ks = stages / kTcMinStagesPerSplit;
+    return ks < 1 ? 1 : ks;
+}
+
+size_t tc_part_floats(int K, int ldw) {
+    const int ks = tc_ksplits(K, ldw);
+    return ks > 1 ? (size_t)ks * 256 * ldw : 0;
+}
+
+// Prefill GEMM for rows [0, T) (T <= 256) of the problem; workspace xa
+// (tc_xa_elems bf16), inv_rms (T floats), part (tc_part_floats) + tickets.
 void launch_tc_gemm(int epi, const GemvProblem& P, int T, const PassView& pass, const KvView& kv,
                     __nv_bfloat16* xa, float* inv_rms, cudaStream_t s) {
     if (T <= 0) return;
+    if (T > kTcMSub * kTcM) {
+        fprintf(stderr, "tc_gemm: %d rows exceed the 256-row prefill chunk\n", T);
+        return;
+    }
     TcLaunch L;
     L.P = P;
     L.pass = pass;
@@ -356,6 +431,9 @@ void launch_tc_gemm(int epi, const GemvProblem& P, int T, const PassView& pass, 
     L.KS = (P.K + 15) / 16;
     L.mtiles = (T + kTcM - 1) / kTcM;
     L.xa = xa;
+    L.ksplits = P.tc_part ? tc_ksplits(P.K, P.ldw) : 1;
+    L.part = P.tc_part;
+    L.tickets = P.tc_tickets;
     tc_rms_kernel<<<(T + 7) / 8, 256, 0, s>>>(P, 0, T, inv_rms);
     const long long total = (long long)L.mtiles * L.KS * 256;
     int blocks = (int)((total + 255) / 256);

@@ -412,7 +412,7 @@ def main():
                                 "speedup_vs_vanilla": (proj_tok_s / arms["vanilla"]["tokens_per_s"])
                                 if "vanilla" in arms else None,
                                 "note": "projection, tokens/iteration = n*alpha+1 (proj/src/cli.cpp:403)"},
-            "roofline": {"kernel": "gemv_kernel<bf16,8,EPI_SILU> (base gate/up, 8192x57344 bf16)",
+            "roofline": {"kernel": "sgemv_kernel<8,EPI_SILU> (stream-K bf16 GEMV, base gate/up 8192x57344)",
                          "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": (achieved / hbm) if achieved else None, "traffic": traffic,
                          "launches_timed": cnt, "bytes_per_launch": site_bytes, "peak_source": peak_kind},

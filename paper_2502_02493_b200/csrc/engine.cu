@@ -10,6 +10,7 @@
 #include <cstring>
 #include <sstream>
 #include <condition_variable>
+#include <map>
 #include <mutex>
 
 #include "common.cuh"
@@ -215,6 +216,7 @@ struct ModelDev {
     void* head = nullptr;  // [d][head_ld]: this rank's vocabulary slice
     int head_ld = 0;
     float* fgain = nullptr;
+    float2* rope = nullptr;  // [max_positions][d_head/2] (cos, sin) of apply_rope's angles
     std::vector<LayerDev> L;
     std::vector<void*> owned;
     int qh() const { return c.n_heads / tp; }
@@ -234,9 +236,27 @@ struct ModelDev {
         owned.push_back(p);
         return p;
     }
+    // Rotary table, computed on the host exactly as apply_rope does
+    // (proj/src/matrix.cpp:171-186): inv_freq = pow(theta, -2p/dh) and
+    // (float)cos / (float)sin of pos * inv_freq in double. The GEMV epilogues
+    // read it instead of evaluating double trigonometry per element.
+    void build_rope() {
+        const int np = c.d_head / 2;
+        std::vector<double> inv_freq(np);
+        for (int p = 0; p < np; ++p) inv_freq[p] = std::pow((double)c.rope_theta, -2.0 * p / c.d_head);
+        std::vector<float2> tab((size_t)c.max_positions * np);
+        for (int pos = 0; pos < c.max_positions; ++pos)
+            for (int p = 0; p < np; ++p) {
+                const double th = (double)pos * inv_freq[p];
+                tab[(size_t)pos * np + p] = make_float2((float)std::cos(th), (float)std::sin(th));
+            }
+        rope = (float2*)alloc(sizeof(float2) * tab.size());
+        CUDA_OK(cudaMemcpy(rope, tab.data(), sizeof(float2) * tab.size(), cudaMemcpyHostToDevice));
+    }
     void allocate(bool share_layers_from_base, const ModelDev* base) {
         const int d = c.d_model, f = f_loc(), V = c.vocab_size, es = (int)dsize(c.weight_dtype);
         head_ld = ldpad(V_loc(), c.weight_dtype);
+        build_rope();
         if (share_layers_from_base) {
             emb = base->emb;
             head = base->head;
@@ -544,6 +564,10 @@ public:
         CUDA_OK(cudaSetDevice(device));
         if (const char* e = std::getenv("ESPEC_PDL")) set_pdl(std::atoi(e) != 0);
         CUDA_OK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+        CUDA_OK(cudaMalloc(&mk_counter_, sizeof(unsigned long long)));
+        CUDA_OK(cudaMemset(mk_counter_, 0, sizeof(unsigned long long)));
+        if (const char* e = std::getenv("ESPEC_MK")) mk_mode_ = std::atoi(e);
+        if (const char* e = std::getenv("ESPEC_MK_PF_KB")) mk_prefetch_ = std::atoll(e) << 10;
         for (auto& e : ev_) CUDA_OK(cudaEventCreate(&e));
         const int cap_b = bc.max_positions + kMaxNodes + kChunk;
         const int cap_d = dc.max_positions + kMaxNodes + kChunk;
@@ -615,6 +639,8 @@ public:
         if (comm_.ticket) cudaFree(comm_.ticket);
         for (auto& e : ev_) cudaEventDestroy(e);
         for (auto& e : site_ev_) cudaEventDestroy(e);
+        mk_clear();
+        if (mk_counter_) cudaFree(mk_counter_);
         cudaStreamDestroy(stream_);
     }
 
@@ -674,9 +700,11 @@ public:
         draft_.release();
         draft_.allocate(true, &base_);
         draft_allocated_ = true;
+        mk_clear();
     }
 
     void init_weights_seeded(int which, uint64_t seed, bool parity) override {
+        mk_clear();
         ModelDev& M = which ? base_ : draft_;
         M.c.seed = seed;
         ensure_allocated(which);
@@ -1131,14 +1159,12 @@ public:
         if (!tp()) {
             p.out = W.h; p.ldo = d; p.resid = W.h; p.ldr = d; p.stats_out = W.stats; p.stat_tiles_out = tiles;
             b.p[0] = p;
-            site(M, kind, gemv_bytes(M, K, d, d, T, 1), [&] { launch_gemv(EPI_RESID, wdt, b, 1, T, ps.view, kv, stream_); });
-            launches_ += chunks(M, T);
+            g_gemv(M, kind, gemv_bytes(M, K, d, d, T, 1), EPI_RESID, b, 1, T, ps, kv);
             return;
         }
         p.out = W.part; p.ldo = d;
         b.p[0] = p;
-        site(M, kind, gemv_bytes(M, K, d, d, T, 1), [&] { launch_gemv(EPI_STORE, wdt, b, 1, T, ps.view, kv, stream_); });
-        launches_ += chunks(M, T);
+        g_gemv(M, kind, gemv_bytes(M, K, d, d, T, 1), EPI_STORE, b, 1, T, ps, kv);
         AllreduceArgs a;
         a.rows = T; a.d = d; a.src = W.part; a.ld_src = d; a.mode = AR_RESID;
         a.out = W.h; a.ldo = d; a.resid = W.h; a.ldr = d; a.stats = W.stats; a.stat_tiles = tiles;
@@ -1146,16 +1172,165 @@ public:
         ++launches_;
     }
 
-    // forward_sequential / forward_fuzzy (proj/src/draft_engine.cpp:35-133)
+    // forward_sequential / forward_fuzzy (proj/src/draft_engine.cpp:35-133).
+    // Decode-sized single-GPU bf16 passes run as ONE megakernel launch
+    // (decode_mk.cu) executing the op list forward_body records; the op list
+    // depends only on (model, plan, T), so it is built once and cached.
     void forward(ModelDev& M, Cache& C, Workspace& W, const LayerPlan* plan, const Pass& ps) {
+        if (mk_usable(M, ps.T)) {
+            forward_mk(M, C, W, plan, ps);
+            return;
+        }
+        forward_body(M, C, W, plan, ps);
+    }
+    bool mk_usable(const ModelDev& M, int T) const {
+        return mk_mode_ && !tp() && T >= 1 && T <= mk_max_rows() && M.c.weight_dtype == DT_BF16 &&
+               M.c.kv_dtype == DT_BF16 && (M.c.d_head == 64 || M.c.d_head == 128);
+    }
+    void mk_clear() {
+        for (auto& kv : mk_progs_)
+            if (kv.second.dev) cudaFree(kv.second.dev);
+        mk_progs_.clear();
+    }
+    void forward_mk(ModelDev& M, Cache& C, Workspace& W, const LayerPlan* plan, const Pass& ps) {
+        const std::string key =
+            std::string(&M == &base_ ? "base" : "draft") + "|" + (plan ? format_plan(*plan) : "-") + "|" + std::to_string(ps.T);
+        auto it = mk_progs_.find(key);
+        if (it == mk_progs_.end()) {
+            MkProg P;
+            mk_rec_ = &P;
+            try {
+                forward_body(M, C, W, plan, ps);
+            } catch (...) {
+                mk_rec_ = nullptr;
+                throw;
+            }
+            mk_rec_ = nullptr;
+            const unsigned long long G = (unsigned long long)mk_grid();
+            unsigned long long acc = 0;
+            for (auto& op : P.ops) {
+                op.arrivals = mk_op_arrivals(op.type);
+                acc += G * (unsigned long long)op.arrivals;
+                op.target = acc;
+            }
+            P.arrivals = acc;
+            const size_t b0 = sizeof(MkOp) * P.ops.size(), b1 = sizeof(GemvProblem) * P.probs.size(),
+                         b2 = sizeof(AttnProblem) * P.aprobs.size();
+            const size_t o1 = (b0 + 255) / 256 * 256, o2 = o1 + (b1 + 255) / 256 * 256;
+            CUDA_OK(cudaMalloc(&P.dev, o2 + b2 + 16));
+            char* d = static_cast<char*>(P.dev);
+            CUDA_OK(cudaMemcpy(d, P.ops.data(), b0, cudaMemcpyHostToDevice));
+            if (b1) CUDA_OK(cudaMemcpy(d + o1, P.probs.data(), b1, cudaMemcpyHostToDevice));
+            if (b2) CUDA_OK(cudaMemcpy(d + o2, P.aprobs.data(), b2, cudaMemcpyHostToDevice));
+            P.d_ops = reinterpret_cast<MkOp*>(d);
+            P.d_probs = reinterpret_cast<GemvProblem*>(d + o1);
+            P.d_aprobs = reinterpret_cast<AttnProblem*>(d + o2);
+            it = mk_progs_.emplace(key, std::move(P)).first;
+        }
+        MkProg& P = it->second;
+        MkArgs a;
+        a.ops = P.d_ops;
+        a.n_ops = (int)P.ops.size();
+        a.probs = P.d_probs;
+        a.aprobs = P.d_aprobs;
+        a.pass = ps.view;
+        a.kv = C.view();
+        a.tok_arena = arena_;
+        a.tok_idx = ps.tok_idx;
+        a.counter = mk_counter_;
+        a.base = mk_base_;
+        a.prefetch_bytes = mk_prefetch_;
+        const double bytes =
+            P.weight_bytes + (double)M.c.n_layers * 2.0 * ps.view.total * M.kvdim() * dsize(M.c.kv_dtype);
+        static const char* trace_path = std::getenv("ESPEC_MK_TRACE");
+        unsigned long long* tr = nullptr;
+        const size_t tr_n = P.ops.size() * (size_t)mk_grid() * 8;
+        if (trace_path) {
+            CUDA_OK(cudaMalloc(&tr, sizeof(unsigned long long) * tr_n));
+            CUDA_OK(cudaMemsetAsync(tr, 0, sizeof(unsigned long long) * tr_n, stream_));
+            a.trace = tr;
+        }
+        site(M, 6, bytes, [&] { CUDA_OK(launch_decode_mk(a, stream_)); });
+        mk_base_ += P.arrivals;
+        ++launches_;
+        if (trace_path) {
+            // debug timeline: <path>.<model>.T<T>.txt, one line per op:
+            // type epi units then grid x {start, staged, done, arrive} (ns)
+            std::vector<unsigned long long> h(tr_n);
+            CUDA_OK(cudaMemcpyAsync(h.data(), tr, sizeof(unsigned long long) * tr_n, cudaMemcpyDeviceToHost, stream_));
+            CUDA_OK(cudaStreamSynchronize(stream_));
+            cudaFree(tr);
+            const std::string fn = std::string(trace_path) + "." + (&M == &base_ ? "base" : "draft") + ".T" +
+                                   std::to_string(ps.T) + ".txt";
+            if (FILE* f = std::fopen(fn.c_str(), "w")) {
+                const int G = mk_grid();
+                for (size_t k = 0; k < P.ops.size(); ++k) {
+                    std::fprintf(f, "%d %d %d", P.ops[k].type, P.ops[k].epi, P.ops[k].units);
+                    for (int c = 0; c < G; ++c)
+                        for (int e = 0; e < 8; ++e) std::fprintf(f, " %llu", h[(k * G + c) * 8 + e]);
+                    std::fprintf(f, "\n");
+                }
+                std::fclose(f);
+            }
+        }
+    }
+
+    // ---- launch-or-record wrappers (forward_body under forward_mk records ops)
+    void g_gemv(ModelDev& M, int kind, double bytes, int epi, const GemvBatch& b, int n, int T, const Pass& ps,
+                const KvView& kv) {
+        if (mk_rec_) {
+            MkOp op;
+            mk_plan_gemv(op, b.p[0].K, b.p[0].ldw, n);
+            op.epi = epi;
+            op.prob0 = (int)mk_rec_->probs.size();
+            for (int i = 0; i < n; ++i) mk_rec_->probs.push_back(b.p[i]);
+            mk_rec_->ops.push_back(op);
+            mk_rec_->weight_bytes += bytes;
+            return;
+        }
+        site(M, kind, bytes, [&] { launch_gemv(epi, M.c.weight_dtype, b, n, T, ps.view, kv, stream_); });
+        launches_ += chunks(M, T);
+    }
+    void g_embed(ModelDev& M, Workspace& W, const Pass& ps) {
+        const int d = M.c.d_model;
+        if (mk_rec_) {
+            MkOp op;
+            op.type = MK_EMBED;
+            op.emb = M.emb;
+            op.h = W.h;
+            op.stats = W.stats;
+            op.d = d;
+            op.stat_tiles = (d + kStatTile - 1) / kStatTile;
+            mk_rec_->ops.push_back(op);
+            return;
+        }
+        launch_embed(M.c.weight_dtype, M.emb, d, arena_, ps.tok_idx, ps.T, W.h, W.stats, stream_);
+        ++launches_;
+    }
+    void g_add(Workspace& W, const float* a, int d, int T) {
+        if (mk_rec_) {
+            MkOp op;
+            op.type = MK_ADD;
+            op.h = W.h;
+            op.a = a;
+            op.stats = W.stats;
+            op.d = d;
+            op.stat_tiles = (d + kStatTile - 1) / kStatTile;
+            mk_rec_->ops.push_back(op);
+            return;
+        }
+        launch_add_stats(W.h, a, d, T, W.stats, stream_);
+        ++launches_;
+    }
+
+    void forward_body(ModelDev& M, Cache& C, Workspace& W, const LayerPlan* plan, const Pass& ps) {
         const ModelCfg& c = M.c;
         const int d = c.d_model, T = ps.T, qd = M.qdim(), f = M.f_loc();
         const int tiles = (d + kStatTile - 1) / kStatTile;
         const int wdt = c.weight_dtype;
         const KvView kv = C.view();
         check_comm();
-        launch_embed(wdt, M.emb, d, arena_, ps.tok_idx, T, W.h, W.stats, stream_);
-        ++launches_;
+        g_embed(M, W, ps);
         std::vector<std::vector<int>> groups;
         if (plan) groups = plan->groups;
         else
@@ -1170,12 +1345,10 @@ public:
                 p.W = L.wqkv; p.K = d; p.N = M.qkv_N(); p.ldw = M.qkv_ld();
                 p.x = W.h; p.ldx = d; p.gain = L.ga; p.stats_in = W.stats; p.stat_tiles_in = tiles; p.eps = c.norm_eps;
                 p.out = W.q + (size_t)i * kChunk * qd; p.ldo = qd;
-                p.n_heads = M.qh(); p.n_kv = M.kvh(); p.dh = c.d_head; p.layer = g[i]; p.rope_theta = c.rope_theta;
+                p.n_heads = M.qh(); p.n_kv = M.kvh(); p.dh = c.d_head; p.layer = g[i]; p.rope = M.rope;
                 qb.p[i] = p;
             }
-            site(M, 0, gemv_bytes(M, d, M.qkv_ld(), M.qkv_N(), T, n),
-                 [&] { launch_gemv(EPI_QKV, wdt, qb, n, T, ps.view, kv, stream_); });
-            launches_ += chunks(M, T);
+            g_gemv(M, 0, gemv_bytes(M, d, M.qkv_ld(), M.qkv_N(), T, n), EPI_QKV, qb, n, T, ps, kv);
             attention(M, C, W, g, ps);
             if (n == 1) {
                 row_parallel_resid(M, W, M.L[g[0]].wo, qd, W.mixed, qd, 2, T, ps, kv);
@@ -1188,8 +1361,7 @@ public:
                     p.out = W.attn + (size_t)i * kChunk * d; p.ldo = d;
                     ob.p[i] = p;
                 }
-                site(M, 2, gemv_bytes(M, qd, d, d, T, n), [&] { launch_gemv(EPI_STORE, wdt, ob, n, T, ps.view, kv, stream_); });
-                launches_ += chunks(M, T);
+                g_gemv(M, 2, gemv_bytes(M, qd, d, d, T, n), EPI_STORE, ob, n, T, ps, kv);
                 if (tp()) {
                     // ONE all-reduce for the whole group's attention outputs
                     const int per = (size_t)n * T * d <= comm_.slot_floats ? n : 1;
@@ -1208,8 +1380,7 @@ public:
             for (int i = 0; i < n; ++i) {
                 const LayerDev& L = M.L[g[i]];
                 if (n > 1) {
-                    launch_add_stats(W.h, W.attn + (size_t)i * kChunk * d, d, T, W.stats, stream_);
-                    ++launches_;
+                    g_add(W, W.attn + (size_t)i * kChunk * d, d, T);
                 }
                 GemvBatch ub;
                 GemvProblem p = gp(W, 0);
@@ -1217,9 +1388,7 @@ public:
                 p.x = W.h; p.ldx = d; p.gain = L.gm; p.stats_in = W.stats; p.stat_tiles_in = tiles; p.eps = c.norm_eps;
                 p.out = W.act; p.ldo = f;
                 ub.p[0] = p;
-                site(M, 3, gemv_bytes(M, d, M.gu_ld(), 2 * f, T, 1),
-                     [&] { launch_gemv(EPI_SILU, wdt, ub, 1, T, ps.view, kv, stream_); });
-                launches_ += chunks(M, T);
+                g_gemv(M, 3, gemv_bytes(M, d, M.gu_ld(), 2 * f, T, 1), EPI_SILU, ub, 1, T, ps, kv);
                 row_parallel_resid(M, W, L.wd, f, W.act, f, 4, T, ps, kv);
             }
         }
@@ -1242,6 +1411,18 @@ public:
                 a.ws = W.attn_ws + W.attn_ws_slot * i;
                 a.tickets = W.attn_tickets + (size_t)W.attn_ticket_slot * i;
                 ab.p[i] = a;
+            }
+            if (mk_rec_) {
+                MkOp op;
+                op.type = MK_ATTN;
+                op.nprob = (int)g.size();
+                op.prob0 = (int)mk_rec_->aprobs.size();
+                op.n_heads = M.qh();
+                op.G = M.qh() / M.kvh();
+                op.dh = M.c.d_head;
+                for (size_t i = 0; i < g.size(); ++i) mk_rec_->aprobs.push_back(ab.p[i]);
+                mk_rec_->ops.push_back(op);
+                continue;
             }
             const double kvb = (double)g.size() * 2.0 * ps.view.total * M.kvdim() * dsize(M.c.kv_dtype);
             site(M, 1, kvb, [&] { launch_attention(ab, (int)g.size(), M.qh(), v, kv, stream_); });
@@ -1893,6 +2074,25 @@ private:
     int site_which_ = -1, site_kind_ = -1, site_n_ = 0;
     double site_ms_ = 0, site_bytes_ = 0;
     long long h2d_bytes_ = 0, d2h_bytes_ = 0;
+    // decode megakernel: programs cached per (model, plan, T); the recording
+    // target while forward() builds one; the device arrival counter
+    struct MkProg {
+        std::vector<MkOp> ops;
+        std::vector<GemvProblem> probs;
+        std::vector<AttnProblem> aprobs;
+        void* dev = nullptr;  // ops | probs | aprobs
+        MkOp* d_ops = nullptr;
+        GemvProblem* d_probs = nullptr;
+        AttnProblem* d_aprobs = nullptr;
+        unsigned long long arrivals = 0;
+        double weight_bytes = 0;
+    };
+    std::map<std::string, MkProg> mk_progs_;
+    MkProg* mk_rec_ = nullptr;
+    unsigned long long* mk_counter_ = nullptr;
+    unsigned long long mk_base_ = 0;
+    int mk_mode_ = 0;  // ESPEC_MK=1 enables the decode megakernel (measured slower than the per-kernel path today)
+    long long mk_prefetch_ = 0;  // ESPEC_MK_PF_KB: L2 prefetch distance per SM
 };
 
 std::unique_ptr<Engine> make_engine(const ModelCfg& base, const ModelCfg& draft, const RunCfg& run, int device,

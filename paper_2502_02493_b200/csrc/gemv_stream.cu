@@ -30,6 +30,8 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "ptx.cuh"
+#include "sgemv_epi.cuh"
 
 namespace espec_dev {
 
@@ -106,194 +108,8 @@ static size_t sg_smem_bytes(int TM, int kcb) {
 }
 
 // ---------------------------------------------------------------------------
-// PTX helpers: mbarrier, 1-D TMA bulk copy, PDL
-// ---------------------------------------------------------------------------
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* b, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(b)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-
-__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-    asm volatile(
-        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-        "{%0,%1,%2,%3};"
-        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-
-// Ticket for "last one finishes": acq_rel at gpu scope orders this warp's
-// preceding partial stores (ordered before lane 0 by __syncwarp) before the
-// increment, and the winner's subsequent loads after it.
-__device__ __forceinline__ unsigned ticket_acq_rel(unsigned* p) {
-    unsigned old;
-    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(p) : "memory");
-    return old;
-}
-
-__device__ __forceinline__ bool sg_better(float v, int i, float bv, int bi) { return v > bv || (v == bv && i < bi); }
-
-__device__ __forceinline__ long long sg_kv_off(const KvView& kv, int layer, int kind, int head, int row) {
-    const int page = kv.page_table[row / kv.page_rows];
-    const int r = row % kv.page_rows;
-    return (long long)page * kv.page_elems + ((((long long)layer * 2 + kind) * kv.n_kv + head) * kv.page_rows + r) * kv.dh;
-}
-
-// ---------------------------------------------------------------------------
 // kernel
 // ---------------------------------------------------------------------------
-
-// Unit epilogue, run by one epilogue warp: lane = column within the 32-column
-// group, v[t] = the unit's full sum for row t (after the k-chunk reduction).
-template <int TM, int EPI>
-__device__ __forceinline__ void sg_epilogue(const SgLaunch& L, const GemvProblem& P, int g, const float (&v)[TM],
-                                            int lane) {
-    const int T = L.T, t0 = L.t0;
-    const int c = g * 32 + lane;
-    if constexpr (EPI == EPI_STORE) {
-#pragma unroll
-        for (int t = 0; t < TM; ++t)
-            if (t < T && c < P.N) P.out[(size_t)(t0 + t) * P.ldo + c] = v[t];
-    } else if constexpr (EPI == EPI_RESID) {
-        // h_mid = h + attn / h_next = h_mid + mlp (proj/src/draft_engine.cpp:15-19) + row stats
-#pragma unroll
-        for (int t = 0; t < TM; ++t) {
-            if (t >= T) break;
-            float sq = 0.f;
-            if (c < P.N) {
-                const float y = __fadd_rn(P.resid[(size_t)(t0 + t) * P.ldr + c], v[t]);
-                P.out[(size_t)(t0 + t) * P.ldo + c] = y;
-                sq = y * y;
-            }
-            sq = warp_sum(sq);
-            if (lane == 0) P.stats_out[(t0 + t) * P.stat_tiles_out + g] = sq;
-        }
-    } else if constexpr (EPI == EPI_SILU) {
-        // packed group = [gate 16 | up 16]: silu(gate) * up (proj/src/model.cpp:197-210)
-        const int a = g * 16 + lane;
-#pragma unroll
-        for (int t = 0; t < TM; ++t) {
-            const float up = __shfl_down_sync(0xffffffffu, v[t], 16);
-            if (t < T && lane < 16 && a < P.N / 2)
-                P.out[(size_t)(t0 + t) * P.ldo + a] = __fmul_rn(__fdiv_rn(v[t], __fadd_rn(1.0f, expf(-v[t]))), up);
-        }
-    } else if constexpr (EPI == EPI_QKV) {
-        // q = rope(h.Wq), k = rope(h.Wk), v = h.Wv ; K/V into the paged cache
-        // (proj/src/model.cpp:130-138, rotary proj/src/matrix.cpp:159-194)
-        const int qd = P.n_heads * P.dh, kd = P.n_kv * P.dh;
-        const int region = c < qd ? 0 : (c < qd + kd ? 1 : 2);
-        const int base = region == 0 ? 0 : (region == 1 ? qd : qd + kd);
-        const int within = c - base;
-        const int head = within / P.dh, i = within - head * P.dh;
-        const double inv_freq = pow((double)P.rope_theta, -2.0 * (i >> 1) / (double)P.dh);
-#pragma unroll
-        for (int t = 0; t < TM; ++t) {
-            const float other = __shfl_xor_sync(0xffffffffu, v[t], 1);
-            if (t >= T || c >= P.N) continue;
-            float y = v[t];
-            if (region < 2) {
-                const double th = (double)L.pass.pos[t0 + t] * inv_freq;
-                const float cs = (float)cos(th), sn = (float)sin(th);
-                y = (i & 1) ? __fadd_rn(__fmul_rn(other, sn), __fmul_rn(v[t], cs))
-                            : __fsub_rn(__fmul_rn(v[t], cs), __fmul_rn(other, sn));
-            }
-            if (region == 0) {
-                P.out[(size_t)(t0 + t) * P.ldo + c] = y;
-            } else {
-                const long long off = sg_kv_off(L.kv, P.layer, region - 1, head, L.pass.rows[t0 + t]) + i;
-                if (L.kv.dtype == DT_BF16) reinterpret_cast<__nv_bfloat16*>(L.kv.pool)[off] = __float2bfloat16_rn(y);
-                else reinterpret_cast<float*>(L.kv.pool)[off] = y;
-            }
-        }
-    } else if constexpr (EPI == EPI_ARGMAX) {
-        // logits = norm(h).E^T ; greedy pick = first maximum (proj/src/matrix.cpp:196-202)
-#pragma unroll
-        for (int t = 0; t < TM; ++t) {
-            if (t >= T) break;
-            float bv = -INFINITY;
-            int bi = 0x7fffffff;
-            if (c < P.vocab) {
-                if (P.logits) P.logits[(size_t)(t0 + t) * P.ld_logits + c] = v[t];
-                bv = v[t];
-                bi = c;
-            }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-                if (sg_better(ov, oi, bv, bi)) {
-                    bv = ov;
-                    bi = oi;
-                }
-            }
-            if (lane == 0) {
-                P.am_val[(t0 + t) * L.ngroups + g] = bv;
-                P.am_idx[(t0 + t) * L.ngroups + g] = bi;
-            }
-        }
-        // last group to finish reduces the per-group maxima (fixed-order-free:
-        // max with lowest-index tie-break is order independent)
-        __syncwarp();
-        unsigned last = 0;
-        if (lane == 0) {
-            last = ticket_acq_rel(&P.tickets[L.ngroups]) == (unsigned)L.ngroups - 1 ? 1u : 0u;
-            if (last) P.tickets[L.ngroups] = 0u;
-        }
-        last = __shfl_sync(0xffffffffu, last, 0);
-        if (last) {
-            for (int t = 0; t < T; ++t) {
-                float fv = -INFINITY;
-                int fi = 0x7fffffff;
-                for (int q = lane; q < L.ngroups; q += 32) {
-                    const float ov = __ldcg(&P.am_val[(t0 + t) * L.ngroups + q]);
-                    const int oi = __ldcg(&P.am_idx[(t0 + t) * L.ngroups + q]);
-                    if (sg_better(ov, oi, fv, fi)) {
-                        fv = ov;
-                        fi = oi;
-                    }
-                }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    const float ov = __shfl_xor_sync(0xffffffffu, fv, o);
-                    const int oi = __shfl_xor_sync(0xffffffffu, fi, o);
-                    if (sg_better(ov, oi, fv, fi)) {
-                        fv = ov;
-                        fi = oi;
-                    }
-                }
-                if (lane == 0) {
-                    P.tok_out[t0 + t] = fi + P.col_base;
-                    if (P.tok_val) P.tok_val[t0 + t] = fv;
-                }
-            }
-        }
-    }
-}
 
 template <int TM, int EPI>
 __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid_constant__ SgLaunch L) {
@@ -429,7 +245,7 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
                             if (jj + c < L.nK) v[t] += ld[c][t];
                 }
             }
-            sg_epilogue<TM, EPI>(L, P, g, v, lane);
+            sg_epilogue<TM, EPI>(SgEpiCtx{L.pass, L.kv, L.T, L.t0, L.ngroups}, P, g, v, lane);
         }
         return;
     }

@@ -15,6 +15,8 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "ptx.cuh"
+#include "attn_mma.cuh"
 
 namespace espec_dev {
 
@@ -67,28 +69,6 @@ struct GemvLaunch {
 
 __device__ __forceinline__ bool am_better(float v, int i, float bv, int bi) {
     return v > bv || (v == bv && i < bi);
-}
-
-__device__ __forceinline__ long long kv_off(const KvView& kv, int layer, int kind, int head, int row) {
-    const int page = kv.page_table[row / kv.page_rows];
-    const int r = row % kv.page_rows;
-    return (long long)page * kv.page_elems +
-           ((((long long)layer * 2 + kind) * kv.n_kv + head) * kv.page_rows + r) * kv.dh;
-}
-
-__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-    asm volatile(
-        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-        "{%0,%1,%2,%3};"
-        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-
-__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
-    const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
-    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-                 : "r"(a));
 }
 
 template <int TM, int EPI>
@@ -259,15 +239,14 @@ __global__ void __launch_bounds__(kThreads) gemv_f32_kernel(const __grid_constan
         const int within = c - base;
         const int head = within / P.dh, i = within - head * P.dh;
         const int pair = i >> 1;
-        const double inv_freq = pow((double)P.rope_theta, -2.0 * pair / (double)P.dh);
 #pragma unroll
         for (int t = 0; t < TM; ++t) {
             const float other = __shfl_xor_sync(0xffffffffu, s[t], 1);
             if (t >= T || c >= P.N) continue;
             float y = s[t];
             if (region < 2) {
-                const double th = (double)L.pass.pos[t0 + t] * inv_freq;
-                const float cs = (float)cos(th), sn = (float)sin(th);
+                const float2 cs_sn = P.rope[(size_t)L.pass.pos[t0 + t] * (P.dh >> 1) + pair];
+                const float cs = cs_sn.x, sn = cs_sn.y;
                 const float x0 = (i & 1) ? other : s[t];
                 const float x1 = (i & 1) ? s[t] : other;
                 y = (i & 1) ? __fadd_rn(__fmul_rn(x0, sn), __fmul_rn(x1, cs))
@@ -536,13 +515,6 @@ struct AttnLaunch {
     int n_heads, G, splits, pblocks;
 };
 
-__device__ __forceinline__ bool visible(const PassView& P, int t, int j) {
-    if (j >= P.total) return false;
-    if (j < P.vis_end[t]) return true;
-    const int o = j - P.tree_base;
-    return o >= 0 && o < 64 && ((P.anc[t] >> o) & 1ull);
-}
-
 template <typename KT>
 __global__ void __launch_bounds__(kAttnThreads) attn_kernel(const __grid_constant__ AttnLaunch L) {
     extern __shared__ __align__(16) float sm[];
@@ -690,328 +662,14 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(const __grid_constan
 // combine through a split workspace, last CTA in fixed order.
 // ---------------------------------------------------------------------------
 
-__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
-    __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
-    return *reinterpret_cast<uint32_t*>(&v);
-}
-
-__device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], const void* p) {
-    const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
-    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-                 : "r"(a));
-}
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    const uint32_t a = (uint32_t)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(a), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
-
 template <int DH>
 __global__ void __launch_bounds__(128) attn_mma_kernel(const __grid_constant__ AttnLaunch L) {
     extern __shared__ __align__(16) unsigned char smraw[];
     __shared__ unsigned s_last;
-    constexpr int LDK = DH + 8;           // bf16 elements per smem row (16 B pad)
-    constexpr int NT = DH / 8;            // n8 tiles over head dims
     pdl_wait();
     pdl_trigger();
-    const AttnProblem& A = L.b.p[blockIdx.z];
-    const int G = L.G, H = L.n_heads, T = L.pass.T, P = T * G;
-    const int n_kv = L.kv.n_kv;
-    const int hk = blockIdx.y % n_kv, mt = blockIdx.y / n_kv;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gid = lane >> 2, tig = lane & 3;
-    const int split = blockIdx.x * 4 + warp;
-    const int j0 = split * 64;
-    const int nr = max(0, min(64, L.pass.total - j0));
-    // one 64-row page buffer per warp: K first, then V into the same buffer
-    // once the scores are computed (halves shared memory: 3 CTAs per SM)
-    __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(smraw) + (size_t)warp * 64 * LDK;
-    __nv_bfloat16* Vs = Ks;
-    const __nv_bfloat16* pool = reinterpret_cast<const __nv_bfloat16*>(L.kv.pool);
-    constexpr int CH = DH / 8;  // 16-byte chunks per row
-    const __nv_bfloat16* vg = nullptr;
-    if (nr > 0) {  // 64-row split = one page: K and V of this head are contiguous 64 x DH runs
-        const __nv_bfloat16* kg = pool + kv_off(L.kv, A.layer, 0, hk, j0);
-        vg = pool + kv_off(L.kv, A.layer, 1, hk, j0);
-#pragma unroll 8
-        for (int i = lane; i < 64 * CH; i += 32) {
-            const int r = i / CH, c = (i % CH) * 8;
-            cp_async16(Ks + r * LDK + c, kg + (size_t)r * DH + c);
-        }
-        cp_async_commit();
-    }
-    // Q A-fragments (pairs 16mt + gid / +8), scaled later on the scores
-    uint32_t qa[DH / 16][4];
-    {
-        const int p0 = mt * 16 + gid, p1 = p0 + 8;
-        const float* q0 = nullptr;
-        const float* q1 = nullptr;
-        if (p0 < P) q0 = A.q + (size_t)(p0 / G) * H * DH + (hk * G + p0 % G) * DH;
-        if (p1 < P) q1 = A.q + (size_t)(p1 / G) * H * DH + (hk * G + p1 % G) * DH;
-#pragma unroll
-        for (int s = 0; s < DH / 16; ++s) {
-            const int c = s * 16 + 2 * tig;
-            float2 a = q0 ? *reinterpret_cast<const float2*>(q0 + c) : make_float2(0.f, 0.f);
-            float2 b = q1 ? *reinterpret_cast<const float2*>(q1 + c) : make_float2(0.f, 0.f);
-            float2 cc = q0 ? *reinterpret_cast<const float2*>(q0 + c + 8) : make_float2(0.f, 0.f);
-            float2 d = q1 ? *reinterpret_cast<const float2*>(q1 + c + 8) : make_float2(0.f, 0.f);
-            qa[s][0] = pack_bf16x2(a.x, a.y);
-            qa[s][1] = pack_bf16x2(b.x, b.y);
-            qa[s][2] = pack_bf16x2(cc.x, cc.y);
-            qa[s][3] = pack_bf16x2(d.x, d.y);
-        }
-    }
-    float m_r[2] = {-INFINITY, -INFINITY}, l_r[2] = {0.f, 0.f};
-    float o[NT][4];
-#pragma unroll
-    for (int d = 0; d < NT; ++d) o[d][0] = o[d][1] = o[d][2] = o[d][3] = 0.f;
-    if (nr > 0) {
-        cp_async_wait<0>();
-        __syncwarp();
-        float sc[8][4];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) sc[j][0] = sc[j][1] = sc[j][2] = sc[j][3] = 0.f;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-#pragma unroll
-            for (int s = 0; s < DH / 16; s += 2) {
-                uint32_t b[4];
-                ldsm_x4(b, Ks + (j * 8 + (lane & 7)) * LDK + s * 16 + (lane >> 3) * 8);
-                mma_bf16_16816(sc[j], qa[s], b[0], b[1]);
-                mma_bf16_16816(sc[j], qa[s + 1], b[2], b[3]);
-            }
-        }
-        // K consumed: stream V into the same buffer while the softmax runs
-        __syncwarp();
-#pragma unroll 8
-        for (int i = lane; i < 64 * CH; i += 32) {
-            const int r = i / CH, c = (i % CH) * 8;
-            cp_async16(Vs + r * LDK + c, vg + (size_t)r * DH + c);
-        }
-        cp_async_commit();
-        // scale + mask, row max / exp / sum over this split's 64 keys
-        const float inv_sqrt = 1.0f / sqrtf((float)DH);
-        const int pr[2] = {mt * 16 + gid, mt * 16 + gid + 8};
-        float mx[2] = {-INFINITY, -INFINITY};
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int ri = e >> 1;
-                const int key = j * 8 + 2 * tig + (e & 1);
-                const bool ok = pr[ri] < P && key < nr && visible(L.pass, pr[ri] / G, j0 + key);
-                sc[j][e] = ok ? __fmul_rn(sc[j][e], inv_sqrt) : -INFINITY;
-                mx[ri] = fmaxf(mx[ri], sc[j][e]);
-            }
-#pragma unroll
-        for (int ri = 0; ri < 2; ++ri) {
-            mx[ri] = fmaxf(mx[ri], __shfl_xor_sync(0xffffffffu, mx[ri], 1));
-            mx[ri] = fmaxf(mx[ri], __shfl_xor_sync(0xffffffffu, mx[ri], 2));
-        }
-        float sum[2] = {0.f, 0.f};
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int ri = e >> 1;
-                const float v = sc[j][e] == -INFINITY ? 0.f : expf(sc[j][e] - mx[ri]);
-                sc[j][e] = v;
-                sum[ri] += v;
-            }
-#pragma unroll
-        for (int ri = 0; ri < 2; ++ri) {
-            sum[ri] += __shfl_xor_sync(0xffffffffu, sum[ri], 1);
-            sum[ri] += __shfl_xor_sync(0xffffffffu, sum[ri], 2);
-            m_r[ri] = mx[ri];
-            l_r[ri] = sum[ri];
-        }
-        cp_async_wait<0>();
-        __syncwarp();
-        // O = P V
-#pragma unroll
-        for (int s = 0; s < 4; ++s) {  // 16-key steps
-            uint32_t pa[4];
-            pa[0] = pack_bf16x2(sc[2 * s][0], sc[2 * s][1]);
-            pa[1] = pack_bf16x2(sc[2 * s][2], sc[2 * s][3]);
-            pa[2] = pack_bf16x2(sc[2 * s + 1][0], sc[2 * s + 1][1]);
-            pa[3] = pack_bf16x2(sc[2 * s + 1][2], sc[2 * s + 1][3]);
-#pragma unroll
-            for (int d = 0; d < NT; d += 2) {
-                uint32_t b[4];
-                // matrices: (keys 16s..+7, dims 8d), (keys +8, dims 8d), (keys 16s.., dims 8d+8), (keys +8, dims 8d+8)
-                const int mi = lane >> 3;
-                ldsm_x4_t(b, Vs + (s * 16 + (mi & 1) * 8 + (lane & 7)) * LDK + d * 8 + (mi >> 1) * 8);
-                mma_bf16_16816(o[d], pa, b[0], b[1]);
-                mma_bf16_16816(o[d + 1], pa, b[2], b[3]);
-            }
-        }
-    }
-    __syncthreads();  // K/V smem free: reuse for the warp combine
-    float* Os = reinterpret_cast<float*>(smraw);           // [4][16][DH]
-    float* Ms = Os + 4 * 16 * DH;                          // [4][16]
-    float* Ls = Ms + 64;                                   // [4][16]
-    float* Fw = Ls + 64;                                   // [4][16] warp weights exp(m_w - M)
-    float* Rm = Fw + 64;                                   // [16] row max
-    float* Rd = Rm + 16;                                   // [16] row denominator
-#pragma unroll
-    for (int d = 0; d < NT; ++d) {
-        const int c = d * 8 + 2 * tig;
-        *reinterpret_cast<float2*>(&Os[(warp * 16 + gid) * DH + c]) = make_float2(o[d][0], o[d][1]);
-        *reinterpret_cast<float2*>(&Os[(warp * 16 + gid + 8) * DH + c]) = make_float2(o[d][2], o[d][3]);
-    }
-    if (tig == 0) {
-        Ms[warp * 16 + gid] = m_r[0];
-        Ms[warp * 16 + gid + 8] = m_r[1];
-        Ls[warp * 16 + gid] = l_r[0];
-        Ls[warp * 16 + gid + 8] = l_r[1];
-    }
-    __syncthreads();
-    if (threadIdx.x < 16) {  // per-row weights, fixed warp order
-        const int r = threadIdx.x;
-        float M = -INFINITY;
-#pragma unroll
-        for (int w = 0; w < 4; ++w) M = fmaxf(M, Ms[w * 16 + r]);
-        float den = 0.f;
-#pragma unroll
-        for (int w = 0; w < 4; ++w) {
-            const float m = Ms[w * 16 + r];
-            float f = 0.f;
-            if (M != -INFINITY && m != -INFINITY) {
-                f = expf(m - M);
-                den = __fmaf_rn(f, Ls[w * 16 + r], den);
-            }
-            Fw[w * 16 + r] = f;
-        }
-        Rm[r] = M;
-        Rd[r] = den;
-    }
-    __syncthreads();
-    const int nchunks = gridDim.x;
-    constexpr int PS = DH + 4;  // workspace row: DH values, M, den (float4-aligned)
-    float* wsb = A.ws + (((size_t)blockIdx.x * gridDim.y + blockIdx.y) * 16) * PS;
-    {
-        // thread -> (row r, 16 consecutive dims)
-        constexpr int CPR = DH / 16;  // threads per row
-        for (int it = threadIdx.x; it < 16 * CPR; it += 128) {
-            const int r = it / CPR, c0 = (it % CPR) * 16;
-            float4 acc[4];
-#pragma unroll
-            for (int v = 0; v < 4; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-            for (int w = 0; w < 4; ++w) {
-                const float f = Fw[w * 16 + r];
-#pragma unroll
-                for (int v = 0; v < 4; ++v) {
-                    const float4 x = *reinterpret_cast<const float4*>(&Os[(w * 16 + r) * DH + c0 + 4 * v]);
-                    acc[v].x = __fmaf_rn(f, x.x, acc[v].x);
-                    acc[v].y = __fmaf_rn(f, x.y, acc[v].y);
-                    acc[v].z = __fmaf_rn(f, x.z, acc[v].z);
-                    acc[v].w = __fmaf_rn(f, x.w, acc[v].w);
-                }
-            }
-            const int p = mt * 16 + r;
-            if (nchunks == 1) {
-                if (p < P) {
-                    const float den = Rd[r];
-                    float* o = A.out + (size_t)(p / G) * H * DH + (hk * G + p % G) * DH + c0;
-#pragma unroll
-                    for (int v = 0; v < 4; ++v)
-                        *reinterpret_cast<float4*>(o + 4 * v) =
-                            den > 0.f ? make_float4(acc[v].x / den, acc[v].y / den, acc[v].z / den, acc[v].w / den)
-                                      : make_float4(0.f, 0.f, 0.f, 0.f);
-                }
-            } else {
-#pragma unroll
-                for (int v = 0; v < 4; ++v) *reinterpret_cast<float4*>(wsb + r * PS + c0 + 4 * v) = acc[v];
-                if (c0 == 0) {
-                    wsb[r * PS + DH] = Rm[r];
-                    wsb[r * PS + DH + 1] = Rd[r];
-                }
-            }
-        }
-    }
-    if (nchunks == 1) return;
-    // Cross-CTA combine (last CTA of this (kv head, m-tile)), fixed chunk order.
-    __syncthreads();
-    unsigned* ticket = A.tickets + blockIdx.y;
-    if (threadIdx.x == 0) {
-        unsigned tk;
-        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(tk) : "l"(ticket) : "memory");
-        s_last = (tk == (unsigned)nchunks - 1) ? 1u : 0u;
-        if (s_last) *ticket = 0u;
-    }
-    __syncthreads();
-    if (!s_last) return;
-    const size_t cstride = (size_t)gridDim.y * 16 * PS;
-    const float* base = A.ws + ((size_t)blockIdx.y * 16) * PS;
-    // per-row chunk weights f = exp(m_ch - M) and denominator, once per row
-    float* fac = Os;              // [nchunks][16]
-    float* sden = Os + 64 * 16;   // [16]
-    // (m, l) of every chunk: one float2 load each, all issued together
-    float2* ml = reinterpret_cast<float2*>(Os + 64 * 16 + 16);  // [nchunks][16]
-    for (int i = threadIdx.x; i < nchunks * 16; i += 128) {
-        const int ch = i >> 4, r = i & 15;
-        ml[i] = __ldcg(reinterpret_cast<const float2*>(base + ch * cstride + r * PS + DH));
-    }
-    __syncthreads();
-    if (threadIdx.x < 16) {
-        const int r = threadIdx.x;
-        float M = -INFINITY;
-        for (int ch = 0; ch < nchunks; ++ch) M = fmaxf(M, ml[ch * 16 + r].x);
-        float den = 0.f;
-        for (int ch = 0; ch < nchunks; ++ch) {
-            const float m = ml[ch * 16 + r].x;
-            float f = 0.f;
-            if (M != -INFINITY && m != -INFINITY) {
-                f = expf(m - M);
-                den = __fmaf_rn(f, ml[ch * 16 + r].y, den);
-            }
-            fac[ch * 16 + r] = f;
-        }
-        sden[r] = den;
-    }
-    __syncthreads();
-    constexpr int CPR = DH / 16;
-    for (int it = threadIdx.x; it < 16 * CPR; it += 128) {
-        const int r = it / CPR, c0 = (it % CPR) * 16;
-        const int p = mt * 16 + r;
-        if (p >= P) continue;
-        float4 acc[4];
-#pragma unroll
-        for (int v = 0; v < 4; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int ch0 = 0; ch0 < nchunks; ch0 += 4) {
-            float4 x[4][4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-#pragma unroll
-                for (int v = 0; v < 4; ++v)
-                    x[q][v] = ch0 + q < nchunks
-                                  ? __ldcg(reinterpret_cast<const float4*>(base + (ch0 + q) * cstride + r * PS + c0 + 4 * v))
-                                  : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                if (ch0 + q >= nchunks) break;
-                const float f = fac[(ch0 + q) * 16 + r];
-#pragma unroll
-                for (int v = 0; v < 4; ++v) {
-                    acc[v].x = __fmaf_rn(f, x[q][v].x, acc[v].x);
-                    acc[v].y = __fmaf_rn(f, x[q][v].y, acc[v].y);
-                    acc[v].z = __fmaf_rn(f, x[q][v].z, acc[v].z);
-                    acc[v].w = __fmaf_rn(f, x[q][v].w, acc[v].w);
-                }
-            }
-        }
-        const float den = sden[r];
-        float* o = A.out + (size_t)(p / G) * H * DH + (hk * G + p % G) * DH + c0;
-#pragma unroll
-        for (int v = 0; v < 4; ++v)
-            *reinterpret_cast<float4*>(o + 4 * v) =
-                den > 0.f ? make_float4(acc[v].x / den, acc[v].y / den, acc[v].z / den, acc[v].w / den)
-                          : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
+    attn_mma_item<DH>(L.b.p[blockIdx.z], L.pass, L.kv, L.n_heads, L.G, blockIdx.x, blockIdx.y, gridDim.x, gridDim.y,
+                      smraw, &s_last, threadIdx.x, 1);
 }
 
 template <int DH>
@@ -1023,7 +681,7 @@ static void attn_mma_launch(const AttnLaunch& L, int nprob, cudaStream_t s) {
     }
     const int mtiles = (L.pass.T * L.G + 15) / 16;
     dim3 grid((splits + 3) / 4, L.kv.n_kv * mtiles, nprob);
-    const size_t smem = std::max<size_t>((size_t)4 * 64 * (DH + 8) * 2, (size_t)(4 * 16 * DH + 256) * 4);
+    const size_t smem = std::max<size_t>((size_t)4 * 64 * (DH + 8) * 2 + 64, (size_t)(4 * 16 * DH + 256) * 4);
     static bool configured = false;
     if (!configured) {
         CK(cudaFuncSetAttribute(attn_mma_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -72,7 +72,7 @@ struct GemvProblem {
     int stat_tiles_out = 0;
     // EPI_QKV
     int n_heads = 0, n_kv = 0, dh = 0, layer = 0;
-    float rope_theta = 10000.f;
+    const float2* rope = nullptr;  // [position][dh/2] (cos, sin), see ModelDev::build_rope
     // EPI_ARGMAX
     int vocab = 0;
     float* logits = nullptr;  // [T][ld_logits] or nullptr
@@ -288,6 +288,45 @@ struct GatherColsArgs {
 void launch_allgather_cols(CommView& c, const GatherColsArgs& a, cudaStream_t s);
 // vocab-parallel argmax: (val, idx) per row from every rank -> first maximum
 void launch_allgather_argmax(CommView& c, int T, const float* val, const int* idx, int* tok_out, cudaStream_t s);
+
+// ---- decode megakernel (decode_mk.cu): one persistent launch per decode pass
+enum MkOpType : int { MK_EMBED = 0, MK_GEMV = 1, MK_ATTN = 2, MK_ADD = 3 };
+struct MkOp {
+    int type = 0, epi = 0, nprob = 0, prob0 = 0;
+    // GEMV: the stream-K plan of sgemv_plan (identical units and reduction order)
+    int KT = 0, kcb = 0, nK = 0, ngroups = 0, units = 0, xld = 0;
+    int rotate = 0;                  // rotated unit order (split-K ops)
+    int arrivals = 0;                // arrivals per CTA when the op completes (1)
+    unsigned long long target = 0;   // cumulative arrivals (launch-relative) at completion
+    // ATTN: AttnProblem[prob0 .. prob0+nprob)
+    int n_heads = 0, G = 0, dh = 0;
+    // EMBED (h = emb[tok]) / ADD (h += a); both write row stats
+    const void* emb = nullptr;
+    float* h = nullptr;
+    const float* a = nullptr;
+    float* stats = nullptr;
+    int d = 0, stat_tiles = 0;
+};
+struct MkArgs {
+    const MkOp* ops = nullptr;
+    int n_ops = 0;
+    const GemvProblem* probs = nullptr;
+    const AttnProblem* aprobs = nullptr;
+    PassView pass;
+    KvView kv;
+    const int* tok_arena = nullptr;  // EMBED: token of row t = tok_arena[tok_idx[t]]
+    const int* tok_idx = nullptr;
+    unsigned long long* counter = nullptr;  // monotonic arrival counter
+    unsigned long long base = 0;            // its value when this launch starts
+    unsigned long long* trace = nullptr;    // optional [n_ops][grid][4] timeline
+    long long prefetch_bytes = 0;           // per-CTA L2 prefetch distance ahead of the ring
+    int stages = 0;
+};
+int mk_max_rows();                                   // T limit of a megakernel pass
+int mk_grid();                                       // CTAs (one per SM)
+int mk_op_arrivals(int type);
+void mk_plan_gemv(MkOp& op, int K, int ldw, int nprob);
+cudaError_t launch_decode_mk(const MkArgs& a, cudaStream_t s);
 
 // Deterministic N(0, sd) init from a counter hash (perf-mode weights).
 void launch_fill_normal(int dtype, void* dst, long long n, float sd, uint64_t seed, cudaStream_t s);

@@ -131,9 +131,8 @@ __device__ __forceinline__ void tc_epilogue(const TcLaunch& L, int t, int g, con
             const int head = within / P.dh, i = within - head * P.dh;
             float y0 = v[j], y1 = v[j + 1];
             if (region < 2) {
-                const double inv_freq = pow((double)P.rope_theta, -2.0 * (i >> 1) / (double)P.dh);
-                const double th = (double)pos * inv_freq;
-                const float cs = (float)cos(th), sn = (float)sin(th);
+                const float2 cs_sn = P.rope[(size_t)pos * (P.dh >> 1) + (i >> 1)];
+                const float cs = cs_sn.x, sn = cs_sn.y;
                 y0 = __fsub_rn(__fmul_rn(v[j], cs), __fmul_rn(v[j + 1], sn));
                 y1 = __fadd_rn(__fmul_rn(v[j], sn), __fmul_rn(v[j + 1], cs));
             }

@@ -63,12 +63,12 @@ SgPlan sgemv_plan(int K, int ldw, int nprob) {
     SgPlan p;
     p.KT = (K + 15) / 16;
     p.ngroups = ldw / 32;
-    // Largest unit (<= 128 blocks = 2048 k-rows) that still leaves >= 4 units
+    // Largest unit (<= 128 blocks = 2048 k-rows) that still leaves >= 2 units
     // per SM, so the contiguous per-CTA ranges balance to within a few %.
     // Depends on (K, N) only: the reduction tree never depends on T.
     static const int min_units = [] {
         const char* e = std::getenv("ESPEC_SG_UNITS_PER_SM");
-        return e ? std::atoi(e) : 4;
+        return e ? std::atoi(e) : 2;
     }();
     int kcb = kSgMaxUnitBlocks;
     while (kcb > 8 && (long long)p.ngroups * ((p.KT + kcb - 1) / kcb) < (long long)min_units * kSgSms) kcb /= 2;

@@ -23,7 +23,11 @@
 // group blocks placed side by side form one N=256 operand (LBO 128 B between
 // the two k-halves of a core matrix column, SBO 256 B between 8-row core
 // matrices); A uses the same layout for its 128 rows.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -77,7 +81,13 @@ constexpr uint32_t kTcIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(k
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
-struct TcLaunch {
+struct alignas(64) TcLaunch {
+    // the packed weights as a 3-D TMA tensor [k-step][group][1 KB block]
+    // (uint32 elements; dims = {256, ngroups, KT}, strides {KT KB, 1 KB}) so one
+    // cp.async.bulk.tensor box (256 x 8 groups x 4 k-steps = 32 KB) lands a
+    // whole stage in the k-step-major order the N=256 UMMA operand needs
+    CUtensorMap tmB;
+    int use_tma;
     GemvProblem P;
     PassView pass;
     KvView kv;
@@ -205,16 +215,26 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
                 tc_mbar_wait(&empty_bar[s], ((uint32_t)(i / kTcStages) & 1u) ^ 1u);
                 const int ks0 = st * kTcStepsPerStage;
                 const int nks = min(kTcStepsPerStage, KS - ks0);
-                tc_mbar_expect(&full_bar[s], (uint32_t)(nm * nks * kTcABlock + nks * ng * 1024));
+                // a tensor box always transfers its full 32 KB (out-of-range
+                // groups / k-steps arrive as zeros)
+                tc_mbar_expect(&full_bar[s], (uint32_t)(nm * nks * kTcABlock + (L.use_tma ? kTcBStage : nks * ng * 1024)));
                 unsigned char* sa = sm + (size_t)s * kTcStageBytes;
                 unsigned char* sb = sa + kTcAStage;
                 for (int m = 0; m < nm; ++m)
                     tc_bulk(sa + (size_t)m * kTcStepsPerStage * kTcABlock,
                             A + ((size_t)m * KS + ks0) * kTcABlock, (uint32_t)(nks * kTcABlock), &full_bar[s]);
-                for (int k = 0; k < nks; ++k)
-                    for (int gl = 0; gl < ng; ++gl)
-                        tc_bulk(sb + (size_t)k * (kTcN / 32) * 1024 + gl * 1024,
-                                B + (((size_t)(g0 + gl)) * KT + ks0 + k) * 1024, 1024u, &full_bar[s]);
+                if (L.use_tma) {
+                    asm volatile(
+                        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+                        "%4}], [%5];" ::"r"(tc_smem(sb)),
+                        "l"(reinterpret_cast<uint64_t>(&L.tmB)), "r"(0), "r"(g0), "r"(ks0), "r"(tc_smem(&full_bar[s]))
+                        : "memory");
+                } else {
+                    for (int k = 0; k < nks; ++k)
+                        for (int gl = 0; gl < ng; ++gl)
+                            tc_bulk(sb + (size_t)k * (kTcN / 32) * 1024 + gl * 1024,
+                                    B + (((size_t)(g0 + gl)) * KT + ks0 + k) * 1024, 1024u, &full_bar[s]);
+                }
             }
         }
     } else if (warp == 1) {
@@ -392,6 +412,28 @@ static void tc_launch_t(const TcLaunch& L, int ntiles, cudaStream_t s) {
     launch_pdl(tc_gemm_kernel<EPI>, dim3(ntiles, 1, L.ksplits), dim3(kTcThreads), (size_t)smem, s, L);
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+static bool tc_encode_b(CUtensorMap& m, const void* W, int KT, int ngroups) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    static const bool off = std::getenv("ESPEC_TC_NO_TMA") != nullptr;
+    if (!encode || off) return false;
+    const cuuint64_t dims[3] = {256, (cuuint64_t)ngroups, (cuuint64_t)KT};
+    const cuuint64_t strides[2] = {(cuuint64_t)KT * 1024, 1024};
+    const cuuint32_t box[3] = {256, (cuuint32_t)(kTcN / 32), (cuuint32_t)kTcStepsPerStage};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<void*>(W), dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 size_t tc_xa_elems(int rows, int K) {
     const int mtiles = (rows + kTcM - 1) / kTcM;
     return (size_t)mtiles * ((K + 15) / 16) * kTcM * 16;
@@ -422,6 +464,7 @@ void launch_tc_gemm(int epi, const GemvProblem& P, int T, const PassView& pass, 
         return;
     }
     TcLaunch L;
+    L.use_tma = tc_encode_b(L.tmB, P.W, (P.K + 15) / 16, P.ldw / 32) ? 1 : 0;
     L.P = P;
     L.pass = pass;
     L.kv = kv;

@@ -508,7 +508,7 @@ static void local_sync_fn(void* ctx, int rank, cudaStream_t s) {
 // ---------------------------------------------------------------------------
 
 constexpr int kChunk = 256;     // max rows per forward pass (prefill is chunked)
-constexpr int kAttnQ = 16;      // query rows per attention launch
+constexpr int kAttnQ = 64;      // query rows per attention launch (prefill chunks: 4 launches per 256 rows)
 constexpr int kMaxNodes = 64;   // drafted tree nodes per iteration (ancestor bitmask)
 
 struct Workspace {

@@ -70,9 +70,18 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
 
+// Item shared memory: two stages of K and V pages (4 x 64 x DH bf16), then
+// the 4-warp combine and the cross-item combine reuse it; the four
+// mbarriers sit above.
+constexpr int kAttnMaxChunks = 256;  // 64-row pages per (kv head, m-tile): contexts up to 16K rows
+constexpr int kAttnBarOffset = 72 * 1024;
+constexpr int kAttnItemSmem = kAttnBarOffset + 64;
+static_assert(4 * 64 * 128 * 2 <= kAttnBarOffset, "double-buffered K/V pages must fit below the barriers");
 // One CTA item of the split-KV attention: 4 warps (threads tid 0..127, named
-// barrier bar_id) = 4 consecutive 64-row key splits (bx) of one kv head and
-// one 16-pair m-tile (by = m-tile * n_kv + kv head). Used by attn_mma_kernel
+// barrier bar_id) over kv.attn_ppi 64-row key pages (chunk bx) of one kv
+// head and one 16-pair m-tile (by = m-tile * n_kv + kv head), 16 keys per
+// warp per page; chunks along the context combine through a split
+// workspace, last item in fixed chunk order. Used by attn_mma_kernel
 // (one item per CTA) and by the decode megakernel (items spread over SMs).
 template <int DH>
 __device__ __forceinline__ void attn_mma_item(const AttnProblem& A, const PassView& pass, const KvView& kv,
@@ -86,38 +95,38 @@ __device__ __forceinline__ void attn_mma_item(const AttnProblem& A, const PassVi
     const int n_kv = kv.n_kv;
     const int hk = by % n_kv, mt = by / n_kv;
     const int warp = tid >> 5, lane = tid & 31, gid = lane >> 2, tig = lane & 3;
-    const int split = bx * 4 + warp;
-    const int j0 = split * 64;
-    const int nr = max(0, min(64, pass.total - j0));
-    // one 64-row page buffer per warp: K first, then V into the same buffer
-    // once the scores are computed (halves shared memory: 3 CTAs per SM)
-    __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(smraw) + (size_t)warp * 64 * LDK;
-    __nv_bfloat16* Vs = Ks;
+    // item = kv.attn_ppi consecutive 64-row pages (chunk bx) of one kv head
+    // and one 16-pair m-tile; warp w takes keys [16w, 16w + 16) of every page
+    // (online softmax across the pages), so each warp's serial chain per page
+    // is 16 + 16 mma and a 16-key softmax. K/V pages are double-buffered.
+    const int ppi = kv.attn_ppi;
+    const int splits = (pass.total + 63) / 64;
+    const int pg0 = bx * ppi, pg1 = min(splits, pg0 + ppi);
     const __nv_bfloat16* pool = reinterpret_cast<const __nv_bfloat16*>(kv.pool);
-    const __nv_bfloat16* vg = nullptr;
-    // K then V arrive as ONE 1-D TMA bulk copy per page each (a 64-row page
-    // of one kv head is a contiguous run) on two per-warp mbarriers placed
-    // after the 4 page buffers; the unpadded rows cost ldmatrix bank
-    // conflicts, far cheaper than per-row copies or 1024 cp.async per warp
-    uint64_t* mb = reinterpret_cast<uint64_t*>(smraw + (size_t)4 * 64 * LDK * 2) + warp * 2;
+    // stage st: K at st*2*64*DH, V at (st*2+1)*64*DH (bf16 elements)
+    __nv_bfloat16* buf = reinterpret_cast<__nv_bfloat16*>(smraw);
+    // one 1-D TMA bulk copy per K or V page (a 64-row page of one kv head is a
+    // contiguous run); mbarriers [stage][K|V] above the buffers
+    uint64_t* mb = reinterpret_cast<uint64_t*>(smraw + kAttnBarOffset);
     // the buffers were last written through the generic proxy (megakernel:
     // activation slots / earlier items); order that before the TMA writes
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    if (lane == 0) {
-        mbar_init(&mb[0], 1);
-        mbar_init(&mb[1], 1);
+    auto issue = [&](int pg) {  // tid 0 only
+        const int st = (pg - pg0) & 1;
+        mbar_arrive_expect_tx(&mb[st * 2], 64 * DH * 2);
+        tma_bulk_g2s(buf + (size_t)(st * 2) * 64 * DH, pool + kv_off(kv, A.layer, 0, hk, pg * 64), 64 * DH * 2,
+                     &mb[st * 2]);
+        mbar_arrive_expect_tx(&mb[st * 2 + 1], 64 * DH * 2);
+        tma_bulk_g2s(buf + (size_t)(st * 2 + 1) * 64 * DH, pool + kv_off(kv, A.layer, 1, hk, pg * 64), 64 * DH * 2,
+                     &mb[st * 2 + 1]);
+    };
+    if (tid == 0) {
+        for (int i = 0; i < 4; ++i) mbar_init(&mb[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncwarp();
-    if (nr > 0) {  // 64-row split = one page: K and V of this head are contiguous 64 x DH runs
-        const __nv_bfloat16* kg = pool + kv_off(kv, A.layer, 0, hk, j0);
-        vg = pool + kv_off(kv, A.layer, 1, hk, j0);
-        if (lane == 0) mbar_arrive_expect_tx(&mb[0], 64 * DH * 2);
-        __syncwarp();
-        if (lane == 0) tma_bulk_g2s(Ks, kg, 64 * DH * 2, &mb[0]);
+        for (int pg = pg0; pg < pg1 && pg < pg0 + 2; ++pg) issue(pg);
     }
     // visibility of this lane's two query rows, loaded once up front (the
-    // loads overlap the K copy instead of sitting in the softmax's path)
+    // loads overlap the K/V copies instead of sitting in the softmax's path)
     int ve[2] = {0, 0};
     unsigned long long an[2] = {0ull, 0ull};
 #pragma unroll
@@ -149,98 +158,108 @@ __device__ __forceinline__ void attn_mma_item(const AttnProblem& A, const PassVi
             qa[s][3] = pack_bf16x2(d.x, d.y);
         }
     }
+    named_bar(bar_id, 128);  // barriers initialised before anyone waits on them
     float m_r[2] = {-INFINITY, -INFINITY}, l_r[2] = {0.f, 0.f};
     float o[NT][4];
 #pragma unroll
     for (int d = 0; d < NT; ++d) o[d][0] = o[d][1] = o[d][2] = o[d][3] = 0.f;
-    if (nr > 0) {
-        mbar_wait(&mb[0], 0);
-        if (dbg && tid == 0) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(dbg[0]));
-        __syncwarp();
-        float sc[8][4];
+    const float inv_sqrt = 1.0f / sqrtf((float)DH);
+    const int pr[2] = {mt * 16 + gid, mt * 16 + gid + 8};
+    for (int pg = pg0; pg < pg1; ++pg) {
+        const int st = (pg - pg0) & 1;
+        const uint32_t ph = (uint32_t)((pg - pg0) >> 1) & 1u;
+        const __nv_bfloat16* Ks = buf + (size_t)(st * 2) * 64 * DH;
+        const __nv_bfloat16* Vs = buf + (size_t)(st * 2 + 1) * 64 * DH;
+        const int j0 = pg * 64 + warp * 16;
+        const int nr = max(0, min(16, pass.total - j0));  // this warp's keys in the page
+        if (nr > 0) {
+            mbar_wait(&mb[st * 2], ph);
+            float sc[2][4];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) sc[j][0] = sc[j][1] = sc[j][2] = sc[j][3] = 0.f;
+            for (int j = 0; j < 2; ++j) sc[j][0] = sc[j][1] = sc[j][2] = sc[j][3] = 0.f;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
+            for (int j = 0; j < 2; ++j) {
 #pragma unroll
-            for (int s = 0; s < DH / 16; s += 2) {
-                uint32_t b[4];
-                ldsm_x4(b, Ks + (j * 8 + (lane & 7)) * LDK + s * 16 + (lane >> 3) * 8);
-                mma_bf16_16816(sc[j], qa[s], b[0], b[1]);
-                mma_bf16_16816(sc[j], qa[s + 1], b[2], b[3]);
+                for (int s = 0; s < DH / 16; s += 2) {
+                    uint32_t b[4];
+                    ldsm_x4(b, Ks + (warp * 16 + j * 8 + (lane & 7)) * DH + s * 16 + (lane >> 3) * 8);
+                    mma_bf16_16816(sc[j], qa[s], b[0], b[1]);
+                    mma_bf16_16816(sc[j], qa[s + 1], b[2], b[3]);
+                }
             }
-        }
-        if (dbg && tid == 0) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(dbg[1]));
-        // K consumed: stream V into the same buffer while the softmax runs
-        __syncwarp();
-        if (lane == 0) mbar_arrive_expect_tx(&mb[1], 64 * DH * 2);
-        __syncwarp();
-        if (lane == 0) tma_bulk_g2s(Vs, vg, 64 * DH * 2, &mb[1]);
-        // scale + mask, row max / exp / sum over this split's 64 keys
-        const float inv_sqrt = 1.0f / sqrtf((float)DH);
-        const int pr[2] = {mt * 16 + gid, mt * 16 + gid + 8};
-        float mx[2] = {-INFINITY, -INFINITY};
+            // scale + mask, online softmax over this page's 16 keys of the warp
+            float mx[2] = {-INFINITY, -INFINITY};
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
+            for (int j = 0; j < 2; ++j)
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int ri = e >> 1;
-                const int key = j * 8 + 2 * tig + (e & 1);
-                const bool ok = pr[ri] < P && key < nr && visible_rows(pass, ve[ri], an[ri], j0 + key);
-                sc[j][e] = ok ? __fmul_rn(sc[j][e], inv_sqrt) : -INFINITY;
-                mx[ri] = fmaxf(mx[ri], sc[j][e]);
+                for (int e = 0; e < 4; ++e) {
+                    const int ri = e >> 1;
+                    const int key = j * 8 + 2 * tig + (e & 1);
+                    const bool ok = pr[ri] < P && key < nr && visible_rows(pass, ve[ri], an[ri], j0 + key);
+                    sc[j][e] = ok ? __fmul_rn(sc[j][e], inv_sqrt) : -INFINITY;
+                    mx[ri] = fmaxf(mx[ri], sc[j][e]);
+                }
+            float alpha[2];
+#pragma unroll
+            for (int ri = 0; ri < 2; ++ri) {
+                mx[ri] = fmaxf(mx[ri], __shfl_xor_sync(0xffffffffu, mx[ri], 1));
+                mx[ri] = fmaxf(mx[ri], __shfl_xor_sync(0xffffffffu, mx[ri], 2));
+                const float mn = fmaxf(m_r[ri], mx[ri]);
+                // rescale of the running sums (exactly 1 while the max holds,
+                // 0 while nothing was visible yet)
+                alpha[ri] = m_r[ri] == -INFINITY ? 0.f : (mn == m_r[ri] ? 1.f : expf(m_r[ri] - mn));
+                m_r[ri] = mn;
+            }
+            float sum[2] = {0.f, 0.f};
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int ri = e >> 1;
+                    const float v = sc[j][e] == -INFINITY ? 0.f : expf(sc[j][e] - m_r[ri]);
+                    sc[j][e] = v;
+                    sum[ri] += v;
+                }
+#pragma unroll
+            for (int ri = 0; ri < 2; ++ri) {
+                sum[ri] += __shfl_xor_sync(0xffffffffu, sum[ri], 1);
+                sum[ri] += __shfl_xor_sync(0xffffffffu, sum[ri], 2);
+                l_r[ri] = __fmaf_rn(l_r[ri], alpha[ri], sum[ri]);
             }
 #pragma unroll
-        for (int ri = 0; ri < 2; ++ri) {
-            mx[ri] = fmaxf(mx[ri], __shfl_xor_sync(0xffffffffu, mx[ri], 1));
-            mx[ri] = fmaxf(mx[ri], __shfl_xor_sync(0xffffffffu, mx[ri], 2));
-        }
-        float sum[2] = {0.f, 0.f};
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int ri = e >> 1;
-                const float v = sc[j][e] == -INFINITY ? 0.f : expf(sc[j][e] - mx[ri]);
-                sc[j][e] = v;
-                sum[ri] += v;
+            for (int d = 0; d < NT; ++d) {
+                o[d][0] *= alpha[0];
+                o[d][1] *= alpha[0];
+                o[d][2] *= alpha[1];
+                o[d][3] *= alpha[1];
             }
-#pragma unroll
-        for (int ri = 0; ri < 2; ++ri) {
-            sum[ri] += __shfl_xor_sync(0xffffffffu, sum[ri], 1);
-            sum[ri] += __shfl_xor_sync(0xffffffffu, sum[ri], 2);
-            m_r[ri] = mx[ri];
-            l_r[ri] = sum[ri];
-        }
-        if (dbg && tid == 0) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(dbg[2]));
-        mbar_wait(&mb[1], 0);
-        if (dbg && tid == 0) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(dbg[3]));
-        __syncwarp();
-        // O = P V
-#pragma unroll
-        for (int s = 0; s < 4; ++s) {  // 16-key steps
+            mbar_wait(&mb[st * 2 + 1], ph);
+            // O += P V over the 16 keys (one k-step)
             uint32_t pa[4];
-            pa[0] = pack_bf16x2(sc[2 * s][0], sc[2 * s][1]);
-            pa[1] = pack_bf16x2(sc[2 * s][2], sc[2 * s][3]);
-            pa[2] = pack_bf16x2(sc[2 * s + 1][0], sc[2 * s + 1][1]);
-            pa[3] = pack_bf16x2(sc[2 * s + 1][2], sc[2 * s + 1][3]);
+            pa[0] = pack_bf16x2(sc[0][0], sc[0][1]);
+            pa[1] = pack_bf16x2(sc[0][2], sc[0][3]);
+            pa[2] = pack_bf16x2(sc[1][0], sc[1][1]);
+            pa[3] = pack_bf16x2(sc[1][2], sc[1][3]);
 #pragma unroll
             for (int d = 0; d < NT; d += 2) {
                 uint32_t b[4];
-                // matrices: (keys 16s..+7, dims 8d), (keys +8, dims 8d), (keys 16s.., dims 8d+8), (keys +8, dims 8d+8)
+                // matrices: (keys 0..7, dims 8d), (keys 8..15, dims 8d), (keys 0..7, dims 8d+8), (keys 8..15, dims 8d+8)
                 const int mi = lane >> 3;
-                ldsm_x4_t(b, Vs + (s * 16 + (mi & 1) * 8 + (lane & 7)) * LDK + d * 8 + (mi >> 1) * 8);
+                ldsm_x4_t(b, Vs + (warp * 16 + (mi & 1) * 8 + (lane & 7)) * DH + d * 8 + (mi >> 1) * 8);
                 mma_bf16_16816(o[d], pa, b[0], b[1]);
                 mma_bf16_16816(o[d + 1], pa, b[2], b[3]);
             }
         }
+        named_bar(bar_id, 128);  // stage st consumed by every warp
+        if (tid == 0 && pg + 2 < pg1) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(pg + 2);
+        }
     }
-    __syncwarp();
-    if (lane == 0) {  // the barriers' memory is reused as plain data afterwards
-        asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&mb[0])) : "memory");
-        asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&mb[1])) : "memory");
+    if (tid == 0) {  // the barriers' memory is plain data from here on
+        for (int i = 0; i < 4; ++i)
+            asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&mb[i])) : "memory");
     }
-    named_bar(bar_id, 128);  // K/V smem free: reuse for the warp combine
     float* Os = reinterpret_cast<float*>(smraw);           // [4][16][DH]
     float* Ms = Os + 4 * 16 * DH;                          // [4][16]
     float* Ls = Ms + 64;                                   // [4][16]
@@ -339,10 +358,10 @@ __device__ __forceinline__ void attn_mma_item(const AttnProblem& A, const PassVi
     const size_t cstride = (size_t)ny * 16 * PS;
     const float* base = A.ws + ((size_t)by * 16) * PS;
     // per-row chunk weights f = exp(m_ch - M) and denominator, once per row
-    float* fac = Os;              // [nchunks][16]
-    float* sden = Os + 64 * 16;   // [16]
+    float* fac = Os;                          // [nchunks <= kAttnMaxChunks][16]
+    float* sden = Os + kAttnMaxChunks * 16;   // [16]
     // (m, l) of every chunk: one float2 load each, all issued together
-    float2* ml = reinterpret_cast<float2*>(Os + 64 * 16 + 16);  // [nchunks][16]
+    float2* ml = reinterpret_cast<float2*>(Os + kAttnMaxChunks * 16 + 16);  // [nchunks][16]
     for (int i = tid; i < nchunks * 16; i += 128) {
         const int ch = i >> 4, r = i & 15;
         ml[i] = __ldcg(reinterpret_cast<const float2*>(base + ch * cstride + r * PS + DH));

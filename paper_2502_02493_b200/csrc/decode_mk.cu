@@ -55,6 +55,7 @@ constexpr int kXld = kMaxKcb * 16 + 8;
 constexpr int kXBytes = kSlots * kTM * kXld * 2;
 constexpr int kRedBuf = kC * kTM * 32;  // floats per reduction buffer
 constexpr int kAuxBytes = kXBytes + kNE * kRedBuf * 4;
+static_assert(kAuxBytes >= kAttnItemSmem, "attention items reuse the activation / reduction area");
 constexpr int kSmemLimit = 227 * 1024 - 1024;
 constexpr long long kSpinLimit = 4000000000LL;  // ~2 s at 1.9 GHz: trap instead of hanging
 }  // namespace
@@ -519,7 +520,7 @@ __global__ void __launch_bounds__(kThreadsMk, 1) decode_mk_kernel(const __grid_c
         if (op.type == MK_ATTN) {
             // warps 0-3: attention items (4 key splits x one kv head x one m-tile)
             const int splits = (A.pass.total + 63) / 64;
-            const int nchunks = (splits + 3) / 4;
+            const int nchunks = (splits + A.kv.attn_ppi - 1) / A.kv.attn_ppi;
             const int mtiles = (T * op.G + 15) / 16;
             const int ny = A.kv.n_kv * mtiles;
             const int items = nchunks * ny * op.nprob;

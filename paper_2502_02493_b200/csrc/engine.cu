@@ -370,6 +370,8 @@ struct Cache {
         v.dh = dh;
         v.dtype = dtype;
         v.page_elems = page_elems;
+        const int cap = n_pages * page_rows;
+        v.attn_ppi = attn_pages_per_item(cap);
         return v;
     }
     // Map pages so rows [0, rows) are backed.

@@ -502,6 +502,15 @@ size_t attn_ws_floats(int T, int n_heads, int dh, int max_rows) {
     // [chunk][n_kv * mtiles][16][dh+4]
     return splits * (size_t)(T * n_heads + 16 * n_heads) * (dh + 4);
 }
+int attn_pages_per_item(int cap) {
+    static const int forced = [] {
+        const char* e = std::getenv("ESPEC_ATTN_PPI");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (forced > 0) return forced;
+    return cap <= 2048 ? 1 : cap <= 4096 ? 2 : cap <= 8192 ? 4 : 8;
+}
+
 size_t attn_tickets(int T, int n_heads, int n_kv) {
     const int G = n_heads / n_kv;
     const int pb = (T * G + 15) / 16;  // >= the fp32 kernel's 64-pair blocks
@@ -675,13 +684,15 @@ __global__ void __launch_bounds__(128) attn_mma_kernel(const __grid_constant__ A
 template <int DH>
 static void attn_mma_launch(const AttnLaunch& L, int nprob, cudaStream_t s) {
     const int splits = (L.pass.total + 63) / 64;
-    if ((splits + 3) / 4 > 64) {
-        fprintf(stderr, "attention: context of %d rows exceeds the 16K-row split-combine limit\n", L.pass.total);
+    const int chunks = (splits + L.kv.attn_ppi - 1) / L.kv.attn_ppi;
+    if (chunks > kAttnMaxChunks) {
+        fprintf(stderr, "attention: context of %d rows exceeds the %d-row split-combine limit\n", L.pass.total,
+                kAttnMaxChunks * 64);
         return;
     }
     const int mtiles = (L.pass.T * L.G + 15) / 16;
-    dim3 grid((splits + 3) / 4, L.kv.n_kv * mtiles, nprob);
-    const size_t smem = std::max<size_t>((size_t)4 * 64 * (DH + 8) * 2 + 64, (size_t)(4 * 16 * DH + 256) * 4);
+    dim3 grid(chunks, L.kv.n_kv * mtiles, nprob);
+    const size_t smem = kAttnItemSmem;
     static bool configured = false;
     if (!configured) {
         CK(cudaFuncSetAttribute(attn_mma_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

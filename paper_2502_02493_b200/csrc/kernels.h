@@ -37,6 +37,10 @@ struct KvView {
     int n_layers = 0, n_kv = 0, dh = 0;
     int dtype = 0;                    // DType
     long long page_elems = 0;         // elements per page (all layers)
+    // 64-row pages per attention item (bf16 path). A function of the cache
+    // capacity only — never of the pass — so every row's reduction tree is
+    // the same in any pass (batch invariance).
+    int attn_ppi = 1;
 };
 
 // Per-pass row metadata (device pointers), indexed by pass row t.
@@ -154,6 +158,9 @@ struct AttnBatch {
     AttnProblem p[kMaxProblems];
 };
 size_t attn_ws_floats(int T, int n_heads, int dh, int max_rows);
+// 64-row pages per bf16 attention item for a cache of `capacity_rows`
+// (ESPEC_ATTN_PPI overrides); see KvView::attn_ppi
+int attn_pages_per_item(int capacity_rows);
 size_t attn_tickets(int T, int n_heads, int n_kv);
 void launch_attention(const AttnBatch& b, int nprob, int n_heads, const PassView& pass, const KvView& kv,
                       cudaStream_t s);

@@ -145,6 +145,10 @@ extern "C" espec_status espec_bench_attn(int T, int n_heads, int n_kv, int dh, i
     kv.dh = dh;
     kv.dtype = DT_BF16;
     kv.page_elems = page_elems;
+    {
+        const int cap = (ctx + 64 + page_rows - 1) / page_rows * page_rows;  // as Cache::view()
+        kv.attn_ppi = attn_pages_per_item(cap);
+    }
     PassView pv;
     pv.T = T;
     pv.rows = rows;

@@ -225,7 +225,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--ctx", type=int, default=512)
-    ap.add_argument("--e2e-tokens", type=int, default=32)
+    ap.add_argument("--e2e-tokens", type=int, default=128)  # the paper protocol: 128 new tokens
     ap.add_argument("--no-arms", action="store_true", help="skip the vanilla / sd comparison arms")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     args = ap.parse_args()

@@ -569,6 +569,7 @@ public:
         CUDA_OK(cudaMalloc(&mk_counter_, sizeof(unsigned long long)));
         CUDA_OK(cudaMemset(mk_counter_, 0, sizeof(unsigned long long)));
         if (const char* e = std::getenv("ESPEC_MK")) mk_mode_ = std::atoi(e);
+        if (const char* e = std::getenv("ESPEC_WIDE_DRAFT")) wide_draft_ = std::atoi(e);
         if (const char* e = std::getenv("ESPEC_MK_PF_KB")) mk_prefetch_ = std::atoll(e) << 10;
         for (auto& e : ev_) CUDA_OK(cudaEventCreate(&e));
         const int cap_b = bc.max_positions + kMaxNodes + kChunk;
@@ -1290,7 +1291,9 @@ public:
             mk_rec_->weight_bytes += bytes;
             return;
         }
+        set_sgemv_wide(&M == &draft_ && wide_draft_);
         site(M, kind, bytes, [&] { launch_gemv(epi, M.c.weight_dtype, b, n, T, ps.view, kv, stream_); });
+        set_sgemv_wide(false);
         launches_ += chunks(M, T);
     }
     void g_embed(ModelDev& M, Workspace& W, const Pass& ps) {
@@ -1455,8 +1458,10 @@ public:
         }
         hb.p[0] = p;
         PassView none;
+        set_sgemv_wide(&M == &draft_ && wide_draft_);
         site(M, 5, gemv_bytes(M, d, M.head_ld, Vl, n, 1),
              [&] { launch_gemv(EPI_ARGMAX, c.weight_dtype, hb, 1, n, none, KvView(), stream_); });
+        set_sgemv_wide(false);
         launches_ += chunks(M, n);
         if (tp()) {
             launch_allgather_argmax(comm_, n, W.best_val, W.best_idx, tok_out, stream_);
@@ -2093,6 +2098,7 @@ private:
     MkProg* mk_rec_ = nullptr;
     unsigned long long* mk_counter_ = nullptr;
     unsigned long long mk_base_ = 0;
+    int wide_draft_ = 1;  // ESPEC_WIDE_DRAFT=0: drafter on the (K, N)-only GEMV plan too
     int mk_mode_ = 0;  // ESPEC_MK=1 enables the decode megakernel (measured slower than the per-kernel path today)
     long long mk_prefetch_ = 0;  // ESPEC_MK_PF_KB: L2 prefetch distance per SM
 };

@@ -57,6 +57,7 @@ struct SgLaunch {
     KvView kv;
     int t0, T;
     int KT, kcb, nK, ngroups, units, xld, stages, rotate;
+    int xrows;  // activation rows held per slot (TM; T for the wide plan, rows >= xrows read zeros)
 };
 
 SgPlan sgemv_plan(int K, int ldw, int nprob) {
@@ -86,25 +87,59 @@ SgPlan sgemv_plan(int K, int ldw, int nprob) {
     return p;
 }
 
+// Wide plan (drafter only, see set_sgemv_wide): T-dependent units as long as
+// the activation slots hold just the pass's T rows — usually the whole K in
+// ONE unit, so no split-K partials, tickets or end-of-launch reductions. The
+// smallest k-chunk count whose per-CTA load is within 20% of the mean is
+// taken, never more chunks than the (K, N) plan (workspace bound).
+static constexpr int kWideSlotBytes = 64 * 1024;
+static bool sgemv_plan_wide(int K, int ldw, int nprob, int T, SgPlan& out) {
+    const SgPlan base = sgemv_plan(K, ldw, nprob);
+    SgPlan p = base;
+    for (int nK = 1; nK <= base.nK; ++nK) {
+        const int kcb = (p.KT + nK - 1) / nK;
+        if ((long long)kSgSlots * T * (kcb * 16 + 8) * 2 > kWideSlotBytes) continue;
+        const long long units = (long long)nprob * nK * p.ngroups;
+        const long long waves = (units + kSgSms - 1) / kSgSms;
+        if (waves * kSgSms * 5 > units * 6) continue;  // > 20% imbalance
+        p.kcb = kcb;
+        p.nK = (p.KT + kcb - 1) / kcb;
+        p.units = nprob * p.nK * p.ngroups;
+        p.grid = p.units < kSgSms ? p.units : kSgSms;
+        bool ok = true;
+        for (int c = 0; c < p.grid && ok; ++c) {
+            const long long s0 = (long long)c * p.units / p.grid, e0 = (long long)(c + 1) * p.units / p.grid;
+            if (e0 > s0 && (e0 - 1) / p.ngroups - s0 / p.ngroups + 1 > kSgSlots) ok = false;
+        }
+        if (!ok) continue;
+        out = p;
+        return true;
+    }
+    return false;
+}
+
+static thread_local bool g_wide = false;
+void set_sgemv_wide(bool on) { g_wide = on; }
+
 size_t sgemv_partial_floats(int K, int ldw) {
     const SgPlan p = sgemv_plan(K, ldw, 1);
     return p.nK > 1 ? (size_t)p.nK * 16 * ldw : 0;
 }
 
-// smem = ring (stages x 8 KB) + activation slots + 2 reduction buffers
-static size_t sg_fixed_bytes(int TM, int kcb) {
-    return (size_t)kSgSlots * TM * (kcb * 16 + 8) * 2 + (size_t)(TM == 8 ? 4 : 2) * kSgConsumers * TM * 32 * 4;
+// smem = ring (stages x 8 KB) + activation slots (xrows rows) + reduction buffers
+static size_t sg_fixed_bytes(int TM, int kcb, int xrows) {
+    return (size_t)kSgSlots * xrows * (kcb * 16 + 8) * 2 + (size_t)(TM == 8 ? 4 : 2) * kSgConsumers * TM * 32 * 4;
 }
 static int sg_stage_bytes(int TM) { return (TM == 8 ? 4 : 2) * kSgConsumers * 1024; }
-static int sg_stages(int TM, int kcb) {
-    const long long room = (long long)kSgSmemLimit - (long long)sg_fixed_bytes(TM, kcb);
+static int sg_stages(int TM, int kcb, int xrows) {
+    const long long room = (long long)kSgSmemLimit - (long long)sg_fixed_bytes(TM, kcb, xrows);
     int st = (int)(room / sg_stage_bytes(TM));
     if (st > kSgMaxStages) st = kSgMaxStages;
     if (st < 2) throw std::runtime_error("sgemv: shared memory too small for the weight ring");
     return st;
 }
-static size_t sg_smem_bytes(int TM, int kcb) {
-    return (size_t)sg_stages(TM, kcb) * sg_stage_bytes(TM) + sg_fixed_bytes(TM, kcb);
+static size_t sg_smem_bytes(int TM, int kcb, int xrows) {
+    return (size_t)sg_stages(TM, kcb, xrows) * sg_stage_bytes(TM) + sg_fixed_bytes(TM, kcb, xrows);
 }
 
 // ---------------------------------------------------------------------------
@@ -120,6 +155,7 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
     __shared__ __align__(8) uint64_t red_full[NE];
     __shared__ __align__(8) uint64_t red_empty[NE];
     __shared__ float inv_rms[kSgSlots][TM];
+    __shared__ __align__(16) uint4 s_xzero[2];  // 32 zero bytes: A rows a slot does not hold
 
     constexpr int kBpw = sg_bpw<TM>();
     constexpr int kStageBlocks = kBpw * kSgConsumers;
@@ -127,7 +163,7 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
     const int stages = L.stages;
     unsigned char* ring = sm;
     __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(sm + (size_t)stages * kStageBytes);
-    const int xslot = TM * L.xld;  // elements per activation slot
+    const int xslot = L.xrows * L.xld;  // elements per activation slot
     float* red = reinterpret_cast<float*>(sm + (size_t)stages * kStageBytes + (size_t)kSgSlots * xslot * 2);
     constexpr int kRedBuf = kSgConsumers * TM * 32;  // floats per reduction buffer
 
@@ -145,6 +181,7 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
     int off = L.rotate ? (R - (start % L.ngroups) % R) % R : 0;
     if (off >= len) off = 0;
 
+    if (tid < 2) s_xzero[tid] = make_uint4(0u, 0u, 0u, 0u);
     if (tid == 0) {
         for (int s = 0; s < stages; ++s) {
             mbar_init(&full_bar[s], 1);
@@ -277,7 +314,7 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
         const int kq = kc >> 2;
         // rows >= T are zero; rows < T: batches of 8 independent float4 loads
         // per thread so the L2 round trips overlap
-        for (int i = T * kq + tid; i < TM * kq; i += kSgConsumers * 32) {
+        for (int i = T * kq + tid; i < L.xrows * kq; i += kSgConsumers * 32) {
             const int t = i / kq, kk = (i - t * kq) * 4;
             *reinterpret_cast<uint2*>(xd + t * L.xld + kk) = make_uint2(0u, 0u);
         }
@@ -330,8 +367,10 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
         const int j = pair % L.nK;
         const int nb = min(L.kcb, L.KT - j * L.kcb);
         const __nv_bfloat16* xb = xs + (size_t)(pair - pair0) * xslot;
-        const __nv_bfloat16* xrow = TM == 16 ? xb + (lane & 7) * L.xld + ((lane >> 3) & 1) * 8 * L.xld + (lane >> 4) * 8
-                                             : xb + (lane & 7) * L.xld + ((lane >> 3) & 1) * 8;
+        const int xr = TM == 16 ? (lane & 7) + ((lane >> 3) & 1) * 8 : (lane & 7);  // ldmatrix row of this lane
+        const bool xz = xr >= L.xrows;  // row not held: read the zero block
+        const __nv_bfloat16* xrow = TM == 16 ? xb + xr * L.xld + (lane >> 4) * 8 : xb + xr * L.xld + ((lane >> 3) & 1) * 8;
+        const uint32_t xzero = smem_u32(&s_xzero[0]);
         float acc[4][4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = acc[q][2] = acc[q][3] = 0.f;
@@ -353,7 +392,7 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
                     asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
                                  : "=r"(w[i][4]), "=r"(w[i][5]), "=r"(w[i][6]), "=r"(w[i][7])
                                  : "r"(wb + 512));
-                    const uint32_t xa = smem_u32(xrow + (b + bi) * 16);
+                    const uint32_t xa = xz ? xzero : smem_u32(xrow + (b + bi) * 16);
                     if constexpr (TM == 16) {
                         asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
                                      : "=r"(a[i][0]), "=r"(a[i][1]), "=r"(a[i][2]), "=r"(a[i][3])
@@ -444,7 +483,9 @@ static void sg_dispatch(int epi, const SgLaunch& L, int grid, size_t smem, cudaS
 void launch_sgemv(int epi, const GemvBatch& b, int nprob, int T, const PassView& pass, const KvView& kv,
                   cudaStream_t s) {
     if (T <= 0 || nprob <= 0) return;
-    const SgPlan p = sgemv_plan(b.p[0].K, b.p[0].ldw, nprob);
+    SgPlan p = sgemv_plan(b.p[0].K, b.p[0].ldw, nprob);
+    bool wide = false;
+    if (g_wide && T <= 8) wide = sgemv_plan_wide(b.p[0].K, b.p[0].ldw, nprob, T, p);
     SgLaunch L;
     L.b = b;
     L.pass = pass;
@@ -464,8 +505,9 @@ void launch_sgemv(int epi, const GemvBatch& b, int nprob, int T, const PassView&
         L.t0 = t0;
         L.T = T - t0 < 16 ? T - t0 : 16;
         const int TM = L.T <= 8 ? 8 : 16;
-        L.stages = sg_stages(TM, p.kcb);
-        const size_t smem = sg_smem_bytes(TM, p.kcb);
+        L.xrows = wide ? L.T : TM;
+        L.stages = sg_stages(TM, p.kcb, L.xrows);
+        const size_t smem = sg_smem_bytes(TM, p.kcb, L.xrows);
         if (TM == 8) sg_dispatch<8>(epi, L, p.grid, smem, s);
         else sg_dispatch<16>(epi, L, p.grid, smem, s);
     }

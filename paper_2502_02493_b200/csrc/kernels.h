@@ -117,6 +117,12 @@ SgPlan sgemv_plan(int K, int ldw, int nprob);
 size_t sgemv_partial_floats(int K, int ldw);
 void launch_sgemv(int epi, const GemvBatch& b, int nprob, int T, const PassView& pass, const KvView& kv,
                   cudaStream_t s);
+// Thread-local: while on, launch_sgemv may pick a T-dependent "wide" plan
+// (whole-K units, activation slots of T rows). Rows then depend on the pass
+// size, so the engine enables it for the DRAFTER only: drafter numerics only
+// steer which tokens are proposed, while the base keeps the (K, N)-only plan
+// that makes greedy verification lossless (batch invariance).
+void set_sgemv_wide(bool on);
 // Prompt prefill (tc_gemm.cu): while prefill mode is on (thread-local, set by
 // the engine around prompt chunks), bf16 launch_gemv calls with more than 16
 // rows run on tcgen05 (M=128 x N=256 tiles, TMEM accumulators) instead of the

@@ -33,11 +33,15 @@ PAIRS = {
 
 
 def _engine(base, draft, run, mk):
+    # the megakernel runs every GEMV on the (K, N)-only plan; compare against
+    # the per-kernel path with the drafter on that plan too (ESPEC_WIDE_DRAFT=0)
     os.environ["ESPEC_MK"] = "1" if mk else "0"
+    os.environ["ESPEC_WIDE_DRAFT"] = "0"
     try:
         eng = E.Engine(base, draft, run)
     finally:
         os.environ.pop("ESPEC_MK", None)
+        os.environ.pop("ESPEC_WIDE_DRAFT", None)
     eng.init_weights(E.Engine.BASE, base.seed, parity=False)
     eng.init_weights(E.Engine.DRAFT, draft.seed, parity=False)
     return eng

@@ -42,6 +42,24 @@ WORKLOADS = {
         draft=dict(vocab_size=128256, d_model=4096, n_layers=32, n_heads=32, n_kv_heads=8, d_head=128, d_mlp=14336,
                    rope_theta=500000.0),
         lp=4, n=5),
+    # BASELINE.json configs[2]: Qwen2-72B base + Qwen2-7B drafter shapes, lp 8
+    # (plan 0|1-7|8-15|16-23|24-26|27); vocab 152064 (no QKV bias: the
+    # reference model family has none)
+    "c3": dict(
+        name="qwen2-72b-base(tp1)+qwen2-7b-drafter, lp8, n5, batch1, greedy",
+        base=dict(vocab_size=152064, d_model=8192, n_layers=80, n_heads=64, n_kv_heads=8, d_head=128, d_mlp=29568,
+                  rope_theta=1000000.0),
+        draft=dict(vocab_size=152064, d_model=3584, n_layers=28, n_heads=28, n_kv_heads=4, d_head=128, d_mlp=18944,
+                   rope_theta=1000000.0),
+        lp=8, n=5),
+    # BASELINE.json configs[3]: Qwen2.5-32B base + Qwen2.5-0.5B drafter, lp 4
+    "c4": dict(
+        name="qwen2.5-32b-base(tp1)+qwen2.5-0.5b-drafter, lp4, n5, batch1, greedy",
+        base=dict(vocab_size=152064, d_model=5120, n_layers=64, n_heads=40, n_kv_heads=8, d_head=128, d_mlp=27648,
+                  rope_theta=1000000.0),
+        draft=dict(vocab_size=152064, d_model=896, n_layers=24, n_heads=14, n_kv_heads=2, d_head=64, d_mlp=4864,
+                   rope_theta=1000000.0),
+        lp=4, n=5),
     # small shapes for quick functional runs of this script
     "mini": dict(
         name="mini pair (functional check only)",
@@ -176,7 +194,7 @@ def cpu_baseline(wl, ctx):
     return {"value": 1.0 / it_s, "unit": "tokens/s", "cores": 1, "kind": "reference",
             "sample": (f"oracle/_ref/ref_bench (unmodified reference core, workers=1): one layer per shape at "
                        f"ctx {ctx} (base T={wl['n'] + 1}, drafter T=1, MHA-equivalent) + LM head rows, "
-                       f"extrapolated to 80/32 layers, 1 token per iteration (m=0); "
+                       f"extrapolated to {wl['base']['n_layers']}/{wl['draft']['n_layers']} layers, 1 token per iteration (m=0); "
                        f"{time.time() - t0:.1f}s of CPU work"),
             "stage_s": parts}
 
@@ -404,7 +422,7 @@ def main():
             "config": {"workload": wl["name"], "ctx": args.ctx, "n": n, "lp": lp,
                        "plan": E.plan_groups(draft.n_layers, lp), "tp": ws,
                        "parallelism": f"tp{ws} (base + drafter)" if ws > 1 else "single GPU",
-                       "l2": "no flush: 157 GB of weights streamed per step >> 126 MB L2"},
+                       "l2": "no flush: the weights streamed per step (GBs) >> 126 MB L2"},
             "speedup_vs_vanilla": (value / arms["vanilla"]["tokens_per_s"]) if "vanilla" in arms else None,
             "draft_ms_per_token": (calib_ms + draft_ms) * per_tok,
             "calibrate_ms_per_token": calib_ms * per_tok, "fuzzy_draft_ms_per_token": draft_ms * per_tok,

@@ -505,7 +505,7 @@ void launch_sgemv(int epi, const GemvBatch& b, int nprob, int T, const PassView&
         L.t0 = t0;
         L.T = T - t0 < 16 ? T - t0 : 16;
         const int TM = L.T <= 8 ? 8 : 16;
-        L.xrows = wide ? L.T : TM;
+        L.xrows = L.T;  // slots hold only the pass rows (layout only: the plan, hence every sum, is unchanged)
         L.stages = sg_stages(TM, p.kcb, L.xrows);
         const size_t smem = sg_smem_bytes(TM, p.kcb, L.xrows);
         if (TM == 8) sg_dispatch<8>(epi, L, p.grid, smem, s);

@@ -39,7 +39,9 @@ constexpr int kSgConsumers = 8;                    // warps 0-7: tensor-core con
 constexpr int kSgProducer = kSgConsumers;          // warp 8: TMA producer
 constexpr int kSgEpi = kSgConsumers + 1;           // warps 9..: unit epilogues, round-robin over units
 // epilogue warps (= reduction buffers): 4 for <= 8 rows, 2 for 16 rows
-template <int TM> constexpr int sg_ne() { return TM == 8 ? 4 : 2; }
+// epilogue warps launched (the reduction buffers actually used, L.ne <= this,
+// are chosen per launch: 2 for 13-16 rows so the weight ring keeps 4 stages)
+template <int TM> constexpr int sg_ne() { return 4; }
 template <int TM> constexpr int sg_threads() { return (kSgConsumers + 1 + sg_ne<TM>()) * 32; }
 // Stage = kBpw(TM) 1 KB blocks per consumer warp: 32 KB (TM=8) / 16 KB (TM=16),
 // so one mbarrier wait (~90 cycles even when already complete) is amortised
@@ -57,7 +59,8 @@ struct SgLaunch {
     KvView kv;
     int t0, T;
     int KT, kcb, nK, ngroups, units, xld, stages, rotate;
-    int xrows;  // activation rows held per slot (TM; T for the wide plan, rows >= xrows read zeros)
+    int xrows;  // activation rows held per slot (rows >= xrows read zeros)
+    int ne;     // epilogue warps / reduction buffers in use (<= sg_ne<TM>())
 };
 
 SgPlan sgemv_plan(int K, int ldw, int nprob) {
@@ -127,8 +130,15 @@ size_t sgemv_partial_floats(int K, int ldw) {
 }
 
 // smem = ring (stages x 8 KB) + activation slots (xrows rows) + reduction buffers
+static int sg_ne_used(int TM, int xrows) {
+    static const int big = [] {  // epilogue warps for 13-16 rows (ESPEC_SG_NE16)
+        const char* e = std::getenv("ESPEC_SG_NE16");
+        return e ? std::atoi(e) : 3;
+    }();
+    return TM == 16 && xrows > 12 ? big : 4;
+}
 static size_t sg_fixed_bytes(int TM, int kcb, int xrows) {
-    return (size_t)kSgSlots * xrows * (kcb * 16 + 8) * 2 + (size_t)(TM == 8 ? 4 : 2) * kSgConsumers * TM * 32 * 4;
+    return (size_t)kSgSlots * xrows * (kcb * 16 + 8) * 2 + (size_t)sg_ne_used(TM, xrows) * kSgConsumers * TM * 32 * 4;
 }
 static int sg_stage_bytes(int TM) { return (TM == 8 ? 4 : 2) * kSgConsumers * 1024; }
 static int sg_stages(int TM, int kcb, int xrows) {
@@ -187,7 +197,7 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
             mbar_init(&full_bar[s], 1);
             mbar_init(&empty_bar[s], kSgConsumers);
         }
-        for (int e = 0; e < NE; ++e) {
+        for (int e = 0; e < L.ne; ++e) {
             mbar_init(&red_full[e], kSgConsumers);
             mbar_init(&red_empty[e], 1);
         }
@@ -230,7 +240,8 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
         // ---------------- epilogue warps: warp 9 finishes even units, warp 10 odd units
         const int e = warp - kSgEpi;
         uint32_t phase = 0;
-        for (int i = e; i < len; i += NE) {
+        if (e >= L.ne) return;
+        for (int i = e; i < len; i += L.ne) {
             const int u = start + (i + off) % len;
             const int g = u % L.ngroups, pair = u / L.ngroups;
             const int prob = pair / L.nK, j = pair - prob * L.nK;
@@ -422,7 +433,7 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
             }
         }
         // hand the warp's partial sums to this unit's epilogue warp
-        const int e = i % NE;
+        const int e = i % L.ne;
         mbar_wait(&red_empty[e], rphase[e] ^ 1u);
         rphase[e] ^= 1u;
         float* rw = red + e * kRedBuf + warp * TM * 32;
@@ -506,6 +517,7 @@ void launch_sgemv(int epi, const GemvBatch& b, int nprob, int T, const PassView&
         L.T = T - t0 < 16 ? T - t0 : 16;
         const int TM = L.T <= 8 ? 8 : 16;
         L.xrows = L.T;  // slots hold only the pass rows (layout only: the plan, hence every sum, is unchanged)
+        L.ne = sg_ne_used(TM, L.xrows);
         L.stages = sg_stages(TM, p.kcb, L.xrows);
         const size_t smem = sg_smem_bytes(TM, p.kcb, L.xrows);
         if (TM == 8) sg_dispatch<8>(epi, L, p.grid, smem, s);

@@ -72,6 +72,18 @@ WORKLOADS = {
 PAPER_ALPHA = 0.82  # Llama-3-70B/8B, MMLU, T=0
 
 
+def pass_bytes(cfg, ctx, tp=1):
+    """Algorithmic HBM bytes of one decode pass of a model (bf16 weights
+    streamed once: QKV, O, gate/up, down per layer + the LM head; the KV
+    cache read once; embeddings are a row gather), per GPU at TP degree tp."""
+    d, L, H, kv, dh, f, V = (cfg[k] for k in ("d_model", "n_layers", "n_heads", "n_kv_heads", "d_head", "d_mlp",
+                                              "vocab_size"))
+    per_layer = d * (H + 2 * kv) * dh + H * dh * d + d * 2 * f + f * d
+    weights = 2.0 * (L * per_layer + d * V) / tp
+    kv_bytes = 2.0 * 2 * ctx * kv * dh * L / tp
+    return weights + kv_bytes
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -427,6 +439,16 @@ def main():
             "draft_ms_per_token": (calib_ms + draft_ms) * per_tok,
             "calibrate_ms_per_token": calib_ms * per_tok, "fuzzy_draft_ms_per_token": draft_ms * per_tok,
             "verify_ms_per_token": verify_ms * per_tok,
+            # per-stage roofline: algorithmic bytes of the stage's
+            # passes / the stage's device time; calibrate = 1 drafter pass + head,
+            # draft = (n-1) fuzzy passes + heads, verify = 1 base pass + head
+            "stage_roofline": {
+                "calibrate": pass_bytes(wl["draft"], args.ctx, ws) / (calib_ms / steps / 1e3) / 1e9 / hbm,
+                "draft": (n - 1) * pass_bytes(wl["draft"], args.ctx, ws) / (draft_ms / steps / 1e3) / 1e9 / hbm,
+                "verify": pass_bytes(wl["base"], args.ctx, ws) / (verify_ms / steps / 1e3) / 1e9 / hbm,
+                "vanilla": (pass_bytes(wl["base"], args.ctx, ws) / (arms["vanilla"]["ms_per_step"] / 1e3) / 1e9 / hbm)
+                if "vanilla" in arms else None,
+                "unit": "fraction of measured HBM GB/s"},
             "stage_ms_per_step": {"calibrate": calib_ms / steps, "draft": draft_ms / steps,
                                   "verify": verify_ms / steps},
             "mean_accept_len": es["emitted"] / steps, "alpha": alpha,

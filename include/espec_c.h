@@ -213,6 +213,10 @@ espec_status espec_bench_tc(int M, int K, int N, int iters, int device, double* 
                             double* flops_per_launch);
 /* Test probe: the prefill GEMM on host fp32 inputs (W logical K x N). */
 espec_status espec_probe_tc(int M, int K, int N, const float* x, const float* w, float* out, int device);
+/* One decode GEMV (epi 0 store / 1 residual over a zero residual) of T <= 16 rows on host
+ * data, x [T][K], w [K][N] (rounded to bf16): the batch-invariance probe (a row's
+ * result must not depend on T). */
+espec_status espec_probe_gemv(int T, int K, int N, int epi, const float* x, const float* w, float* out, int device);
 /* Instrumentation: time the paged bf16 decode/verify attention for T causal
  * query rows at the end of a ctx-row context (nprob layers batched). */
 espec_status espec_bench_attn(int T, int n_heads, int n_kv, int d_head, int ctx, int nprob, int iters, int device,

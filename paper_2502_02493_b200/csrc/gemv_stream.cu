@@ -387,13 +387,20 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
         for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = acc[q][2] = acc[q][3] = 0.f;
         for (int b = 0; b < nb; b += kStageBlocks) {
             mbar_wait(&full_bar[stage], phase);
-            // this warp's blocks of the stage: b + warp*kBpw + i
-            uint32_t w[kBpw][8];
-            uint32_t a[kBpw][4];
+            // This warp's run of 4 blocks. Both row variants use the SAME
+            // block -> warp map (warp w owns blocks 4w..4w+3 of every 32-block
+            // group of the unit; the 16-row variant's 16-block stages hold half
+            // a group, so half of the warps sit a stage out), hence the same
+            // per-row sum order whatever the pass size (batch invariance).
+            constexpr int kRun = 4;
+            const int bbase = TM == 8 ? warp * kRun
+                                      : (((b / kStageBlocks) & 1) == (warp >> 2) ? (warp & 3) * kRun : kStageBlocks);
+            uint32_t w[kRun][8];
+            uint32_t a[kRun][4];
 #pragma unroll
-            for (int i = 0; i < kBpw; ++i) {
-                const int bi = warp * kBpw + i;
-                if (b + bi < nb) {
+            for (int i = 0; i < kRun; ++i) {
+                const int bi = bbase + i;
+                if (bi < kStageBlocks && b + bi < nb) {
                     // canonical K-major block: core matrices (n8, khalf) at
                     // (2*n8 + khalf)*128 B -> b0/b1 of n8 tiles 0,1 then 2,3
                     const uint32_t wb = smem_u32(ring + (size_t)stage * kStageBytes + bi * 1024 + lane * 16);
@@ -417,8 +424,8 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
                 }
             }
 #pragma unroll
-            for (int i = 0; i < kBpw; ++i) {
-                if (b + warp * kBpw + i < nb) {
+            for (int i = 0; i < kRun; ++i) {
+                if (bbase + i < kStageBlocks && b + bbase + i < nb) {
                     mma16816(acc[0], a[i], w[i][0], w[i][1]);
                     mma16816(acc[1], a[i], w[i][2], w[i][3]);
                     mma16816(acc[2], a[i], w[i][4], w[i][5]);

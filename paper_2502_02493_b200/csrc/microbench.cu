@@ -310,3 +310,44 @@ extern "C" espec_status espec_probe_tc(int M, int K, int N, const float* x_host,
     cudaFree(xa);
     return err == cudaSuccess ? ESPEC_OK : ESPEC_CUDA;
 }
+
+// One decode GEMV (EPI_STORE or EPI_RESID with zero residual) on host data:
+// x [T][K] fp32, w [K][N] fp32 (rounded to bf16, packed), out [T][N]. Used by
+// the batch-invariance tests (a row's result must not depend on T).
+extern "C" espec_status espec_probe_gemv(int T, int K, int N, int epi, const float* x_host, const float* w_host,
+                                         float* out_host, int device) {
+    if (T < 1 || T > 16 || K % 16 || N % 32 || (epi != EPI_STORE && epi != EPI_RESID)) return ESPEC_CONFIG;
+    if (cudaSetDevice(device) != cudaSuccess) return ESPEC_CUDA;
+    std::vector<__nv_bfloat16> wb((size_t)K * N);
+    for (size_t i = 0; i < wb.size(); ++i) wb[i] = __float2bfloat16_rn(w_host[i]);
+    void *Wl = nullptr, *W = nullptr;
+    float *x = nullptr, *out = nullptr, *resid = nullptr, *stats = nullptr, *part = nullptr;
+    unsigned* tickets = nullptr;
+    cudaMalloc(&Wl, (size_t)K * N * 2);
+    cudaMalloc(&W, packed_elems(K, N) * 2);
+    cudaMemcpy(Wl, wb.data(), (size_t)K * N * 2, cudaMemcpyHostToDevice);
+    launch_pack(Wl, K, N, W, false, 0);
+    cudaMalloc(&x, sizeof(float) * 16 * K);
+    cudaMalloc(&out, sizeof(float) * 16 * N);
+    cudaMalloc(&resid, sizeof(float) * 16 * N);
+    cudaMalloc(&stats, sizeof(float) * 16 * (N / 32 + 1));
+    const size_t pf = std::max<size_t>(sgemv_partial_floats(K, N), 16);
+    cudaMalloc(&part, sizeof(float) * pf);
+    cudaMalloc(&tickets, sizeof(unsigned) * (N / 32 + 1));
+    cudaMemset(tickets, 0, sizeof(unsigned) * (N / 32 + 1));
+    cudaMemset(resid, 0, sizeof(float) * 16 * N);
+    cudaMemcpy(x, x_host, sizeof(float) * (size_t)T * K, cudaMemcpyHostToDevice);
+    GemvBatch b;
+    GemvProblem& P = b.p[0];
+    P.W = W; P.K = K; P.N = N; P.ldw = N; P.x = x; P.ldx = K; P.out = out; P.ldo = N;
+    P.partial = part; P.tickets = tickets;
+    P.resid = resid; P.ldr = N; P.stats_out = stats; P.stat_tiles_out = N / 32;
+    PassView pv;
+    KvView kv;
+    launch_sgemv(epi, b, 1, T, pv, kv, 0);
+    cudaMemcpy(out_host, out, sizeof(float) * (size_t)T * N, cudaMemcpyDeviceToHost);
+    const cudaError_t err = cudaGetLastError();
+    cudaFree(Wl); cudaFree(W); cudaFree(x); cudaFree(out); cudaFree(resid); cudaFree(stats); cudaFree(part);
+    cudaFree(tickets);
+    return err == cudaSuccess ? ESPEC_OK : ESPEC_CUDA;
+}

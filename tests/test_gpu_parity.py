@@ -311,3 +311,62 @@ def test_bf16_truncated_drafter_accepts_and_is_lossless():
         eng.close()
     assert outs["vanilla"] == outs["easyspec"]
     assert alphas["easyspec"] > 0.0  # random-init pair: any acceptance exercises the accept path
+
+
+def test_bf16_rows_bitwise_independent_of_pass_size():
+    """Batch invariance across the decode-GEMV variants: the
+    logits of row t are bit-identical whether it is the last row of a (t+1)-row
+    pass (8-row variant for t < 8) or one row of a 16-row pass (16-row variant,
+    3 epilogue warps), for the base model's (K, N)-only plan."""
+    base, draft = _bf16_pair()
+    eng = E.Engine(base, draft, E.RunConfig(n=5, lp_size=2))
+    eng.init_weights(E.Engine.BASE, base.seed, parity=False)
+    eng.init_weights(E.Engine.DRAFT, draft.seed, parity=False)
+    rng = np.random.default_rng(17)
+    toks = [int(t) for t in rng.integers(0, base.vocab_size, size=16)]
+    full, hfull = eng.forward(E.Engine.BASE, toks)
+    for t in (0, 3, 7, 8, 12, 15):
+        part, hpart = eng.forward(E.Engine.BASE, toks[: t + 1])
+        assert np.array_equal(part[t], full[t]), t
+        assert np.array_equal(hpart[t], hfull[t]), t
+    eng.close()
+
+
+@pytest.mark.parametrize("widths,n", [([3, 2, 1], 3), (None, 8)])
+def test_bf16_greedy_trees_and_long_chains_equal_vanilla(widths, n):
+    """Greedy losslessness when the verify pass leaves the 8-row GEMV variant:
+    a [3,2,1] tree (16 verify rows) and an n = 8 chain (9 rows)."""
+    base, draft = _bf16_pair()
+    outs = {}
+    for alg in ("vanilla", "easyspec"):
+        run = E.RunConfig(algorithm=alg, n=n if alg != "vanilla" else 5, widths=widths if alg != "vanilla" else None,
+                          lp_size=2, max_new_tokens=40)
+        eng = E.Engine(base, draft, run)
+        eng.init_weights(E.Engine.BASE, base.seed, parity=False)
+        eng.init_weights(E.Engine.DRAFT, draft.seed, parity=False)
+        outs[alg], _ = eng.generate(bytes(range(40, 100)))
+        eng.close()
+    assert outs["vanilla"] == outs["easyspec"]
+
+
+@pytest.mark.parametrize("K,N", [(512, 1536), (4096, 4096), (28672, 8192)])
+def test_decode_gemv_row_bitwise_independent_of_rows(K, N):
+    """espec_probe_gemv: row 0 of the decode GEMV is bit-identical for every
+    pass size T = 1..16 (8-row and 16-row kernel variants, any epilogue-warp
+    count), for the store and residual epilogues."""
+    import ctypes as C
+    L = E.lib()
+    F = C.POINTER(C.c_float)
+    L.espec_probe_gemv.argtypes = [C.c_int] * 4 + [F, F, F, C.c_int]
+    rng = np.random.default_rng(K + N)
+    x = rng.standard_normal((16, K)).astype(np.float32)
+    w = (rng.standard_normal((K, N)) * 0.02).astype(np.float32)
+    ref = None
+    for T in (1, 2, 5, 8, 9, 12, 13, 16):
+        for epi in (0, 1):
+            out = np.zeros((T, N), np.float32)
+            assert L.espec_probe_gemv(T, K, N, epi, x.ctypes.data_as(F), w.ctypes.data_as(F),
+                                      out.ctypes.data_as(F), 0) == 0
+            if ref is None:
+                ref = out[0].copy()
+            assert np.array_equal(out[0], ref), (T, epi)

@@ -105,28 +105,60 @@ template <int EPI>
 __device__ __forceinline__ void tc_epilogue(const TcLaunch& L, int t, int g, const float (&v)[32]) {
     const GemvProblem& P = L.P;
     const int c0 = g * 32;
+    // (each thread owns one row: 16-byte vector stores when the group is
+    // whole and the row pointer aligned, which every engine shape satisfies)
     if constexpr (EPI == EPI_STORE) {
         float* o = P.out + (size_t)t * P.ldo + c0;
+        if (c0 + 32 <= P.N && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
-            if (c0 + j < P.N) o[j] = v[j];
+            for (int j = 0; j < 32; j += 4)
+                *reinterpret_cast<float4*>(o + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if (c0 + j < P.N) o[j] = v[j];
+        }
     } else if constexpr (EPI == EPI_RESID) {
         float* o = P.out + (size_t)t * P.ldo + c0;
         const float* r = P.resid + (size_t)t * P.ldr + c0;
         float sq = 0.f;
+        if (c0 + 32 <= P.N && ((reinterpret_cast<uintptr_t>(o) | reinterpret_cast<uintptr_t>(r)) & 15) == 0) {
+            float4 rr[8];
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
-            if (c0 + j < P.N) {
-                const float y = __fadd_rn(r[j], v[j]);
-                o[j] = y;
-                sq = __fmaf_rn(y, y, sq);
+            for (int q = 0; q < 8; ++q) rr[q] = *reinterpret_cast<const float4*>(r + 4 * q);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const float y0 = __fadd_rn(rr[q].x, v[4 * q]), y1 = __fadd_rn(rr[q].y, v[4 * q + 1]);
+                const float y2 = __fadd_rn(rr[q].z, v[4 * q + 2]), y3 = __fadd_rn(rr[q].w, v[4 * q + 3]);
+                *reinterpret_cast<float4*>(o + 4 * q) = make_float4(y0, y1, y2, y3);
+                sq = __fmaf_rn(y0, y0, sq);
+                sq = __fmaf_rn(y1, y1, sq);
+                sq = __fmaf_rn(y2, y2, sq);
+                sq = __fmaf_rn(y3, y3, sq);
             }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if (c0 + j < P.N) {
+                    const float y = __fadd_rn(r[j], v[j]);
+                    o[j] = y;
+                    sq = __fmaf_rn(y, y, sq);
+                }
+        }
         P.stats_out[t * P.stat_tiles_out + g] = sq;
     } else if constexpr (EPI == EPI_SILU) {
         float* o = P.out + (size_t)t * P.ldo + g * 16;
+        float y[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-            if (g * 16 + j < P.N / 2) o[j] = __fmul_rn(__fdiv_rn(v[j], __fadd_rn(1.0f, expf(-v[j]))), v[16 + j]);
+        for (int j = 0; j < 16; ++j) y[j] = __fmul_rn(__fdiv_rn(v[j], __fadd_rn(1.0f, expf(-v[j]))), v[16 + j]);
+        if (g * 16 + 16 <= P.N / 2 && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
+#pragma unroll
+            for (int j = 0; j < 16; j += 4) *reinterpret_cast<float4*>(o + j) = make_float4(y[j], y[j + 1], y[j + 2], y[j + 3]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                if (g * 16 + j < P.N / 2) o[j] = y[j];
+        }
     } else if constexpr (EPI == EPI_QKV) {
         const int qd = P.n_heads * P.dh, kd = P.n_kv * P.dh;
         const int pos = L.pass.pos[t];

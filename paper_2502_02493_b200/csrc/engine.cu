@@ -570,6 +570,7 @@ public:
         CUDA_OK(cudaMemset(mk_counter_, 0, sizeof(unsigned long long)));
         if (const char* e = std::getenv("ESPEC_MK")) mk_mode_ = std::atoi(e);
         if (const char* e = std::getenv("ESPEC_WIDE_DRAFT")) wide_draft_ = std::atoi(e);
+        if (const char* e = std::getenv("ESPEC_FUSE_ADDS")) fuse_adds_ = std::atoi(e);
         if (const char* e = std::getenv("ESPEC_MK_PF_KB")) mk_prefetch_ = std::atoll(e) << 10;
         for (auto& e : ev_) CUDA_OK(cudaEventCreate(&e));
         const int cap_b = bc.max_positions + kMaxNodes + kChunk;
@@ -1154,13 +1155,14 @@ public:
     // partial, the NVLink all-reduce sums partials in rank order and applies
     // the residual + stats.
     void row_parallel_resid(ModelDev& M, Workspace& W, void* Wm, int K, const float* x, int ldx, int kind, int T,
-                            const Pass& ps, const KvView& kv) {
+                            const Pass& ps, const KvView& kv, const float* resid2 = nullptr) {
         const int d = M.c.d_model, tiles = (d + kStatTile - 1) / kStatTile, wdt = M.c.weight_dtype;
         GemvBatch b;
         GemvProblem p = gp(W, 0);
         p.W = Wm; p.K = K; p.N = d; p.ldw = d; p.x = x; p.ldx = ldx;
         if (!tp()) {
             p.out = W.h; p.ldo = d; p.resid = W.h; p.ldr = d; p.stats_out = W.stats; p.stat_tiles_out = tiles;
+            p.resid2 = resid2; p.ldr2 = d;
             b.p[0] = p;
             g_gemv(M, kind, gemv_bytes(M, K, d, d, T, 1), EPI_RESID, b, 1, T, ps, kv);
             return;
@@ -1340,6 +1342,9 @@ public:
         if (plan) groups = plan->groups;
         else
             for (int l = 0; l < c.n_layers; ++l) groups.push_back({l});
+        // fuzzy groups: the residual adds h += attn_i ride on the O / down GEMV
+        // epilogues (bf16 decode GEMV, one GPU); otherwise separate add kernels
+        const bool fuse = wdt == DT_BF16 && !tp() && T <= 16 && fuse_adds_;
         for (const auto& g : groups) {
             const int n = (int)g.size();
             // attention of every layer in the group reads the group-entry state
@@ -1364,6 +1369,9 @@ public:
                     p.W = M.L[g[i]].wo; p.K = qd; p.N = d; p.ldw = d;
                     p.x = W.mixed + (size_t)i * kChunk * qd; p.ldx = qd;
                     p.out = W.attn + (size_t)i * kChunk * d; p.ldo = d;
+                    if (i == 0 && fuse) {  // h += attn_0 in the epilogue (+ row stats)
+                        p.out = W.h; p.resid = W.h; p.ldr = d; p.stats_out = W.stats; p.stat_tiles_out = tiles;
+                    }
                     ob.p[i] = p;
                 }
                 g_gemv(M, 2, gemv_bytes(M, qd, d, d, T, n), EPI_STORE, ob, n, T, ps, kv);
@@ -1384,7 +1392,7 @@ public:
             // residual / MLP chain stays sequential (proj/src/draft_engine.cpp:112-130)
             for (int i = 0; i < n; ++i) {
                 const LayerDev& L = M.L[g[i]];
-                if (n > 1) {
+                if (n > 1 && !fuse) {
                     g_add(W, W.attn + (size_t)i * kChunk * d, d, T);
                 }
                 GemvBatch ub;
@@ -1394,7 +1402,8 @@ public:
                 p.out = W.act; p.ldo = f;
                 ub.p[0] = p;
                 g_gemv(M, 3, gemv_bytes(M, d, M.gu_ld(), 2 * f, T, 1), EPI_SILU, ub, 1, T, ps, kv);
-                row_parallel_resid(M, W, L.wd, f, W.act, f, 4, T, ps, kv);
+                row_parallel_resid(M, W, L.wd, f, W.act, f, 4, T, ps, kv,
+                                   fuse && n > 1 && i + 1 < n ? W.attn + (size_t)(i + 1) * kChunk * d : nullptr);
             }
         }
     }
@@ -2099,6 +2108,7 @@ private:
     unsigned long long* mk_counter_ = nullptr;
     unsigned long long mk_base_ = 0;
     int wide_draft_ = 1;  // ESPEC_WIDE_DRAFT=0: drafter on the (K, N)-only GEMV plan too
+    int fuse_adds_ = 1;   // ESPEC_FUSE_ADDS=0: fuzzy-group residual adds as separate kernels
     int mk_mode_ = 0;  // ESPEC_MK=1 enables the decode megakernel (measured slower than the per-kernel path today)
     long long mk_prefetch_ = 0;  // ESPEC_MK_PF_KB: L2 prefetch distance per SM
 };

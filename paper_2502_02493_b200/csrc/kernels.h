@@ -70,8 +70,10 @@ struct GemvProblem {
     // epilogue
     float* out = nullptr;
     int ldo = 0;
-    const float* resid = nullptr;
+    const float* resid = nullptr;   // RESID (and a fused STORE, bf16 decode GEMV only): out = resid + x.W
     int ldr = 0;
+    const float* resid2 = nullptr;  // RESID, bf16 decode GEMV only: out = (resid + x.W) + resid2
+    int ldr2 = 0;
     float* stats_out = nullptr;
     int stat_tiles_out = 0;
     // EPI_QKV

@@ -26,25 +26,31 @@ __device__ __forceinline__ void sg_epilogue(const SgEpiCtx& L, const GemvProblem
                                             int lane) {
     const int T = L.T, t0 = L.t0;
     const int c = g * 32 + lane;
-    if constexpr (EPI == EPI_STORE) {
-#pragma unroll
-        for (int t = 0; t < TM; ++t)
-            if (t < T && c < P.N) P.out[(size_t)(t0 + t) * P.ldo + c] = v[t];
-    } else if constexpr (EPI == EPI_RESID) {
-        // h_mid = h + attn / h_next = h_mid + mlp (proj/src/draft_engine.cpp:15-19) + row stats
+    if (EPI == EPI_RESID || (EPI == EPI_STORE && P.resid != nullptr)) {
+        // h_mid = h + attn / h_next = h_mid + mlp (proj/src/draft_engine.cpp:15-19) + row stats.
+        // Fuzzy groups fuse their residual adds here (same fp32 operations, same
+        // order as separate add kernels): a STORE problem with `resid` is the
+        // group's first h += attn_0; `resid2` adds the next layer's attn_{i+1}
+        // right after h += mlp_i.
 #pragma unroll
         for (int t = 0; t < TM; ++t) {
             if (t >= T) break;
             float sq = 0.f;
             if (c < P.N) {
-                const float y = __fadd_rn(P.resid[(size_t)(t0 + t) * P.ldr + c], v[t]);
+                float y = __fadd_rn(__ldcg(P.resid + (size_t)(t0 + t) * P.ldr + c), v[t]);
+                if (EPI == EPI_RESID && P.resid2 != nullptr) y = __fadd_rn(y, __ldcg(P.resid2 + (size_t)(t0 + t) * P.ldr2 + c));
                 P.out[(size_t)(t0 + t) * P.ldo + c] = y;
                 sq = y * y;
             }
             sq = warp_sum(sq);
             if (lane == 0) P.stats_out[(t0 + t) * P.stat_tiles_out + g] = sq;
         }
-    } else if constexpr (EPI == EPI_SILU) {
+    } else if constexpr (EPI == EPI_STORE) {
+#pragma unroll
+        for (int t = 0; t < TM; ++t)
+            if (t < T && c < P.N) P.out[(size_t)(t0 + t) * P.ldo + c] = v[t];
+    }
+    if constexpr (EPI == EPI_SILU) {
         // packed group = [gate 16 | up 16]: silu(gate) * up (proj/src/model.cpp:197-210)
         const int a = g * 16 + lane;
 #pragma unroll

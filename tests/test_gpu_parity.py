@@ -370,3 +370,25 @@ def test_decode_gemv_row_bitwise_independent_of_rows(K, N):
             if ref is None:
                 ref = out[0].copy()
             assert np.array_equal(out[0], ref), (T, epi)
+
+
+@pytest.mark.parametrize("T", [1, 4, 13])
+def test_bf16_fused_group_adds_bitwise_equal_separate_adds(T):
+    """Fuzzy groups fold h += attn_i into the O / down GEMV epilogues; the
+    result must be bit-identical to the separate add kernels (ESPEC_FUSE_ADDS=0)."""
+    base, draft = _bf16_pair()
+    rng = np.random.default_rng(T)
+    toks = [int(t) for t in rng.integers(0, base.vocab_size, size=T)]
+    res = {}
+    for fuse in ("1", "0"):
+        os.environ["ESPEC_FUSE_ADDS"] = fuse
+        try:
+            eng = E.Engine(base, draft, E.RunConfig(n=5, lp_size=2))
+        finally:
+            os.environ.pop("ESPEC_FUSE_ADDS", None)
+        eng.init_weights(E.Engine.BASE, base.seed, parity=False)
+        eng.init_weights(E.Engine.DRAFT, draft.seed, parity=False)
+        res[fuse] = [eng.forward(E.Engine.DRAFT, toks, plan=p) for p in ("lp=2", "lp=3")]
+        eng.close()
+    for (la, ha), (lb, hb) in zip(res["1"], res["0"]):
+        assert np.array_equal(la, lb) and np.array_equal(ha, hb)

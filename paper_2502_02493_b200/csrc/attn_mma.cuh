@@ -70,6 +70,37 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
 
+// 16 output values (one pair row, 16 consecutive dims) = acc / den: fp32, or
+// bf16 rounded to nearest (exactly what the O GEMV's staging would do) when
+// the consumer takes bf16 activations
+template <int DH>
+__device__ __forceinline__ void attn_store_row(const AttnProblem& A, size_t off, const float4 (&acc)[4], float den) {
+    float y[16];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+        y[4 * v] = den > 0.f ? acc[v].x / den : 0.f;
+        y[4 * v + 1] = den > 0.f ? acc[v].y / den : 0.f;
+        y[4 * v + 2] = den > 0.f ? acc[v].z / den : 0.f;
+        y[4 * v + 3] = den > 0.f ? acc[v].w / den : 0.f;
+    }
+    if (A.out_bf16) {
+        uint32_t pk[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const __nv_bfloat162 b = __floats2bfloat162_rn(y[2 * j], y[2 * j + 1]);
+            pk[j] = *reinterpret_cast<const uint32_t*>(&b);
+        }
+        uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(A.out) + off);
+        o[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        o[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+    } else {
+        float* o = A.out + off;
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+            *reinterpret_cast<float4*>(o + 4 * v) = make_float4(y[4 * v], y[4 * v + 1], y[4 * v + 2], y[4 * v + 3]);
+    }
+}
+
 // Item shared memory: two stages of K and V pages (4 x 64 x DH bf16), then
 // the 4-warp combine and the cross-item combine reuse it; the four
 // mbarriers sit above.
@@ -325,13 +356,7 @@ __device__ __forceinline__ void attn_mma_item(const AttnProblem& A, const PassVi
             const int p = mt * 16 + r;
             if (nchunks == 1) {
                 if (p < P) {
-                    const float den = Rd[r];
-                    float* o = A.out + (size_t)(p / G) * H * DH + (hk * G + p % G) * DH + c0;
-#pragma unroll
-                    for (int v = 0; v < 4; ++v)
-                        *reinterpret_cast<float4*>(o + 4 * v) =
-                            den > 0.f ? make_float4(acc[v].x / den, acc[v].y / den, acc[v].z / den, acc[v].w / den)
-                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+                    attn_store_row<DH>(A, (size_t)(p / G) * H * DH + (hk * G + p % G) * DH + c0, acc, Rd[r]);
                 }
             } else {
 #pragma unroll
@@ -414,13 +439,7 @@ __device__ __forceinline__ void attn_mma_item(const AttnProblem& A, const PassVi
                 }
             }
         }
-        const float den = sden[r];
-        float* o = A.out + (size_t)(p / G) * H * DH + (hk * G + p % G) * DH + c0;
-#pragma unroll
-        for (int v = 0; v < 4; ++v)
-            *reinterpret_cast<float4*>(o + 4 * v) =
-                den > 0.f ? make_float4(acc[v].x / den, acc[v].y / den, acc[v].z / den, acc[v].w / den)
-                          : make_float4(0.f, 0.f, 0.f, 0.f);
+        attn_store_row<DH>(A, (size_t)(p / G) * H * DH + (hk * G + p % G) * DH + c0, acc, sden[r]);
     }
 }
 

@@ -417,6 +417,27 @@ __global__ void __launch_bounds__(kThreadsMk, 1) decode_mk_kernel(const __grid_c
                     *reinterpret_cast<uint2*>(xd + t * xld + kk) = make_uint2(0u, 0u);
                 }
                 constexpr int U = 8;
+                if (P.x_bf16) {
+                    // activations already bf16 (producer-rounded): straight copy
+                    const __nv_bfloat16* xb16 = reinterpret_cast<const __nv_bfloat16*>(P.x);
+                    for (int i0 = tid; i0 < T * kq; i0 += (kC * 32) * U) {
+                        uint2 v[U];
+        #pragma unroll
+                        for (int q = 0; q < U; ++q) {
+                            const int i = i0 + q * (kC * 32);
+                            const int t = i / kq, k = k0 + (i - t * kq) * 4;
+                            v[q] = make_uint2(0u, 0u);
+                            if (i < T * kq && k < P.K) v[q] = __ldcg(reinterpret_cast<const uint2*>(xb16 + (size_t)(0 + t) * P.ldx + k));
+                        }
+        #pragma unroll
+                        for (int q = 0; q < U; ++q) {
+                            const int i = i0 + q * (kC * 32);
+                            if (i >= T * kq) break;
+                            const int t = i / kq, kk = (i - t * kq) * 4;
+                            *reinterpret_cast<uint2*>(xd + t * xld + kk) = v[q];
+                        }
+                    }
+                } else
                 for (int i0 = tid; i0 < T * kq; i0 += kC * 32 * U) {
                     float4 v[U], gn[U];
 #pragma unroll

@@ -520,6 +520,10 @@ struct Workspace {
     float* mixed = nullptr;   // [G][kChunk][H*dh]
     float* attn = nullptr;    // [G][kChunk][d]
     float* act = nullptr;     // [kChunk][f]
+    // decode passes (bf16 weights, T <= 16): attention output and SiLU output
+    // as bf16, the form the O / down GEMVs stage anyway (half the bytes)
+    __nv_bfloat16* mixed_b16 = nullptr;  // [G][kChunk][H*dh]
+    __nv_bfloat16* act_b16 = nullptr;    // [kChunk][f]
     float* logits = nullptr;  // [8][head_ld] (parity probes)
     float* am_val = nullptr;
     int* am_idx = nullptr;
@@ -571,6 +575,7 @@ public:
         if (const char* e = std::getenv("ESPEC_MK")) mk_mode_ = std::atoi(e);
         if (const char* e = std::getenv("ESPEC_WIDE_DRAFT")) wide_draft_ = std::atoi(e);
         if (const char* e = std::getenv("ESPEC_FUSE_ADDS")) fuse_adds_ = std::atoi(e);
+        if (const char* e = std::getenv("ESPEC_B16_ACTS")) b16_acts_ = std::atoi(e);
         if (const char* e = std::getenv("ESPEC_MK_PF_KB")) mk_prefetch_ = std::atoll(e) << 10;
         for (auto& e : ev_) CUDA_OK(cudaEventCreate(&e));
         const int cap_b = bc.max_positions + kMaxNodes + kChunk;
@@ -990,6 +995,10 @@ public:
         W.mixed = (float*)wsalloc(sizeof(float) * (size_t)G * kChunk * qd);
         W.attn = (float*)wsalloc(sizeof(float) * (size_t)G * kChunk * d);
         W.act = (float*)wsalloc(sizeof(float) * (size_t)kChunk * f);
+        if (c.weight_dtype == DT_BF16) {
+            W.mixed_b16 = (__nv_bfloat16*)wsalloc(sizeof(__nv_bfloat16) * (size_t)G * kChunk * qd);
+            W.act_b16 = (__nv_bfloat16*)wsalloc(sizeof(__nv_bfloat16) * (size_t)kChunk * f);
+        }
         W.logits = (float*)wsalloc(sizeof(float) * 8 * (size_t)ldpad(c.vocab_size, c.weight_dtype));
         const int dt = c.weight_dtype;
         const int head_tiles = gemv_col_tiles(d, Vl, dt);
@@ -1155,11 +1164,11 @@ public:
     // partial, the NVLink all-reduce sums partials in rank order and applies
     // the residual + stats.
     void row_parallel_resid(ModelDev& M, Workspace& W, void* Wm, int K, const float* x, int ldx, int kind, int T,
-                            const Pass& ps, const KvView& kv, const float* resid2 = nullptr) {
+                            const Pass& ps, const KvView& kv, const float* resid2 = nullptr, int x_bf16 = 0) {
         const int d = M.c.d_model, tiles = (d + kStatTile - 1) / kStatTile, wdt = M.c.weight_dtype;
         GemvBatch b;
         GemvProblem p = gp(W, 0);
-        p.W = Wm; p.K = K; p.N = d; p.ldw = d; p.x = x; p.ldx = ldx;
+        p.W = Wm; p.K = K; p.N = d; p.ldw = d; p.x = x; p.ldx = ldx; p.x_bf16 = x_bf16;
         if (!tp()) {
             p.out = W.h; p.ldo = d; p.resid = W.h; p.ldr = d; p.stats_out = W.stats; p.stat_tiles_out = tiles;
             p.resid2 = resid2; p.ldr2 = d;
@@ -1187,6 +1196,12 @@ public:
             return;
         }
         forward_body(M, C, W, plan, ps);
+    }
+    // decode passes whose attention takes the bf16 item path: its output (and
+    // the SiLU output) stay bf16 for the O / down GEMVs
+    bool attn_b16(const ModelDev& M, int T) const {
+        return M.c.weight_dtype == DT_BF16 && M.c.kv_dtype == DT_BF16 && T <= 16 &&
+               (M.c.d_head == 64 || M.c.d_head == 128) && b16_acts_;
     }
     bool mk_usable(const ModelDev& M, int T) const {
         return mk_mode_ && !tp() && T >= 1 && T <= mk_max_rows() && M.c.weight_dtype == DT_BF16 &&
@@ -1345,6 +1360,7 @@ public:
         // fuzzy groups: the residual adds h += attn_i ride on the O / down GEMV
         // epilogues (bf16 decode GEMV, one GPU); otherwise separate add kernels
         const bool fuse = wdt == DT_BF16 && !tp() && T <= 16 && fuse_adds_;
+        const int b16 = attn_b16(M, T) ? 1 : 0;
         for (const auto& g : groups) {
             const int n = (int)g.size();
             // attention of every layer in the group reads the group-entry state
@@ -1361,13 +1377,15 @@ public:
             g_gemv(M, 0, gemv_bytes(M, d, M.qkv_ld(), M.qkv_N(), T, n), EPI_QKV, qb, n, T, ps, kv);
             attention(M, C, W, g, ps);
             if (n == 1) {
-                row_parallel_resid(M, W, M.L[g[0]].wo, qd, W.mixed, qd, 2, T, ps, kv);
+                row_parallel_resid(M, W, M.L[g[0]].wo, qd, b16 ? (const float*)W.mixed_b16 : W.mixed, qd, 2, T, ps, kv,
+                                   nullptr, b16);
             } else {
                 GemvBatch ob;
                 for (int i = 0; i < n; ++i) {
                     GemvProblem p = gp(W, i);
                     p.W = M.L[g[i]].wo; p.K = qd; p.N = d; p.ldw = d;
-                    p.x = W.mixed + (size_t)i * kChunk * qd; p.ldx = qd;
+                    p.x = b16 ? (const float*)(W.mixed_b16 + (size_t)i * kChunk * qd) : W.mixed + (size_t)i * kChunk * qd;
+                    p.ldx = qd; p.x_bf16 = b16;
                     p.out = W.attn + (size_t)i * kChunk * d; p.ldo = d;
                     if (i == 0 && fuse) {  // h += attn_0 in the epilogue (+ row stats)
                         p.out = W.h; p.resid = W.h; p.ldr = d; p.stats_out = W.stats; p.stat_tiles_out = tiles;
@@ -1399,11 +1417,11 @@ public:
                 GemvProblem p = gp(W, 0);
                 p.W = L.wgu; p.K = d; p.N = M.gu_N(); p.ldw = M.gu_ld();
                 p.x = W.h; p.ldx = d; p.gain = L.gm; p.stats_in = W.stats; p.stat_tiles_in = tiles; p.eps = c.norm_eps;
-                p.out = W.act; p.ldo = f;
+                p.out = b16 ? (float*)W.act_b16 : W.act; p.ldo = f; p.out_bf16 = b16;
                 ub.p[0] = p;
                 g_gemv(M, 3, gemv_bytes(M, d, M.gu_ld(), 2 * f, T, 1), EPI_SILU, ub, 1, T, ps, kv);
-                row_parallel_resid(M, W, L.wd, f, W.act, f, 4, T, ps, kv,
-                                   fuse && n > 1 && i + 1 < n ? W.attn + (size_t)(i + 1) * kChunk * d : nullptr);
+                row_parallel_resid(M, W, L.wd, f, b16 ? (const float*)W.act_b16 : W.act, f, 4, T, ps, kv,
+                                   fuse && n > 1 && i + 1 < n ? W.attn + (size_t)(i + 1) * kChunk * d : nullptr, b16);
             }
         }
     }
@@ -1420,7 +1438,12 @@ public:
             for (size_t i = 0; i < g.size(); ++i) {
                 AttnProblem a;
                 a.q = W.q + i * (size_t)kChunk * qd + (size_t)t0 * qd;
-                a.out = W.mixed + i * (size_t)kChunk * qd + (size_t)t0 * qd;
+                if (attn_b16(M, ps.T)) {
+                    a.out = reinterpret_cast<float*>(W.mixed_b16 + i * (size_t)kChunk * qd + (size_t)t0 * qd);
+                    a.out_bf16 = 1;
+                } else {
+                    a.out = W.mixed + i * (size_t)kChunk * qd + (size_t)t0 * qd;
+                }
                 a.layer = g[i];
                 a.ws = W.attn_ws + W.attn_ws_slot * i;
                 a.tickets = W.attn_tickets + (size_t)W.attn_ticket_slot * i;
@@ -2109,6 +2132,7 @@ private:
     unsigned long long mk_base_ = 0;
     int wide_draft_ = 1;  // ESPEC_WIDE_DRAFT=0: drafter on the (K, N)-only GEMV plan too
     int fuse_adds_ = 1;   // ESPEC_FUSE_ADDS=0: fuzzy-group residual adds as separate kernels
+    int b16_acts_ = 1;    // ESPEC_B16_ACTS=0: attention / SiLU outputs in fp32
     int mk_mode_ = 0;  // ESPEC_MK=1 enables the decode megakernel (measured slower than the per-kernel path today)
     long long mk_prefetch_ = 0;  // ESPEC_MK_PF_KB: L2 prefetch distance per SM
 };

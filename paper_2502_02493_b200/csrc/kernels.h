@@ -59,6 +59,9 @@ struct GemvProblem {
     int K = 0, N = 0, ldw = 0;
     const float* x = nullptr;
     int ldx = 0;
+    // bf16 decode GEMV only: x holds bf16 activations (no RMSNorm prologue;
+    // the producer already rounded them exactly as the staging would)
+    int x_bf16 = 0;
     // fused RMSNorm prologue (gain == nullptr: none)
     const float* gain = nullptr;
     const float* stats_in = nullptr;
@@ -70,6 +73,7 @@ struct GemvProblem {
     // epilogue
     float* out = nullptr;
     int ldo = 0;
+    int out_bf16 = 0;               // EPI_SILU, bf16 decode GEMV only: out holds bf16
     const float* resid = nullptr;   // RESID (and a fused STORE, bf16 decode GEMV only): out = resid + x.W
     int ldr = 0;
     const float* resid2 = nullptr;  // RESID, bf16 decode GEMV only: out = (resid + x.W) + resid2
@@ -157,7 +161,8 @@ void launch_add_stats(float* h, const float* a, int d, int T, float* stats, cuda
 
 struct AttnProblem {
     const float* q = nullptr;   // [T][H*dh]
-    float* out = nullptr;       // [T][H*dh]
+    float* out = nullptr;       // [T][H*dh] (fp32, or bf16 when out_bf16)
+    int out_bf16 = 0;           // bf16 item path only
     int layer = 0;
     float* ws = nullptr;        // split partials
     unsigned* tickets = nullptr;

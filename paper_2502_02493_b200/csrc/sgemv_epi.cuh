@@ -56,8 +56,13 @@ __device__ __forceinline__ void sg_epilogue(const SgEpiCtx& L, const GemvProblem
 #pragma unroll
         for (int t = 0; t < TM; ++t) {
             const float up = __shfl_down_sync(0xffffffffu, v[t], 16);
-            if (t < T && lane < 16 && a < P.N / 2)
-                P.out[(size_t)(t0 + t) * P.ldo + a] = __fmul_rn(__fdiv_rn(v[t], __fadd_rn(1.0f, expf(-v[t]))), up);
+            if (t < T && lane < 16 && a < P.N / 2) {
+                const float y = __fmul_rn(__fdiv_rn(v[t], __fadd_rn(1.0f, expf(-v[t]))), up);
+                if (P.out_bf16)
+                    reinterpret_cast<__nv_bfloat16*>(P.out)[(size_t)(t0 + t) * P.ldo + a] = __float2bfloat16_rn(y);
+                else
+                    P.out[(size_t)(t0 + t) * P.ldo + a] = y;
+            }
         }
     } else if constexpr (EPI == EPI_QKV) {
         // q = rope(h.Wq), k = rope(h.Wk), v = h.Wv ; K/V into the paged cache

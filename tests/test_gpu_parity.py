@@ -372,23 +372,26 @@ def test_decode_gemv_row_bitwise_independent_of_rows(K, N):
             assert np.array_equal(out[0], ref), (T, epi)
 
 
+@pytest.mark.parametrize("switch", ["ESPEC_FUSE_ADDS", "ESPEC_B16_ACTS"])
 @pytest.mark.parametrize("T", [1, 4, 13])
-def test_bf16_fused_group_adds_bitwise_equal_separate_adds(T):
-    """Fuzzy groups fold h += attn_i into the O / down GEMV epilogues; the
-    result must be bit-identical to the separate add kernels (ESPEC_FUSE_ADDS=0)."""
+def test_bf16_decode_fusions_bitwise_equal_unfused(switch, T):
+    """Fuzzy groups fold h += attn_i into the O / down GEMV epilogues, and decode
+    passes keep the attention / SiLU outputs in bf16 for the O / down GEMVs; both
+    must be bit-identical to the unfused path (the switch set to 0)."""
     base, draft = _bf16_pair()
     rng = np.random.default_rng(T)
     toks = [int(t) for t in rng.integers(0, base.vocab_size, size=T)]
     res = {}
-    for fuse in ("1", "0"):
-        os.environ["ESPEC_FUSE_ADDS"] = fuse
+    for on in ("1", "0"):
+        os.environ[switch] = on
         try:
             eng = E.Engine(base, draft, E.RunConfig(n=5, lp_size=2))
         finally:
-            os.environ.pop("ESPEC_FUSE_ADDS", None)
+            os.environ.pop(switch, None)
         eng.init_weights(E.Engine.BASE, base.seed, parity=False)
         eng.init_weights(E.Engine.DRAFT, draft.seed, parity=False)
-        res[fuse] = [eng.forward(E.Engine.DRAFT, toks, plan=p) for p in ("lp=2", "lp=3")]
+        res[on] = [eng.forward(E.Engine.DRAFT, toks, plan=p) for p in ("lp=2", "lp=3")]
+        res[on].append(eng.forward(E.Engine.BASE, toks))
         eng.close()
     for (la, ha), (lb, hb) in zip(res["1"], res["0"]):
         assert np.array_equal(la, lb) and np.array_equal(ha, hb)

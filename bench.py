@@ -258,6 +258,8 @@ def main():
     ap.add_argument("--e2e-tokens", type=int, default=128)  # the paper protocol: 128 new tokens
     ap.add_argument("--no-arms", action="store_true", help="skip the vanilla / sd comparison arms")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--temperature", type=float, default=0.0,
+                    help="sampling temperature of every arm (0 = greedy, the BASELINE metric)")
     args = ap.parse_args()
     assert args.warmup >= 1
     wl = WORKLOADS[args.workload]
@@ -285,7 +287,8 @@ def main():
                          **wl["base"])
     draft = E.ModelConfig(max_positions=max_pos, seed=9, tied_head=False, weight_dtype=E.BF16, kv_dtype=E.BF16,
                           **wl["draft"])
-    run = E.RunConfig(algorithm="easyspec", n=n, lp_size=lp, temperature=0.0, max_new_tokens=(warm + steps + 2) * (n + 1))
+    run = E.RunConfig(algorithm="easyspec", n=n, lp_size=lp, temperature=args.temperature,
+                      max_new_tokens=(warm + steps + 2) * (n + 1))
     eng = E.Engine(base, draft, run, device=dev, tp_size=ws, tp_rank=rank)
     if ws > 1:
         eng.link_process_group()  # all-gather the NVLink receive-region IPC handles
@@ -311,7 +314,7 @@ def main():
         return x
 
     def arm(alg, site=None, clocks=False):
-        eng.set_run(E.RunConfig(algorithm=alg, n=n, lp_size=lp, temperature=0.0,
+        eng.set_run(E.RunConfig(algorithm=alg, n=n, lp_size=lp, temperature=args.temperature,
                                 max_new_tokens=(warm + steps + 2) * (n + 1)))
         eng.begin(prompt)
         for _ in range(warm):  # first warm-up step includes the prompt prefill
@@ -390,7 +393,7 @@ def main():
     # e2e through the C ABI: host prompt ids -> host tokens, prefill included
     e2e = None
     if args.e2e_tokens > 0:
-        eng.set_run(E.RunConfig(algorithm="easyspec", n=n, lp_size=lp, temperature=0.0,
+        eng.set_run(E.RunConfig(algorithm="easyspec", n=n, lp_size=lp, temperature=args.temperature,
                                 max_new_tokens=args.e2e_tokens))
         eng.generate_tokens(prompt)  # warm-up request
         h0, d0 = eng.io_bytes()
@@ -426,7 +429,8 @@ def main():
         # paper's alpha; calibration then covers m+1 rows (same weight bytes).
         proj_tok_s = (n * PAPER_ALPHA + 1) / (it_ms / 1000.0)
         line = {
-            "metric": "decode tokens/s (EasySpec, greedy)",
+            "metric": "decode tokens/s (EasySpec, greedy)" if args.temperature == 0 else
+                      f"decode tokens/s (EasySpec, T={args.temperature})",
             "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": steps, "warmup": warm,
             "ms_per_step": it_ms, "higher_is_better": True, "scaling": "strong" if ws > 1 else "weak",
             "vs_baseline": None,

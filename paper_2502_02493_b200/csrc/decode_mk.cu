@@ -127,7 +127,6 @@ struct WeightCursor {
     const MkArgs& A;
     int cta, grid;
     int k = -1, i = 0, len = 0, off = 0, start = 0, b = 0, nb = 0;
-    int attn_k = -1;  // an attention op the cursor just passed (-1: none)
     const char* base = nullptr;
     __device__ WeightCursor(const MkArgs& a, int c, int g) : A(a), cta(c), grid(g) {}
     __device__ bool next(const char*& src, uint32_t& bytes) {
@@ -138,7 +137,6 @@ struct WeightCursor {
             }
             do {
                 if (++k >= A.n_ops) return false;
-                if (A.ops[k].type == MK_ATTN) attn_k = k;
             } while (A.ops[k].type != MK_GEMV);
             const MkOp& op = A.ops[k];
             start = (int)((long long)cta * op.units / grid);
@@ -166,24 +164,6 @@ struct WeightCursor {
         base = reinterpret_cast<const char*>(A.probs[op.prob0 + prob].W) + ((size_t)g * op.KT + kb0) * 1024;
     }
 };
-
-// L2 prefetch of an attention op's K and V pages (one contiguous 64-row x
-// d_head run per (layer, K|V, kv head, page)), spread over the CTAs.
-__device__ __forceinline__ void prefetch_kv(const MkArgs& A, int k, int cta, int grid) {
-    const MkOp& op = A.ops[k];
-    const KvView& kv = A.kv;
-    const int pages = (A.pass.total + kv.page_rows - 1) / kv.page_rows;
-    const int runs = op.nprob * 2 * kv.n_kv * pages;
-    const uint32_t bytes = (uint32_t)kv.page_rows * kv.dh * 2;
-    for (int r = cta; r < runs; r += grid) {
-        const int pi = r % pages, rest = r / pages;
-        const int hk = rest % kv.n_kv, rest2 = rest / kv.n_kv;
-        const int kind = rest2 & 1, pz = rest2 >> 1;
-        const int layer = A.aprobs[op.prob0 + pz].layer;
-        const __nv_bfloat16* p = reinterpret_cast<const __nv_bfloat16*>(kv.pool) + kv_off(kv, layer, kind, hk, pi * kv.page_rows);
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-    }
-}
 
 __global__ void __launch_bounds__(kThreadsMk, 1) decode_mk_kernel(const __grid_constant__ MkArgs A) {
     extern __shared__ __align__(1024) unsigned char sm[];
@@ -241,32 +221,14 @@ __global__ void __launch_bounds__(kThreadsMk, 1) decode_mk_kernel(const __grid_c
 
     if (warp == kProd) {
         // ---- producer: the weights of every GEMV of the pass, in op order,
-        // into the smem ring; a second cursor runs A.prefetch_bytes ahead
-        // issuing L2 prefetches, so HBM keeps streaming (into L2) through the
-        // dependency waits, attention and split-K tails that stall the ring
+        // into the smem ring (never waits for activations, only for slots)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            WeightCursor ring_cur(A, cta, grid), pf_cur(A, cta, grid);
-            long long ahead = 0;
+            WeightCursor cur(A, cta, grid);
             const char* src;
             uint32_t bytes;
-            while (ring_cur.next(src, bytes)) {
-                if (ring_cur.attn_k >= 0) {
-                    // the ring has reached the weights after an attention op:
-                    // pull that op's K/V pages into L2 now so its loads (issued
-                    // once the QKV op completes) hit L2 instead of queueing
-                    // behind the weight stream in HBM
-                    prefetch_kv(A, ring_cur.attn_k, cta, grid);
-                    ring_cur.attn_k = -1;
-                }
-                const char* psrc;
-                uint32_t pbytes;
-                while (ahead < A.prefetch_bytes + (long long)bytes && pf_cur.next(psrc, pbytes)) {
-                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(psrc), "r"(pbytes) : "memory");
-                    ahead += pbytes;
-                }
-                ahead -= bytes;
+            while (cur.next(src, bytes)) {
                 mbar_wait(&empty_bar[stage], phase ^ 1u);
                 mbar_arrive_expect_tx(&full_bar[stage], bytes);
                 tma_bulk_g2s(ring + (size_t)stage * kStageBytes, src, bytes, &full_bar[stage]);

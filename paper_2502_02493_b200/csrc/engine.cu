@@ -576,7 +576,6 @@ public:
         if (const char* e = std::getenv("ESPEC_WIDE_DRAFT")) wide_draft_ = std::atoi(e);
         if (const char* e = std::getenv("ESPEC_FUSE_ADDS")) fuse_adds_ = std::atoi(e);
         if (const char* e = std::getenv("ESPEC_B16_ACTS")) b16_acts_ = std::atoi(e);
-        if (const char* e = std::getenv("ESPEC_MK_PF_KB")) mk_prefetch_ = std::atoll(e) << 10;
         for (auto& e : ev_) CUDA_OK(cudaEventCreate(&e));
         const int cap_b = bc.max_positions + kMaxNodes + kChunk;
         const int cap_d = dc.max_positions + kMaxNodes + kChunk;
@@ -1259,7 +1258,6 @@ public:
         a.tok_idx = ps.tok_idx;
         a.counter = mk_counter_;
         a.base = mk_base_;
-        a.prefetch_bytes = mk_prefetch_;
         const double bytes =
             P.weight_bytes + (double)M.c.n_layers * 2.0 * ps.view.total * M.kvdim() * dsize(M.c.kv_dtype);
         static const char* trace_path = std::getenv("ESPEC_MK_TRACE");
@@ -2134,7 +2132,6 @@ private:
     int fuse_adds_ = 1;   // ESPEC_FUSE_ADDS=0: fuzzy-group residual adds as separate kernels
     int b16_acts_ = 1;    // ESPEC_B16_ACTS=0: attention / SiLU outputs in fp32
     int mk_mode_ = 0;  // ESPEC_MK=1 enables the decode megakernel (measured slower than the per-kernel path today)
-    long long mk_prefetch_ = 0;  // ESPEC_MK_PF_KB: L2 prefetch distance per SM
 };
 
 std::unique_ptr<Engine> make_engine(const ModelCfg& base, const ModelCfg& draft, const RunCfg& run, int device,

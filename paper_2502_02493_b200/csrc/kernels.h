@@ -339,7 +339,6 @@ struct MkArgs {
     unsigned long long* counter = nullptr;  // monotonic arrival counter
     unsigned long long base = 0;            // its value when this launch starts
     unsigned long long* trace = nullptr;    // optional [n_ops][grid][4] timeline
-    long long prefetch_bytes = 0;           // per-CTA L2 prefetch distance ahead of the ring
     int stages = 0;
 };
 int mk_max_rows();                                   // T limit of a megakernel pass

@@ -228,10 +228,11 @@ __global__ void __launch_bounds__(kThreadsMk, 1) decode_mk_kernel(const __grid_c
             WeightCursor cur(A, cta, grid);
             const char* src;
             uint32_t bytes;
+            const uint64_t pol = l2_policy_evict_first();  // weights are read once (see gemv_stream.cu)
             while (cur.next(src, bytes)) {
                 mbar_wait(&empty_bar[stage], phase ^ 1u);
                 mbar_arrive_expect_tx(&full_bar[stage], bytes);
-                tma_bulk_g2s(ring + (size_t)stage * kStageBytes, src, bytes, &full_bar[stage]);
+                tma_bulk_g2s_hint(ring + (size_t)stage * kStageBytes, src, bytes, &full_bar[stage], pol);
                 if (++stage == stages) {
                     stage = 0;
                     phase ^= 1u;

@@ -60,6 +60,7 @@ struct SgLaunch {
     int t0, T;
     int KT, kcb, nK, ngroups, units, xld, stages, rotate;
     int xrows;  // activation rows held per slot (rows >= xrows read zeros)
+    int ef;     // weights loaded with an L2 evict-first policy (ESPEC_SG_EVICT_FIRST, default 1)
     int ne;     // epilogue warps / reduction buffers in use (<= sg_ne<TM>())
 };
 
@@ -212,6 +213,7 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
+            const uint64_t pol = l2_policy_evict_first();
             for (int i = 0; i < len; ++i) {
                 const int u = start + (i + off) % len;
                 const int g = u % L.ngroups, pair = u / L.ngroups;
@@ -222,7 +224,11 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
                     const uint32_t bytes = (uint32_t)min(kStageBlocks, nb - b) * 1024u;
                     mbar_wait(&empty_bar[stage], phase ^ 1u);
                     mbar_arrive_expect_tx(&full_bar[stage], bytes);
-                    tma_bulk_g2s(ring + (size_t)stage * kStageBytes, src + (size_t)b * 1024, bytes, &full_bar[stage]);
+                    if (L.ef)
+                        tma_bulk_g2s_hint(ring + (size_t)stage * kStageBytes, src + (size_t)b * 1024, bytes,
+                                          &full_bar[stage], pol);
+                    else
+                        tma_bulk_g2s(ring + (size_t)stage * kStageBytes, src + (size_t)b * 1024, bytes, &full_bar[stage]);
                     if (++stage == stages) {
                         stage = 0;
                         phase ^= 1u;
@@ -546,6 +552,14 @@ void launch_sgemv(int epi, const GemvBatch& b, int nprob, int T, const PassView&
         const int TM = L.T <= 8 ? 8 : 16;
         L.xrows = L.T;  // slots hold only the pass rows (layout only: the plan, hence every sum, is unchanged)
         L.ne = sg_ne_used(TM, L.xrows);
+        // The weights stream through L2 exactly once: marking them evict-first
+        // keeps L2 for what the dependency chain re-reads (activations, row
+        // statistics, split-K partials, KV pages) — measured -6.7 % per step.
+        static const int ef = [] {
+            const char* e = std::getenv("ESPEC_SG_EVICT_FIRST");
+            return e ? std::atoi(e) : 1;
+        }();
+        L.ef = ef;
         L.stages = sg_stages(TM, p.kcb, L.xrows);
         const size_t smem = sg_smem_bytes(TM, p.kcb, L.xrows);
         if (TM == 8) sg_dispatch<8>(epi, L, p.grid, smem, s);

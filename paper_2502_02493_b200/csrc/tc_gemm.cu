@@ -241,6 +241,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
             asm volatile("griddepcontrol.wait;" ::: "memory");
             const char* A = reinterpret_cast<const char*>(L.xa);
             const char* B = reinterpret_cast<const char*>(L.P.W);
+            uint64_t pol;
+            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
             const size_t KT = (size_t)KS;
             for (int st = st0; st < st1; ++st) {
                 const int i = st - st0, s = i % kTcStages;
@@ -256,10 +258,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
                     tc_bulk(sa + (size_t)m * kTcStepsPerStage * kTcABlock,
                             A + ((size_t)m * KS + ks0) * kTcABlock, (uint32_t)(nks * kTcABlock), &full_bar[s]);
                 if (L.use_tma) {
+                    // weights are read once per launch: L2 evict-first
                     asm volatile(
-                        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
-                        "%4}], [%5];" ::"r"(tc_smem(sb)),
-                        "l"(reinterpret_cast<uint64_t>(&L.tmB)), "r"(0), "r"(g0), "r"(ks0), "r"(tc_smem(&full_bar[s]))
+                        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+                        "[%1, {%2, %3, %4}], [%5], %6;" ::"r"(tc_smem(sb)),
+                        "l"(reinterpret_cast<uint64_t>(&L.tmB)), "r"(0), "r"(g0), "r"(ks0), "r"(tc_smem(&full_bar[s])),
+                        "l"(pol)
                         : "memory");
                 } else {
                     for (int k = 0; k < nks; ++k)

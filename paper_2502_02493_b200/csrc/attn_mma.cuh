@@ -144,12 +144,16 @@ __device__ __forceinline__ void attn_mma_item(const AttnProblem& A, const PassVi
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     auto issue = [&](int pg) {  // tid 0 only
         const int st = (pg - pg0) & 1;
-        mbar_arrive_expect_tx(&mb[st * 2], 64 * DH * 2);
-        tma_bulk_g2s(buf + (size_t)(st * 2) * 64 * DH, pool + kv_off(kv, A.layer, 0, hk, pg * 64), 64 * DH * 2,
-                     &mb[st * 2]);
-        mbar_arrive_expect_tx(&mb[st * 2 + 1], 64 * DH * 2);
-        tma_bulk_g2s(buf + (size_t)(st * 2 + 1) * 64 * DH, pool + kv_off(kv, A.layer, 1, hk, pg * 64), 64 * DH * 2,
-                     &mb[st * 2 + 1]);
+        uint64_t pol = 0;
+        if (kv.l2_hint == 1) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+        if (kv.l2_hint == 2) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+        for (int kind = 0; kind < 2; ++kind) {
+            void* dst = buf + (size_t)(st * 2 + kind) * 64 * DH;
+            const void* src = pool + kv_off(kv, A.layer, kind, hk, pg * 64);
+            mbar_arrive_expect_tx(&mb[st * 2 + kind], 64 * DH * 2);
+            if (kv.l2_hint) tma_bulk_g2s_hint(dst, src, 64 * DH * 2, &mb[st * 2 + kind], pol);
+            else tma_bulk_g2s(dst, src, 64 * DH * 2, &mb[st * 2 + kind]);
+        }
     };
     if (tid == 0) {
         for (int i = 0; i < 4; ++i) mbar_init(&mb[i], 1);

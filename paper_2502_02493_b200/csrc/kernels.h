@@ -41,6 +41,7 @@ struct KvView {
     // capacity only — never of the pass — so every row's reduction tree is
     // the same in any pass (batch invariance).
     int attn_ppi = 1;
+    int l2_hint = 0;  // attention page loads: 0 default, 1 evict-first, 2 evict-last L2 policy
 };
 
 // Per-pass row metadata (device pointers), indexed by pass row t.

@@ -209,6 +209,7 @@ __device__ __forceinline__ void attn_mma_item(const AttnProblem& A, const PassVi
         const int nr = max(0, min(16, pass.total - j0));  // this warp's keys in the page
         if (nr > 0) {
             mbar_wait(&mb[st * 2], ph);
+            if (dbg && pg == pg0 && lane == 0) atomicMax(dbg + 2, gtimer());
             float sc[2][4];
 #pragma unroll
             for (int j = 0; j < 2; ++j) sc[j][0] = sc[j][1] = sc[j][2] = sc[j][3] = 0.f;
@@ -291,6 +292,7 @@ __device__ __forceinline__ void attn_mma_item(const AttnProblem& A, const PassVi
             issue(pg + 2);
         }
     }
+    if (dbg && lane == 0) atomicMax(dbg + 3, gtimer());
     if (tid == 0) {  // the barriers' memory is plain data from here on
         for (int i = 0; i < 4; ++i)
             asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&mb[i])) : "memory");
@@ -375,6 +377,7 @@ __device__ __forceinline__ void attn_mma_item(const AttnProblem& A, const PassVi
     if (nchunks == 1) return;
     // Cross-CTA combine (last CTA of this (kv head, m-tile)), fixed chunk order.
     named_bar(bar_id, 128);
+    if (dbg && tid == 0) atomicMax(dbg + 4, gtimer());
     unsigned* ticket = A.tickets + by;
     if (tid == 0) {
         unsigned tk;
@@ -445,6 +448,7 @@ __device__ __forceinline__ void attn_mma_item(const AttnProblem& A, const PassVi
         }
         attn_store_row<DH>(A, (size_t)(p / G) * H * DH + (hk * G + p % G) * DH + c0, acc, sden[r]);
     }
+    if (dbg && tid == 0) atomicMax(dbg + 5, gtimer());
 }
 
 }  // namespace espec_dev

@@ -56,6 +56,11 @@ __device__ __forceinline__ void st_f(__nv_bfloat16* p, float v) { *p = __float2b
 
 // Programmatic dependent launch: every kernel waits for its predecessor's
 // memory before touching dependent data and lets its successor launch early.
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 

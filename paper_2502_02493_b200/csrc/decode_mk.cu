@@ -107,11 +107,6 @@ __device__ __forceinline__ void mk_wait(const MkArgs& A, int k) {
 // The CTA's arrival for an op, by ONE thread after a barrier over every
 // thread that worked on the op (release is cumulative over their writes).
 // One arrival per CTA per op keeps the counter's atomics to gridDim.x.
-__device__ __forceinline__ unsigned long long gtimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
 // Optional per-(op, CTA) timeline (ESPEC_MK_TRACE): consumer start, inputs
 // staged, consumer done, arrival — nanoseconds of %globaltimer.
 __device__ __forceinline__ void mk_trace(const MkArgs& A, int k, int ev) {

@@ -27,6 +27,7 @@
 #include <cstdlib>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -62,6 +63,7 @@ struct SgLaunch {
     int xrows;  // activation rows held per slot (rows >= xrows read zeros)
     int ef;     // weights loaded with an L2 evict-first policy (ESPEC_SG_EVICT_FIRST, default 1)
     int ne;     // epilogue warps / reduction buffers in use (<= sg_ne<TM>())
+    unsigned long long* trace;  // diagnostic timeline (ESPEC_SG_TRACE) or nullptr
 };
 
 SgPlan sgemv_plan(int K, int ldw, int nprob) {
@@ -157,6 +159,19 @@ static size_t sg_smem_bytes(int TM, int kcb, int xrows) {
 // kernel
 // ---------------------------------------------------------------------------
 
+// Diagnostic timeline (ESPEC_SG_TRACE, tools/sg_trace.py): per CTA,
+// %globaltimer (max over the recording threads) at 0 CTA start, 1 consumers
+// past griddepcontrol.wait, 2 activations staged, 3 consumers done,
+// 4 epilogue warps done.
+constexpr int kSgTraceEv = 16;
+__device__ __forceinline__ void sg_tr(unsigned long long* tr, int ev) {
+    if (tr) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+        atomicMax(tr + (size_t)blockIdx.x * kSgTraceEv + ev, t);
+    }
+}
+
 template <int TM, int EPI>
 __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid_constant__ SgLaunch L) {
     extern __shared__ __align__(1024) unsigned char sm[];
@@ -205,6 +220,7 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    if (tid == 0) sg_tr(L.trace, 0);
     // let the next kernel in the stream start its weight prefetch early
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
@@ -241,6 +257,7 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
 
     // x, stats, workspaces and outputs are shared with earlier kernels
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (tid == 0) sg_tr(L.trace, 1);
 
     if (warp >= kSgEpi) {
         // ---------------- epilogue warps: warp 9 finishes even units, warp 10 odd units
@@ -301,6 +318,7 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
             }
             sg_epilogue<TM, EPI>(SgEpiCtx{L.pass, L.kv, L.T, L.t0, L.ngroups}, P, g, v, lane);
         }
+        if (lane == 0) sg_tr(L.trace, 4);
         return;
     }
 
@@ -392,6 +410,7 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
         }
     }
     named_bar(1, kSgConsumers * 32);
+    if (tid == 0) sg_tr(L.trace, 2);
 
     int stage = 0;
     uint32_t phase = 0;
@@ -484,6 +503,7 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
         __syncwarp();
         if (lane == 0) mbar_arrive(&red_full[e]);
     }
+    if (lane == 0) sg_tr(L.trace, 3);
 }
 
 // ---------------------------------------------------------------------------
@@ -525,6 +545,53 @@ static void sg_dispatch(int epi, const SgLaunch& L, int grid, size_t smem, cudaS
     }
 }
 
+// ESPEC_SG_TRACE="K,N,T,n[,cnt]": trace cnt consecutive launches (any shape)
+// starting at the n-th launch of that shape; the buffer is allocated and
+// zeroed up front so the traced launches sit in an undisturbed stream.
+static struct {
+    int K = -1, N = -1, T = -1, n = -1, cnt = 1, next = -1, seen = 0;
+    unsigned long long* buf = nullptr;
+    std::string head;
+} g_trace;
+
+static int sg_trace_slot(const GemvBatch& b, int nprob, int T, int epi, const SgPlan& p) {
+    static bool parsed = false;
+    if (!parsed) {
+        parsed = true;
+        if (const char* e = std::getenv("ESPEC_SG_TRACE")) {
+            std::sscanf(e, "%d,%d,%d,%d,%d", &g_trace.K, &g_trace.N, &g_trace.T, &g_trace.n, &g_trace.cnt);
+            const size_t bytes = sizeof(unsigned long long) * kSgTraceEv * kSgSms * g_trace.cnt;
+            cudaMalloc(&g_trace.buf, bytes);
+            cudaMemset(g_trace.buf, 0, bytes);
+            cudaDeviceSynchronize();
+        }
+    }
+    if (!g_trace.buf) return -1;
+    if (g_trace.next < 0 && b.p[0].K == g_trace.K && b.p[0].N == g_trace.N && T == g_trace.T &&
+        g_trace.seen++ == g_trace.n)
+        g_trace.next = 0;
+    if (g_trace.next < 0 || g_trace.next >= g_trace.cnt) return -1;
+    char hd[160];
+    std::snprintf(hd, sizeof hd, "epi %d K %d N %d T %d nprob %d units %d nK %d grid %d\n", epi, b.p[0].K, b.p[0].N, T,
+                  nprob, p.units, p.nK, p.grid);
+    g_trace.head += hd;
+    return g_trace.next++;
+}
+
+static void sg_trace_dump(cudaStream_t s) {
+    std::vector<unsigned long long> h((size_t)kSgTraceEv * kSgSms * g_trace.cnt);
+    cudaStreamSynchronize(s);
+    cudaMemcpy(h.data(), g_trace.buf, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost);
+    if (FILE* f = std::fopen("gpurun_out/sg_trace.txt", "w")) {
+        std::fputs(g_trace.head.c_str(), f);
+        for (size_t r = 0; r < h.size() / kSgTraceEv; ++r) {
+            for (int e = 0; e < kSgTraceEv; ++e) std::fprintf(f, " %llu", h[r * kSgTraceEv + e]);
+            std::fprintf(f, "\n");
+        }
+        std::fclose(f);
+    }
+}
+
 void launch_sgemv(int epi, const GemvBatch& b, int nprob, int T, const PassView& pass, const KvView& kv,
                   cudaStream_t s) {
     if (T <= 0 || nprob <= 0) return;
@@ -562,8 +629,11 @@ void launch_sgemv(int epi, const GemvBatch& b, int nprob, int T, const PassView&
         L.ef = ef;
         L.stages = sg_stages(TM, p.kcb, L.xrows);
         const size_t smem = sg_smem_bytes(TM, p.kcb, L.xrows);
+        const int tslot = sg_trace_slot(b, nprob, L.T, epi, p);
+        L.trace = tslot >= 0 ? g_trace.buf + (size_t)tslot * kSgTraceEv * kSgSms : nullptr;
         if (TM == 8) sg_dispatch<8>(epi, L, p.grid, smem, s);
         else sg_dispatch<16>(epi, L, p.grid, smem, s);
+        if (tslot == g_trace.cnt - 1) sg_trace_dump(s);
     }
 }
 

@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <type_traits>
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -522,6 +523,7 @@ struct AttnLaunch {
     PassView pass;
     KvView kv;
     int n_heads, G, splits, pblocks;
+    unsigned long long* trace = nullptr;  // diagnostic timeline (ESPEC_ATTN_TRACE) or nullptr
 };
 
 template <typename KT>
@@ -675,10 +677,14 @@ template <int DH>
 __global__ void __launch_bounds__(128) attn_mma_kernel(const __grid_constant__ AttnLaunch L) {
     extern __shared__ __align__(16) unsigned char smraw[];
     __shared__ unsigned s_last;
+    unsigned long long* tr =
+        L.trace ? L.trace + (((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 8 : nullptr;
+    if (tr && threadIdx.x == 0) atomicMax(tr, gtimer());
     pdl_wait();
+    if (tr && threadIdx.x == 0) atomicMax(tr + 1, gtimer());
     pdl_trigger();
     attn_mma_item<DH>(L.b.p[blockIdx.z], L.pass, L.kv, L.n_heads, L.G, blockIdx.x, blockIdx.y, gridDim.x, gridDim.y,
-                      smraw, &s_last, threadIdx.x, 1);
+                      smraw, &s_last, threadIdx.x, 1, tr);
 }
 
 template <int DH>
@@ -698,7 +704,42 @@ static void attn_mma_launch(const AttnLaunch& L, int nprob, cudaStream_t s) {
         CK(cudaFuncSetAttribute(attn_mma_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured = true;
     }
-    CK(launch_pdl(attn_mma_kernel<DH>, grid, dim3(128), smem, s, L));
+    // diagnostic: ESPEC_ATTN_TRACE=T,n traces the n-th launch with T pass rows (per CTA, %globaltimer
+    // at 0 start, 1 past griddepcontrol.wait, 2 first K page, 3 pages done,
+    // 4 partial written, 5 combine done) into gpurun_out/attn_trace.txt
+    static int tT = -1, tn = -1;
+    static bool parsed = false;
+    if (!parsed) {
+        parsed = true;
+        if (const char* e = std::getenv("ESPEC_ATTN_TRACE")) std::sscanf(e, "%d,%d", &tT, &tn);
+    }
+    static unsigned long long* tbuf = nullptr;
+    static int seen = 0;
+    const size_t nblk = (size_t)grid.x * grid.y * grid.z;
+    AttnLaunch Lt = L;
+    bool traced = false;
+    if (tn >= 0 && L.pass.T == tT && seen++ == tn && nblk <= 4096) {
+        if (!tbuf) CK(cudaMalloc(&tbuf, sizeof(unsigned long long) * 8 * 4096));
+        CK(cudaMemset(tbuf, 0, sizeof(unsigned long long) * 8 * 4096));
+        CK(cudaDeviceSynchronize());
+        Lt.trace = tbuf;
+        traced = true;
+    }
+    CK(launch_pdl(attn_mma_kernel<DH>, grid, dim3(128), smem, s, Lt));
+    if (traced) {
+        std::vector<unsigned long long> h(8 * nblk);
+        CK(cudaStreamSynchronize(s));
+        CK(cudaMemcpy(h.data(), tbuf, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost));
+        if (FILE* f = std::fopen("gpurun_out/attn_trace.txt", "w")) {
+            std::fprintf(f, "grid %d %d %d T %d total %d ppi %d\n", grid.x, grid.y, grid.z, L.pass.T, L.pass.total,
+                         L.kv.attn_ppi);
+            for (size_t b = 0; b < nblk; ++b) {
+                for (int e = 0; e < 8; ++e) std::fprintf(f, " %llu", h[b * 8 + e]);
+                std::fprintf(f, "\n");
+            }
+            std::fclose(f);
+        }
+    }
 }
 
 void launch_attention(const AttnBatch& b, int nprob, int n_heads, const PassView& pass, const KvView& kv,

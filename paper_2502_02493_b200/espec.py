@@ -22,7 +22,8 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libespec_b200.so")
+# ESPEC_LIB: load another in-tree build (A/B of two builds on one box)
+LIB_PATH = os.path.join(_HERE, os.environ.get("ESPEC_LIB", "libespec_b200.so"))
 
 F32, BF16 = 0, 1
 ALGORITHMS = {"vanilla": 0, "sd": 1, "sd_tree": 2, "easyspec": 3}

@@ -264,11 +264,35 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
         const int e = warp - kSgEpi;
         uint32_t phase = 0;
         if (e >= L.ne) return;
+        __shared__ int s_pos[16];
+        __shared__ long long s_kvrow[16];
+        if constexpr (EPI == EPI_QKV) {
+            // the pass's row metadata (rotary position, paged-KV row base),
+            // once per CTA while the consumers run their first unit — not two
+            // dependent loads on every unit's epilogue
+            if (e == 0 && lane < L.T) {
+                s_pos[lane] = L.pass.pos[L.t0 + lane];
+                const int row = L.pass.rows[L.t0 + lane];
+                s_kvrow[lane] = (long long)L.kv.page_table[row / L.kv.page_rows] * L.kv.page_elems +
+                                (long long)(row % L.kv.page_rows) * L.kv.dh;
+            }
+            named_bar(3, L.ne * 32);
+        }
+        constexpr bool kResid = TM == 8 && (EPI == EPI_RESID || EPI == EPI_STORE);
         for (int i = e; i < len; i += L.ne) {
             const int u = start + (i + off) % len;
             const int g = u % L.ngroups, pair = u / L.ngroups;
             const int prob = pair / L.nK, j = pair - prob * L.nK;
             const GemvProblem& P = L.b.p[prob];
+            // residual rows of this unit's columns, loaded before its sums
+            // arrive (only the unit's finisher writes them, so they are final)
+            float pre[TM];
+            if constexpr (kResid) {
+                const int c = g * 32 + lane;
+#pragma unroll
+                for (int t = 0; t < TM; ++t)
+                    pre[t] = t < L.T && c < P.N && P.resid != nullptr ? __ldcg(P.resid + (size_t)(L.t0 + t) * P.ldr + c) : 0.f;
+            }
             mbar_wait(&red_full[e], phase);
             phase ^= 1u;
             const float* rb = red + e * kRedBuf;
@@ -302,21 +326,28 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
                 const float* q = P.partial + g * 32 + lane;
 #pragma unroll
                 for (int t = 0; t < TM; ++t) v[t] = 0.f;
-                for (int jj = 0; jj < L.nK; jj += 4) {
-                    float ld[4][TM];
+                constexpr int JB = TM == 8 ? 4 : 4;  // chunks per batch of loads
+                for (int jj = 0; jj < L.nK; jj += JB) {
+                    float ld[JB][TM];
 #pragma unroll
-                    for (int c = 0; c < 4; ++c)
+                    for (int c = 0; c < JB; ++c)
 #pragma unroll
                         for (int t = 0; t < TM; ++t)
                             ld[c][t] = (jj + c < L.nK && t < L.T) ? __ldcg(q + ((size_t)(jj + c) * 16 + t) * ldw) : 0.f;
 #pragma unroll
-                    for (int c = 0; c < 4; ++c)
+                    for (int c = 0; c < JB; ++c)
 #pragma unroll
                         for (int t = 0; t < TM; ++t)
                             if (jj + c < L.nK) v[t] += ld[c][t];
                 }
             }
-            sg_epilogue<TM, EPI>(SgEpiCtx{L.pass, L.kv, L.T, L.t0, L.ngroups}, P, g, v, lane);
+            SgEpiCtx ctx{L.pass, L.kv, L.T, L.t0, L.ngroups};
+            if constexpr (EPI == EPI_QKV) {
+                ctx.pos = s_pos;
+                ctx.kv_row = s_kvrow;
+            }
+            if constexpr (kResid) ctx.pre = pre;
+            sg_epilogue<TM, EPI>(ctx, P, g, v, lane);
         }
         if (lane == 0) sg_tr(L.trace, 4);
         return;

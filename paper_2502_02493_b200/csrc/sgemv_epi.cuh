@@ -17,6 +17,9 @@ struct SgEpiCtx {
     // page_table[row / page_rows] * page_elems + (row % page_rows) * dh
     const int* pos = nullptr;
     const long long* kv_row = nullptr;
+    // optional residual rows already loaded by the caller (resid of the
+    // unit's column for rows t < T)
+    const float* pre = nullptr;
 };
 
 // Unit epilogue, run by one epilogue warp: lane = column within the 32-column
@@ -37,8 +40,9 @@ __device__ __forceinline__ void sg_epilogue(const SgEpiCtx& L, const GemvProblem
             if (t >= T) break;
             float sq = 0.f;
             if (c < P.N) {
-                float y = __fadd_rn(__ldcg(P.resid + (size_t)(t0 + t) * P.ldr + c), v[t]);
-                if (EPI == EPI_RESID && P.resid2 != nullptr) y = __fadd_rn(y, __ldcg(P.resid2 + (size_t)(t0 + t) * P.ldr2 + c));
+                float y = __fadd_rn(L.pre ? L.pre[t] : __ldcg(P.resid + (size_t)(t0 + t) * P.ldr + c), v[t]);
+                if (EPI == EPI_RESID && P.resid2 != nullptr)
+                    y = __fadd_rn(y, __ldcg(P.resid2 + (size_t)(t0 + t) * P.ldr2 + c));
                 P.out[(size_t)(t0 + t) * P.ldo + c] = y;
                 sq = y * y;
             }

@@ -293,6 +293,16 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
                 for (int t = 0; t < TM; ++t)
                     pre[t] = t < L.T && c < P.N && P.resid != nullptr ? __ldcg(P.resid + (size_t)(L.t0 + t) * P.ldr + c) : 0.f;
             }
+            // QKV: the rotary factors of this unit's column (q / k regions)
+            float2 rope[TM];
+            if constexpr (EPI == EPI_QKV && TM == 8) {
+                const int c = g * 32 + lane;
+                const int i = (c % P.dh) >> 1;  // q and k regions start at multiples of dh
+                const bool rot = c < (P.n_heads + P.n_kv) * P.dh;
+#pragma unroll
+                for (int t = 0; t < TM; ++t)
+                    rope[t] = rot && t < L.T ? P.rope[(size_t)s_pos[t] * (P.dh >> 1) + i] : make_float2(1.f, 0.f);
+            }
             mbar_wait(&red_full[e], phase);
             phase ^= 1u;
             const float* rb = red + e * kRedBuf;
@@ -345,6 +355,7 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
             if constexpr (EPI == EPI_QKV) {
                 ctx.pos = s_pos;
                 ctx.kv_row = s_kvrow;
+                if (TM == 8) ctx.rope = rope;
             }
             if constexpr (kResid) ctx.pre = pre;
             sg_epilogue<TM, EPI>(ctx, P, g, v, lane);

@@ -20,6 +20,8 @@ struct SgEpiCtx {
     // optional residual rows already loaded by the caller (resid of the
     // unit's column for rows t < T)
     const float* pre = nullptr;
+    // optional rotary factors (cos, sin) of the unit's column for rows t < T
+    const float2* rope = nullptr;
 };
 
 // Unit epilogue, run by one epilogue warp: lane = column within the 32-column
@@ -83,7 +85,7 @@ __device__ __forceinline__ void sg_epilogue(const SgEpiCtx& L, const GemvProblem
             float y = v[t];
             if (region < 2) {
                 const int pos = L.pos ? L.pos[t] : L.pass.pos[t0 + t];
-                const float2 cs_sn = P.rope[(size_t)pos * (P.dh >> 1) + (i >> 1)];
+                const float2 cs_sn = L.rope ? L.rope[t] : P.rope[(size_t)pos * (P.dh >> 1) + (i >> 1)];
                 const float cs = cs_sn.x, sn = cs_sn.y;
                 y = (i & 1) ? __fadd_rn(__fmul_rn(other, sn), __fmul_rn(v[t], cs))
                             : __fsub_rn(__fmul_rn(v[t], cs), __fmul_rn(other, sn));

@@ -23,6 +23,7 @@
 // Programmatic dependent launch: the producer starts streaming weights
 // before `griddepcontrol.wait`, so a GEMV's HBM pipeline fills while the
 // previous kernel (which produces x) drains; consumers wait before reading x.
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <stdexcept>
@@ -64,7 +65,17 @@ struct SgLaunch {
     int ef;     // weights loaded with an L2 evict-first policy (ESPEC_SG_EVICT_FIRST, default 1)
     int ne;     // epilogue warps / reduction buffers in use (<= sg_ne<TM>())
     unsigned long long* trace;  // diagnostic timeline (ESPEC_SG_TRACE) or nullptr
+    // Tail pool (ESPEC_SG_POOL): the last pool_f groups of every (problem,
+    // k-chunk) pair are not in any CTA's static range; CTAs that hold the
+    // pair's activations claim them one by one (pool_ctr[pair]) after their
+    // static range, absorbing the spread in per-SM finish times. A unit's sums
+    // do not depend on which CTA computes it (bitwise-identical results).
+    int pool_f, nstatic;
+    unsigned* pool_ctr;
 };
+
+constexpr int kSgPoolBanks = 16, kSgPoolPairs = 512;
+__device__ unsigned g_sg_pool[kSgPoolBanks * kSgPoolPairs];
 
 SgPlan sgemv_plan(int K, int ldw, int nprob) {
     SgPlan p;
@@ -194,17 +205,23 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
     constexpr int kRedBuf = kSgConsumers * TM * 32;  // floats per reduction buffer
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int start = (int)((long long)blockIdx.x * L.units / gridDim.x);
-    const int end = (int)((long long)(blockIdx.x + 1) * L.units / gridDim.x);
-    const int pair0 = start / L.ngroups;
+    const int nlin = L.pool_f ? L.nstatic : L.units;  // static (range-assigned) units
+    const int Gs = L.ngroups - L.pool_f;              // static groups per pair
+    // static index -> unit (pair-major, groups [0, Gs) of every pair)
+    auto sunit = [&](int x) { return (x / Gs) * L.ngroups + x % Gs; };
+    const int start = (int)((long long)blockIdx.x * nlin / gridDim.x);
+    const int end = (int)((long long)(blockIdx.x + 1) * nlin / gridDim.x);
+    const int pair0 = sunit(start) / L.ngroups;
+    __shared__ int s_stage_unit[kSgMaxStages];  // pool units: unit id of the stage that starts it (-1: done)
+    __shared__ int s_red_unit[sg_ne<TM>()];     // pool units: unit id handed to epilogue warp e (-1: done)
     // Processing order: the range rotated so that units with g = 0 (mod R),
     // R the nominal range length, come first. Every CTA then handles group g
     // near step (g mod R) whatever its k-chunk, so the k-chunks of one group
     // finish at about the same time and the final (last-chunk) reductions are
     // spread over the kernel instead of piling up at its end.
     const int len = end - start;
-    const int R = (L.units + gridDim.x - 1) / gridDim.x;
-    int off = L.rotate ? (R - (start % L.ngroups) % R) % R : 0;
+    const int R = (nlin + gridDim.x - 1) / gridDim.x;
+    int off = L.rotate && !L.pool_f ? (R - (start % L.ngroups) % R) % R : 0;
     if (off >= len) off = 0;
 
     if (tid < 2) s_xzero[tid] = make_uint4(0u, 0u, 0u, 0u);
@@ -230,8 +247,7 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
             int stage = 0;
             uint32_t phase = 0;
             const uint64_t pol = l2_policy_evict_first();
-            for (int i = 0; i < len; ++i) {
-                const int u = start + (i + off) % len;
+            auto stream_unit = [&](int u) {
                 const int g = u % L.ngroups, pair = u / L.ngroups;
                 const int prob = pair / L.nK, j = pair - prob * L.nK;
                 const int kb0 = j * L.kcb, nb = min(L.kcb, L.KT - kb0);
@@ -239,6 +255,7 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
                 for (int b = 0; b < nb; b += kStageBlocks) {
                     const uint32_t bytes = (uint32_t)min(kStageBlocks, nb - b) * 1024u;
                     mbar_wait(&empty_bar[stage], phase ^ 1u);
+                    if (b == 0) s_stage_unit[stage] = u;  // released by the arrive below
                     mbar_arrive_expect_tx(&full_bar[stage], bytes);
                     if (L.ef)
                         tma_bulk_g2s_hint(ring + (size_t)stage * kStageBytes, src + (size_t)b * 1024, bytes,
@@ -250,6 +267,27 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
                         phase ^= 1u;
                     }
                 }
+            };
+            for (int i = 0; i < len; ++i) stream_unit(sunit(start + (i + off) % len));
+            if (L.pool_f) {
+                // claim the pool units of the pairs this CTA holds; the last of
+                // the F + (CTAs holding the pair) claims resets the counter
+                auto cta_of = [&](long long x) { return (int)(((x + 1) * gridDim.x - 1) / nlin); };
+                const int p_hi = len > 0 ? sunit(end - 1) / L.ngroups : pair0 - 1;
+                for (int pr = p_hi; pr >= pair0 && len > 0; --pr) {
+                    const unsigned holders =
+                        (unsigned)(cta_of((long long)(pr + 1) * Gs - 1) - cta_of((long long)pr * Gs) + 1);
+                    for (;;) {
+                        const unsigned k = atomicAdd(&L.pool_ctr[pr], 1u);
+                        if (k == (unsigned)L.pool_f + holders - 1u) atomicExch(&L.pool_ctr[pr], 0u);
+                        if (k >= (unsigned)L.pool_f) break;
+                        stream_unit(pr * L.ngroups + Gs + (int)k);
+                    }
+                }
+                // sentinel stage: no data, unit -1
+                mbar_wait(&empty_bar[stage], phase ^ 1u);
+                s_stage_unit[stage] = -1;
+                mbar_arrive(&full_bar[stage]);
             }
         }
         return;
@@ -279,8 +317,19 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
             named_bar(3, L.ne * 32);
         }
         constexpr bool kResid = TM == 8 && (EPI == EPI_RESID || EPI == EPI_STORE);
-        for (int i = e; i < len; i += L.ne) {
-            const int u = start + (i + off) % len;
+        int i = e;
+        for (;; i += L.ne) {
+            const bool pooled = i >= len;
+            if (pooled && !L.pool_f) break;
+            int u;
+            if (pooled) {
+                // pool unit: its id arrives with its sums
+                mbar_wait(&red_full[e], phase);
+                u = s_red_unit[e];
+                if (u < 0) break;
+            } else {
+                u = sunit(start + (i + off) % len);
+            }
             const int g = u % L.ngroups, pair = u / L.ngroups;
             const int prob = pair / L.nK, j = pair - prob * L.nK;
             const GemvProblem& P = L.b.p[prob];
@@ -303,7 +352,7 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
                 for (int t = 0; t < TM; ++t)
                     rope[t] = rot && t < L.T ? P.rope[(size_t)s_pos[t] * (P.dh >> 1) + i] : make_float2(1.f, 0.f);
             }
-            mbar_wait(&red_full[e], phase);
+            if (!pooled) mbar_wait(&red_full[e], phase);
             phase ^= 1u;
             const float* rb = red + e * kRedBuf;
             float v[TM];
@@ -366,7 +415,7 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
 
     // ---------------- consumers (warps 0-7)
     const int T = L.T, t0 = L.t0;
-    const int pair1 = end > start ? (end - 1) / L.ngroups : pair0;
+    const int pair1 = end > start ? sunit(end - 1) / L.ngroups : pair0;
     const int kc = L.kcb * 16;
     for (int s = 0; s <= pair1 - pair0; ++s) {
         const int pair = pair0 + s, prob = pair / L.nK, j = pair - prob * L.nK;
@@ -460,8 +509,19 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
 #pragma unroll
     for (int e = 0; e < NE; ++e) rphase[e] = 0u;
     const int gid = lane >> 2, tig = lane & 3;
-    for (int i = 0; i < len; ++i) {
-        const int u = start + (i + off) % len;
+    int i = 0;
+    for (;; ++i) {
+        const bool pooled = i >= len;
+        if (pooled && !L.pool_f) break;
+        int u;
+        if (pooled) {
+            // pool unit (or the producer's end sentinel) announced with its first stage
+            mbar_wait(&full_bar[stage], phase);
+            u = s_stage_unit[stage];
+            if (u < 0) break;
+        } else {
+            u = sunit(start + (i + off) % len);
+        }
         const int pair = u / L.ngroups;
         const int j = pair % L.nK;
         const int nb = min(L.kcb, L.KT - j * L.kcb);
@@ -474,7 +534,7 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
 #pragma unroll
         for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = acc[q][2] = acc[q][3] = 0.f;
         for (int b = 0; b < nb; b += kStageBlocks) {
-            mbar_wait(&full_bar[stage], phase);
+            if (!(pooled && b == 0)) mbar_wait(&full_bar[stage], phase);
             // This warp's run of 4 blocks. Both row variants use the SAME
             // block -> warp map (warp w owns blocks 4w..4w+3 of every 32-block
             // group of the unit; the 16-row variant's 16-block stages hold half
@@ -532,6 +592,7 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
         mbar_wait(&red_empty[e], rphase[e] ^ 1u);
         rphase[e] ^= 1u;
         float* rw = red + e * kRedBuf + warp * TM * 32;
+        if (warp == 0 && lane == 0) s_red_unit[e] = u;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int col = q * 8 + 2 * tig;
@@ -544,6 +605,17 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&red_full[e]);
+    }
+    if (L.pool_f) {
+        // end sentinel to every epilogue warp (each waits on its next index)
+        for (int q = 0; q < L.ne; ++q) {
+            const int e = (i + q) % L.ne;
+            mbar_wait(&red_empty[e], rphase[e] ^ 1u);
+            rphase[e] ^= 1u;
+            if (warp == 0 && lane == 0) s_red_unit[e] = -1;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&red_full[e]);
+        }
     }
     if (lane == 0) sg_tr(L.trace, 3);
 }
@@ -655,6 +727,40 @@ void launch_sgemv(int epi, const GemvBatch& b, int nprob, int T, const PassView&
         return e ? std::atoi(e) : 0;  // measured slower on B200 (DRAM locality); off by default
     }();
     L.rotate = rotate;
+    // tail pool (see SgLaunch): ESPEC_SG_POOL = percent of each pair's groups
+    // (12 % measured best of 8 / 12 / 16: -1.5 % per EasySpec step, -4 % vanilla)
+    static const int pool_pct = [] {
+        const char* e = std::getenv("ESPEC_SG_POOL");
+        return e ? std::atoi(e) : 12;
+    }();
+    L.pool_f = 0;
+    L.nstatic = p.units;
+    L.pool_ctr = nullptr;
+    {
+        const int npairs = p.units / p.ngroups;
+        const int F = p.ngroups * pool_pct / 100;
+        const int Gs = p.ngroups - F;
+        const long long ns = (long long)npairs * Gs;
+        bool ok = pool_pct > 0 && F >= 1 && Gs >= 1 && p.units >= 4 * p.grid && npairs <= kSgPoolPairs && ns >= p.grid;
+        for (int c = 0; c < p.grid && ok; ++c) {
+            const long long s0 = (long long)c * ns / p.grid, e0 = (long long)(c + 1) * ns / p.grid;
+            if (e0 > s0 && (e0 - 1) / Gs - s0 / Gs + 1 > kSgSlots) ok = false;
+        }
+        if (ok) {
+            static unsigned* base[64] = {nullptr};
+            static std::atomic<unsigned> bank{0};
+            int dev = 0;
+            cudaGetDevice(&dev);
+            if (!base[dev]) {
+                void* a = nullptr;
+                cudaGetSymbolAddress(&a, g_sg_pool);
+                base[dev] = static_cast<unsigned*>(a);
+            }
+            L.pool_f = F;
+            L.nstatic = (int)ns;
+            L.pool_ctr = base[dev] + (size_t)(bank++ % kSgPoolBanks) * kSgPoolPairs;
+        }
+    }
     for (int t0 = 0; t0 < T; t0 += 16) {
         L.t0 = t0;
         L.T = T - t0 < 16 ? T - t0 : 16;

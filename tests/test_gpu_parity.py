@@ -395,3 +395,40 @@ def test_bf16_decode_fusions_bitwise_equal_unfused(switch, T):
         eng.close()
     for (la, ha), (lb, hb) in zip(res["1"], res["0"]):
         assert np.array_equal(la, lb) and np.array_equal(ha, hb)
+
+
+_POOL_PROBE = r"""
+import sys, hashlib, ctypes as C, numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_2502_02493_b200 import espec as E
+L = E.lib(); F = C.POINTER(C.c_float)
+L.espec_probe_gemv.argtypes = [C.c_int] * 4 + [F, F, F, C.c_int]
+h = hashlib.sha256()
+for K, N, T in ((8192, 10240, 6), (4096, 14336, 1), (28672, 8192, 8), (8192, 8192, 13)):
+    rng = np.random.default_rng(K + N + T)
+    x = rng.standard_normal((16, K)).astype(np.float32)
+    w = (rng.standard_normal((K, N)) * 0.02).astype(np.float32)
+    for epi in (0, 1):
+        out = np.zeros((T, N), np.float32)
+        assert L.espec_probe_gemv(T, K, N, epi, x.ctypes.data_as(F), w.ctypes.data_as(F), out.ctypes.data_as(F), 0) == 0
+        h.update(out.tobytes())
+print(h.hexdigest())
+"""
+
+
+def test_decode_gemv_tail_pool_bitwise_equal_static():
+    """The tail pool hands the last groups of every (problem, k-chunk) pair to
+    whichever CTA claims them first; outputs must be bit-identical to fully
+    static ranges (ESPEC_SG_POOL=0) — run in fresh processes, as the switch is
+    read once per process."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    digests = {}
+    for pct in ("0", "12", "30"):
+        env = dict(os.environ, ESPEC_SG_POOL=pct)
+        r = subprocess.run([sys.executable, "-c", _POOL_PROBE, root], env=env, capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        digests[pct] = r.stdout.strip().splitlines()[-1]
+    assert digests["0"] == digests["12"] == digests["30"], digests

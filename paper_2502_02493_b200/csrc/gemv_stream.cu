@@ -45,10 +45,9 @@ constexpr int kSgEpi = kSgConsumers + 1;           // warps 9..: unit epilogues,
 // are chosen per launch: 2 for 13-16 rows so the weight ring keeps 4 stages)
 template <int TM> constexpr int sg_ne() { return 4; }
 template <int TM> constexpr int sg_threads() { return (kSgConsumers + 1 + sg_ne<TM>()) * 32; }
-// Stage = kBpw(TM) 1 KB blocks per consumer warp: 32 KB (TM=8) / 16 KB (TM=16),
-// so one mbarrier wait (~90 cycles even when already complete) is amortised
-// over several mma blocks.
-template <int TM> constexpr int sg_bpw() { return TM == 8 ? 4 : 2; }
+// Stage = 32 (TM=8; TM=16 by default) or 16 (TM=16, ESPEC_SG_SBLK16=16) 1 KB
+// blocks, so one mbarrier wait (~90 cycles even when already complete) is
+// amortised over several mma blocks (see sg_sblk).
 constexpr int kSgMaxStages = 16;
 constexpr int kSgSlots = 2;      // (problem, k-chunk) activation slots per CTA
 constexpr int kSgMaxUnitBlocks = 128;              // 2048 k-rows per unit
@@ -64,6 +63,8 @@ struct SgLaunch {
     int xrows;  // activation rows held per slot (rows >= xrows read zeros)
     int ef;     // weights loaded with an L2 evict-first policy (ESPEC_SG_EVICT_FIRST, default 1)
     int ne;     // epilogue warps / reduction buffers in use (<= sg_ne<TM>())
+    int sblk;   // 1 KB blocks per ring stage (TM=8: 32; TM=16: 16 or 32, see sg_sblk)
+    int rrows;  // rows per warp in a reduction buffer (TM=8: 8; TM=16: the pass rows)
     unsigned long long* trace;  // diagnostic timeline (ESPEC_SG_TRACE) or nullptr
     // Tail pool (ESPEC_SG_POOL): the last pool_f groups of every (problem,
     // k-chunk) pair are not in any CTA's static range; CTAs that hold the
@@ -151,19 +152,37 @@ static int sg_ne_used(int TM, int xrows) {
     }();
     return TM == 16 && xrows > 12 ? big : 4;
 }
+// Reduction buffers hold only the rows a pass has (rows >= T are never read
+// back): at T = 9-12 that is up to 28 KB more weight ring per SM.
+static int sg_red_rows(int TM, int xrows) { return TM == 8 ? 8 : xrows; }
 static size_t sg_fixed_bytes(int TM, int kcb, int xrows) {
-    return (size_t)kSgSlots * xrows * (kcb * 16 + 8) * 2 + (size_t)sg_ne_used(TM, xrows) * kSgConsumers * TM * 32 * 4;
+    return (size_t)kSgSlots * xrows * (kcb * 16 + 8) * 2 +
+           (size_t)sg_ne_used(TM, xrows) * kSgConsumers * sg_red_rows(TM, xrows) * 32 * 4;
 }
-static int sg_stage_bytes(int TM) { return (TM == 8 ? 4 : 2) * kSgConsumers * 1024; }
+// 16-row stages: 32 blocks (one 32-block group: every consumer warp takes its
+// 4-block run each stage) whenever two such stages fit, else 16 blocks (half a
+// group; half of the warps sit a stage out). Measured at T = 9 (C2 base
+// gate/up): 16-block stages 178 us, 32-block 157 us. ESPEC_SG_SBLK16=16 forces
+// the 16-block stages.
+static int sg_sblk(int TM, int kcb, int xrows) {
+    static const int force16 = [] {
+        const char* e = std::getenv("ESPEC_SG_SBLK16");
+        return e && std::atoi(e) == 16;
+    }();
+    if (TM == 8) return 32;
+    const long long room = (long long)kSgSmemLimit - (long long)sg_fixed_bytes(TM, kcb, xrows);
+    return !force16 && room >= 2 * 32 * 1024 ? 32 : 16;
+}
+static int sg_stage_bytes(int TM, int kcb, int xrows) { return sg_sblk(TM, kcb, xrows) * 1024; }
 static int sg_stages(int TM, int kcb, int xrows) {
     const long long room = (long long)kSgSmemLimit - (long long)sg_fixed_bytes(TM, kcb, xrows);
-    int st = (int)(room / sg_stage_bytes(TM));
+    int st = (int)(room / sg_stage_bytes(TM, kcb, xrows));
     if (st > kSgMaxStages) st = kSgMaxStages;
     if (st < 2) throw std::runtime_error("sgemv: shared memory too small for the weight ring");
     return st;
 }
 static size_t sg_smem_bytes(int TM, int kcb, int xrows) {
-    return (size_t)sg_stages(TM, kcb, xrows) * sg_stage_bytes(TM) + sg_fixed_bytes(TM, kcb, xrows);
+    return (size_t)sg_stages(TM, kcb, xrows) * sg_stage_bytes(TM, kcb, xrows) + sg_fixed_bytes(TM, kcb, xrows);
 }
 
 // ---------------------------------------------------------------------------
@@ -183,7 +202,7 @@ __device__ __forceinline__ void sg_tr(unsigned long long* tr, int ev) {
     }
 }
 
-template <int TM, int EPI>
+template <int TM, int EPI, int SB>
 __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid_constant__ SgLaunch L) {
     extern __shared__ __align__(1024) unsigned char sm[];
     __shared__ __align__(8) uint64_t full_bar[kSgMaxStages];
@@ -194,15 +213,15 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
     __shared__ float inv_rms[kSgSlots][TM];
     __shared__ __align__(16) uint4 s_xzero[2];  // 32 zero bytes: A rows a slot does not hold
 
-    constexpr int kBpw = sg_bpw<TM>();
-    constexpr int kStageBlocks = kBpw * kSgConsumers;
+    constexpr int kStageBlocks = SB;  // == L.sblk (compile-time: a runtime stage size costs 13 % at T = 16)
     constexpr int kStageBytes = kStageBlocks * 1024;
     const int stages = L.stages;
     unsigned char* ring = sm;
     __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(sm + (size_t)stages * kStageBytes);
     const int xslot = L.xrows * L.xld;  // elements per activation slot
     float* red = reinterpret_cast<float*>(sm + (size_t)stages * kStageBytes + (size_t)kSgSlots * xslot * 2);
-    constexpr int kRedBuf = kSgConsumers * TM * 32;  // floats per reduction buffer
+    const int RR = TM == 8 ? 8 : L.rrows;           // rows per warp slice of a reduction buffer
+    const int kRedBuf = kSgConsumers * RR * 32;     // floats per reduction buffer
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nlin = L.pool_f ? L.nstatic : L.units;  // static (range-assigned) units
@@ -360,7 +379,8 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
             for (int t = 0; t < TM; ++t) {
                 float acc = 0.f;
 #pragma unroll
-                for (int w = 0; w < kSgConsumers; ++w) acc += rb[(w * TM + t) * 32 + lane];
+                if (t < RR)
+                    for (int w = 0; w < kSgConsumers; ++w) acc += rb[(w * RR + t) * 32 + lane];
                 v[t] = acc;
             }
             __syncwarp();
@@ -541,8 +561,9 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
             // a group, so half of the warps sit a stage out), hence the same
             // per-row sum order whatever the pass size (batch invariance).
             constexpr int kRun = 4;
-            const int bbase = TM == 8 ? warp * kRun
-                                      : (((b / kStageBlocks) & 1) == (warp >> 2) ? (warp & 3) * kRun : kStageBlocks);
+            const int bbase = TM == 8 || kStageBlocks == 32
+                                  ? warp * kRun
+                                  : (((b / kStageBlocks) & 1) == (warp >> 2) ? (warp & 3) * kRun : kStageBlocks);
             uint32_t w[kRun][8];
             uint32_t a[kRun][4];
 #pragma unroll
@@ -591,14 +612,14 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
         const int e = i % L.ne;
         mbar_wait(&red_empty[e], rphase[e] ^ 1u);
         rphase[e] ^= 1u;
-        float* rw = red + e * kRedBuf + warp * TM * 32;
+        float* rw = red + e * kRedBuf + warp * RR * 32;
         if (warp == 0 && lane == 0) s_red_unit[e] = u;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int col = q * 8 + 2 * tig;
             rw[gid * 32 + col] = acc[q][0];
             rw[gid * 32 + col + 1] = acc[q][1];
-            if (TM == 16) {
+            if (TM == 16 && gid + 8 < RR) {
                 rw[(gid + 8) * 32 + col] = acc[q][2];
                 rw[(gid + 8) * 32 + col + 1] = acc[q][3];
             }
@@ -628,11 +649,11 @@ static bool g_pdl = true;
 void set_pdl(bool on) { g_pdl = on; }
 bool pdl_enabled() { return g_pdl; }
 
-template <int TM, int EPI>
+template <int TM, int EPI, int SB>
 static void sg_launch_t(const SgLaunch& L, int grid, size_t smem, cudaStream_t s) {
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(sgemv_kernel<TM, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSgSmemLimit);
+        cudaFuncSetAttribute(sgemv_kernel<TM, EPI, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSgSmemLimit);
         configured = true;
     }
     cudaLaunchConfig_t cfg{};
@@ -645,17 +666,17 @@ static void sg_launch_t(const SgLaunch& L, int grid, size_t smem, cudaStream_t s
     attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, sgemv_kernel<TM, EPI>, L);
+    cudaLaunchKernelEx(&cfg, sgemv_kernel<TM, EPI, SB>, L);
 }
 
-template <int TM>
+template <int TM, int SB>
 static void sg_dispatch(int epi, const SgLaunch& L, int grid, size_t smem, cudaStream_t s) {
     switch (epi) {
-        case EPI_STORE: sg_launch_t<TM, EPI_STORE>(L, grid, smem, s); break;
-        case EPI_RESID: sg_launch_t<TM, EPI_RESID>(L, grid, smem, s); break;
-        case EPI_SILU: sg_launch_t<TM, EPI_SILU>(L, grid, smem, s); break;
-        case EPI_QKV: sg_launch_t<TM, EPI_QKV>(L, grid, smem, s); break;
-        case EPI_ARGMAX: sg_launch_t<TM, EPI_ARGMAX>(L, grid, smem, s); break;
+        case EPI_STORE: sg_launch_t<TM, EPI_STORE, SB>(L, grid, smem, s); break;
+        case EPI_RESID: sg_launch_t<TM, EPI_RESID, SB>(L, grid, smem, s); break;
+        case EPI_SILU: sg_launch_t<TM, EPI_SILU, SB>(L, grid, smem, s); break;
+        case EPI_QKV: sg_launch_t<TM, EPI_QKV, SB>(L, grid, smem, s); break;
+        case EPI_ARGMAX: sg_launch_t<TM, EPI_ARGMAX, SB>(L, grid, smem, s); break;
     }
 }
 
@@ -767,6 +788,8 @@ void launch_sgemv(int epi, const GemvBatch& b, int nprob, int T, const PassView&
         const int TM = L.T <= 8 ? 8 : 16;
         L.xrows = L.T;  // slots hold only the pass rows (layout only: the plan, hence every sum, is unchanged)
         L.ne = sg_ne_used(TM, L.xrows);
+        L.sblk = sg_sblk(TM, p.kcb, L.xrows);
+        L.rrows = sg_red_rows(TM, L.xrows);
         // The weights stream through L2 exactly once: marking them evict-first
         // keeps L2 for what the dependency chain re-reads (activations, row
         // statistics, split-K partials, KV pages) — measured -6.7 % per step.
@@ -779,8 +802,9 @@ void launch_sgemv(int epi, const GemvBatch& b, int nprob, int T, const PassView&
         const size_t smem = sg_smem_bytes(TM, p.kcb, L.xrows);
         const int tslot = sg_trace_slot(b, nprob, L.T, epi, p);
         L.trace = tslot >= 0 ? g_trace.buf + (size_t)tslot * kSgTraceEv * kSgSms : nullptr;
-        if (TM == 8) sg_dispatch<8>(epi, L, p.grid, smem, s);
-        else sg_dispatch<16>(epi, L, p.grid, smem, s);
+        if (TM == 8) sg_dispatch<8, 32>(epi, L, p.grid, smem, s);
+        else if (L.sblk == 32) sg_dispatch<16, 32>(epi, L, p.grid, smem, s);
+        else sg_dispatch<16, 16>(epi, L, p.grid, smem, s);
         if (tslot == g_trace.cnt - 1) sg_trace_dump(s);
     }
 }

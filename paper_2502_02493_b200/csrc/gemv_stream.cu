@@ -23,6 +23,7 @@
 // Programmatic dependent launch: the producer starts streaming weights
 // before `griddepcontrol.wait`, so a GEMV's HBM pipeline fills while the
 // previous kernel (which produces x) drains; consumers wait before reading x.
+#include <algorithm>
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
@@ -63,6 +64,8 @@ struct SgLaunch {
     int xrows;  // activation rows held per slot (rows >= xrows read zeros)
     int ef;     // weights loaded with an L2 evict-first policy (ESPEC_SG_EVICT_FIRST, default 1)
     int ne;     // epilogue warps / reduction buffers in use (<= sg_ne<TM>())
+    int nslots; // activation slots (kSgSlots, or 1 with pair-aligned CTA ranges)
+    int aligned;  // pair-aligned ranges: every CTA's static range lies in ONE (problem, k-chunk) pair
     int sblk;   // 1 KB blocks per ring stage (TM=8: 32; TM=16: 16 or 32, see sg_sblk)
     int rrows;  // rows per warp in a reduction buffer (TM=8: 8; TM=16: the pass rows)
     unsigned long long* trace;  // diagnostic timeline (ESPEC_SG_TRACE) or nullptr
@@ -145,44 +148,49 @@ size_t sgemv_partial_floats(int K, int ldw) {
 }
 
 // smem = ring (stages x 8 KB) + activation slots (xrows rows) + reduction buffers
-static int sg_ne_used(int TM, int xrows) {
-    static const int big = [] {  // epilogue warps for 13-16 rows (ESPEC_SG_NE16)
+static int sg_ne_used(int TM, int xrows, int ns) {
+    static const int big = [] {  // epilogue warps for 13-16 rows (ESPEC_SG_NE16; default 4 with one slot, else 3)
         const char* e = std::getenv("ESPEC_SG_NE16");
-        return e ? std::atoi(e) : 3;
+        return e ? std::max(1, std::min(4, std::atoi(e))) : 0;
     }();
-    return TM == 16 && xrows > 12 ? big : 4;
+    static const int mid = [] {  // epilogue warps for 9-12 rows (ESPEC_SG_NE9)
+        const char* e = std::getenv("ESPEC_SG_NE9");
+        return e ? std::max(1, std::min(4, std::atoi(e))) : 4;
+    }();
+    if (TM == 8) return 4;
+    return xrows > 12 ? (big ? big : ns == 1 ? 4 : 3) : mid;
 }
 // Reduction buffers hold only the rows a pass has (rows >= T are never read
 // back): at T = 9-12 that is up to 28 KB more weight ring per SM.
 static int sg_red_rows(int TM, int xrows) { return TM == 8 ? 8 : xrows; }
-static size_t sg_fixed_bytes(int TM, int kcb, int xrows) {
-    return (size_t)kSgSlots * xrows * (kcb * 16 + 8) * 2 +
-           (size_t)sg_ne_used(TM, xrows) * kSgConsumers * sg_red_rows(TM, xrows) * 32 * 4;
+static size_t sg_fixed_bytes(int TM, int kcb, int xrows, int ns) {
+    return (size_t)ns * xrows * (kcb * 16 + 8) * 2 +
+           (size_t)sg_ne_used(TM, xrows, ns) * kSgConsumers * sg_red_rows(TM, xrows) * 32 * 4;
 }
 // 16-row stages: 32 blocks (one 32-block group: every consumer warp takes its
 // 4-block run each stage) whenever two such stages fit, else 16 blocks (half a
 // group; half of the warps sit a stage out). Measured at T = 9 (C2 base
 // gate/up): 16-block stages 178 us, 32-block 157 us. ESPEC_SG_SBLK16=16 forces
 // the 16-block stages.
-static int sg_sblk(int TM, int kcb, int xrows) {
+static int sg_sblk(int TM, int kcb, int xrows, int ns) {
     static const int force16 = [] {
         const char* e = std::getenv("ESPEC_SG_SBLK16");
         return e && std::atoi(e) == 16;
     }();
     if (TM == 8) return 32;
-    const long long room = (long long)kSgSmemLimit - (long long)sg_fixed_bytes(TM, kcb, xrows);
+    const long long room = (long long)kSgSmemLimit - (long long)sg_fixed_bytes(TM, kcb, xrows, ns);
     return !force16 && room >= 2 * 32 * 1024 ? 32 : 16;
 }
-static int sg_stage_bytes(int TM, int kcb, int xrows) { return sg_sblk(TM, kcb, xrows) * 1024; }
-static int sg_stages(int TM, int kcb, int xrows) {
-    const long long room = (long long)kSgSmemLimit - (long long)sg_fixed_bytes(TM, kcb, xrows);
-    int st = (int)(room / sg_stage_bytes(TM, kcb, xrows));
+static int sg_stage_bytes(int TM, int kcb, int xrows, int ns) { return sg_sblk(TM, kcb, xrows, ns) * 1024; }
+static int sg_stages(int TM, int kcb, int xrows, int ns) {
+    const long long room = (long long)kSgSmemLimit - (long long)sg_fixed_bytes(TM, kcb, xrows, ns);
+    int st = (int)(room / sg_stage_bytes(TM, kcb, xrows, ns));
     if (st > kSgMaxStages) st = kSgMaxStages;
     if (st < 2) throw std::runtime_error("sgemv: shared memory too small for the weight ring");
     return st;
 }
-static size_t sg_smem_bytes(int TM, int kcb, int xrows) {
-    return (size_t)sg_stages(TM, kcb, xrows) * sg_stage_bytes(TM, kcb, xrows) + sg_fixed_bytes(TM, kcb, xrows);
+static size_t sg_smem_bytes(int TM, int kcb, int xrows, int ns) {
+    return (size_t)sg_stages(TM, kcb, xrows, ns) * sg_stage_bytes(TM, kcb, xrows, ns) + sg_fixed_bytes(TM, kcb, xrows, ns);
 }
 
 // ---------------------------------------------------------------------------
@@ -219,7 +227,7 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
     unsigned char* ring = sm;
     __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(sm + (size_t)stages * kStageBytes);
     const int xslot = L.xrows * L.xld;  // elements per activation slot
-    float* red = reinterpret_cast<float*>(sm + (size_t)stages * kStageBytes + (size_t)kSgSlots * xslot * 2);
+    float* red = reinterpret_cast<float*>(sm + (size_t)stages * kStageBytes + (size_t)L.nslots * xslot * 2);
     const int RR = TM == 8 ? 8 : L.rrows;           // rows per warp slice of a reduction buffer
     const int kRedBuf = kSgConsumers * RR * 32;     // floats per reduction buffer
 
@@ -228,8 +236,20 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
     const int Gs = L.ngroups - L.pool_f;              // static groups per pair
     // static index -> unit (pair-major, groups [0, Gs) of every pair)
     auto sunit = [&](int x) { return (x / Gs) * L.ngroups + x % Gs; };
-    const int start = (int)((long long)blockIdx.x * nlin / gridDim.x);
-    const int end = (int)((long long)(blockIdx.x + 1) * nlin / gridDim.x);
+    // Pair-aligned ranges (L.aligned): pair p owns CTAs [p*G/np, (p+1)*G/np)
+    // and splits its Gs static groups evenly over them.
+    const int npairs = nlin / Gs;
+    auto pcta0 = [&](int pr) { return (int)((long long)pr * gridDim.x / npairs); };
+    int start, end;
+    if (L.aligned) {
+        const int pr = (int)(((long long)(blockIdx.x + 1) * npairs - 1) / gridDim.x);
+        const int c0 = pcta0(pr), np = pcta0(pr + 1) - c0, c = (int)blockIdx.x - c0;
+        start = pr * Gs + (int)((long long)c * Gs / np);
+        end = pr * Gs + (int)((long long)(c + 1) * Gs / np);
+    } else {
+        start = (int)((long long)blockIdx.x * nlin / gridDim.x);
+        end = (int)((long long)(blockIdx.x + 1) * nlin / gridDim.x);
+    }
     const int pair0 = sunit(start) / L.ngroups;
     __shared__ int s_stage_unit[kSgMaxStages];  // pool units: unit id of the stage that starts it (-1: done)
     __shared__ int s_red_unit[sg_ne<TM>()];     // pool units: unit id handed to epilogue warp e (-1: done)
@@ -240,7 +260,7 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
     // spread over the kernel instead of piling up at its end.
     const int len = end - start;
     const int R = (nlin + gridDim.x - 1) / gridDim.x;
-    int off = L.rotate && !L.pool_f ? (R - (start % L.ngroups) % R) % R : 0;
+    int off = L.rotate && !L.pool_f && !L.aligned ? (R - (start % L.ngroups) % R) % R : 0;
     if (off >= len) off = 0;
 
     if (tid < 2) s_xzero[tid] = make_uint4(0u, 0u, 0u, 0u);
@@ -295,7 +315,8 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
                 const int p_hi = len > 0 ? sunit(end - 1) / L.ngroups : pair0 - 1;
                 for (int pr = p_hi; pr >= pair0 && len > 0; --pr) {
                     const unsigned holders =
-                        (unsigned)(cta_of((long long)(pr + 1) * Gs - 1) - cta_of((long long)pr * Gs) + 1);
+                        L.aligned ? (unsigned)(pcta0(pr + 1) - pcta0(pr))
+                                  : (unsigned)(cta_of((long long)(pr + 1) * Gs - 1) - cta_of((long long)pr * Gs) + 1);
                     for (;;) {
                         const unsigned k = atomicAdd(&L.pool_ctr[pr], 1u);
                         if (k == (unsigned)L.pool_f + holders - 1u) atomicExch(&L.pool_ctr[pr], 0u);
@@ -782,13 +803,38 @@ void launch_sgemv(int epi, const GemvBatch& b, int nprob, int T, const PassView&
             L.pool_ctr = base[dev] + (size_t)(bank++ % kSgPoolBanks) * kSgPoolPairs;
         }
     }
+    static const int align16 = [] {
+        const char* e = std::getenv("ESPEC_SG_ALIGN16");
+        return e ? std::atoi(e) : 1;
+    }();
     for (int t0 = 0; t0 < T; t0 += 16) {
         L.t0 = t0;
         L.T = T - t0 < 16 ? T - t0 : 16;
         const int TM = L.T <= 8 ? 8 : 16;
         L.xrows = L.T;  // slots hold only the pass rows (layout only: the plan, hence every sum, is unchanged)
-        L.ne = sg_ne_used(TM, L.xrows);
-        L.sblk = sg_sblk(TM, p.kcb, L.xrows);
+        // 16-row passes: pair-aligned CTA ranges need ONE activation slot, so
+        // T x 4 KB more weight ring per SM (the ring depth bounds these
+        // launches). A unit's sums do not depend on which CTA runs it, so this
+        // is layout only. Taken when the largest per-CTA load is no larger than
+        // with balanced ranges (pairs get floor/ceil(G / npairs) CTAs) and the two-slot
+        // ring is under 96 KB. Measured (isolated, C2 base): gate/up T = 16
+        // 214 -> 167 us, head 463 -> 376 us; the 14-pair down projection
+        // (10-11 CTAs per pair) was 13-19 % slower, hence the balance rule.
+        L.aligned = 0;
+        L.nslots = kSgSlots;
+        if (TM == 16 && align16 &&
+            (long long)sg_stages(TM, p.kcb, L.xrows, kSgSlots) * sg_stage_bytes(TM, p.kcb, L.xrows, kSgSlots) <
+                96 * 1024) {
+            const int Gs = p.ngroups - L.pool_f, nlin = L.nstatic, npairs = nlin / Gs;
+            const int minc = p.grid / npairs;
+            if (minc >= 1 && Gs >= (p.grid + npairs - 1) / npairs &&
+                (Gs + minc - 1) / minc <= (nlin + p.grid - 1) / p.grid) {
+                L.aligned = 1;
+                L.nslots = 1;
+            }
+        }
+        L.ne = sg_ne_used(TM, L.xrows, L.nslots);
+        L.sblk = sg_sblk(TM, p.kcb, L.xrows, L.nslots);
         L.rrows = sg_red_rows(TM, L.xrows);
         // The weights stream through L2 exactly once: marking them evict-first
         // keeps L2 for what the dependency chain re-reads (activations, row
@@ -798,8 +844,8 @@ void launch_sgemv(int epi, const GemvBatch& b, int nprob, int T, const PassView&
             return e ? std::atoi(e) : 1;
         }();
         L.ef = ef;
-        L.stages = sg_stages(TM, p.kcb, L.xrows);
-        const size_t smem = sg_smem_bytes(TM, p.kcb, L.xrows);
+        L.stages = sg_stages(TM, p.kcb, L.xrows, L.nslots);
+        const size_t smem = sg_smem_bytes(TM, p.kcb, L.xrows, L.nslots);
         const int tslot = sg_trace_slot(b, nprob, L.T, epi, p);
         L.trace = tslot >= 0 ? g_trace.buf + (size_t)tslot * kSgTraceEv * kSgSms : nullptr;
         if (TM == 8) sg_dispatch<8, 32>(epi, L, p.grid, smem, s);

@@ -227,7 +227,11 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
     unsigned char* ring = sm;
     __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(sm + (size_t)stages * kStageBytes);
     const int xslot = L.xrows * L.xld;  // elements per activation slot
-    float* red = reinterpret_cast<float*>(sm + (size_t)stages * kStageBytes + (size_t)L.nslots * xslot * 2);
+    // 8-row passes always use two slots and balanced ranges (compile-time, so
+    // their code is unchanged by the 16-row options)
+    const bool aligned = TM == 16 && L.aligned;
+    const int nslots = TM == 8 ? kSgSlots : L.nslots;
+    float* red = reinterpret_cast<float*>(sm + (size_t)stages * kStageBytes + (size_t)nslots * xslot * 2);
     const int RR = TM == 8 ? 8 : L.rrows;           // rows per warp slice of a reduction buffer
     const int kRedBuf = kSgConsumers * RR * 32;     // floats per reduction buffer
 
@@ -238,10 +242,10 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
     auto sunit = [&](int x) { return (x / Gs) * L.ngroups + x % Gs; };
     // Pair-aligned ranges (L.aligned): pair p owns CTAs [p*G/np, (p+1)*G/np)
     // and splits its Gs static groups evenly over them.
-    const int npairs = nlin / Gs;
-    auto pcta0 = [&](int pr) { return (int)((long long)pr * gridDim.x / npairs); };
+    auto pcta0 = [&](int pr) { return (int)((long long)pr * gridDim.x / (nlin / Gs)); };
     int start, end;
-    if (L.aligned) {
+    if (aligned) {
+        const int npairs = nlin / Gs;
         const int pr = (int)(((long long)(blockIdx.x + 1) * npairs - 1) / gridDim.x);
         const int c0 = pcta0(pr), np = pcta0(pr + 1) - c0, c = (int)blockIdx.x - c0;
         start = pr * Gs + (int)((long long)c * Gs / np);
@@ -260,7 +264,7 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
     // spread over the kernel instead of piling up at its end.
     const int len = end - start;
     const int R = (nlin + gridDim.x - 1) / gridDim.x;
-    int off = L.rotate && !L.pool_f && !L.aligned ? (R - (start % L.ngroups) % R) % R : 0;
+    int off = L.rotate && !L.pool_f && !aligned ? (R - (start % L.ngroups) % R) % R : 0;
     if (off >= len) off = 0;
 
     if (tid < 2) s_xzero[tid] = make_uint4(0u, 0u, 0u, 0u);
@@ -315,7 +319,7 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
                 const int p_hi = len > 0 ? sunit(end - 1) / L.ngroups : pair0 - 1;
                 for (int pr = p_hi; pr >= pair0 && len > 0; --pr) {
                     const unsigned holders =
-                        L.aligned ? (unsigned)(pcta0(pr + 1) - pcta0(pr))
+                        aligned ? (unsigned)(pcta0(pr + 1) - pcta0(pr))
                                   : (unsigned)(cta_of((long long)(pr + 1) * Gs - 1) - cta_of((long long)pr * Gs) + 1);
                     for (;;) {
                         const unsigned k = atomicAdd(&L.pool_ctr[pr], 1u);

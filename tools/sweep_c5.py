@@ -22,14 +22,15 @@ import bench  # noqa: E402
 from paper_2502_02493_b200 import espec as E  # noqa: E402
 
 CTXS = [int(x) for x in sys.argv[1].split(",")] if len(sys.argv) > 1 else [512, 2048, 8192]
-LPS = [1, 2, 4, 8]
-NS = [3, 5, 8]
+# ESPEC_C5_LPS / ESPEC_C5_NS override the grid (e.g. ESPEC_C5_NS=8,12,15 for 9-16 row verify passes)
+LPS = [int(x) for x in os.environ.get("ESPEC_C5_LPS", "1,2,4,8").split(",")]
+NS = [int(x) for x in os.environ.get("ESPEC_C5_NS", "3,5,8").split(",")]
 WARM, STEPS = 2, 4
 
 
 def main():
     wl = bench.WORKLOADS["c2"]
-    mp = max(CTXS) + (WARM + STEPS + 2) * 9 + 64
+    mp = max(CTXS) + (WARM + STEPS + 2) * (max(NS) + 1) + 64
     base = E.ModelConfig(max_positions=mp, seed=7, tied_head=False, weight_dtype=E.BF16, kv_dtype=E.BF16, **wl["base"])
     draft = E.ModelConfig(max_positions=mp, seed=9, tied_head=False, weight_dtype=E.BF16, kv_dtype=E.BF16,
                           **wl["draft"])

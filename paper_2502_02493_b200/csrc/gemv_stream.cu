@@ -823,7 +823,9 @@ void launch_sgemv(int epi, const GemvBatch& b, int nprob, int T, const PassView&
         // with balanced ranges (pairs get floor/ceil(G / npairs) CTAs) and the two-slot
         // ring is under 96 KB. Measured (isolated, C2 base): gate/up T = 16
         // 214 -> 167 us, head 463 -> 376 us; the 14-pair down projection
-        // (10-11 CTAs per pair) was 13-19 % slower, hence the balance rule.
+        // (10-11 CTAs per pair) was 13-19 % slower, hence the balance rule
+        // (ESPEC_SG_ALIGN16=0 off, =2 ignores it: down T = 16 135 -> 128 us,
+        // T = 12-14 +2-12 %).
         L.aligned = 0;
         L.nslots = kSgSlots;
         if (TM == 16 && align16 &&
@@ -832,7 +834,7 @@ void launch_sgemv(int epi, const GemvBatch& b, int nprob, int T, const PassView&
             const int Gs = p.ngroups - L.pool_f, nlin = L.nstatic, npairs = nlin / Gs;
             const int minc = p.grid / npairs;
             if (minc >= 1 && Gs >= (p.grid + npairs - 1) / npairs &&
-                (Gs + minc - 1) / minc <= (nlin + p.grid - 1) / p.grid) {
+                (align16 == 2 || (Gs + minc - 1) / minc <= (nlin + p.grid - 1) / p.grid)) {
                 L.aligned = 1;
                 L.nslots = 1;
             }

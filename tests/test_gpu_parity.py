@@ -372,6 +372,29 @@ def test_decode_gemv_row_bitwise_independent_of_rows(K, N):
             assert np.array_equal(out[0], ref), (T, epi)
 
 
+def test_decode_gemv_row_bitwise_pair_aligned_ranges():
+    """The 8192 x 10240 (base QKV) shape takes pair-aligned one-slot CTA ranges
+    at 11-16 pass rows (gemv_stream.cu launch_sgemv) and balanced two-slot
+    ranges at 9-10, 8-row kernels below: row 0 must stay bit-identical."""
+    import ctypes as C
+    L = E.lib()
+    F = C.POINTER(C.c_float)
+    L.espec_probe_gemv.argtypes = [C.c_int] * 4 + [F, F, F, C.c_int]
+    K, N = 8192, 10240
+    rng = np.random.default_rng(7)
+    x = rng.standard_normal((16, K)).astype(np.float32)
+    w = (rng.standard_normal((K, N)) * 0.02).astype(np.float32)
+    ref = None
+    for T in (1, 8, 9, 12, 16):
+        for epi in (0, 1):
+            out = np.zeros((T, N), np.float32)
+            assert L.espec_probe_gemv(T, K, N, epi, x.ctypes.data_as(F), w.ctypes.data_as(F),
+                                      out.ctypes.data_as(F), 0) == 0
+            if ref is None:
+                ref = out[0].copy()
+            assert np.array_equal(out[0], ref), (T, epi)
+
+
 @pytest.mark.parametrize("switch", ["ESPEC_FUSE_ADDS", "ESPEC_B16_ACTS"])
 @pytest.mark.parametrize("T", [1, 4, 13])
 def test_bf16_decode_fusions_bitwise_equal_unfused(switch, T):

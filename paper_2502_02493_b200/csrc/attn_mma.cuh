@@ -424,17 +424,20 @@ __device__ __forceinline__ void attn_mma_item(const AttnProblem& A, const PassVi
         float4 acc[4];
 #pragma unroll
         for (int v = 0; v < 4; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int ch0 = 0; ch0 < nchunks; ch0 += 4) {
-            float4 x[4][4];
+        // CB chunks' loads in flight per round trip (the sum order is the
+        // chunk order whatever CB is)
+        constexpr int CB = 8;
+        for (int ch0 = 0; ch0 < nchunks; ch0 += CB) {
+            float4 x[CB][4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
+            for (int q = 0; q < CB; ++q)
 #pragma unroll
                 for (int v = 0; v < 4; ++v)
                     x[q][v] = ch0 + q < nchunks
                                   ? __ldcg(reinterpret_cast<const float4*>(base + (ch0 + q) * cstride + r * PS + c0 + 4 * v))
                                   : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
+            for (int q = 0; q < CB; ++q) {
                 if (ch0 + q >= nchunks) break;
                 const float f = fac[(ch0 + q) * 16 + r];
 #pragma unroll

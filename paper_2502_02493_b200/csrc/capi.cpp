@@ -78,6 +78,9 @@ espec_status guard(espec_engine* e, F&& f) {
     } catch (const Error& x) {
         e->err = x.what();
         return (espec_status)x.status;
+    } catch (const espec_dev::DevError& x) {
+        e->err = x.what();
+        return (espec_status)x.code;
     } catch (const std::exception& x) {
         e->err = x.what();
         return ESPEC_CHECK;
@@ -117,6 +120,9 @@ espec_status espec_engine_create(const espec_model_cfg* base, const espec_model_
     } catch (const Error& x) {
         g_create_error = x.what();
         return (espec_status)x.status;
+    } catch (const espec_dev::DevError& x) {
+        g_create_error = x.what();
+        return (espec_status)x.code;
     } catch (const std::exception& x) {
         g_create_error = x.what();
         return ESPEC_CHECK;

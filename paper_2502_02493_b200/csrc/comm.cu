@@ -30,11 +30,7 @@
 
 namespace espec_dev {
 
-#define CCK(x)                                                                                   \
-    do {                                                                                         \
-        cudaError_t e_ = (x);                                                                    \
-        if (e_ != cudaSuccess) fprintf(stderr, "CUDA error %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, __LINE__); \
-    } while (0)
+#define CCK(x) DEV_CK(x)
 
 constexpr int kCommThreads = 256;
 constexpr int kCommMaxCtas = 32;
@@ -75,7 +71,10 @@ __device__ void comm_signal_wait(const CommView& c, uint64_t seq, int par) {
                     printf("espec collective: rank %d timed out waiting for rank %d (seq %llu, flag %llu, block %d/%d)\n",
                            c.rank, s, (unsigned long long)seq, (unsigned long long)ld_acquire_sys(f), blockIdx.x,
                            gridDim.x);
-                    asm volatile("trap;");
+                    // reported as ESPEC_NCCL at the iteration's outcome read
+                    // (the context stays usable; the engine must be rebuilt)
+                    if (c.err) atomicExch(c.err, kCommErrTimeout);
+                    break;
                 }
             }
         }
@@ -140,10 +139,9 @@ __global__ void __launch_bounds__(kCommThreads, 6) allreduce_rows_kernel(CommVie
 
 void launch_allreduce_rows(CommView& c, const AllreduceArgs& a, cudaStream_t s) {
     if (a.rows <= 0) return;
-    if ((size_t)a.rows * a.d > c.slot_floats) {
-        fprintf(stderr, "allreduce: %d x %d exceeds the %zu-float comm slot\n", a.rows, a.d, c.slot_floats);
-        return;
-    }
+    if ((size_t)a.rows * a.d > c.slot_floats)
+        dev_fail(DEV_ERR_COMM, "allreduce: " + std::to_string(a.rows) + " x " + std::to_string(a.d) + " exceeds the " +
+                                   std::to_string(c.slot_floats) + "-float comm slot");
     const uint64_t seq = ++c.seq;
     if (getenv("ESPEC_TRACE_COMM")) fprintf(stderr, "[comm] rank %d allreduce seq %llu rows %d\n", c.rank, (unsigned long long)seq, a.rows);
     const int groups = a.rows * ((a.d + 31) / 32);
@@ -188,10 +186,9 @@ __global__ void __launch_bounds__(kCommThreads, 6) allgather_cols_kernel(CommVie
 
 void launch_allgather_cols(CommView& c, const GatherColsArgs& a, cudaStream_t s) {
     if (a.rows <= 0) return;
-    if ((size_t)a.rows * a.cols > c.slot_floats) {
-        fprintf(stderr, "allgather: %d x %d exceeds the comm slot\n", a.rows, a.cols);
-        return;
-    }
+    if ((size_t)a.rows * a.cols > c.slot_floats)
+        dev_fail(DEV_ERR_COMM, "allgather: " + std::to_string(a.rows) + " x " + std::to_string(a.cols) +
+                                   " exceeds the comm slot");
     const uint64_t seq = ++c.seq;
     long long n = (long long)a.rows * a.cols;
     int ctas = (int)((n + kCommThreads * 4 - 1) / (kCommThreads * 4));
@@ -246,6 +243,8 @@ __global__ void allgather_argmax_kernel(CommView c, uint64_t seq, int T, const f
 
 void launch_allgather_argmax(CommView& c, int T, const float* val, const int* idx, int* tok_out, cudaStream_t s) {
     if (T <= 0) return;
+    if ((size_t)2 * T > c.slot_floats)
+        dev_fail(DEV_ERR_COMM, "argmax all-gather: " + std::to_string(T) + " rows exceed the comm slot");
     const uint64_t seq = ++c.seq;
     if (getenv("ESPEC_TRACE_COMM")) fprintf(stderr, "[comm] rank %d argmax seq %llu\n", c.rank, (unsigned long long)seq);
     if (c.local_sync) {

@@ -588,14 +588,10 @@ int mk_grid() {
 }
 
 cudaError_t launch_decode_mk(const MkArgs& a, cudaStream_t s) {
-    static bool configured = false;
+    static unsigned long long configured = 0;
     const int stages = mk_stages();
     const size_t smem = (size_t)stages * kStageBytes + kAuxBytes;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(decode_mk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    ensure_smem((const void*)decode_mk_kernel, (int)smem, configured);
     MkArgs A = a;
     A.stages = stages;
     cudaLaunchConfig_t cfg{};

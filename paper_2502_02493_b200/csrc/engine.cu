@@ -615,6 +615,9 @@ public:
         arena_cap_ = err_off_ + 64;
         CUDA_OK(cudaMalloc(&arena_, sizeof(int) * (size_t)arena_cap_));
         CUDA_OK(cudaMemset(arena_, 0, sizeof(int) * (size_t)arena_cap_));
+        comm_.err = arena_ + err_off_;
+        CUDA_OK(cudaMalloc(&pool_.dev, sizeof(unsigned) * sgemv_pool_words()));
+        sgemv_pool_reset(pool_, stream_);
         CUDA_OK(cudaMallocHost(&outcome_host_, sizeof(int) * (size_t)(err_off_ - out_off_ + 1)));
         // T > 0 / tree-level buffers: logits and dists per drafted row
         const int V = bc.vocab_size;
@@ -640,6 +643,7 @@ public:
         staging_.destroy();
         for (void* p : ws_owned_) cudaFree(p);
         cudaFree(arena_);
+        cudaFree(pool_.dev);
         if (temp_) cudaFree(temp_);
         cudaFreeHost(outcome_host_);
         cudaFree(dlogits_);
@@ -1314,7 +1318,7 @@ public:
             return;
         }
         set_sgemv_wide(&M == &draft_ && wide_draft_);
-        site(M, kind, bytes, [&] { launch_gemv(epi, M.c.weight_dtype, b, n, T, ps.view, kv, stream_); });
+        site(M, kind, bytes, [&] { launch_gemv(epi, M.c.weight_dtype, b, n, T, ps.view, kv, stream_, &pool_); });
         set_sgemv_wide(false);
         launches_ += chunks(M, T);
     }
@@ -1497,7 +1501,7 @@ public:
         PassView none;
         set_sgemv_wide(&M == &draft_ && wide_draft_);
         site(M, 5, gemv_bytes(M, d, M.head_ld, Vl, n, 1),
-             [&] { launch_gemv(EPI_ARGMAX, c.weight_dtype, hb, 1, n, none, KvView(), stream_); });
+             [&] { launch_gemv(EPI_ARGMAX, c.weight_dtype, hb, 1, n, none, KvView(), stream_, &pool_); });
         set_sgemv_wide(false);
         launches_ += chunks(M, n);
         if (tp()) {
@@ -1561,6 +1565,9 @@ public:
         bcache_.reset();
         dcache_.reset();
         staging_.reset();
+        // a launch that ended early (error) may have left claim counters set
+        sgemv_pool_reset(pool_, stream_);
+        CUDA_OK(cudaMemsetAsync(arena_ + cur_off_, 0, sizeof(int) * 2, stream_));
         CUDA_OK(cudaMemcpyAsync(arena_, committed_.data(), sizeof(int) * committed_.size(), cudaMemcpyHostToDevice,
                                 stream_));
         h2d_bytes_ += (long long)(sizeof(int) * committed_.size());
@@ -1604,6 +1611,7 @@ public:
                                      "drafted token carries zero draft probability",
                                      "sibling candidates exhaust the draft distribution",
                                      "sampling from an all-zero distribution"};
+        if (err == kCommErrTimeout) throw Error(ST_NCCL, "tensor-parallel collective: a peer never arrived");
         if (err == 1) throw Error(ST_DOMAIN, msgs[1]);
         if (err > 1 && err <= 5) throw Error(ST_CHECK, msgs[err]);
         const int used = outcome_host_[cur_off_ - lo];
@@ -1649,9 +1657,16 @@ public:
             head(base_, bws_, (int)rows.size() - 1, 1, arena_ + n0, nullptr);
             CUDA_OK(cudaMemcpyAsync(outcome_host_, arena_ + n0, sizeof(int), cudaMemcpyDeviceToHost, stream_));
             d2h_bytes_ += sizeof(int);
+            if (tp()) {  // a collective timeout is reported through the error slot
+                CUDA_OK(cudaMemcpyAsync(outcome_host_ + (err_off_ - out_off_), arena_ + err_off_, sizeof(int),
+                                        cudaMemcpyDeviceToHost, stream_));
+                d2h_bytes_ += sizeof(int);
+            }
             CUDA_OK(cudaEventRecord(ev_[3], stream_));
             CUDA_OK(cudaEventSynchronize(ev_[3]));
             CUDA_OK(cudaGetLastError());
+            if (tp() && outcome_host_[err_off_ - out_off_] == kCommErrTimeout)
+                throw Error(ST_NCCL, "tensor-parallel collective: a peer never arrived");
         } else {
             // sample_from(softmax_temp(logits)) (orchestrator.cpp:457-460)
             head(base_, bws_, (int)rows.size() - 1, 1, arena_ + am_off_, blogits_);
@@ -2101,6 +2116,7 @@ private:
     Xoshiro rng_{1};
     // tensor parallelism
     CommView comm_;
+    SgPool pool_;  // decode-GEMV tail-pool counters of this engine's stream
     std::shared_ptr<LocalGroup> local_group_;
     void* comm_mem_ = nullptr;
     std::vector<void*> ipc_opened_;

@@ -676,11 +676,8 @@ bool pdl_enabled() { return g_pdl; }
 
 template <int TM, int EPI, int SB>
 static void sg_launch_t(const SgLaunch& L, int grid, size_t smem, cudaStream_t s) {
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(sgemv_kernel<TM, EPI, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSgSmemLimit);
-        configured = true;
-    }
+    static unsigned long long configured = 0;
+    ensure_smem((const void*)sgemv_kernel<TM, EPI, SB>, kSgSmemLimit, configured);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(sg_threads<TM>());
@@ -691,7 +688,7 @@ static void sg_launch_t(const SgLaunch& L, int grid, size_t smem, cudaStream_t s
     attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, sgemv_kernel<TM, EPI, SB>, L);
+    DEV_CK(cudaLaunchKernelEx(&cfg, sgemv_kernel<TM, EPI, SB>, L));
 }
 
 template <int TM, int SB>
@@ -752,8 +749,15 @@ static void sg_trace_dump(cudaStream_t s) {
     }
 }
 
+size_t sgemv_pool_words() { return (size_t)kSgPoolBanks * kSgPoolPairs; }
+
+void sgemv_pool_reset(SgPool& p, cudaStream_t s) {
+    if (p.dev) DEV_CK(cudaMemsetAsync(p.dev, 0, sizeof(unsigned) * sgemv_pool_words(), s));
+    p.next = 0;
+}
+
 void launch_sgemv(int epi, const GemvBatch& b, int nprob, int T, const PassView& pass, const KvView& kv,
-                  cudaStream_t s) {
+                  cudaStream_t s, SgPool* pool) {
     if (T <= 0 || nprob <= 0) return;
     SgPlan p = sgemv_plan(b.p[0].K, b.p[0].ldw, nprob);
     bool wide = false;
@@ -793,18 +797,19 @@ void launch_sgemv(int epi, const GemvBatch& b, int nprob, int T, const PassView&
             if (e0 > s0 && (e0 - 1) / Gs - s0 / Gs + 1 > kSgSlots) ok = false;
         }
         if (ok) {
-            static unsigned* base[64] = {nullptr};
-            static std::atomic<unsigned> bank{0};
-            int dev = 0;
-            cudaGetDevice(&dev);
-            if (!base[dev]) {
-                void* a = nullptr;
-                cudaGetSymbolAddress(&a, g_sg_pool);
-                base[dev] = static_cast<unsigned*>(a);
-            }
             L.pool_f = F;
             L.nstatic = (int)ns;
-            L.pool_ctr = base[dev] + (size_t)(bank++ % kSgPoolBanks) * kSgPoolPairs;
+        }
+    }
+    static SgPool g_pool[64];  // pool == nullptr: per-device process-wide banks
+    if (L.pool_f && !pool) {
+        int dev = 0;
+        DEV_CK(cudaGetDevice(&dev));
+        pool = &g_pool[dev & 63];
+        if (!pool->dev) {
+            void* a = nullptr;
+            DEV_CK(cudaGetSymbolAddress(&a, g_sg_pool));
+            pool->dev = static_cast<unsigned*>(a);
         }
     }
     static const int align16 = [] {
@@ -813,6 +818,10 @@ void launch_sgemv(int epi, const GemvBatch& b, int nprob, int T, const PassView&
     }();
     for (int t0 = 0; t0 < T; t0 += 16) {
         L.t0 = t0;
+        // a fresh counter bank per pass: a pass's producers claim pool units
+        // before griddepcontrol.wait, i.e. possibly while the previous pass
+        // (same call or previous launch) is still claiming from its bank
+        if (L.pool_f) L.pool_ctr = pool->dev + (size_t)(pool->next++ % kSgPoolBanks) * kSgPoolPairs;
         L.T = T - t0 < 16 ? T - t0 : 16;
         const int TM = L.T <= 8 ? 8 : 16;
         L.xrows = L.T;  // slots hold only the pass rows (layout only: the plan, hence every sum, is unchanged)

@@ -21,13 +21,25 @@
 
 namespace espec_dev {
 
-#define CK(x)                                                                                   \
-    do {                                                                                        \
-        cudaError_t e_ = (x);                                                                   \
-        if (e_ != cudaSuccess) {                                                                \
-            fprintf(stderr, "CUDA error %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, __LINE__); \
-        }                                                                                       \
-    } while (0)
+#define CK(x) DEV_CK(x)
+
+void dev_fail(int code, const std::string& msg) { throw DevError(code, msg); }
+
+void dev_check(cudaError_t e, const char* what, const char* file, int line) {
+    if (e == cudaSuccess) return;
+    (void)cudaGetLastError();  // clear a non-sticky launch error so the engine stays usable
+    dev_fail(DEV_ERR_CUDA, std::string(what) + " failed: " + cudaGetErrorString(e) + " (" + file + ":" +
+                               std::to_string(line) + ")");
+}
+
+void ensure_smem(const void* kernel, int bytes, unsigned long long& mask) {
+    int dev = 0;
+    DEV_CK(cudaGetDevice(&dev));
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (mask & bit) return;
+    DEV_CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    mask |= bit;
+}
 
 // ---------------------------------------------------------------------------
 // GEMV planning
@@ -321,12 +333,8 @@ __global__ void __launch_bounds__(kThreads) gemv_f32_kernel(const __grid_constan
 template <int TM, int EPI>
 static void gemv_launch_t(const GemvLaunch& L, int nprob, cudaStream_t s) {
     const size_t smem = sizeof(float) * (size_t)max(L.kc * TM, 8 * TM * kTileN);
-    static bool configured = false;
-    if (!configured) {
-        CK(cudaFuncSetAttribute(gemv_f32_kernel<TM, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                8 * 8 * kTileN * (int)sizeof(float)));
-        configured = true;
-    }
+    static unsigned long long configured = 0;
+    ensure_smem((const void*)gemv_f32_kernel<TM, EPI>, 8 * 8 * kTileN * (int)sizeof(float), configured);
     dim3 grid(L.tiles, L.splits, nprob);
     CK(launch_pdl(gemv_f32_kernel<TM, EPI>, grid, dim3(kThreads), smem, s, L));
 }
@@ -362,14 +370,14 @@ int gemv_col_tiles(int K, int N, int wdtype) {
 }
 
 void launch_gemv(int epi, int wdtype, const GemvBatch& b, int nprob, int T, const PassView& pass,
-                 const KvView& kv, cudaStream_t s) {
+                 const KvView& kv, cudaStream_t s, SgPool* pool) {
     if (T <= 0 || nprob <= 0) return;
     if (wdtype == DT_BF16) {
         if (g_prefill && T > 16 && epi != EPI_ARGMAX && b.p[0].tc_xa != nullptr) {
             for (int i = 0; i < nprob; ++i) launch_tc_gemm(epi, b.p[i], T, pass, kv, b.p[i].tc_xa, b.p[i].tc_rms, s);
             return;
         }
-        launch_sgemv(epi, b, nprob, T, pass, kv, s);
+        launch_sgemv(epi, b, nprob, T, pass, kv, s, pool);
         return;
     }
     GemvLaunch L;
@@ -691,19 +699,14 @@ template <int DH>
 static void attn_mma_launch(const AttnLaunch& L, int nprob, cudaStream_t s) {
     const int splits = (L.pass.total + 63) / 64;
     const int chunks = (splits + L.kv.attn_ppi - 1) / L.kv.attn_ppi;
-    if (chunks > kAttnMaxChunks) {
-        fprintf(stderr, "attention: context of %d rows exceeds the %d-row split-combine limit\n", L.pass.total,
-                kAttnMaxChunks * 64);
-        return;
-    }
+    if (chunks > kAttnMaxChunks)
+        dev_fail(DEV_ERR_CUDA, "attention: context of " + std::to_string(L.pass.total) + " rows exceeds the " +
+                                   std::to_string(kAttnMaxChunks * 64) + "-row split-combine limit");
     const int mtiles = (L.pass.T * L.G + 15) / 16;
     dim3 grid(chunks, L.kv.n_kv * mtiles, nprob);
     const size_t smem = kAttnItemSmem;
-    static bool configured = false;
-    if (!configured) {
-        CK(cudaFuncSetAttribute(attn_mma_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        configured = true;
-    }
+    static unsigned long long configured = 0;
+    ensure_smem((const void*)attn_mma_kernel<DH>, (int)smem, configured);
     // diagnostic: ESPEC_ATTN_TRACE=T,n traces the n-th launch with T pass rows (per CTA, %globaltimer
     // at 0 start, 1 past griddepcontrol.wait, 2 first K page, 3 pages done,
     // 4 partial written, 5 combine done) into gpurun_out/attn_trace.txt
@@ -754,22 +757,16 @@ void launch_attention(const AttnBatch& b, int nprob, int n_heads, const PassView
     L.splits = (pass.total + kAttnRows - 1) / kAttnRows;
     L.pblocks = (pass.T * L.G + kAttnPairs - 1) / kAttnPairs;
     const size_t smem = sizeof(float) * ((size_t)(kAttnPairs + kAttnRows) * (kv.dh + 1) + kAttnPairs * kAttnRows);
-    static bool configured[2] = {false, false};
+    static unsigned long long configured[2] = {0, 0};
     dim3 grid(L.splits, kv.n_kv * L.pblocks, nprob);
     if (kv.dtype == DT_BF16 && kv.page_rows == 64 && (kv.dh == 64 || kv.dh == 128)) {
         if (kv.dh == 128) attn_mma_launch<128>(L, nprob, s);
         else attn_mma_launch<64>(L, nprob, s);
     } else if (kv.dtype == DT_BF16) {
-        if (!configured[1]) {
-            CK(cudaFuncSetAttribute(attn_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-            configured[1] = true;
-        }
+        ensure_smem((const void*)attn_kernel<__nv_bfloat16>, 200 * 1024, configured[1]);
         CK(launch_pdl(attn_kernel<__nv_bfloat16>, grid, dim3(kAttnThreads), smem, s, L));
     } else {
-        if (!configured[0]) {
-            CK(cudaFuncSetAttribute(attn_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-            configured[0] = true;
-        }
+        ensure_smem((const void*)attn_kernel<float>, 200 * 1024, configured[0]);
         CK(launch_pdl(attn_kernel<float>, grid, dim3(kAttnThreads), smem, s, L));
     }
 }

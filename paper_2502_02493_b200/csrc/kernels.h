@@ -17,7 +17,28 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <stdexcept>
+#include <string>
+
 namespace espec_dev {
+
+// Host-side failure of a launch wrapper: a rejected launch, a capacity guard
+// or a collective that cannot run. Thrown (never printed and swallowed); the
+// engine's C ABI maps `code` onto espec_status (7 CUDA, 8 collective).
+enum : int { DEV_ERR_CUDA = 7, DEV_ERR_COMM = 8 };
+struct DevError : std::runtime_error {
+    int code;
+    DevError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] void dev_fail(int code, const std::string& msg);
+// cudaError_t -> DevError(DEV_ERR_CUDA) with the call site.
+void dev_check(cudaError_t e, const char* what, const char* file, int line);
+#define DEV_CK(x) ::espec_dev::dev_check((x), #x, __FILE__, __LINE__)
+// cudaFuncAttributeMaxDynamicSharedMemorySize is per device context: set it
+// once per (kernel, device). `mask` is the kernel's own bit set of devices.
+// Thread-safe enough for the engine's use (one host thread per engine; a
+// racing duplicate set is harmless).
+void ensure_smem(const void* kernel, int bytes, unsigned long long& mask);
 
 enum DType : int { DT_F32 = 0, DT_BF16 = 1 };
 
@@ -122,8 +143,18 @@ struct SgPlan {
 };
 SgPlan sgemv_plan(int K, int ldw, int nprob);
 size_t sgemv_partial_floats(int K, int ldw);
+// Tail-pool claim counters of one stream (engine): banks rotate per launch
+// PASS (16-row slice), so two in-flight passes never share counters even when
+// PDL lets a pass's producer claim before its predecessor finished.
+struct SgPool {
+    unsigned* dev = nullptr;  // [sgemv_pool_words()], zeroed by sgemv_pool_reset
+    unsigned next = 0;        // next bank (host)
+};
+size_t sgemv_pool_words();
+void sgemv_pool_reset(SgPool& p, cudaStream_t s);
+// pool == nullptr: a process-wide bank set (single-stream microbenchmarks only)
 void launch_sgemv(int epi, const GemvBatch& b, int nprob, int T, const PassView& pass, const KvView& kv,
-                  cudaStream_t s);
+                  cudaStream_t s, SgPool* pool = nullptr);
 // Thread-local: while on, launch_sgemv may pick a T-dependent "wide" plan
 // (whole-K units, activation slots of T rows). Rows then depend on the pass
 // size, so the engine enables it for the DRAFTER only: drafter numerics only
@@ -152,7 +183,7 @@ void launch_pack(const void* logical, int K, int ldw, void* packed, bool unpack,
 
 // y = epilogue(norm?(x) · W) for T rows, over nprob same-shape problems.
 void launch_gemv(int epi, int wdtype, const GemvBatch& b, int nprob, int T, const PassView& pass,
-                 const KvView& kv, cudaStream_t s);
+                 const KvView& kv, cudaStream_t s, SgPool* pool = nullptr);
 
 // h[t] = embedding[tok[t]] (fp32), + stats.
 void launch_embed(int wdtype, const void* emb, int d, const int* tok_arena, const int* tok_idx, int T,
@@ -262,6 +293,7 @@ void launch_verify_sample(const VerifyArgs& a, cudaStream_t s);
 
 // ---- tensor-parallel collectives over NVLink peer memory (comm.cu) ----
 constexpr int kMaxTp = 8;
+constexpr int kCommErrTimeout = 6;  // engine error-slot code (see EngineImpl::sync_outcome)
 struct CommView {
     int rank = 0, world = 1;
     size_t slot_floats = 0;          // floats per (parity, sender) slot
@@ -270,6 +302,7 @@ struct CommView {
     float* peer_recv[kMaxTp] = {};   // every rank's recv region (self included)
     uint64_t* peer_flags[kMaxTp] = {};
     unsigned* ticket = nullptr;      // local: last-CTA election
+    int* err = nullptr;              // engine error slot: kCommErrTimeout when a peer never arrives
     uint64_t seq = 0;                // collectives issued so far (host side)
     int early_trigger = 1;           // PDL-trigger the successor before waiting (GPUs not shared)
     int debug = 0;                   // ESPEC_TRACE_COMM: device-side trace

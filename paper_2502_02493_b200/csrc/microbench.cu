@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <vector>
 
 #include "../../include/espec_c.h"
@@ -12,7 +13,7 @@
 
 using namespace espec_dev;
 
-extern "C" espec_status espec_bench_gemv(int K, int N, int T, int nprob, int epi, int iters, int device,
+static espec_status espec_bench_gemv_impl(int K, int N, int T, int nprob, int epi, int iters, int device,
                                          double* us_per_launch, double* bytes_per_launch) {
     if (K <= 0 || N <= 0 || T <= 0 || T > 16 || nprob < 1 || nprob > kMaxProblems || iters < 1) return ESPEC_CONFIG;
     if (epi != EPI_STORE && epi != EPI_RESID && epi != EPI_SILU) return ESPEC_CONFIG;
@@ -90,7 +91,7 @@ extern "C" espec_status espec_bench_gemv(int K, int N, int T, int nprob, int epi
 
 // Decode/verify attention over a paged bf16 cache in isolation: T query rows
 // (the last T rows of a ctx-row context, causal), n_heads = G * n_kv.
-extern "C" espec_status espec_bench_attn(int T, int n_heads, int n_kv, int dh, int ctx, int nprob, int iters,
+static espec_status espec_bench_attn_impl(int T, int n_heads, int n_kv, int dh, int ctx, int nprob, int iters,
                                          int device, double* us_per_launch, double* bytes_per_launch) {
     if (T < 1 || T > 16 || n_kv < 1 || n_heads % n_kv || (dh != 64 && dh != 128) || ctx < T || nprob < 1 ||
         nprob > kMaxProblems || iters < 1)
@@ -192,7 +193,7 @@ extern "C" espec_status espec_bench_attn(int T, int n_heads, int n_kv, int dh, i
 }
 
 // Prefill GEMM (tcgen05) in isolation: M rows x K -> N (store epilogue).
-extern "C" espec_status espec_bench_tc(int M, int K, int N, int iters, int device, double* us_per_launch,
+static espec_status espec_bench_tc_impl(int M, int K, int N, int iters, int device, double* us_per_launch,
                                        double* flops_per_launch) {
     if (M < 1 || M > 256 || K % 16 || N % 32 || iters < 1) return ESPEC_CONFIG;
     if (cudaSetDevice(device) != cudaSuccess) return ESPEC_CUDA;
@@ -257,7 +258,7 @@ extern "C" espec_status espec_bench_tc(int M, int K, int N, int iters, int devic
 
 // Correctness probe of the prefill GEMM: out = bf16(x) . W for M rows with
 // host fp32 inputs (W logical K x N, row-major), packed on device.
-extern "C" espec_status espec_probe_tc(int M, int K, int N, const float* x_host, const float* w_host, float* out_host,
+static espec_status espec_probe_tc_impl(int M, int K, int N, const float* x_host, const float* w_host, float* out_host,
                                        int device) {
     if (M < 1 || M > 256 || K % 16 || N % 32) return ESPEC_CONFIG;
     if (cudaSetDevice(device) != cudaSuccess) return ESPEC_CUDA;
@@ -314,7 +315,7 @@ extern "C" espec_status espec_probe_tc(int M, int K, int N, const float* x_host,
 // One decode GEMV (EPI_STORE or EPI_RESID with zero residual) on host data:
 // x [T][K] fp32, w [K][N] fp32 (rounded to bf16, packed), out [T][N]. Used by
 // the batch-invariance tests (a row's result must not depend on T).
-extern "C" espec_status espec_probe_gemv(int T, int K, int N, int epi, const float* x_host, const float* w_host,
+static espec_status espec_probe_gemv_impl(int T, int K, int N, int epi, const float* x_host, const float* w_host,
                                          float* out_host, int device) {
     if (T < 1 || T > 16 || K % 16 || N % 32 || (epi != EPI_STORE && epi != EPI_RESID)) return ESPEC_CONFIG;
     if (cudaSetDevice(device) != cudaSuccess) return ESPEC_CUDA;
@@ -350,4 +351,41 @@ extern "C" espec_status espec_probe_gemv(int T, int K, int N, int epi, const flo
     cudaFree(Wl); cudaFree(W); cudaFree(x); cudaFree(out); cudaFree(resid); cudaFree(stats); cudaFree(part);
     cudaFree(tickets);
     return err == cudaSuccess ? ESPEC_OK : ESPEC_CUDA;
+}
+
+// The launch wrappers throw DevError on a rejected launch; nothing crosses
+// the C ABI as an exception.
+template <typename F>
+static espec_status mb_guard(F&& f) {
+    try {
+        return f();
+    } catch (const DevError& x) {
+        fprintf(stderr, "%s\n", x.what());
+        return (espec_status)x.code;
+    } catch (const std::exception& x) {
+        fprintf(stderr, "%s\n", x.what());
+        return ESPEC_CHECK;
+    }
+}
+
+extern "C" espec_status espec_bench_gemv(int K, int N, int T, int nprob, int epi, int iters, int device,
+                                         double* us_per_launch, double* bytes_per_launch) {
+    return mb_guard([&] { return espec_bench_gemv_impl(K, N, T, nprob, epi, iters, device, us_per_launch, bytes_per_launch); });
+}
+extern "C" espec_status espec_bench_attn(int T, int n_heads, int n_kv, int d_head, int ctx, int nprob, int iters,
+                                         int device, double* us_per_launch, double* bytes_per_launch) {
+    return mb_guard([&] {
+        return espec_bench_attn_impl(T, n_heads, n_kv, d_head, ctx, nprob, iters, device, us_per_launch, bytes_per_launch);
+    });
+}
+extern "C" espec_status espec_bench_tc(int M, int K, int N, int iters, int device, double* us_per_launch,
+                                       double* flops_per_launch) {
+    return mb_guard([&] { return espec_bench_tc_impl(M, K, N, iters, device, us_per_launch, flops_per_launch); });
+}
+extern "C" espec_status espec_probe_tc(int M, int K, int N, const float* x, const float* w, float* out, int device) {
+    return mb_guard([&] { return espec_probe_tc_impl(M, K, N, x, w, out, device); });
+}
+extern "C" espec_status espec_probe_gemv(int T, int K, int N, int epi, const float* x, const float* w, float* out,
+                                         int device) {
+    return mb_guard([&] { return espec_probe_gemv_impl(T, K, N, epi, x, w, out, device); });
 }

@@ -25,11 +25,7 @@ namespace espec_dev {
 constexpr int kSThreads = 1024;
 constexpr int kSWarps = kSThreads / 32;
 
-#define SCK(x)                                                                                   \
-    do {                                                                                         \
-        cudaError_t e_ = (x);                                                                    \
-        if (e_ != cudaSuccess) fprintf(stderr, "CUDA error %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, __LINE__); \
-    } while (0)
+#define SCK(x) DEV_CK(x)
 
 __device__ __forceinline__ bool s_better(float v, int i, float bv, int bi) { return v > bv || (v == bv && i < bi); }
 

@@ -439,13 +439,10 @@ __global__ void tc_pack_a_kernel(GemvProblem P, int t0, int T, int KS, int mtile
 
 template <int EPI>
 static void tc_launch_t(const TcLaunch& L, int ntiles, cudaStream_t s) {
-    static bool configured = false;
+    static unsigned long long configured = 0;
     const int smem = kTcStages * kTcStageBytes;
-    if (!configured) {
-        cudaFuncSetAttribute(tc_gemm_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        configured = true;
-    }
-    launch_pdl(tc_gemm_kernel<EPI>, dim3(ntiles, 1, L.ksplits), dim3(kTcThreads), (size_t)smem, s, L);
+    ensure_smem((const void*)tc_gemm_kernel<EPI>, smem, configured);
+    DEV_CK(launch_pdl(tc_gemm_kernel<EPI>, dim3(ntiles, 1, L.ksplits), dim3(kTcThreads), (size_t)smem, s, L));
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
@@ -495,10 +492,8 @@ size_t tc_part_floats(int K, int ldw) {
 void launch_tc_gemm(int epi, const GemvProblem& P, int T, const PassView& pass, const KvView& kv,
                     __nv_bfloat16* xa, float* inv_rms, cudaStream_t s) {
     if (T <= 0) return;
-    if (T > kTcMSub * kTcM) {
-        fprintf(stderr, "tc_gemm: %d rows exceed the 256-row prefill chunk\n", T);
-        return;
-    }
+    if (T > kTcMSub * kTcM)
+        dev_fail(DEV_ERR_CUDA, "tc_gemm: " + std::to_string(T) + " rows exceed the 256-row prefill chunk");
     TcLaunch L;
     L.use_tma = tc_encode_b(L.tmB, P.W, (P.K + 15) / 16, P.ldw / 32) ? 1 : 0;
     L.P = P;
@@ -513,17 +508,18 @@ void launch_tc_gemm(int epi, const GemvProblem& P, int T, const PassView& pass, 
     L.part = P.tc_part;
     L.tickets = P.tc_tickets;
     tc_rms_kernel<<<(T + 7) / 8, 256, 0, s>>>(P, 0, T, inv_rms);
+    DEV_CK(cudaGetLastError());
     const long long total = (long long)L.mtiles * L.KS * 256;
     int blocks = (int)((total + 255) / 256);
     if (blocks > 148 * 16) blocks = 148 * 16;
-    launch_pdl(tc_pack_a_kernel, dim3(blocks), dim3(256), 0, s, P, 0, T, L.KS, L.mtiles, (const float*)inv_rms, xa);
+    DEV_CK(launch_pdl(tc_pack_a_kernel, dim3(blocks), dim3(256), 0, s, P, 0, T, L.KS, L.mtiles, (const float*)inv_rms, xa));
     const int ntiles = (P.ldw / 32 + kTcN / 32 - 1) / (kTcN / 32);
     switch (epi) {
         case EPI_STORE: tc_launch_t<EPI_STORE>(L, ntiles, s); break;
         case EPI_RESID: tc_launch_t<EPI_RESID>(L, ntiles, s); break;
         case EPI_SILU: tc_launch_t<EPI_SILU>(L, ntiles, s); break;
         case EPI_QKV: tc_launch_t<EPI_QKV>(L, ntiles, s); break;
-        default: fprintf(stderr, "tc_gemm: epilogue %d not supported for prefill\n", epi);
+        default: dev_fail(DEV_ERR_CUDA, "tc_gemm: epilogue " + std::to_string(epi) + " not supported for prefill");
     }
 }
 

@@ -72,6 +72,12 @@ typedef struct {
     int max_new_tokens;
     uint64_t seed;
     int calibration;
+    /* 1 reproduces the reference's CheckError when a greedy (T = 0) tree's
+     * first sibling is rejected with siblings left (verifier.cpp:146-158:
+     * the one-hot draft mass is exhausted); 0 (default) accepts the sibling
+     * equal to the base argmax instead — identical outputs whenever the
+     * reference does not throw. */
+    int strict_greedy_tree;
 } espec_run_cfg;
 
 /* Devices used by one engine. One engine drives one GPU; a tensor-parallel
@@ -161,6 +167,64 @@ espec_status espec_generate(espec_engine* eng, const uint8_t* prompt, int prompt
 espec_status espec_begin(espec_engine* eng, const int32_t* tokens, int n_tokens);
 espec_status espec_step(espec_engine* eng, int32_t* emitted, int* n_emitted, espec_iteration* trace);
 int espec_done(const espec_engine* eng);
+
+/* ---- Stage-level API: one speculative iteration driven stage by stage, the
+ * split of Generation::run_iteration_speculative (orchestrator.cpp:407-436)
+ * into the reference's stages. Order per iteration: calibrate -> draft ->
+ * verify -> resolve_draft_cache -> commit_outcome (espec_step runs the same
+ * five in one call). Out-of-order calls return ESPEC_STRUCTURE. */
+#define ESPEC_MAX_NODES 64
+
+/* espec::DraftTree (draft_engine.hpp:63-84): nodes level by level, siblings
+ * contiguous in selection order; parent -1 = child of the committed context;
+ * prob_index indexes the draft distributions; cache_row = drafter-cache flat
+ * row (-1 for the never-forwarded last level). */
+typedef struct {
+    uint64_t id; /* iteration the tree belongs to */
+    int n_nodes, root_children, n_levels, n_dists;
+    int32_t widths[ESPEC_MAX_NODES];
+    int32_t token[ESPEC_MAX_NODES], parent[ESPEC_MAX_NODES], depth[ESPEC_MAX_NODES];
+    int32_t prob_index[ESPEC_MAX_NODES], cache_row[ESPEC_MAX_NODES];
+    int32_t first_child[ESPEC_MAX_NODES], n_children[ESPEC_MAX_NODES];
+    /* optional: caller buffer of dist_capacity x vocab floats that receives
+     * DraftTree::dists (softmax_temp rows; one-hot at T = 0) */
+    float* dists;
+    int dist_capacity;
+} espec_tree;
+
+/* espec::VerificationOutcome (verifier.hpp:14-21). */
+typedef struct {
+    uint64_t id;
+    int m, n;
+    int32_t bonus;
+    int32_t accepted_path[ESPEC_MAX_NODES];
+    int32_t accepted_tokens[ESPEC_MAX_NODES];
+} espec_outcome;
+
+/* Start a generation over token ids and prefill both caches with what the
+ * first iteration would (base: every prompt row but the frontier token;
+ * drafter: the prompt's whole 256-row chunks). */
+espec_status espec_prefill(espec_engine* eng, const int32_t* tokens, int n_tokens);
+/* drafter_leading_pass (orchestrator.cpp:256-300): the uncached committed
+ * suffix through one precise drafter pass (the bonus calibration that
+ * rewrites the draft KV; fuzzy in the no-calibration arm). root_logits
+ * (optional, vocab floats) receives the drafter logits of the last row. */
+espec_status espec_calibrate(espec_engine* eng, float* root_logits);
+/* draft_stage -> draft_tree (orchestrator.cpp:302-331, draft_engine.cpp:188-289):
+ * the fuzzy layer-parallel passes. tree (optional) receives the DraftTree. */
+espec_status espec_draft(espec_engine* eng, espec_tree* tree);
+/* verify_stage + verify_tree (orchestrator.cpp:333-388, verifier.cpp:86-177):
+ * one base pass over [frontier + tree], acceptance, base-cache commit. tree
+ * NULL verifies the tree as drafted; otherwise it must be this iteration's
+ * tree (same id and shape) and its tokens replace the drafted ones. */
+espec_status espec_verify(espec_engine* eng, const espec_tree* tree, espec_outcome* outcome);
+/* resolve_draft_cache (orchestrator.cpp:390-405): discard the fuzzy rows
+ * (calibrated EasySpec) or commit the accepted path's staged rows. outcome
+ * NULL = this iteration's; otherwise it must match it. */
+espec_status espec_resolve_draft_cache(espec_engine* eng, const espec_outcome* outcome);
+/* run_iteration_speculative's tail (orchestrator.cpp:414-428): commit the
+ * accepted tokens + bonus, emit min(m + 1, remaining) into emitted. */
+espec_status espec_commit_outcome(espec_engine* eng, int32_t* emitted, int* n_emitted, espec_iteration* trace);
 
 /* IterationHook view (proj/include/espec/orchestrator.hpp:46-55): committed
  * token count and K/V rows [row0, row0+n) of one layer of the drafter (0) or

@@ -26,6 +26,7 @@
 #include "espec/layer_plan.hpp"
 #include "espec/model.hpp"
 #include "espec/orchestrator.hpp"
+#include "espec/verifier.hpp"
 
 using namespace espec;
 using json = nlohmann::ordered_json;
@@ -208,6 +209,162 @@ json run_case(const GenCase& gc) {
     } catch (const Error& e) {
         j["error"] = e.what();
     }
+    return j;
+}
+
+// The reference's speculative iteration re-driven stage by stage through its
+// PUBLIC functions (forward_sequential / forward_fuzzy / draft_tree /
+// verify_tree / KvCache), restating Generation's private glue
+// (stage_suffix, drafter_leading_pass, verify_stage, resolve_draft_cache,
+// proj/src/orchestrator.cpp:225-436), so every iteration's DraftTree and
+// VerificationOutcome can be dumped. main() checks that the tokens equal
+// generate()'s for the same case, which pins the restated glue.
+json run_stages(const GenCase& gc) {
+    const Model base = init_model(gc.base);
+    Model draft;
+    if (gc.draft_seed != 0) {
+        ModelConfig dc = gc.base;
+        dc.n_layers = gc.keep;
+        dc.seed = gc.draft_seed;
+        draft = init_model(dc);
+    } else {
+        draft = gc.keep == 0 ? base : make_truncated_draft(base, gc.keep);
+    }
+    const RunConfig& cfg = gc.run;
+    const bool easy = cfg.algorithm == Algorithm::easyspec;
+    const LayerPlan plan = !easy ? plan_groups(draft.config.n_layers, 1)
+                                 : (cfg.plan_override ? parse_plan_override(*cfg.plan_override)
+                                                      : plan_groups(draft.config.n_layers, cfg.lp_size));
+    const std::vector<int> widths = cfg.effective_widths();
+    KvCache bcache(base.config.n_layers, base.config.d_model), dcache(draft.config.n_layers, draft.config.d_model);
+    Xoshiro256ss rng(cfg.seed);
+    ForwardCounters counters;
+    std::vector<Token> committed = bos_bytes(gc.prompt), generated;
+    int draft_cached = 0;
+    auto suffix = [&](KvCache& cache, int cached, bool fuzzy, std::vector<Token>& toks) {
+        std::vector<int> parents;
+        for (int i = cached; i < static_cast<int>(committed.size()); ++i) {
+            parents.push_back(parents.empty() ? kCommittedTail
+                                              : cache.committed_len() + static_cast<int>(parents.size()) - 1);
+            toks.push_back(committed[static_cast<std::size_t>(i)]);
+        }
+        return cache.stage_append(parents, fuzzy);
+    };
+    auto batch_for = [](const KvCache& cache, const std::vector<int>& rows, const TreeMask* mask, bool cal) {
+        ForwardBatch b;
+        b.flat_rows = rows;
+        for (int r : rows) b.positions.push_back(cache.position_of(r));
+        b.mask = mask;
+        b.calibrate_writes = cal;
+        return b;
+    };
+    json iters = json::array();
+    json j;
+    j["name"] = gc.name;
+    try {
+        while (static_cast<int>(generated.size()) < cfg.max_new_tokens) {
+            // drafter_leading_pass
+            const bool calibrated = easy && cfg.calibration, fuzzy_pass = easy && !cfg.calibration;
+            std::vector<Token> ctoks;
+            const std::vector<int> crow = suffix(dcache, draft_cached, fuzzy_pass, ctoks);
+            Matrix hidden;
+            {
+                const TreeMask mask = dcache.build_tree_mask();
+                const ForwardBatch b = batch_for(dcache, crow, &mask, calibrated);
+                const Matrix h_in = embed(draft, ctoks);
+                hidden = fuzzy_pass ? forward_fuzzy(draft, plan, h_in, dcache, b)
+                                    : forward_sequential(draft, h_in, dcache, b);
+            }
+            dcache.commit_path(crow);
+            draft_cached = static_cast<int>(committed.size());
+            const Matrix root = lm_logits(draft, Matrix(1, hidden.cols, {hidden.row(hidden.rows - 1).begin(),
+                                                                         hidden.row(hidden.rows - 1).end()}));
+            // draft_stage
+            const DraftTree tree = draft_tree(draft, plan, dcache, root.row(0), widths, cfg.temperature, rng,
+                                              counters, easy, nullptr);
+            // verify_stage
+            std::vector<Token> vtoks;
+            const std::vector<int> vchain = suffix(bcache, bcache.committed_len(), false, vtoks);
+            const int first_node_row = vchain.back() + 1;
+            std::vector<int> tparents;
+            for (const auto& nd : tree.nodes) {
+                tparents.push_back(nd.parent < 0 ? vchain.back() : first_node_row + nd.parent);
+                vtoks.push_back(nd.token);
+            }
+            const std::vector<int> node_rows = bcache.stage_append(tparents, false);
+            std::vector<int> all_rows = vchain;
+            all_rows.insert(all_rows.end(), node_rows.begin(), node_rows.end());
+            const TreeMask bmask = bcache.build_tree_mask();
+            const Matrix logits =
+                lm_logits(base, forward_sequential(base, embed(base, vtoks), bcache,
+                                                   batch_for(bcache, all_rows, &bmask, false)));
+            std::vector<ProbVector> bd;
+            const int frontier = static_cast<int>(vchain.size()) - 1;
+            for (int i = 0; i <= tree.node_count(); ++i)
+                bd.push_back(softmax_temp(logits.row(frontier + i), cfg.temperature));
+            const VerificationOutcome out = verify_tree(tree, bd, cfg.temperature, rng);
+            std::vector<int> commit_rows = vchain;
+            for (int ni : out.accepted_path) commit_rows.push_back(node_rows[static_cast<std::size_t>(ni)]);
+            bcache.commit_path(commit_rows);
+            // resolve_draft_cache
+            if (calibrated) {
+                dcache.discard_staged();
+            } else {
+                std::vector<int> rows;
+                for (int ni : out.accepted_path) {
+                    const int r = tree.nodes[static_cast<std::size_t>(ni)].cache_row;
+                    if (r < 0) break;
+                    rows.push_back(r);
+                }
+                dcache.commit_path(rows);
+                draft_cached += static_cast<int>(rows.size());
+            }
+            for (Token t : out.accepted_tokens) committed.push_back(t);
+            committed.push_back(out.bonus_token);
+            const int emit = std::min(out.m + 1, cfg.max_new_tokens - static_cast<int>(generated.size()));
+            for (int i = 0; i < emit; ++i)
+                generated.push_back(committed[committed.size() - static_cast<std::size_t>(out.m + 1) +
+                                              static_cast<std::size_t>(i)]);
+            json t = json::object(), ids = json::array();
+            std::vector<int> tok, par, dep, pi, cr, fc, nc;
+            for (const auto& nd : tree.nodes) {
+                tok.push_back(nd.token);
+                par.push_back(nd.parent);
+                dep.push_back(nd.depth);
+                pi.push_back(nd.prob_index);
+                cr.push_back(nd.cache_row);
+                fc.push_back(nd.first_child);
+                nc.push_back(nd.n_children);
+            }
+            t["token"] = tok;
+            t["parent"] = par;
+            t["depth"] = dep;
+            t["prob_index"] = pi;
+            t["cache_row"] = cr;
+            t["first_child"] = fc;
+            t["n_children"] = nc;
+            t["root_children"] = tree.root_children;
+            t["n_dists"] = static_cast<int>(tree.dists.size());
+            // first draft distribution's top entries (pins dists without the full V rows)
+            double dsum = 0.0;
+            for (const auto& d : tree.dists)
+                for (float v : d.probs) dsum += v;
+            t["dists_sum"] = dsum;
+            iters.push_back(json{{"tree", t},
+                                 {"m", out.m},
+                                 {"n", out.n},
+                                 {"path", out.accepted_path},
+                                 {"accepted", out.accepted_tokens},
+                                 {"bonus", out.bonus_token},
+                                 {"draft_committed", dcache.committed_len()},
+                                 {"base_committed", bcache.committed_len()}});
+        }
+        j["tokens"] = generated;
+        j["error"] = nullptr;
+    } catch (const Error& e) {
+        j["error"] = e.what();
+    }
+    j["iterations"] = iters;
     return j;
 }
 
@@ -398,11 +555,38 @@ int main(int argc, char** argv) {
     cases.push_back({"t3_tree_nocal", tiny(8, 7, 32, 2, 16, 64, 256), 4,
                      run_cfg(Algorithm::easyspec, 4, {2, 2, 1, 1}, 2, 3.0f, 48, 4, false), "tree search"});
 
+    {
+        // A greedy tree whose first sibling IS rejected (independent drafter,
+        // alpha < 1): the reference raises CheckError("sibling candidates
+        // exhaust the draft distribution", proj/src/verifier.cpp:146-158).
+        // Appended last so the earlier fixtures stay byte-identical.
+        GenCase g{"greedy_tree_throws_indep", tiny(8, 11, 64, 4, 16, 128, 256), 5,
+                  run_cfg(Algorithm::easyspec, 4, {2, 2, 1, 1}, 2, 0.0f, 24, 1), "independent"};
+        g.draft_seed = 9;
+        cases.push_back(g);
+    }
     json gens = json::array();
     for (const auto& gc : cases) gens.push_back(run_case(gc));
     {
         std::ofstream f(out_dir + "/ref_generate.json");
         f << gens.dump() << "\n";
+    }
+    // per-iteration trees and outcomes of every speculative case, from the
+    // stage-by-stage restatement pinned against generate()
+    json stages = json::array();
+    for (std::size_t i = 0; i < cases.size(); ++i) {
+        if (cases[i].run.algorithm == Algorithm::vanilla) continue;
+        json st = run_stages(cases[i]);
+        const json& g = gens[i];
+        if (st["error"] != g["error"] || (g["error"].is_null() && st["tokens"] != g["tokens"])) {
+            std::cerr << "stage restatement diverges from generate() on " << cases[i].name << "\n";
+            return 1;
+        }
+        stages.push_back(st);
+    }
+    {
+        std::ofstream f(out_dir + "/ref_stages.json");
+        f << stages.dump() << "\n";
     }
     std::cout << "wrote " << out_dir << "/ref_numerics.json and ref_generate.json (" << cases.size()
               << " generation cases)\n";

@@ -11,6 +11,7 @@ using namespace espec;
 struct espec_engine {
     std::unique_ptr<Engine> impl;
     std::string err;
+    int vocab = 0;
 };
 
 static thread_local std::string g_create_error;
@@ -48,6 +49,7 @@ RunCfg to_run(const espec_run_cfg* r) {
     c.max_new_tokens = r->max_new_tokens;
     c.seed = r->seed;
     c.calibration = r->calibration;
+    c.strict_greedy_tree = r->strict_greedy_tree;
     return c;
 }
 
@@ -114,6 +116,7 @@ espec_status espec_engine_create(const espec_model_cfg* base, const espec_model_
             delete e;
             throw;
         }
+        e->vocab = base->vocab_size;
         *out = e;
         g_create_error.clear();
         return ESPEC_OK;
@@ -288,6 +291,116 @@ espec_status espec_generate_tokens(espec_engine* eng, const int32_t* tokens, int
 
 espec_status espec_sync(espec_engine* eng) {
     return guard(eng, [&] { eng->impl->sync(); });
+}
+
+}  // extern "C"
+
+// ---- stage-level API
+namespace {
+void tree_to_c(const TreeOut& t, espec_tree* o, int vocab) {
+    const int nn = (int)t.token.size();
+    if (nn > ESPEC_MAX_NODES) throw Error(ST_SHAPE, "tree exceeds ESPEC_MAX_NODES");
+    o->id = t.id;
+    o->n_nodes = nn;
+    o->root_children = t.root_children;
+    o->n_levels = (int)t.widths.size();
+    o->n_dists = t.n_dists;
+    for (int i = 0; i < o->n_levels && i < ESPEC_MAX_NODES; ++i) o->widths[i] = t.widths[i];
+    for (int j = 0; j < nn; ++j) {
+        o->token[j] = t.token[j];
+        o->parent[j] = t.parent[j];
+        o->depth[j] = t.depth[j];
+        o->prob_index[j] = t.prob_index[j];
+        o->cache_row[j] = t.cache_row[j];
+        o->first_child[j] = t.first_child[j];
+        o->n_children[j] = t.n_children[j];
+    }
+    if (o->dists) {
+        if (o->dist_capacity < t.n_dists) throw Error(ST_SHAPE, "dist buffer holds fewer rows than the tree's dists");
+        std::memcpy(o->dists, t.dists.data(), sizeof(float) * (size_t)t.n_dists * vocab);
+    }
+}
+TreeOut tree_from_c(const espec_tree* c) {
+    if (c->n_nodes < 0 || c->n_nodes > ESPEC_MAX_NODES) throw Error(ST_SHAPE, "tree node count out of range");
+    TreeOut t;
+    t.id = c->id;
+    t.token.assign(c->token, c->token + c->n_nodes);
+    t.parent.assign(c->parent, c->parent + c->n_nodes);
+    return t;
+}
+}  // namespace
+
+extern "C" {
+
+espec_status espec_prefill(espec_engine* eng, const int32_t* tokens, int n_tokens) {
+    return guard(eng, [&] {
+        if (!tokens || n_tokens <= 0) throw Error(ST_CONFIG, "empty prompt");
+        eng->impl->prefill(std::vector<int>(tokens, tokens + n_tokens));
+    });
+}
+
+espec_status espec_calibrate(espec_engine* eng, float* root_logits) {
+    return guard(eng, [&] { eng->impl->calibrate(root_logits); });
+}
+
+espec_status espec_draft(espec_engine* eng, espec_tree* tree) {
+    return guard(eng, [&] {
+        if (!tree) {
+            eng->impl->draft(nullptr, false);
+            return;
+        }
+        TreeOut t;
+        eng->impl->draft(&t, tree->dists != nullptr);
+        tree_to_c(t, tree, eng->vocab);
+    });
+}
+
+espec_status espec_verify(espec_engine* eng, const espec_tree* tree, espec_outcome* outcome) {
+    return guard(eng, [&] {
+        OutcomeOut o;
+        if (tree) {
+            const TreeOut t = tree_from_c(tree);
+            eng->impl->verify(&t, &o);
+        } else {
+            eng->impl->verify(nullptr, &o);
+        }
+        if (outcome) {
+            outcome->id = o.id;
+            outcome->m = o.m;
+            outcome->n = o.n;
+            outcome->bonus = o.bonus;
+            for (int i = 0; i < o.m; ++i) {
+                outcome->accepted_path[i] = o.path[i];
+                outcome->accepted_tokens[i] = o.tokens[i];
+            }
+        }
+    });
+}
+
+espec_status espec_resolve_draft_cache(espec_engine* eng, const espec_outcome* outcome) {
+    return guard(eng, [&] {
+        if (!outcome) {
+            eng->impl->resolve_draft_cache(nullptr);
+            return;
+        }
+        if (outcome->m < 0 || outcome->m > ESPEC_MAX_NODES) throw Error(ST_SHAPE, "outcome m out of range");
+        OutcomeOut o;
+        o.id = outcome->id;
+        o.m = outcome->m;
+        o.path.assign(outcome->accepted_path, outcome->accepted_path + outcome->m);
+        eng->impl->resolve_draft_cache(&o);
+    });
+}
+
+espec_status espec_commit_outcome(espec_engine* eng, int32_t* emitted, int* n_emitted, espec_iteration* trace) {
+    return guard(eng, [&] {
+        std::vector<int> em;
+        const IterationTrace t = eng->impl->commit_outcome(em);
+        if (emitted)
+            for (size_t i = 0; i < em.size(); ++i) emitted[i] = em[i];
+        if (n_emitted) *n_emitted = (int)em.size();
+        if (trace) fill_trace(t, trace);
+    });
 }
 
 }  // extern "C"

@@ -1560,6 +1560,7 @@ public:
                      std::to_string(room) + ")");
         committed_ = tokens;
         generated_ = 0;
+        it_.phase = 0;
         draft_cached_ = 0;
         rng_ = Xoshiro(run_.seed);  // Generation's RNG (proj/src/orchestrator.cpp:150)
         bcache_.reset();
@@ -1703,55 +1704,100 @@ public:
         return tr;
     }
 
-    // run_iteration_speculative (proj/src/orchestrator.cpp:407-436)
-    IterationTrace step_speculative(std::vector<int>& emitted) {
+    // ---- one speculative iteration, split into the reference's stages
+    // (Generation::run_iteration_speculative, proj/src/orchestrator.cpp:407-436):
+    // stage_calibrate = drafter_leading_pass (256-300), stage_draft =
+    // draft_stage / draft_tree (302-331), stage_verify = verify_stage +
+    // verify_tree (333-388), stage_resolve = resolve_draft_cache (390-405),
+    // stage_commit = the commit/emit tail of run_iteration_speculative
+    // (414-428). step() runs all five back to back; the C ABI exposes each.
+    struct Node { int parent, depth, prob_index, first_child = -1, n_children = 0, cache_row = -1; };
+    struct Iter {
+        int phase = 0;  // 0 idle, 1 calibrated, 2 drafted, 3 verified, 4 resolved
+        uint64_t id = 0;
         IterationTrace tr;
-        tr.n = run_.n;
+        bool easy = false, calibrated = false, fuzzy_lead = false, sampled = false, need_logits = false;
+        int n_comm = 0, lead_T = 0, n_dists = 0;
+        std::vector<Node> nodes;
+        std::vector<int> chain_rows, node_rows;
+        int m = 0, bonus = 0;
+        std::vector<int> path, acc_tokens;
+    } it_;
+    uint64_t iter_seq_ = 0;
+
+    void expect_phase(int want, const char* stage) {
+        if (committed_.empty()) throw Error(ST_CONFIG, "call begin() / prefill() first");
+        if (run_.algorithm == ALG_VANILLA) throw Error(ST_CONFIG, std::string(stage) + ": vanilla runs no speculative stages");
+        if (it_.phase == 5) throw Error(ST_STRUCTURE, std::string(stage) + ": the iteration failed; call begin() / prefill()");
+        if (it_.phase != want) {
+            static const char* names[] = {"commit_outcome", "calibrate", "draft", "verify", "resolve_draft_cache"};
+            throw Error(ST_STRUCTURE, std::string(stage) + " called out of order (after " + names[it_.phase] + ")");
+        }
+    }
+
+    // drafter_leading_pass (orchestrator.cpp:256-300): the uncached committed
+    // suffix (prompt on iteration 0, else accepted + bonus) through one
+    // precise pass (fuzzy in the no-calibration arm), committed; root logits
+    // = head of its last row. Greedy chains take the level-1 token straight
+    // from the head's argmax epilogue (select_children with k = 1).
+    void stage_calibrate(float* root_logits_host) {
+        expect_phase(0, "calibrate");
+        Iter& I = it_;
+        I = Iter();
+        I.id = ++iter_seq_;
+        I.tr.n = run_.n;
         staging_.reset();
-        const bool easy = run_.algorithm == ALG_EASYSPEC;
-        const bool calibrated = easy && run_.calibration;
-        const bool fuzzy_lead = easy && !run_.calibration;
-        const bool sampled = run_.temperature > 0.f;
+        I.easy = run_.algorithm == ALG_EASYSPEC;
+        I.calibrated = I.easy && run_.calibration;
+        I.fuzzy_lead = I.easy && !run_.calibration;
+        I.sampled = run_.temperature > 0.f;
         bool wide = false;
         for (int w : widths_) wide |= w > 1;
-        const bool need_logits = sampled || wide;  // else: argmax straight from the head epilogue
-        const int n_comm = (int)committed_.size();
-        const int V = draft_.c.vocab_size;
-        if (sampled) {
+        I.need_logits = I.sampled || wide;  // else: argmax straight from the head epilogue
+        I.n_comm = (int)committed_.size();
+        if (I.sampled) {
             long long nodes = 0, level = 1;
             for (int w : widths_) nodes += (level *= w);
             upload_uniforms((int)std::min<long long>(kMaxDraws, 2 * nodes + 2));
         }
         reset_flags();
-
-        // ---- drafter leading pass = bonus calibration (orchestrator.cpp:256-300)
         CUDA_OK(cudaEventRecord(ev_[0], stream_));
-        std::vector<int> lead_rows = chain_pass(draft_, dcache_, dws_, draft_cached_, n_comm,
-                                                fuzzy_lead ? &plan_ : nullptr, fuzzy_lead, true, 0);
-        draft_cached_ = n_comm;
-        if (fuzzy_lead) ++tr.fuzzy_forwards;
-        else ++tr.sequential_forwards;
-        const int lead_T = (int)lead_rows.size();
+        std::vector<int> lead_rows = chain_pass(draft_, dcache_, dws_, draft_cached_, I.n_comm,
+                                                I.fuzzy_lead ? &plan_ : nullptr, I.fuzzy_lead, true, 0);
+        draft_cached_ = I.n_comm;
+        if (I.fuzzy_lead) ++I.tr.fuzzy_forwards;
+        else ++I.tr.sequential_forwards;
+        I.lead_T = (int)lead_rows.size();
+        const bool store = I.need_logits || root_logits_host;
+        head(draft_, dws_, I.lead_T - 1, 1, I.need_logits ? arena_ + am_off_ : arena_ + tree_off_,
+             store ? dlogits_ : nullptr);
         CUDA_OK(cudaEventRecord(ev_[1], stream_));
+        if (root_logits_host) {
+            const int V = draft_.c.vocab_size;
+            CUDA_OK(cudaMemcpyAsync(root_logits_host, dlogits_, sizeof(float) * V, cudaMemcpyDeviceToHost, stream_));
+            d2h_bytes_ += (long long)sizeof(float) * V;
+            CUDA_OK(cudaStreamSynchronize(stream_));
+        }
+        I.phase = 1;
+    }
 
-        // ---- draft_tree (proj/src/draft_engine.cpp:188-289)
-        // Host tree shape: nodes level by level, siblings contiguous; the
-        // tokens live on device (tree arena). Dist index 0 = the root row,
-        // then one per forwarded frontier row in order (prob_index).
-        struct Node { int parent, depth, prob_index, first_child = -1, n_children = 0, cache_row = -1; };
-        std::vector<Node> nodes;
+    // draft_tree (proj/src/draft_engine.cpp:188-289): level-1 children from
+    // the root row, then n-1 token-parallel passes (fuzzy under the plan for
+    // EasySpec), the last level selected but never forwarded. Host tree
+    // shape: nodes level by level, siblings contiguous; tokens live on device.
+    // Dist index 0 = the root row, then one per forwarded frontier row.
+    void stage_draft() {
+        expect_phase(1, "draft");
+        Iter& I = it_;
+        const int V = draft_.c.vocab_size;
+        std::vector<Node>& nodes = I.nodes;
         std::vector<int> frontier;
         for (int i = 0; i < widths_[0]; ++i) {
             nodes.push_back({-1, 1, 0});
             frontier.push_back(i);
         }
-        int n_dists = 1;
-        if (!need_logits) {
-            head(draft_, dws_, lead_T - 1, 1, arena_ + tree_off_, nullptr);
-        } else {
-            head(draft_, dws_, lead_T - 1, 1, arena_ + am_off_, dlogits_);
-            select_level(0, 1, {widths_[0]}, {0}, V);
-        }
+        I.n_dists = 1;
+        if (I.need_logits) select_level(0, 1, {widths_[0]}, {0}, V);
         for (int level = 1; level <= run_.n - 1 && !frontier.empty(); ++level) {
             std::vector<int> parents, tok;
             for (int idx : frontier) {
@@ -1759,14 +1805,14 @@ public:
                 parents.push_back(nd.parent < 0 ? kTail : nodes[nd.parent].cache_row);
                 tok.push_back(tree_off_ + idx);
             }
-            std::vector<int> rows = dcache_.stage_append(parents, easy);
+            std::vector<int> rows = dcache_.stage_append(parents, I.easy);
             for (size_t i = 0; i < frontier.size(); ++i) nodes[frontier[i]].cache_row = rows[i];
             Pass ps = make_pass(dcache_, rows, tok);
-            forward(draft_, dcache_, dws_, easy ? &plan_ : nullptr, ps);
-            if (easy) ++tr.fuzzy_forwards;
-            else ++tr.sequential_forwards;
+            forward(draft_, dcache_, dws_, I.easy ? &plan_ : nullptr, ps);
+            if (I.easy) ++I.tr.fuzzy_forwards;
+            else ++I.tr.sequential_forwards;
             std::vector<int> next, first_child, widths;
-            const int dist0 = n_dists;
+            const int dist0 = I.n_dists;
             for (size_t i = 0; i < frontier.size(); ++i) {
                 const int idx = frontier[i];
                 nodes[idx].first_child = (int)nodes.size();
@@ -1779,21 +1825,85 @@ public:
                 }
             }
             const int nf = (int)frontier.size();
-            if (!need_logits) {
+            if (!I.need_logits) {
                 // width 1: children of consecutive frontier rows are consecutive nodes
                 head(draft_, dws_, 0, nf, arena_ + tree_off_ + first_child[0], nullptr);
             } else {
                 head(draft_, dws_, 0, nf, arena_ + am_off_, dlogits_ + (size_t)dist0 * logits_ld_);
                 select_level(dist0, nf, widths, first_child, V);
             }
-            n_dists += nf;
+            I.n_dists += nf;
             frontier = next;
         }
-        tr.drafted_nodes = (int)nodes.size();
+        I.tr.drafted_nodes = (int)nodes.size();
         CUDA_OK(cudaEventRecord(ev_[2], stream_));
+        I.phase = 2;
+    }
 
-        // ---- verify_stage (orchestrator.cpp:333-388)
-        const int nn = (int)nodes.size();
+    // The drafted tree as the reference's DraftTree (draft_engine.hpp:63-84).
+    // One D2H copy of the node tokens (and, on request, the draft
+    // distributions: softmax_temp rows, one-hot at T = 0).
+    void read_tree(TreeOut& out, bool want_dists) {
+        if (it_.phase < 2) throw Error(ST_STRUCTURE, "no drafted tree (call draft first)");
+        const Iter& I = it_;
+        const int nn = (int)I.nodes.size(), V = draft_.c.vocab_size;
+        out = TreeOut();
+        out.id = I.id;
+        out.widths = widths_;
+        out.token.resize(nn);
+        CUDA_OK(cudaMemcpyAsync(out.token.data(), arena_ + tree_off_, sizeof(int) * nn, cudaMemcpyDeviceToHost,
+                                stream_));
+        d2h_bytes_ += (long long)sizeof(int) * nn;
+        out.n_dists = I.n_dists;
+        if (want_dists && I.sampled) {
+            out.dists.resize((size_t)I.n_dists * V);
+            CUDA_OK(cudaMemcpyAsync(out.dists.data(), ddists_, sizeof(float) * out.dists.size(), cudaMemcpyDeviceToHost,
+                                    stream_));
+            d2h_bytes_ += (long long)sizeof(float) * out.dists.size();
+        }
+        CUDA_OK(cudaStreamSynchronize(stream_));
+        for (int j = 0; j < nn; ++j) {
+            const Node& n = I.nodes[j];
+            out.parent.push_back(n.parent);
+            out.depth.push_back(n.depth);
+            out.prob_index.push_back(n.prob_index);
+            out.cache_row.push_back(n.cache_row);
+            out.first_child.push_back(n.first_child);
+            out.n_children.push_back(n.n_children);
+            if (n.parent < 0) ++out.root_children;
+        }
+        if (want_dists && !I.sampled) {
+            // T = 0: softmax_temp is a one-hot at the first maximum, i.e. at
+            // the row's top-1 child (select_children's first pick)
+            out.dists.assign((size_t)I.n_dists * V, 0.f);
+            std::vector<int> first(I.n_dists, -1);
+            for (int j = 0; j < nn; ++j)
+                if (first[I.nodes[j].prob_index] < 0) first[I.nodes[j].prob_index] = j;
+            for (int d = 0; d < I.n_dists; ++d)
+                if (first[d] >= 0) out.dists[(size_t)d * V + out.token[first[d]]] = 1.f;
+        }
+    }
+
+    // verify_stage (orchestrator.cpp:333-388) + verify_tree (verifier.cpp:86-177).
+    // `caller` (optional) is a tree the caller may have edited: its shape must
+    // be the drafted one; its tokens replace the drafted tokens.
+    void stage_verify(const TreeOut* caller) {
+        expect_phase(2, "verify");
+        Iter& I = it_;
+        const int nn = (int)I.nodes.size(), V = base_.c.vocab_size;
+        if (caller) {
+            if (caller->id != I.id) throw Error(ST_STRUCTURE, "tree does not belong to this iteration's draft");
+            if ((int)caller->token.size() != nn || (int)caller->parent.size() != nn)
+                throw Error(ST_SHAPE, "tree node count differs from the drafted tree");
+            for (int j = 0; j < nn; ++j) {
+                if (caller->parent[j] != I.nodes[j].parent)
+                    throw Error(ST_STRUCTURE, "tree shape differs from the drafted tree");
+                if (caller->token[j] < 0 || caller->token[j] >= V) cfg_fail("tree token outside vocabulary");
+            }
+            CUDA_OK(cudaMemcpyAsync(arena_ + tree_off_, staging_.push(caller->token.data(), nn, stream_),
+                                    sizeof(int) * nn, cudaMemcpyDeviceToDevice, stream_));
+        }
+        const int n_comm = I.n_comm;
         // committed tokens the base has no rows for: all but the frontier token
         // are prefilled chunk-wise first (equivalent to one pass: causal rows).
         if (n_comm - 1 > bcache_.committed)
@@ -1801,32 +1911,31 @@ public:
         std::vector<int> parents, tok;
         parents.push_back(kTail);
         tok.push_back(n_comm - 1);
-        std::vector<int> chain_rows = bcache_.stage_append(parents, false);
-        const int first_node_row = chain_rows.back() + 1;
+        I.chain_rows = bcache_.stage_append(parents, false);
+        const int first_node_row = I.chain_rows.back() + 1;
         parents.clear();
-        for (int j = 0; j < nn; ++j) {
-            parents.push_back(nodes[j].parent < 0 ? chain_rows.back() : first_node_row + nodes[j].parent);
-        }
-        std::vector<int> node_rows = bcache_.stage_append(parents, false);
-        std::vector<int> all_rows = chain_rows;
-        all_rows.insert(all_rows.end(), node_rows.begin(), node_rows.end());
+        for (int j = 0; j < nn; ++j)
+            parents.push_back(I.nodes[j].parent < 0 ? I.chain_rows.back() : first_node_row + I.nodes[j].parent);
+        I.node_rows = bcache_.stage_append(parents, false);
+        std::vector<int> all_rows = I.chain_rows;
+        all_rows.insert(all_rows.end(), I.node_rows.begin(), I.node_rows.end());
         for (int j = 0; j < nn; ++j) tok.push_back(tree_off_ + j);
         Pass ps = make_pass(bcache_, all_rows, tok);
         forward(base_, bcache_, bws_, nullptr, ps);
-        ++tr.base_forwards;
-        head(base_, bws_, 0, 1 + nn, arena_ + am_off_, sampled ? blogits_ : nullptr);
+        ++I.tr.base_forwards;
+        head(base_, bws_, 0, 1 + nn, arena_ + am_off_, I.sampled ? blogits_ : nullptr);
         // acceptance on device
         std::vector<int> np(nn), nfc(nn), nnc(nn), nti(nn), npi(nn);
         int root_children = 0;
         for (int j = 0; j < nn; ++j) {
-            np[j] = nodes[j].parent;
-            nfc[j] = nodes[j].first_child;
-            nnc[j] = nodes[j].n_children;
+            np[j] = I.nodes[j].parent;
+            nfc[j] = I.nodes[j].first_child;
+            nnc[j] = I.nodes[j].n_children;
             nti[j] = tree_off_ + j;
-            npi[j] = nodes[j].prob_index;
-            if (nodes[j].parent < 0) ++root_children;
+            npi[j] = I.nodes[j].prob_index;
+            if (I.nodes[j].parent < 0) ++root_children;
         }
-        if (!sampled) {
+        if (!I.sampled) {
             AcceptArgs aa;
             aa.n_nodes = nn;
             aa.n_levels = run_.n;
@@ -1840,6 +1949,8 @@ public:
             aa.outcome = arena_ + out_off_;
             aa.tok_arena_w = arena_;
             aa.commit_at = n_comm;
+            aa.strict_siblings = run_.strict_greedy_tree;
+            aa.err = arena_ + err_off_;
             launch_accept_greedy(aa, stream_);
         } else {
             softmax(blogits_, bdists_, 0, 1 + nn, V);
@@ -1865,47 +1976,120 @@ public:
             launch_verify_sample(va, stream_);
         }
         ++launches_;
-        sync_outcome(run_.n);
-
-        const int m = outcome_host_[0], bonus = outcome_host_[1];
-        std::vector<int> path(outcome_host_ + 2, outcome_host_ + 2 + m);
+        try {
+            sync_outcome(run_.n);
+        } catch (...) {
+            // the iteration is void (its rows stay staged): only begin() recovers
+            I.phase = 5;
+            throw;
+        }
+        I.m = outcome_host_[0];
+        I.bonus = outcome_host_[1];
+        I.path.assign(outcome_host_ + 2, outcome_host_ + 2 + I.m);
+        I.acc_tokens.assign(outcome_host_ + 2 + run_.n, outcome_host_ + 2 + run_.n + I.m);
         // base keeps the chain + accepted path (orchestrator.cpp:379-383)
-        std::vector<int> commit_rows = chain_rows;
-        for (int ni : path) commit_rows.push_back(node_rows[ni]);
+        std::vector<int> commit_rows = I.chain_rows;
+        for (int ni : I.path) commit_rows.push_back(I.node_rows[ni]);
         std::vector<int> src, dst;
         bcache_.commit_path(commit_rows, src, dst);
         move_rows(bcache_, src, dst);
-        // resolve_draft_cache (orchestrator.cpp:390-405)
-        if (calibrated) {
+        I.phase = 3;
+    }
+
+    // resolve_draft_cache (orchestrator.cpp:390-405)
+    void stage_resolve() {
+        expect_phase(3, "resolve_draft_cache");
+        Iter& I = it_;
+        if (I.calibrated) {
             dcache_.discard();
         } else {
-            std::vector<int> drows;
-            for (int ni : path) {
-                if (nodes[ni].cache_row < 0) break;
-                drows.push_back(nodes[ni].cache_row);
+            std::vector<int> drows, src, dst;
+            for (int ni : I.path) {
+                if (I.nodes[ni].cache_row < 0) break;  // the last level is never staged
+                drows.push_back(I.nodes[ni].cache_row);
             }
             dcache_.commit_path(drows, src, dst);
             move_rows(dcache_, src, dst);
             draft_cached_ += (int)drows.size();
         }
-        for (int i = 0; i < m; ++i) committed_.push_back(outcome_host_[2 + run_.n + i]);
-        committed_.push_back(bonus);
+        I.phase = 4;
+    }
+
+    // run_iteration_speculative's tail (orchestrator.cpp:414-428): commit
+    // accepted + bonus, emit min(m + 1, remaining).
+    IterationTrace stage_commit(std::vector<int>& emitted) {
+        expect_phase(4, "commit_outcome");
+        Iter& I = it_;
+        for (int t : I.acc_tokens) committed_.push_back(t);
+        committed_.push_back(I.bonus);
         const int remaining = run_.max_new_tokens - generated_;
-        const int emit = std::min(m + 1, remaining);
-        for (int i = 0; i < emit; ++i) emitted.push_back(committed_[committed_.size() - (m + 1) + i]);
+        const int emit = std::min(I.m + 1, remaining);
+        for (int i = 0; i < emit; ++i) emitted.push_back(committed_[committed_.size() - (I.m + 1) + i]);
         generated_ += emit;
-        tr.m = m;
+        IterationTrace tr = I.tr;
+        tr.m = I.m;
         tr.emitted = emit;
-        tr.bonus = bonus;
+        tr.bonus = I.bonus;
         float ms = 0;
         CUDA_OK(cudaEventElapsedTime(&ms, ev_[0], ev_[1]));
-        if (calibrated) tr.calibrate_ms = ms;
+        if (I.calibrated) tr.calibrate_ms = ms;
         else tr.draft_ms = ms;
         CUDA_OK(cudaEventElapsedTime(&ms, ev_[1], ev_[2]));
         tr.draft_ms += ms;
         CUDA_OK(cudaEventElapsedTime(&tr.verify_ms, ev_[2], ev_[3]));
+        tr.committed = (int)committed_.size();
+        tr.draft_committed = dcache_.committed;
+        tr.base_committed = bcache_.committed;
+        I.phase = 0;
         return tr;
     }
+
+    IterationTrace step_speculative(std::vector<int>& emitted) {
+        stage_calibrate(nullptr);
+        stage_draft();
+        stage_verify(nullptr);
+        stage_resolve();
+        return stage_commit(emitted);
+    }
+
+    // ---- Engine stage interface (C ABI espec_prefill ... espec_commit_outcome)
+    void prefill(const std::vector<int>& tokens) override {
+        begin(tokens);
+        const int n = (int)tokens.size();
+        // base: every prompt row but the frontier token (verify_stage re-inputs
+        // it with the tree); drafter: the whole chunks before the final one, so
+        // the leading pass runs exactly the chunk step() would run.
+        if (n - 1 > 0) chain_pass(base_, bcache_, bws_, 0, n - 1, nullptr, false, true, 0);
+        const int dpre = ((n - 1) / kChunk) * kChunk;
+        if (dpre > 0 && run_.algorithm != ALG_VANILLA) {
+            chain_pass(draft_, dcache_, dws_, 0, dpre, nullptr, false, true, 0);
+            draft_cached_ = dpre;
+        }
+        CUDA_OK(cudaStreamSynchronize(stream_));
+    }
+    void calibrate(float* root_logits) override { stage_calibrate(root_logits); }
+    void draft(TreeOut* out, bool want_dists) override {
+        stage_draft();
+        if (out) read_tree(*out, want_dists);
+    }
+    void tree(TreeOut& out, bool want_dists) override { read_tree(out, want_dists); }
+    void verify(const TreeOut* caller, OutcomeOut* out) override {
+        stage_verify(caller);
+        if (out) {
+            out->m = it_.m;
+            out->n = run_.n;
+            out->bonus = it_.bonus;
+            out->path = it_.path;
+            out->tokens = it_.acc_tokens;
+            out->id = it_.id;
+        }
+    }
+    void resolve_draft_cache(const OutcomeOut* o) override {
+        if (o && (o->id != it_.id || o->m != it_.m || o->path != it_.path))
+            throw Error(ST_STRUCTURE, "outcome does not belong to this iteration's verification");
+        stage_resolve();
+    }
+    IterationTrace commit_outcome(std::vector<int>& emitted) override { return stage_commit(emitted); }
 
     // select_children (proj/src/draft_engine.cpp:141-186) for `rows`
     // frontier rows whose logits sit at dist indices [dist0, dist0+rows):

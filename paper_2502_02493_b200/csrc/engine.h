@@ -54,6 +54,7 @@ struct RunCfg {
     int max_new_tokens = 64;
     uint64_t seed = 1;
     int calibration = 1;
+    int strict_greedy_tree = 0;  // 1: the reference's greedy multi-sibling CheckError (verifier.cpp:146-158)
     std::vector<int> effective_widths() const;
 };
 
@@ -76,6 +77,20 @@ struct IterationTrace {
     int bonus = 0;
 };
 
+// DraftTree (proj/include/espec/draft_engine.hpp:63-84) as plain arrays.
+struct TreeOut {
+    uint64_t id = 0;  // iteration the tree was drafted in
+    std::vector<int> widths, token, parent, depth, prob_index, cache_row, first_child, n_children;
+    int root_children = 0, n_dists = 0;
+    std::vector<float> dists;  // [n_dists][V] when requested
+};
+// VerificationOutcome (proj/include/espec/verifier.hpp:14-21).
+struct OutcomeOut {
+    uint64_t id = 0;
+    int m = 0, n = 0, bonus = 0;
+    std::vector<int> path, tokens;
+};
+
 class Engine;
 // tp > 1: this engine is shard `rank` of a tensor-parallel group (one per
 // GPU); link the group with comm_link (one process) or comm_ipc_* (one
@@ -96,6 +111,15 @@ public:
     virtual bool done() const = 0;
     virtual IterationTrace step(std::vector<int>& emitted) = 0;
     virtual std::vector<int> generate(const std::vector<int>& tokens, std::vector<IterationTrace>* traces) = 0;
+    // Stage-level iteration (run_iteration_speculative split at the
+    // reference's stage boundaries, proj/src/orchestrator.cpp:256-428).
+    virtual void prefill(const std::vector<int>& tokens) = 0;
+    virtual void calibrate(float* root_logits) = 0;
+    virtual void draft(TreeOut* out, bool want_dists) = 0;
+    virtual void tree(TreeOut& out, bool want_dists) = 0;
+    virtual void verify(const TreeOut* caller, OutcomeOut* out) = 0;
+    virtual void resolve_draft_cache(const OutcomeOut* outcome) = 0;
+    virtual IterationTrace commit_outcome(std::vector<int>& emitted) = 0;
     // Parity probes.
     virtual void forward_chain(int which, const std::vector<int>& tokens, const std::string& plan, float* logits,
                                float* hidden) = 0;

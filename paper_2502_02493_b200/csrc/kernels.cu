@@ -825,6 +825,10 @@ __global__ void accept_greedy_kernel(AcceptArgs a) {
                 acc = ni;
                 break;
             }
+            if (a.strict_siblings && i + 1 < count) {
+                if (a.err) *a.err = 4;  // "sibling candidates exhaust the draft distribution"
+                break;
+            }
         }
         if (acc < 0) break;
         a.outcome[2 + m] = acc;

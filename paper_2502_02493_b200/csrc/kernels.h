@@ -225,6 +225,13 @@ struct AcceptArgs {
     int* outcome = nullptr;              // [2 + 2*n_levels]: m, bonus, path[n_levels], tokens[n_levels]
     int* tok_arena_w = nullptr;          // accepted tokens + bonus are appended at commit_at
     int commit_at = 0;
+    // 1: the reference's rule (proj/src/verifier.cpp:146-158) — at T = 0 the
+    // draft distribution is one-hot at the first sibling, so rejecting it
+    // with more siblings left raises CheckError (err = 4); 0: accept the
+    // sibling equal to the base argmax (identical whenever the reference
+    // does not throw)
+    int strict_siblings = 0;
+    int* err = nullptr;
 };
 void launch_accept_greedy(const AcceptArgs& a, cudaStream_t s);
 

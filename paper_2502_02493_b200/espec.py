@@ -48,7 +48,25 @@ class _ModelCfg(C.Structure):
 class _RunCfg(C.Structure):
     _fields_ = [("algorithm", C.c_int), ("n", C.c_int), ("widths", C.POINTER(C.c_int)), ("lp_size", C.c_int),
                 ("plan_override", C.c_char_p), ("temperature", C.c_float), ("max_new_tokens", C.c_int),
-                ("seed", C.c_uint64), ("calibration", C.c_int)]
+                ("seed", C.c_uint64), ("calibration", C.c_int), ("strict_greedy_tree", C.c_int)]
+
+
+MAX_NODES = 64  # ESPEC_MAX_NODES
+
+
+class _Tree(C.Structure):
+    """espec_tree = espec::DraftTree (draft_engine.hpp:63-84)."""
+    _fields_ = [("id", C.c_uint64), ("n_nodes", C.c_int), ("root_children", C.c_int), ("n_levels", C.c_int),
+                ("n_dists", C.c_int), ("widths", C.c_int32 * MAX_NODES)] + \
+               [(n, C.c_int32 * MAX_NODES) for n in ("token", "parent", "depth", "prob_index", "cache_row",
+                                                     "first_child", "n_children")] + \
+               [("dists", C.POINTER(C.c_float)), ("dist_capacity", C.c_int)]
+
+
+class _Outcome(C.Structure):
+    """espec_outcome = espec::VerificationOutcome (verifier.hpp:14-21)."""
+    _fields_ = [("id", C.c_uint64), ("m", C.c_int), ("n", C.c_int), ("bonus", C.c_int32),
+                ("accepted_path", C.c_int32 * MAX_NODES), ("accepted_tokens", C.c_int32 * MAX_NODES)]
 
 
 class _DevMap(C.Structure):
@@ -106,6 +124,12 @@ def lib():
         L.espec_comm_link.argtypes = [P(V), C.c_int]
         L.espec_comm_export.argtypes = [V, C.c_void_p]
         L.espec_comm_import.argtypes = [V, C.c_void_p, C.c_int]
+        L.espec_prefill.argtypes = [V, P(C.c_int32), C.c_int]
+        L.espec_calibrate.argtypes = [V, P(C.c_float)]
+        L.espec_draft.argtypes = [V, P(_Tree)]
+        L.espec_verify.argtypes = [V, P(_Tree), P(_Outcome)]
+        L.espec_resolve_draft_cache.argtypes = [V, P(_Outcome)]
+        L.espec_commit_outcome.argtypes = [V, P(C.c_int32), P(C.c_int), P(_Iter)]
         _lib = L
     return _lib
 
@@ -161,6 +185,8 @@ class RunConfig:
     max_new_tokens: int = 64
     seed: int = 1
     calibration: bool = True
+    # reproduce the reference's greedy multi-sibling CheckError (verifier.cpp:146-158)
+    strict_greedy_tree: bool = False
 
     def effective_widths(self) -> List[int]:
         return list(self.widths) if self.widths else [1] * self.n
@@ -217,7 +243,8 @@ class Engine:
         po = (run.plan_override or "").encode()
         self._keep = [w, po]
         return _RunCfg(ALGORITHMS[run.algorithm], run.n, _i(w), run.lp_size, po, run.temperature,
-                       run.max_new_tokens, run.seed, 1 if run.calibration else 0)
+                       run.max_new_tokens, run.seed, 1 if run.calibration else 0,
+                       1 if run.strict_greedy_tree else 0)
 
     def _check(self, st: int):
         if st:
@@ -330,6 +357,66 @@ class Engine:
         self._check(lib().espec_step(self._h, _i(em), C.byref(n), C.byref(tr)))
         return list(em[: n.value]), _trace(tr)
 
+    # ---- stage-level iteration (Generation's stages, orchestrator.cpp:256-428)
+    def prefill(self, tokens: Sequence[int]):
+        t = np.ascontiguousarray(tokens, np.int32)
+        self._check(lib().espec_prefill(self._h, _i(t), len(t)))
+
+    def calibrate(self, want_logits: bool = False):
+        """drafter_leading_pass; returns the root logits (vocab floats) on request."""
+        out = np.zeros(self.base_cfg.vocab_size, np.float32) if want_logits else None
+        self._check(lib().espec_calibrate(self._h, _f(out)))
+        return out
+
+    def draft(self, want_dists: bool = False) -> "DraftTree":
+        """draft_stage / draft_tree -> the drafted tree."""
+        t = _Tree()
+        buf = None
+        if want_dists:
+            buf = np.zeros((MAX_NODES + 1, self.base_cfg.vocab_size), np.float32)
+            t.dists = _f(buf)
+            t.dist_capacity = MAX_NODES + 1
+        self._check(lib().espec_draft(self._h, C.byref(t)))
+        return DraftTree._from(t, buf)
+
+    def verify(self, tree: Optional["DraftTree"] = None) -> "Outcome":
+        """verify_stage + verify_tree; `tree` (this iteration's, tokens possibly
+        edited) or None for the tree as drafted."""
+        o = _Outcome()
+        ct = tree._c() if tree is not None else None
+        self._check(lib().espec_verify(self._h, C.byref(ct) if ct is not None else None, C.byref(o)))
+        return Outcome(o.id, o.m, o.n, o.bonus, list(o.accepted_path[: o.m]), list(o.accepted_tokens[: o.m]))
+
+    def resolve_draft_cache(self, outcome: Optional["Outcome"] = None):
+        o = None
+        if outcome is not None:
+            o = _Outcome(outcome.id, outcome.m, outcome.n, outcome.bonus)
+            for i, p in enumerate(outcome.path):
+                o.accepted_path[i] = p
+        self._check(lib().espec_resolve_draft_cache(self._h, C.byref(o) if o is not None else None))
+
+    def commit_outcome(self):
+        em = np.zeros(MAX_NODES + 2, np.int32)
+        n = C.c_int(0)
+        tr = _Iter()
+        self._check(lib().espec_commit_outcome(self._h, _i(em), C.byref(n), C.byref(tr)))
+        return list(em[: n.value]), _trace(tr)
+
+    def iterate_stages(self, edit=None):
+        """One speculative iteration through the five stage calls (what
+        espec_step fuses); `edit(tree)` may rewrite the tree's tokens before
+        verification. Returns (emitted, trace, tree, outcome)."""
+        self.calibrate()
+        tree = self.draft()
+        if edit is not None:
+            edit(tree)
+            out = self.verify(tree)
+        else:
+            out = self.verify()
+        self.resolve_draft_cache(out)
+        em, tr = self.commit_outcome()
+        return em, tr, tree, out
+
     def done(self) -> bool:
         return bool(lib().espec_done(self._h))
 
@@ -371,6 +458,56 @@ class Engine:
 
     def sync(self):
         self._check(lib().espec_sync(self._h))
+
+
+@dataclass
+class DraftTree:
+    """espec::DraftTree (draft_engine.hpp:63-84) as lists."""
+    id: int
+    root_children: int
+    widths: List[int]
+    token: List[int]
+    parent: List[int]
+    depth: List[int]
+    prob_index: List[int]
+    cache_row: List[int]
+    first_child: List[int]
+    n_children: List[int]
+    n_dists: int
+    dists: Optional[np.ndarray] = None
+
+    @staticmethod
+    def _from(t: _Tree, buf) -> "DraftTree":
+        n = t.n_nodes
+        g = lambda k: list(getattr(t, k)[:n])  # noqa: E731
+        return DraftTree(t.id, t.root_children, list(t.widths[: t.n_levels]), g("token"), g("parent"), g("depth"),
+                         g("prob_index"), g("cache_row"), g("first_child"), g("n_children"), t.n_dists,
+                         None if buf is None else buf[: t.n_dists].copy())
+
+    def _c(self) -> _Tree:
+        t = _Tree()
+        t.id = self.id
+        t.n_nodes = len(self.token)
+        t.root_children = self.root_children
+        t.n_levels = len(self.widths)
+        for i, w in enumerate(self.widths):
+            t.widths[i] = w
+        for k in ("token", "parent", "depth", "prob_index", "cache_row", "first_child", "n_children"):
+            arr = getattr(t, k)
+            for i, v in enumerate(getattr(self, k)):
+                arr[i] = v
+        return t
+
+
+@dataclass
+class Outcome:
+    """espec::VerificationOutcome (verifier.hpp:14-21)."""
+    id: int
+    m: int
+    n: int
+    bonus: int
+    path: List[int]
+    tokens: List[int]
 
 
 def exchange_ipc_handles(local: bytes, group=None) -> List[bytes]:

@@ -2,8 +2,10 @@ import os
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-if ROOT not in sys.path:
-    sys.path.insert(0, ROOT)
+TESTS = os.path.dirname(os.path.abspath(__file__))
+for p in (ROOT, TESTS):  # tests share fixtures helpers (e.g. test_gpu_parity._engine_for_case)
+    if p not in sys.path:
+        sys.path.insert(0, p)
 
 
 def pytest_configure(config):

@@ -131,7 +131,9 @@ def test_all_singleton_fuzzy_equals_sequential_bitwise():
         assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
 
 
-GREEDY_CHAINS = [c for c in GEN if c["run"]["temperature"] == 0.0 and max(c["run"]["widths"]) == 1]
+# fixtures where the reference raised are covered in test_gpu_stages.py
+GREEDY_CHAINS = [c for c in GEN if c["error"] is None and c["run"]["temperature"] == 0.0
+                 and max(c["run"]["widths"]) == 1]
 
 
 @pytest.mark.parametrize("case", GREEDY_CHAINS, ids=[c["name"] for c in GREEDY_CHAINS])
@@ -158,7 +160,7 @@ def test_generate_matches_reference_tokens(case):
             np.testing.assert_allclose(got, last[key][layer], rtol=1e-4, atol=1e-2 * max(1, n))
 
 
-SAMPLED_OR_TREES = [c for c in GEN if c not in GREEDY_CHAINS]
+SAMPLED_OR_TREES = [c for c in GEN if c not in GREEDY_CHAINS and c["error"] is None]
 
 
 @pytest.mark.parametrize("case", SAMPLED_OR_TREES, ids=[c["name"] for c in SAMPLED_OR_TREES])

@@ -240,6 +240,16 @@ espec_status espec_committed(espec_engine* eng, int32_t* tokens, int cap, int* n
 espec_status espec_forward(espec_engine* eng, int which, const int32_t* tokens, int n, const char* plan,
                            float* logits, float* hidden);
 
+/* Parity probe at decode shapes: prefill `prompt` on a fresh cache of one
+ * model, then ONE decode-sized pass over n <= 64 rows forming a tree
+ * (parents[j] = -1: child of the prompt tail, else an earlier row j' < j) —
+ * the verify_stage / draft_tree pass (orchestrator.cpp:333-388,
+ * draft_engine.cpp:235-287) with its tree mask. logits n x V, hidden n x D
+ * (either may be NULL). Ends any generation in progress. */
+espec_status espec_forward_tree(espec_engine* eng, int which, const int32_t* prompt, int n_prompt,
+                                const int32_t* tokens, const int32_t* parents, int n, const char* plan, float* logits,
+                                float* hidden);
+
 /* Layer plans (proj/src/layer_plan.cpp:54-128) -> formatted plan string. */
 espec_status espec_plan_groups(int n_layers, int lp_size, char* out, int out_len);
 espec_status espec_parse_plan(const char* spec, char* out, int out_len);

@@ -235,6 +235,16 @@ espec_status espec_forward(espec_engine* eng, int which, const int32_t* tokens, 
     });
 }
 
+espec_status espec_forward_tree(espec_engine* eng, int which, const int32_t* prompt, int n_prompt,
+                                const int32_t* tokens, const int32_t* parents, int n, const char* plan, float* logits,
+                                float* hidden) {
+    return guard(eng, [&] {
+        if (!prompt || !tokens || !parents) throw Error(ST_CONFIG, "forward_tree: null input");
+        eng->impl->forward_tree(which, std::vector<int>(prompt, prompt + n_prompt), std::vector<int>(tokens, tokens + n),
+                                std::vector<int>(parents, parents + n), plan ? plan : "", logits, hidden);
+    });
+}
+
 espec_status espec_plan_groups(int n_layers, int lp_size, char* out, int out_len) {
     try {
         return copy_plan(plan_groups(n_layers, lp_size), out, out_len);

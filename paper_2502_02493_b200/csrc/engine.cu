@@ -971,15 +971,18 @@ public:
         if (name == "wo") return mat_read(L.wo, dt, qd, d, 0, out, d);
         if (name == "w_down") return mat_read(L.wd, dt, f, d, 0, out, d);
         if (name == "w_gate" || name == "w_up") {
-            const int half = name == "w_up" ? 16 : 0;
-            std::vector<float> blk((size_t)d * 16);
-            for (int t = 0; t < f / 16; ++t) {
-                mat_read(L.wgu, dt, d, M.gu_ld(), t * 32 + half, blk.data(), 16);
-                for (int r = 0; r < d; ++r)
-                    for (int j = 0; j < 16; ++j) out[(size_t)r * f + t * 16 + j] = blk[(size_t)r * 16 + j];
-            }
+            // one unpack of the interleaved [gate16 | up16] matrix, de-interleaved on the host
+            const int half = name == "w_up" ? 16 : 0, ld = M.gu_ld();
+            std::vector<float> all((size_t)d * ld);
+            mat_read(L.wgu, dt, d, ld, 0, all.data(), ld);
+            for (int r = 0; r < d; ++r)
+                for (int t = 0; t < f / 16; ++t)
+                    for (int j = 0; j < 16; ++j)
+                        out[(size_t)r * f + t * 16 + j] = all[(size_t)r * ld + t * 32 + half + j];
             return;
         }
+        if (name == "attn_norm_gain") { CUDA_OK(cudaMemcpy(out, L.ga, 4 * d, cudaMemcpyDeviceToHost)); return; }
+        if (name == "mlp_norm_gain") { CUDA_OK(cudaMemcpy(out, L.gm, 4 * d, cudaMemcpyDeviceToHost)); return; }
         throw Error(ST_CONFIG, "unknown tensor " + name);
     }
 
@@ -2184,6 +2187,72 @@ public:
         }
         std::vector<int> a, b;
         C.commit_path(rows, a, b);
+        CUDA_OK(cudaStreamSynchronize(stream_));
+        CUDA_OK(cudaGetLastError());
+        committed_.clear();
+    }
+
+    // Parity probe at decode shapes: prefill `prompt` (chunked; tcgen05 for
+    // > 16-row chunks), then ONE decode-sized pass over T staged rows whose
+    // tree is given by `parents` (-1 = child of the committed tail, j = row j
+    // of this pass): the verify_stage / draft_tree pass shape
+    // (orchestrator.cpp:333-388, draft_engine.cpp:235-287) with its tree mask.
+    // Returns the T rows' logits and final hidden states.
+    void forward_tree(int which, const std::vector<int>& prompt, const std::vector<int>& tokens,
+                      const std::vector<int>& parents, const std::string& plan_spec, float* logits,
+                      float* hidden) override {
+        ModelDev& M = which ? base_ : draft_;
+        Cache& C = which ? bcache_ : dcache_;
+        Workspace& W = which ? bws_ : dws_;
+        CUDA_OK(cudaStreamSynchronize(stream_));
+        const int np = (int)prompt.size(), T = (int)tokens.size();
+        if (T < 1 || T > kMaxNodes) cfg_fail("forward_tree: 1..64 tree rows");
+        if ((int)parents.size() != T) cfg_fail("forward_tree: one parent per row");
+        if (np < 1 || np + T > M.c.max_positions) cfg_fail("forward_tree: prompt + rows exceed max_positions");
+        for (int t : prompt)
+            if (t < 0 || t >= M.c.vocab_size) cfg_fail("token outside vocabulary");
+        for (int t : tokens)
+            if (t < 0 || t >= M.c.vocab_size) cfg_fail("token outside vocabulary");
+        LayerPlan plan;
+        const LayerPlan* pp = nullptr;
+        if (!plan_spec.empty()) {
+            plan = plan_spec.rfind("lp=", 0) == 0 ? plan_groups(M.c.n_layers, std::stoi(plan_spec.substr(3)))
+                                                  : parse_plan_override(plan_spec);
+            if (plan.n_layers() != M.c.n_layers) cfg_fail("plan does not cover the model");
+            if (which == 1 && plan.max_group_size() > 1) cfg_fail("fuzzy probes run on the drafter");
+            pp = &plan;
+        }
+        C.reset();
+        staging_.reset();
+        it_.phase = 0;
+        std::vector<int> all = prompt;
+        all.insert(all.end(), tokens.begin(), tokens.end());
+        CUDA_OK(cudaMemcpyAsync(arena_, staging_.push(all.data(), all.size(), stream_), sizeof(int) * all.size(),
+                                cudaMemcpyDeviceToDevice, stream_));
+        chain_pass(M, C, W, 0, np, nullptr, false, true, 0);
+        std::vector<int> prow, tok;
+        std::vector<int> rows;
+        for (int j = 0; j < T; ++j) {
+            if (parents[j] >= j || parents[j] < -1) cfg_fail("forward_tree: parents must precede their rows");
+            tok.push_back(np + j);
+        }
+        // stage level by level in row order (a parent is staged before its child)
+        for (int j = 0; j < T; ++j) prow.push_back(parents[j] < 0 ? kTail : C.committed + parents[j]);
+        rows = C.stage_append(prow, pp != nullptr);
+        Pass ps = make_pass(C, rows, tok);
+        set_prefill_mode(false);
+        forward(M, C, W, pp, ps);
+        const int d = M.c.d_model, V = M.c.vocab_size;
+        if (hidden) CUDA_OK(cudaMemcpyAsync(hidden, W.h, sizeof(float) * T * d, cudaMemcpyDeviceToHost, stream_));
+        for (int r0 = 0; r0 < T; r0 += 8) {
+            const int k = std::min(8, T - r0);
+            head(M, W, r0, k, arena_ + out_off_, W.logits, ldpad(M.c.vocab_size, M.c.weight_dtype));
+            if (logits)
+                CUDA_OK(cudaMemcpy2DAsync(logits + (size_t)r0 * V, sizeof(float) * V, W.logits,
+                                          sizeof(float) * ldpad(M.c.vocab_size, M.c.weight_dtype),
+                                          sizeof(float) * V, k, cudaMemcpyDeviceToHost, stream_));
+        }
+        C.discard();
         CUDA_OK(cudaStreamSynchronize(stream_));
         CUDA_OK(cudaGetLastError());
         committed_.clear();

@@ -123,6 +123,9 @@ public:
     // Parity probes.
     virtual void forward_chain(int which, const std::vector<int>& tokens, const std::string& plan, float* logits,
                                float* hidden) = 0;
+    virtual void forward_tree(int which, const std::vector<int>& prompt, const std::vector<int>& tokens,
+                              const std::vector<int>& parents, const std::string& plan, float* logits,
+                              float* hidden) = 0;
     virtual int cache_rows(int which, int layer, int row0, int n, float* k, float* v) = 0;
     virtual int cache_committed(int which) const = 0;
     virtual const std::vector<int>& committed() const = 0;

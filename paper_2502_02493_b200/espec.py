@@ -125,6 +125,8 @@ def lib():
         L.espec_comm_export.argtypes = [V, C.c_void_p]
         L.espec_comm_import.argtypes = [V, C.c_void_p, C.c_int]
         L.espec_prefill.argtypes = [V, P(C.c_int32), C.c_int]
+        L.espec_forward_tree.argtypes = [V, C.c_int, P(C.c_int32), C.c_int, P(C.c_int32), P(C.c_int32), C.c_int,
+                                         C.c_char_p, P(C.c_float), P(C.c_float)]
         L.espec_calibrate.argtypes = [V, P(C.c_float)]
         L.espec_draft.argtypes = [V, P(_Tree)]
         L.espec_verify.argtypes = [V, P(_Tree), P(_Outcome)]
@@ -435,6 +437,20 @@ class Engine:
         hidden = np.zeros((len(t), cfg.d_model), np.float32)
         self._check(lib().espec_forward(self._h, which, _i(t), len(t), (plan or "").encode(), _f(logits),
                                         _f(hidden)))
+        return logits, hidden
+
+    def forward_tree(self, which: int, prompt: Sequence[int], tokens: Sequence[int], parents: Sequence[int],
+                     plan: Optional[str] = None):
+        """Prefill `prompt`, then one decode-sized pass over a tree of rows
+        (parents: -1 = child of the prompt tail, j = an earlier row)."""
+        cfg = self.base_cfg if which == self.BASE else self.draft_cfg
+        p = np.ascontiguousarray(prompt, np.int32)
+        t = np.ascontiguousarray(tokens, np.int32)
+        par = np.ascontiguousarray(parents, np.int32)
+        logits = np.zeros((len(t), cfg.vocab_size), np.float32)
+        hidden = np.zeros((len(t), cfg.d_model), np.float32)
+        self._check(lib().espec_forward_tree(self._h, which, _i(p), len(p), _i(t), _i(par), len(t),
+                                             (plan or "").encode(), _f(logits), _f(hidden)))
         return logits, hidden
 
     def cache_view(self, which: int, layer: int, row0: int = 0, n: Optional[int] = None):

@@ -172,12 +172,21 @@ def _mha_equiv(cfg):
     return cfg["d_model"], cfg["n_heads"], cfg["d_head"], cfg["d_mlp"]
 
 
-def cpu_iteration_seconds(wl, ctx, reps=1, cache=None):
+def _plan_sizes(n_layers, lp):
+    """Group sizes of plan_groups(n_layers, lp) (proj/src/layer_plan.cpp:54-82,
+    through the engine's C ABI: host logic only, no GPU needed)."""
+    from paper_2502_02493_b200 import espec as E
+    return [int(g.split("-")[-1]) - int(g.split("-")[0]) + 1 for g in E.plan_groups(n_layers, lp).split("|")]
+
+
+def cpu_iteration_seconds(wl, ctx, workers=1, reps=1, cache=None):
     """Extrapolated wall time of one EasySpec iteration of the reference CPU
-    path (workers=1) with m = 0 accepted drafts: calibration pass over 1 row,
-    n-1 draft passes over 1 row, base verification over n+1 rows — each pass
-    = layers x (sampled one-layer body) + the LM head rows it scores."""
-    n = wl["n"]
+    path with m = 0 accepted drafts: calibration = one precise drafter pass
+    over 1 row; n-1 fuzzy draft passes over 1 row, each = the plan's groups
+    through forward_fuzzy with a WorkerPool of `workers` threads (singleton
+    groups = one layer); base verification over n+1 rows; plus the LM head
+    rows each pass scores."""
+    n, lp = wl["n"], wl["lp"]
     b, d = wl["base"], wl["draft"]
     cache = cache if cache is not None else {}
 
@@ -188,6 +197,14 @@ def cpu_iteration_seconds(wl, ctx, reps=1, cache=None):
             cache[key] = (r["mask_ms"] + r["attn_ms"] + r["mlp_ms"] + r["rest_ms"]) / 1000.0
         return cache[key]
 
+    def group(cfg, g, T):
+        if g == 1:
+            return layer(cfg, T)
+        key = ("group", cfg["d_model"], g, T, workers)
+        if key not in cache:
+            cache[key] = _ref_bench("group", *_mha_equiv(cfg), g, T, ctx, workers, reps)["group_ms"] / 1000.0
+        return cache[key]
+
     def head(cfg, T):
         key = ("head", cfg["d_model"], T)
         if key not in cache:
@@ -195,20 +212,29 @@ def cpu_iteration_seconds(wl, ctx, reps=1, cache=None):
         return cache[key]
 
     calib = d["n_layers"] * layer(d, 1) + head(d, 1)
-    draft = (n - 1) * (d["n_layers"] * layer(d, 1) + head(d, 1))
+    fuzzy_pass = sum(group(d, g, 1) for g in _plan_sizes(d["n_layers"], lp))
+    draft = (n - 1) * (fuzzy_pass + head(d, 1))
     verify = b["n_layers"] * layer(b, n + 1) + head(b, n + 1)
     return calib + draft + verify, {"calibrate_s": calib, "draft_s": draft, "verify_s": verify}
 
 
 def cpu_baseline(wl, ctx):
+    """The reference CPU path at its stock worker count (RunConfig.workers = 0
+    -> the largest plan group = lp, proj/src/orchestrator.cpp:152,
+    proj/src/worker_pool.cpp:73-84) and at workers = 1."""
     t0 = time.time()
-    it_s, parts = cpu_iteration_seconds(wl, ctx)
-    return {"value": 1.0 / it_s, "unit": "tokens/s", "cores": 1, "kind": "reference",
-            "sample": (f"oracle/_ref/ref_bench (unmodified reference core, workers=1): one layer per shape at "
-                       f"ctx {ctx} (base T={wl['n'] + 1}, drafter T=1, MHA-equivalent) + LM head rows, "
-                       f"extrapolated to {wl['base']['n_layers']}/{wl['draft']['n_layers']} layers, 1 token per iteration (m=0); "
-                       f"{time.time() - t0:.1f}s of CPU work"),
-            "stage_s": parts}
+    cache = {}
+    lp = wl["lp"]
+    it_lp, parts_lp = cpu_iteration_seconds(wl, ctx, workers=lp, cache=cache)
+    it_1, parts_1 = cpu_iteration_seconds(wl, ctx, workers=1, cache=cache)
+    return {"value": 1.0 / it_lp, "unit": "tokens/s", "cores": lp, "kind": "reference",
+            "sample": (f"oracle/_ref/ref_bench (unmodified reference core): one layer per shape at ctx {ctx} "
+                       f"(base T={wl['n'] + 1}, drafter T=1, MHA-equivalent widths) and each fuzzy group through "
+                       f"forward_fuzzy + WorkerPool, + LM head rows, extrapolated to "
+                       f"{wl['base']['n_layers']}/{wl['draft']['n_layers']} layers, 1 token per iteration (m=0); "
+                       f"value at workers={lp} (the reference's auto setting); {time.time() - t0:.1f}s of CPU work"),
+            "stage_s": parts_lp,
+            "workers_1": {"value": 1.0 / it_1, "cores": 1, "stage_s": parts_1}}
 
 
 def run_reference(args, wl):
@@ -217,12 +243,13 @@ def run_reference(args, wl):
         return 0
     cache = {}
     times = []
+    lp = wl["lp"]
     t_start = time.time()
     for i in range(args.warmup + args.steps):
         # each step re-samples the dominant term (one base layer at T=n+1);
-        # drafter layers and LM heads are sampled once (warm-up)
+        # drafter layers, fuzzy groups and LM heads are sampled once (warm-up)
         cache.pop(("layer", wl["base"]["d_model"], wl["n"] + 1), None)
-        it_s, parts = cpu_iteration_seconds(wl, args.ctx, cache=cache)
+        it_s, parts = cpu_iteration_seconds(wl, args.ctx, workers=lp, cache=cache)
         if i >= args.warmup:
             times.append(it_s)
     it = statistics.median(times)
@@ -233,10 +260,10 @@ def run_reference(args, wl):
             "data": "synthetic", "impl": "reference",
             "config": {"workload": wl["name"], "ctx": args.ctx, "n": wl["n"], "lp": wl["lp"],
                        "note": "reference CPU core; 1 token per iteration (m=0)"},
-            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": 1, "kind": "reference",
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": lp, "kind": "reference",
                              "sample": f"per step: one base layer (T={wl['n'] + 1}, ctx {args.ctx}) timed, "
-                                       f"extrapolated; drafter layers + heads sampled once; "
-                                       f"{time.time() - t_start:.0f}s total"},
+                                       f"extrapolated; drafter layers, fuzzy groups (forward_fuzzy, "
+                                       f"WorkerPool({lp})) + heads sampled once; {time.time() - t_start:.0f}s total"},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "stage_s": parts}
     print(json.dumps(line), flush=True)
@@ -263,6 +290,19 @@ def main():
     args = ap.parse_args()
     assert args.warmup >= 1
     wl = WORKLOADS[args.workload]
+    # --gpus N without a torchrun environment: launch the N ranks ourselves
+    # (one process per GPU), exactly as the driver's torchrun line would
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        return subprocess.call(cmd)
+    ws_env = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws_env != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws_env}")
     if args.impl == "reference":
         return run_reference(args, wl)
 
@@ -357,7 +397,10 @@ def main():
     # base gate/up GEMV (the largest per-kernel launch)
     mk = os.environ.get("ESPEC_MK", "0") != "0"
     site_kind = 6 if mk else 3
-    es = arm("easyspec", site=(1, site_kind), clocks=True)
+    # headline: no per-launch events inside the timed region (they would
+    # break PDL overlap of the timed kernel site); the roofline comes from a
+    # separate pass of the same arm below
+    es = arm("easyspec", clocks=True)
     t_max = max_over_ranks(es["ms"])
     tokens_all = sum_over_ranks(es["emitted"])
     value = tokens_all / (t_max / 1000.0)
@@ -377,16 +420,21 @@ def main():
                              draft_ms_per_token=sum(t.draft_ms for t in r["traces"]) / max(r["emitted"], 1),
                              verify_ms_per_step=sum(t.verify_ms for t in r["traces"]) / steps)
 
-    # roofline of the dominant kernel (base gate/up GEMV, bf16 weights streamed once)
+    # roofline of the dominant kernel (base gate/up GEMV, bf16 weights streamed
+    # once): its launches timed with CUDA events on the engine stream during a
+    # separate pass of the EasySpec arm (same steps, same shapes)
+    rf = arm("easyspec", site=(1, site_kind))
     hbm, peak_kind = peaks()
-    cnt, site_ms, site_bytes = es["site"]
+    cnt, site_ms, site_bytes = rf["site"]
     achieved = site_bytes / (site_ms / cnt / 1000.0) / 1e9 if cnt else None
-    traffic = None
+    gu_shape = f"{wl['base']['d_model']}x{2 * wl['base']['d_mlp'] // ws}"
+    traffic, traffic_src = None, None
     tp = os.path.join(ROOT, "profiles", "roofline_traffic.json")
-    if os.path.exists(tp):
-        try:
-            traffic = json.load(open(tp)).get("base_pass_dram_bytes_per_launch" if mk else
-                                               "base_gate_up_dram_bytes_per_launch")
+    if os.path.exists(tp) and not mk and ws == 1:
+        try:  # ncu --set full dram__bytes of this workload's gate/up launch
+            ent = json.load(open(tp)).get("workloads", {}).get(args.workload)
+            if ent and ent.get("shape") == gu_shape:
+                traffic, traffic_src = ent["dram_bytes_per_launch"], ent["source"]
         except Exception:
             traffic = None
 
@@ -417,7 +465,7 @@ def main():
                        f"{args.e2e_tokens} new tokens"}
 
     cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu:
+    if rank == 0 and not args.no_cpu:
         try:
             cpu = cpu_baseline(wl, args.ctx)
         except Exception as ex:  # the checker binary is built here, not on the box
@@ -461,12 +509,16 @@ def main():
                                 "speedup_vs_vanilla": (proj_tok_s / arms["vanilla"]["tokens_per_s"])
                                 if "vanilla" in arms else None,
                                 "note": "projection, tokens/iteration = n*alpha+1 (proj/src/cli.cpp:403)"},
-            "roofline": {"kernel": "decode_mk_kernel (one launch = base verify pass: 80 layers x [QKV, attention, O, "
+            "roofline": {"kernel": "decode_mk_kernel (one launch = base verify pass: all layers x [QKV, attention, O, "
                                    "gate/up, down], T=n+1 rows; bytes = bf16 weights + KV + activations)" if mk else
-                                   "sgemv_kernel<8,EPI_SILU> (stream-K bf16 GEMV, base gate/up 8192x57344)",
+                                   f"sgemv_kernel<8,EPI_SILU> (stream-K bf16 GEMV, base gate/up {gu_shape}, "
+                                   f"T={n + 1})",
                          "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": (achieved / hbm) if achieved else None, "traffic": traffic,
-                         "launches_timed": cnt, "bytes_per_launch": site_bytes, "peak_source": peak_kind},
+                         "traffic_source": traffic_src,
+                         "launches_timed": cnt, "bytes_per_launch": site_bytes, "peak_source": peak_kind,
+                         "timing": "CUDA events around each launch on the engine stream, in a separate pass of "
+                                   "the EasySpec arm (the headline pass runs without them)"},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": es["launches"],

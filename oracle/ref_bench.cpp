@@ -13,9 +13,15 @@
 // depend on values; init_model's Box-Muller would take minutes at this size).
 //
 //   ref_bench layer <d_model> <n_heads> <d_head> <d_mlp> <T> <ctx> <reps>
+//   ref_bench group <d_model> <n_heads> <d_head> <d_mlp> <g> <T> <ctx> <workers> <reps>
+//       one fuzzy group of g layers through forward_fuzzy
+//       (proj/src/draft_engine.cpp:64-133) with a WorkerPool of `workers`
+//       threads (proj/src/worker_pool.cpp:27-50): the reference's own
+//       layer-parallel executor
 //   ref_bench head  <d_model> <vocab> <T> <reps>
 //   ref_bench c1    <algorithm> <max_new_tokens> <reps>
 #include <algorithm>
+#include <cmath>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -27,6 +33,7 @@
 #include "espec/kv_cache.hpp"
 #include "espec/model.hpp"
 #include "espec/orchestrator.hpp"
+#include "espec/worker_pool.hpp"
 
 using namespace espec;
 using Clock = std::chrono::steady_clock;
@@ -124,6 +131,75 @@ static int cmd_layer(int argc, char** argv) {
     return 0;
 }
 
+static void fill_layer(LayerWeights& L, int d, int f, uint32_t seed) {
+    const float ps = 2.0f / std::sqrt((float)d);
+    L.wq = Matrix(d, d); fill(L.wq, seed + 1, ps);
+    L.wk = Matrix(d, d); fill(L.wk, seed + 2, ps);
+    L.wv = Matrix(d, d); fill(L.wv, seed + 3, ps);
+    L.wo = Matrix(d, d); fill(L.wo, seed + 4, ps);
+    L.w_gate = Matrix(d, f); fill(L.w_gate, seed + 5, ps);
+    L.w_up = Matrix(d, f); fill(L.w_up, seed + 6, ps);
+    L.w_down = Matrix(f, d); fill(L.w_down, seed + 7, 2.0f / std::sqrt((float)f));
+    L.attn_norm_gain = Matrix(1, d);
+    L.mlp_norm_gain = Matrix(1, d);
+    for (float& v : L.attn_norm_gain.data) v = 1.f;
+    for (float& v : L.mlp_norm_gain.data) v = 1.f;
+}
+
+static int cmd_group(int argc, char** argv) {
+    if (argc < 11) return 2;
+    const int d = atoi(argv[2]), H = atoi(argv[3]), dh = atoi(argv[4]), f = atoi(argv[5]);
+    const int g = atoi(argv[6]), T = atoi(argv[7]), ctx = atoi(argv[8]), workers = atoi(argv[9]);
+    const int reps = atoi(argv[10]);
+    Model m;
+    m.config.d_model = d;
+    m.config.n_heads = H;
+    m.config.d_head = dh;
+    m.config.d_mlp = f;
+    m.config.n_layers = g;
+    m.config.max_positions = ctx + T + 8;
+    m.weights.layers.resize(g);
+    for (int l = 0; l < g; ++l) fill_layer(m.weights.layers[l], d, f, 16u * l);
+    LayerPlan plan;
+    plan.groups.push_back({});
+    for (int l = 0; l < g; ++l) plan.groups[0].push_back(l);
+    plan.lp_size = g;
+    KvCache cache(g, d);
+    if (ctx > 0) {
+        std::vector<int> parents;
+        for (int i = 0; i < ctx; ++i) parents.push_back(i == 0 ? kCommittedTail : i - 1);
+        const auto rows = cache.stage_append(parents, false);
+        Matrix k(ctx, d), v(ctx, d);
+        fill(k, 8, 1.f);
+        fill(v, 9, 1.f);
+        for (int l = 0; l < g; ++l) cache.write_rows(l, rows, k, v);
+        cache.commit_path(rows);
+    }
+    WorkerPool pool(workers);
+    FuzzyOptions opt;
+    opt.pool = &pool;
+    double best = 1e30;
+    for (int r = 0; r < reps; ++r) {
+        std::vector<int> parents;
+        for (int i = 0; i < T; ++i) parents.push_back(i == 0 ? kCommittedTail : cache.committed_len() + i - 1);
+        ForwardBatch batch;
+        batch.flat_rows = cache.stage_append(parents, true);
+        for (int row : batch.flat_rows) batch.positions.push_back(cache.position_of(row));
+        Matrix h(T, d);
+        fill(h, 10 + r, 1.f);
+        const auto t0 = Clock::now();
+        const TreeMask mask = cache.build_tree_mask();
+        batch.mask = &mask;
+        const Matrix out = forward_fuzzy(m, plan, h, cache, batch, opt);
+        best = std::min(best, ms_since(t0));
+        if (out.data.empty()) return 3;
+        cache.discard_staged();
+    }
+    printf("{\"mode\":\"group\",\"d_model\":%d,\"g\":%d,\"T\":%d,\"ctx\":%d,\"workers\":%d,\"group_ms\":%.4f}\n", d,
+           g, T, ctx, pool.worker_count() ? pool.worker_count() : 1, best);
+    return 0;
+}
+
 static int cmd_head(int argc, char** argv) {
     if (argc < 6) return 2;
     const int d = atoi(argv[2]), V = atoi(argv[3]), T = atoi(argv[4]), reps = atoi(argv[5]);
@@ -186,6 +262,7 @@ int main(int argc, char** argv) {
     const std::string mode = argv[1];
     if (mode == "layer") return cmd_layer(argc, argv);
     if (mode == "head") return cmd_head(argc, argv);
+    if (mode == "group") return cmd_group(argc, argv);
     if (mode == "c1") return cmd_c1(argc, argv);
     return 2;
 }

@@ -250,6 +250,21 @@ espec_status espec_forward_tree(espec_engine* eng, int which, const int32_t* pro
                                 const int32_t* tokens, const int32_t* parents, int n, const char* plan, float* logits,
                                 float* hidden);
 
+/* prefix_distribution (proj/src/orchestrator.cpp:494-526): independent
+ * generations of the run config's max_new_tokens tokens over `tokens`, run r
+ * seeded SplitMix64(seed + 0x9E37 (r + 1)).next() as in the reference, for
+ * r = first_run, first_run + run_stride, ... < runs (one host thread's share of
+ * the reference's loop; 0 / 1 = all runs). Writes the distinct emitted
+ * prefixes in lexicographic order (cap x max_new_tokens int32) and their
+ * counts; *n_distinct = how many. */
+espec_status espec_prefix_distribution(espec_engine* eng, const int32_t* tokens, int n_tokens, int64_t runs,
+                                       int64_t first_run, int64_t run_stride, int32_t* prefixes, int64_t* counts,
+                                       int cap, int* n_distinct);
+/* total_variation (orchestrator.cpp:528-553) of two prefix distributions
+ * (lexicographically sorted, prefixes of `len` tokens); -1 on bad counts. */
+double espec_total_variation(const int32_t* pa, const int64_t* ca, int na, const int32_t* pb, const int64_t* cb,
+                             int nb, int len, int64_t runs_a, int64_t runs_b);
+
 /* Layer plans (proj/src/layer_plan.cpp:54-128) -> formatted plan string. */
 espec_status espec_plan_groups(int n_layers, int lp_size, char* out, int out_len);
 espec_status espec_parse_plan(const char* spec, char* out, int out_len);

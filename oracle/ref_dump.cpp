@@ -571,6 +571,28 @@ int main(int argc, char** argv) {
         std::ofstream f(out_dir + "/ref_generate.json");
         f << gens.dump() << "\n";
     }
+    // criterion 2's configuration (proj/tests/acceptance_main.cpp:156-183):
+    // prefix_distribution over 2000 runs of easyspec and vanilla, exact counts
+    // (the per-run seeds are deterministic, so a bit-exact engine reproduces
+    // every count, not just the law)
+    {
+        const Model base = init_model(tiny(4, 21));
+        const Model draft = make_truncated_draft(base, 3);
+        RunConfig rc = run_cfg(Algorithm::easyspec, 3, {2, 2, 2}, 2, 0.8f, 2, 11);
+        const char* text = "easyspec";
+        const std::span<const std::uint8_t> pr{reinterpret_cast<const std::uint8_t*>(text), 8};
+        json pj = json::object();
+        pj["runs"] = 2000;
+        for (Algorithm a : {Algorithm::easyspec, Algorithm::vanilla}) {
+            rc.algorithm = a;
+            const auto dist = prefix_distribution(base, draft, rc, pr, 2000, 1);
+            json e = json::array();
+            for (const auto& [k, v] : dist) e.push_back(json{{"prefix", k}, {"count", v}});
+            pj[to_string(a)] = e;
+        }
+        std::ofstream f(out_dir + "/ref_prefix.json");
+        f << pj.dump() << "\n";
+    }
     // per-iteration trees and outcomes of every speculative case, from the
     // stage-by-stage restatement pinned against generate()
     json stages = json::array();

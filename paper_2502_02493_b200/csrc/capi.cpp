@@ -1,4 +1,5 @@
 // extern "C" boundary (include/espec_c.h) over the C++ engine.
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -411,6 +412,54 @@ espec_status espec_commit_outcome(espec_engine* eng, int32_t* emitted, int* n_em
         if (n_emitted) *n_emitted = (int)em.size();
         if (trace) fill_trace(t, trace);
     });
+}
+
+}  // extern "C"
+
+extern "C" {
+
+espec_status espec_prefix_distribution(espec_engine* eng, const int32_t* tokens, int n_tokens, int64_t runs,
+                                       int64_t first_run, int64_t run_stride, int32_t* prefixes, int64_t* counts,
+                                       int cap, int* n_distinct) {
+    return guard(eng, [&] {
+        if (!tokens || n_tokens <= 0) throw Error(ST_CONFIG, "empty prompt");
+        const auto dist = eng->impl->prefix_distribution(std::vector<int>(tokens, tokens + n_tokens), (long)runs,
+                                                         (long)first_run, (long)run_stride);
+        if (n_distinct) *n_distinct = (int)dist.size();
+        if ((int)dist.size() > cap) throw Error(ST_SHAPE, "prefix buffer holds fewer entries than distinct prefixes");
+        size_t len = 0;
+        int i = 0;
+        for (const auto& kv : dist) {
+            if (i == 0) len = kv.first.size();
+            if (kv.first.size() != len) throw Error(ST_CHECK, "prefixes of different lengths");
+            for (size_t j = 0; j < len; ++j) prefixes[(size_t)i * len + j] = kv.first[j];
+            counts[i++] = kv.second;
+        }
+    });
+}
+
+double espec_total_variation(const int32_t* pa, const int64_t* ca, int na, const int32_t* pb, const int64_t* cb,
+                             int nb, int len, int64_t runs_a, int64_t runs_b) {
+    // total_variation (orchestrator.cpp:528-553): both lists in lexicographic order
+    if (runs_a <= 0 || runs_b <= 0 || len <= 0) return -1.0;
+    auto less = [len](const int32_t* x, const int32_t* y) {
+        return std::lexicographical_compare(x, x + len, y, y + len);
+    };
+    double dist = 0.0;
+    int i = 0, j = 0;
+    while (i < na || j < nb) {
+        double a = 0.0, b = 0.0;
+        if (j == nb || (i < na && less(pa + (size_t)i * len, pb + (size_t)j * len))) {
+            a = (double)ca[i++] / (double)runs_a;
+        } else if (i == na || less(pb + (size_t)j * len, pa + (size_t)i * len)) {
+            b = (double)cb[j++] / (double)runs_b;
+        } else {
+            a = (double)ca[i++] / (double)runs_a;
+            b = (double)cb[j++] / (double)runs_b;
+        }
+        dist += a > b ? a - b : b - a;
+    }
+    return dist / 2.0;
 }
 
 }  // extern "C"

@@ -2144,6 +2144,35 @@ public:
         return out;
     }
 
+    // prefix_distribution (proj/src/orchestrator.cpp:494-526): `runs`
+    // independent generations of run.max_new_tokens tokens; run r is seeded
+    // SplitMix64(seed + 0x9E37 (r + 1)).next() exactly as the reference, so
+    // the empirical law is comparable run for run. Runs are serial on this
+    // engine's stream (the reference spreads them over host threads).
+    // first / stride select one host thread's share of the reference's loop
+    // (`for r = thread_index; r < runs; r += n_threads`).
+    std::map<std::vector<int>, long> prefix_distribution(const std::vector<int>& tokens, long runs, long first,
+                                                         long stride) override {
+        if (runs <= 0) cfg_fail("prefix_distribution needs runs > 0");
+        if (first < 0 || stride < 1) cfg_fail("prefix_distribution: first >= 0 and stride >= 1");
+        const RunCfg saved = run_;
+        std::map<std::vector<int>, long> out;
+        try {
+            for (long r = first; r < runs; r += stride) {
+                uint64_t z = saved.seed + 0x9E37ULL * (uint64_t)(r + 1) + 0x9E3779B97F4A7C15ULL;
+                z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+                z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+                run_.seed = z ^ (z >> 31);
+                ++out[generate(tokens, nullptr)];
+            }
+        } catch (...) {
+            run_ = saved;
+            throw;
+        }
+        run_ = saved;
+        return out;
+    }
+
     void forward_chain(int which, const std::vector<int>& tokens, const std::string& plan_spec, float* logits,
                        float* hidden) override {
         ModelDev& M = which ? base_ : draft_;

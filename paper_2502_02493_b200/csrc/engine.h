@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -111,6 +112,9 @@ public:
     virtual bool done() const = 0;
     virtual IterationTrace step(std::vector<int>& emitted) = 0;
     virtual std::vector<int> generate(const std::vector<int>& tokens, std::vector<IterationTrace>* traces) = 0;
+    // prefix_distribution (proj/src/orchestrator.cpp:494-526)
+    virtual std::map<std::vector<int>, long> prefix_distribution(const std::vector<int>& tokens, long runs,
+                                                                 long first = 0, long stride = 1) = 0;
     // Stage-level iteration (run_iteration_speculative split at the
     // reference's stage boundaries, proj/src/orchestrator.cpp:256-428).
     virtual void prefill(const std::vector<int>& tokens) = 0;

@@ -125,6 +125,11 @@ def lib():
         L.espec_comm_export.argtypes = [V, C.c_void_p]
         L.espec_comm_import.argtypes = [V, C.c_void_p, C.c_int]
         L.espec_prefill.argtypes = [V, P(C.c_int32), C.c_int]
+        L.espec_prefix_distribution.argtypes = [V, P(C.c_int32), C.c_int, C.c_int64, C.c_int64, C.c_int64,
+                                                P(C.c_int32), P(C.c_int64), C.c_int, P(C.c_int)]
+        L.espec_total_variation.restype = C.c_double
+        L.espec_total_variation.argtypes = [P(C.c_int32), P(C.c_int64), C.c_int, P(C.c_int32), P(C.c_int64), C.c_int,
+                                            C.c_int, C.c_int64, C.c_int64]
         L.espec_forward_tree.argtypes = [V, C.c_int, P(C.c_int32), C.c_int, P(C.c_int32), P(C.c_int32), C.c_int,
                                          C.c_char_p, P(C.c_float), P(C.c_float)]
         L.espec_calibrate.argtypes = [V, P(C.c_float)]
@@ -453,6 +458,18 @@ class Engine:
                                              (plan or "").encode(), _f(logits), _f(hidden)))
         return logits, hidden
 
+    def prefix_distribution(self, prompt: bytes, runs: int, first: int = 0, stride: int = 1, cap: int = 1 << 16):
+        """prefix_distribution (orchestrator.cpp:494-526) over runs first,
+        first + stride, ... -> {prefix tuple: count}."""
+        t = np.asarray(tokenize(prompt), np.int32)
+        L = self.run.max_new_tokens
+        pre = np.zeros((cap, L), np.int32)
+        cnt = np.zeros(cap, np.int64)
+        nd = C.c_int(0)
+        self._check(lib().espec_prefix_distribution(self._h, _i(t), len(t), runs, first, stride, _i(pre),
+                                                    cnt.ctypes.data_as(C.POINTER(C.c_int64)), cap, C.byref(nd)))
+        return {tuple(int(x) for x in pre[i]): int(cnt[i]) for i in range(nd.value)}
+
     def cache_view(self, which: int, layer: int, row0: int = 0, n: Optional[int] = None):
         cfg = self.base_cfg if which == self.BASE else self.draft_cfg
         committed = C.c_int(0)
@@ -573,6 +590,47 @@ def tp_generate(engines: Sequence[Engine], prompt: bytes = None, tokens: Sequenc
     if err:
         raise err[0]
     return out
+
+
+def prefix_distribution(engines: Sequence["Engine"], prompt: bytes, runs: int) -> dict:
+    """The reference's threaded prefix_distribution (orchestrator.cpp:494-526):
+    engine t (one host thread each, its own stream) runs r = t, t + n, ... and
+    the partial counts are merged; identical to one engine running them all."""
+    import threading
+    parts = [None] * len(engines)
+    err = []
+
+    def work(t):
+        try:
+            parts[t] = engines[t].prefix_distribution(prompt, runs, first=t, stride=len(engines))
+        except Exception as ex:  # surfaced below
+            err.append(ex)
+
+    th = [threading.Thread(target=work, args=(t,)) for t in range(len(engines))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if err:
+        raise err[0]
+    merged = {}
+    for p in parts:
+        for k, v in p.items():
+            merged[k] = merged.get(k, 0) + v
+    return merged
+
+
+def total_variation(a: dict, b: dict, runs_a: int, runs_b: int) -> float:
+    """total_variation (orchestrator.cpp:528-553) through the C ABI."""
+    keys_a, keys_b = sorted(a), sorted(b)
+    n = len((keys_a or keys_b)[0])
+    pa = np.asarray(keys_a, np.int32).reshape(-1, n)
+    pb = np.asarray(keys_b, np.int32).reshape(-1, n)
+    ca = np.asarray([a[k] for k in keys_a], np.int64)
+    cb = np.asarray([b[k] for k in keys_b], np.int64)
+    P64 = C.POINTER(C.c_int64)
+    return lib().espec_total_variation(_i(pa), ca.ctypes.data_as(P64), len(keys_a), _i(pb), cb.ctypes.data_as(P64),
+                                       len(keys_b), n, runs_a, runs_b)
 
 
 def plan_groups(n_layers: int, lp_size: int) -> str:

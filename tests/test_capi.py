@@ -67,3 +67,16 @@ def test_vocab_mismatch_rejected():
         E.Engine(E.tiny_config(4, 1), E.ModelConfig(vocab_size=300, d_model=32, n_heads=2, d_head=16, d_mlp=64,
                                                      n_layers=2), E.RunConfig(n=4, lp_size=2))
     assert ei.value.kind == "config"
+
+
+def test_total_variation_matches_definition():
+    """espec_total_variation = total_variation (proj/src/orchestrator.cpp:
+    528-553) on the reference's own criterion-2 prefix counts."""
+    golden = json.load(open(os.path.join(ROOT, "tests", "golden", "ref_prefix.json")))
+    runs = golden["runs"]
+    a = {tuple(e["prefix"]): e["count"] for e in golden["easyspec"]}
+    b = {tuple(e["prefix"]): e["count"] for e in golden["vanilla"]}
+    keys = set(a) | set(b)
+    want = 0.5 * sum(abs(a.get(k, 0) - b.get(k, 0)) / runs for k in keys)
+    assert abs(E.total_variation(a, b, runs, runs) - want) < 1e-12
+    assert E.total_variation(a, a, runs, runs) == 0.0

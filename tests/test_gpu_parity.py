@@ -181,29 +181,46 @@ def test_generate_sampled_and_trees_match_reference(case):
                 want["base_committed"])
 
 
-def test_sampled_easyspec_first_token_distribution_matches_vanilla():
-    """Statistical losslessness on device (acceptance criterion 2,
-    proj/tests/acceptance_main.cpp:156-183, reduced): the first generated
-    token of T = 0.8 EasySpec with a 2-wide tree follows the same law as
-    vanilla sampling. TV over 2500 seeds each; bound 0.08 (sampling noise of
-    two 2500-run histograms over this support is ~0.03)."""
+PREFIX = json.load(open(os.path.join(GOLDEN, "ref_prefix.json")))
+
+
+def _crit2_engine(alg):
+    """Acceptance criterion 2's pair and run (proj/tests/acceptance_main.cpp:156-183)."""
     base = E.tiny_config(4, 21, max_positions=64)
-    dcfg = replace(base, n_layers=3)
-    counts = {}
-    runs = 2500
-    for alg, widths in (("vanilla", [1, 1, 1]), ("easyspec", [2, 2, 2])):
-        run = E.RunConfig(algorithm=alg, n=3, widths=widths, lp_size=2, temperature=0.8, max_new_tokens=1, seed=1)
-        eng = E.truncated_pair(base, 3, run)
-        hist = {}
-        for r in range(runs):
-            eng.set_run(replace(run, seed=1000 + r))
-            toks, _ = eng.generate(b"easyspec")
-            hist[toks[0]] = hist.get(toks[0], 0) + 1
-        counts[alg] = hist
-        eng.close()
-    keys = set(counts["vanilla"]) | set(counts["easyspec"])
-    tv = 0.5 * sum(abs(counts["vanilla"].get(k, 0) - counts["easyspec"].get(k, 0)) / runs for k in keys)
-    assert tv < 0.08, tv
+    run = E.RunConfig(algorithm=alg, n=3, widths=[2, 2, 2], lp_size=2, temperature=0.8, max_new_tokens=2, seed=11)
+    return E.truncated_pair(base, 3, run)
+
+
+@pytest.mark.parametrize("alg", ["easyspec", "vanilla"])
+def test_prefix_distribution_matches_reference_counts(alg):
+    """prefix_distribution (orchestrator.cpp:494-526) on device: the same
+    per-run seeds give the reference's exact counts for every 2-token prefix
+    over 2000 runs (bit-exact sampling, not just the same law)."""
+    want = {tuple(e["prefix"]): e["count"] for e in PREFIX[alg]}
+    eng = _crit2_engine(alg)
+    assert eng.prefix_distribution(b"easyspec", PREFIX["runs"]) == want
+    eng.close()
+    engines = [_crit2_engine(alg) for _ in range(3)]  # threaded split: same counts
+    assert E.prefix_distribution(engines, b"easyspec", PREFIX["runs"]) == want
+    for e in engines:
+        e.close()
+
+
+def test_statistical_losslessness_criterion_2():
+    """Acceptance criterion 2 at full strength (proj/tests/acceptance_main.cpp:
+    156-183): T = 0.8 EasySpec with a [2,2,2] tree vs vanilla, first 2
+    tokens, 2 x 200k runs, TV < 0.01."""
+    runs = 200_000
+    dist = {}
+    for alg in ("easyspec", "vanilla"):
+        engines = [_crit2_engine(alg) for _ in range(4)]  # 4 host threads, as the reference's threads
+        dist[alg] = E.prefix_distribution(engines, b"easyspec", runs)
+        for e in engines:
+            e.close()
+    tv = E.total_variation(dist["easyspec"], dist["vanilla"], runs, runs)
+    print(f"criterion 2: TV(easyspec, vanilla) = {tv:.5f} over 2 x {runs} runs, "
+          f"{len(dist['easyspec'])}/{len(dist['vanilla'])} distinct prefixes")
+    assert tv < 0.01, tv
 
 
 def test_calibrated_drafter_cache_equals_fresh_prefill_every_iteration():

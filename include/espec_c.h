@@ -269,6 +269,66 @@ double espec_total_variation(const int32_t* pa, const int64_t* ca, int na, const
 espec_status espec_plan_groups(int n_layers, int lp_size, char* out, int out_len);
 espec_status espec_parse_plan(const char* spec, char* out, int out_len);
 
+/* ---- Host-side analysis API ------------------------
+ * Calls without an engine report their error text through
+ * espec_create_error(). */
+
+/* RunReport's derived metrics (proj/include/espec/report.hpp:40-57) from the
+ * engine's iteration traces; stage times are the measured device times. */
+typedef struct {
+    int n_iterations;
+    int has_alpha;             /* vanilla drafts nothing */
+    double alpha;              /* sum m / sum n (report.cpp:77-78) */
+    int64_t tokens_emitted;
+    double mean_accept_len;    /* emitted / iterations */
+    double tokens_per_s;       /* emitted / device seconds of the three stages */
+    double draft_per_100_s;    /* stage seconds per 100 emitted tokens (report.cpp:80-84) */
+    double verify_per_100_s;
+    double calibrate_per_100_s;
+    double draft_total_per_100_s; /* draft + calibrate (report.cpp:85) */
+    double total_s;
+    double speedup_vs_vanilla; /* vanilla_baseline_s / total_s (report.cpp:87-90), 1 if total is 0 */
+} espec_report;
+
+/* aggregate(traces, vanilla_baseline_sim) (proj/src/report.cpp:51-95):
+ * ESPEC_CONFIG "cannot aggregate an empty trace list" / "traces emitted zero
+ * tokens" as the reference throws. vanilla_baseline_s: device seconds the
+ * vanilla arm takes for the same number of tokens. */
+espec_status espec_aggregate(const espec_iteration* traces, int n_traces, double vanilla_baseline_s,
+                             espec_report* out);
+/* emit_report (report.cpp:97-171): format 0 = JSON (the reference's keys;
+ * "sim" and "wall" both carry measured device seconds — no cost simulator on
+ * this path), 1 = CSV header + row. *len receives the text length;
+ * ESPEC_SHAPE if it does not fit in cap bytes (NUL included). */
+espec_status espec_report_emit(const espec_report* report, const espec_iteration* traces, int n_traces,
+                               const char* algorithm, int n, const int* widths, int n_widths, int lp_size,
+                               int format, char* out, int cap, int* len);
+
+/* ESPEC1 model file (proj/include/espec/model_io.hpp, proj/src/model_io.cpp):
+ * "ESPEC1\n", u64 header length, JSON header (config + tensor manifest), raw
+ * little-endian fp32 tensors. espec_model_file_config parses and validates a
+ * file (every check of load_model, with its IoError texts as ESPEC_IO) and
+ * returns its config (MHA, tied head, fp32). */
+espec_status espec_model_file_config(const char* path, espec_model_cfg* cfg);
+/* load_model into model `which` (0 drafter, 1 base) of an engine whose config
+ * matches the file's; save_model of model `which` (reference-representable
+ * models: MHA, tied head, rope base 10000). */
+espec_status espec_load_model_file(espec_engine* eng, int which, const char* path);
+espec_status espec_save_model_file(espec_engine* eng, int which, const char* path);
+
+/* probe_similarity (proj/src/draft_engine.cpp:291-357) on the drafter: for
+ * each lp size, one fuzzy and one precise pass over every corpus sequence
+ * (token ids; sequence s = tokens[offsets[s] .. offsets[s+1])) on fresh
+ * caches, mean cosine similarity (double, matrix.cpp:139-157) of h_in, q, k,
+ * v and the attention output over every parallelized layer and row. Ends any
+ * generation in progress. */
+typedef struct {
+    int lp_size;
+    double h, q, k, v, attn_out;
+} espec_similarity_row;
+espec_status espec_probe_similarity(espec_engine* eng, const int* lp_sizes, int n_lp, const int32_t* tokens,
+                                    const int* offsets, int n_seqs, espec_similarity_row* rows);
+
 /* generate() over already-tokenized input (the same loop as espec_generate
  * without the byte tokenizer; vocabularies larger than 258). */
 espec_status espec_generate_tokens(espec_engine* eng, const int32_t* tokens, int n_tokens, int32_t* out_tokens,

@@ -27,6 +27,8 @@
 #include "espec/model.hpp"
 #include "espec/orchestrator.hpp"
 #include "espec/verifier.hpp"
+#include "espec/model_io.hpp"
+#include "espec/report.hpp"
 
 using namespace espec;
 using json = nlohmann::ordered_json;
@@ -609,6 +611,115 @@ int main(int argc, char** argv) {
     {
         std::ofstream f(out_dir + "/ref_stages.json");
         f << stages.dump() << "\n";
+    }
+    // ---- host-side analysis API -----------------------------------
+    //   report aggregation  -> aggregate / emit_report  proj/src/report.cpp:51-173
+    //   similarity probe    -> probe_similarity         proj/src/draft_engine.cpp:291-372
+    //   ESPEC1 model file   -> save_model / load_model  proj/src/model_io.cpp:76-190
+    {
+        json host;
+        // Report aggregation over real traces of two generations; stage times
+        // replaced by k * 2^-10 s (exactly representable as the engine's float
+        // milliseconds) so both sides aggregate the same numbers bit for bit.
+        json reps = json::array();
+        for (const char* nm : {"fixa_easyspec", "t1_tree_wide", "t3_chain_easyspec", "fixa_vanilla"}) {
+            const GenCase* gc = nullptr;
+            for (const auto& c : cases)
+                if (c.name == nm) gc = &c;
+            const Model base = init_model(gc->base);
+            const Model draft = gc->keep == 0 ? base : make_truncated_draft(base, gc->keep);
+            const std::string& text = gc->prompt;
+            const auto res = generate(base, draft, gc->run,
+                                      std::span<const std::uint8_t>(
+                                          reinterpret_cast<const std::uint8_t*>(text.data()), text.size()),
+                                      nullptr);
+            std::vector<IterationTrace> tr = res.report.iterations;
+            json jt = json::array();
+            for (std::size_t i = 0; i < tr.size(); ++i) {
+                auto& t = tr[i];
+                t.draft_wall = t.draft_sim = double((i * 7) % 13 + 1) / 1024.0;
+                t.verify_wall = t.verify_sim = double((i * 5) % 11 + 3) / 1024.0;
+                t.calibrate_wall = t.calibrate_sim = gc->run.algorithm == Algorithm::vanilla
+                                                         ? 0.0
+                                                         : double(i % 3 + 1) / 1024.0;
+                jt.push_back(json{{"m", t.m}, {"n", t.n}, {"drafted_nodes", t.drafted_nodes},
+                                  {"emitted", t.emitted}, {"draft", t.draft_wall}, {"verify", t.verify_wall},
+                                  {"calibrate", t.calibrate_wall}, {"sequential_forwards", t.sequential_forwards},
+                                  {"fuzzy_forwards", t.fuzzy_forwards}, {"base_forwards", t.base_forwards}});
+            }
+            const double vanilla = 0.0185546875 * static_cast<double>(res.tokens.size());
+            RunReport r = aggregate(tr, vanilla);
+            r.algorithm = to_string(gc->run.algorithm);
+            r.n = gc->run.n;
+            r.widths = gc->run.effective_widths();
+            r.lp_size = gc->run.lp_size;
+            reps.push_back(json{{"case", nm}, {"algorithm", r.algorithm}, {"n", r.n}, {"widths", r.widths},
+                                {"lp_size", r.lp_size}, {"vanilla_baseline", vanilla}, {"traces", jt},
+                                {"has_alpha", r.has_alpha}, {"alpha", r.alpha},
+                                {"tokens_emitted", r.tokens_emitted},
+                                {"tokens_per_s_wall", r.tokens_per_s_wall},
+                                {"per100", {r.per100_wall.draft, r.per100_wall.verify, r.per100_wall.calibrate}},
+                                {"draft_total_per100", r.draft_total_per100_sim}, {"total", r.total_sim},
+                                {"speedup", r.speedup_vs_vanilla}, {"csv", emit_report(r, ReportFormat::csv)}});
+        }
+        {
+            bool threw = false;
+            try {
+                aggregate(std::vector<IterationTrace>{}, 1.0);
+            } catch (const ConfigError& e) {
+                threw = true;
+                host["empty_error"] = e.what();
+            }
+            if (!threw) return 1;
+            IterationTrace z;
+            try {
+                aggregate(std::vector<IterationTrace>{z}, 1.0);
+            } catch (const ConfigError& e) {
+                host["zero_error"] = e.what();
+            }
+        }
+        host["reports"] = reps;
+        // Similarity probe (Table 4): a 9-layer drafter, lp 1..4 and an explicit
+        // corpus of two sequences.
+        {
+            const Model dm = init_model(tiny(9, 45));
+            const std::vector<std::vector<Token>> corpus = {bos_bytes("layer parallel drafting"),
+                                                            bos_bytes("fuzzy")};
+            const std::vector<int> lps = {1, 2, 3, 4};
+            const auto rows = probe_similarity(dm, lps, corpus);
+            json jr = json::array();
+            for (const auto& r : rows)
+                jr.push_back(json{{"lp_size", r.lp_size}, {"h", r.h}, {"q", r.q}, {"k", r.k}, {"v", r.v},
+                                  {"attn_out", r.attn_out}});
+            json jc = json::array();
+            for (const auto& c : corpus) jc.push_back(c);
+            host["similarity"] = json{{"config", cfg_json(dm.config)}, {"lp_sizes", lps}, {"corpus", jc},
+                                      {"rows", jr}, {"csv", similarity_csv(rows)}};
+        }
+        // ESPEC1 file written by the reference's save_model, plus what
+        // load_model makes of it (a greedy generation to replay after loading).
+        {
+            ModelConfig mc = tiny(3, 31, 16, 2, 8, 32, 64);
+            const Model m = init_model(mc);
+            save_model(m, out_dir + "/ref_tiny.espec1");
+            const Model back = load_model(out_dir + "/ref_tiny.espec1");
+            const Model dr = make_truncated_draft(back, 2);
+            RunConfig rc = run_cfg(Algorithm::easyspec, 3, {2, 1, 1}, 2, 0.8f, 16, 5);
+            const std::string text = "espec1";
+            const auto res = generate(back, dr, rc,
+                                      std::span<const std::uint8_t>(
+                                          reinterpret_cast<const std::uint8_t*>(text.data()), text.size()),
+                                      nullptr);
+            host["model_file"] = json{{"file", "ref_tiny.espec1"}, {"config", cfg_json(mc)},
+                                      {"embedding_sum", tensor_sum(back.weights.embedding)},
+                                      {"w_down_2_sum", tensor_sum(back.weights.layers[2].w_down)},
+                                      {"prompt", text}, {"keep", 2}, {"run", json{{"n", 3}, {"widths", {2, 1, 1}}, {"lp_size", 2},
+                                                                  {"temperature", 0.8}, {"max_new_tokens", 16},
+                                                                  {"seed", 5}}},
+                                      {"tokens", res.tokens}};
+        }
+        std::ofstream f(out_dir + "/ref_hostapi.json");
+        f << host.dump() << "\n";
     }
     std::cout << "wrote " << out_dir << "/ref_numerics.json and ref_generate.json (" << cases.size()
               << " generation cases)\n";

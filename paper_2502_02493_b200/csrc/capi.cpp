@@ -6,6 +6,7 @@
 
 #include "../../include/espec_c.h"
 #include "engine.h"
+#include "host_api.h"
 
 using namespace espec;
 
@@ -13,6 +14,7 @@ struct espec_engine {
     std::unique_ptr<Engine> impl;
     std::string err;
     int vocab = 0;
+    ModelCfg cfg[2];  // drafter, base
 };
 
 static thread_local std::string g_create_error;
@@ -90,6 +92,40 @@ espec_status guard(espec_engine* e, F&& f) {
     }
 }
 
+template <typename F>
+espec_status guard_free(F&& f) {
+    try {
+        f();
+        g_create_error.clear();
+        return ESPEC_OK;
+    } catch (const Error& x) {
+        g_create_error = x.what();
+        return (espec_status)x.status;
+    } catch (const std::exception& x) {
+        g_create_error = x.what();
+        return ESPEC_CHECK;
+    }
+}
+
+IterationTrace from_c(const espec_iteration& o) {
+    IterationTrace t;
+    t.m = o.m;
+    t.n = o.n;
+    t.drafted_nodes = o.drafted_nodes;
+    t.emitted = o.emitted;
+    t.sequential_forwards = o.sequential_forwards;
+    t.fuzzy_forwards = o.fuzzy_forwards;
+    t.base_forwards = o.base_forwards;
+    t.committed = o.committed;
+    t.draft_committed = o.draft_committed;
+    t.base_committed = o.base_committed;
+    t.bonus = o.bonus;
+    t.calibrate_ms = o.calibrate_ms;
+    t.draft_ms = o.draft_ms;
+    t.verify_ms = o.verify_ms;
+    return t;
+}
+
 espec_status copy_plan(const LayerPlan& p, char* out, int out_len) {
     const std::string s = format_plan(p);
     if ((int)s.size() + 1 > out_len) return ESPEC_SHAPE;
@@ -118,6 +154,8 @@ espec_status espec_engine_create(const espec_model_cfg* base, const espec_model_
             throw;
         }
         e->vocab = base->vocab_size;
+        e->cfg[0] = to_model(draft);
+        e->cfg[1] = to_model(base);
         *out = e;
         g_create_error.clear();
         return ESPEC_OK;
@@ -460,6 +498,106 @@ double espec_total_variation(const int32_t* pa, const int64_t* ca, int na, const
         dist += a > b ? a - b : b - a;
     }
     return dist / 2.0;
+}
+
+espec_status espec_aggregate(const espec_iteration* traces, int n_traces, double vanilla_baseline_s,
+                             espec_report* out) {
+    if (!out || (n_traces > 0 && !traces)) return ESPEC_CONFIG;
+    return guard_free([&] {
+        std::vector<IterationTrace> t;
+        for (int i = 0; i < n_traces; ++i) t.push_back(from_c(traces[i]));
+        const ReportAgg r = aggregate_traces(t, vanilla_baseline_s);
+        out->n_iterations = r.iterations;
+        out->has_alpha = r.has_alpha;
+        out->alpha = r.alpha;
+        out->tokens_emitted = r.tokens_emitted;
+        out->mean_accept_len = r.mean_accept_len;
+        out->tokens_per_s = r.tokens_per_s;
+        out->draft_per_100_s = r.draft_per100;
+        out->verify_per_100_s = r.verify_per100;
+        out->calibrate_per_100_s = r.calibrate_per100;
+        out->draft_total_per_100_s = r.draft_total_per100;
+        out->total_s = r.total;
+        out->speedup_vs_vanilla = r.speedup_vs_vanilla;
+    });
+}
+
+espec_status espec_report_emit(const espec_report* report, const espec_iteration* traces, int n_traces,
+                               const char* algorithm, int n, const int* widths, int n_widths, int lp_size,
+                               int format, char* out, int cap, int* len) {
+    if (!report || !algorithm || (n_traces > 0 && !traces) || (n_widths > 0 && !widths)) return ESPEC_CONFIG;
+    return guard_free([&] {
+        ReportAgg r;
+        r.iterations = report->n_iterations;
+        r.has_alpha = report->has_alpha != 0;
+        r.alpha = report->alpha;
+        r.tokens_emitted = (long)report->tokens_emitted;
+        r.mean_accept_len = report->mean_accept_len;
+        r.tokens_per_s = report->tokens_per_s;
+        r.draft_per100 = report->draft_per_100_s;
+        r.verify_per100 = report->verify_per_100_s;
+        r.calibrate_per100 = report->calibrate_per_100_s;
+        r.draft_total_per100 = report->draft_total_per_100_s;
+        r.total = report->total_s;
+        r.speedup_vs_vanilla = report->speedup_vs_vanilla;
+        std::vector<IterationTrace> t;
+        for (int i = 0; i < n_traces; ++i) t.push_back(from_c(traces[i]));
+        std::string text;
+        if (format == 1) text = report_csv(r, algorithm, n, lp_size);
+        else if (format == 0) text = report_json(r, t, algorithm, n, std::vector<int>(widths, widths + n_widths), lp_size);
+        else throw Error(ST_CONFIG, "report format must be 0 (json) or 1 (csv)");
+        if (len) *len = (int)text.size();
+        if (!out || (int)text.size() + 1 > cap) throw Error(ST_SHAPE, "report text does not fit the buffer");
+        std::memcpy(out, text.c_str(), text.size() + 1);
+    });
+}
+
+espec_status espec_model_file_config(const char* path, espec_model_cfg* cfg) {
+    if (!path || !cfg) return ESPEC_CONFIG;
+    return guard_free([&] {
+        const ModelFileInfo info = read_model_file(path, true);
+        const ModelCfg& m = info.cfg;
+        cfg->vocab_size = m.vocab_size;
+        cfg->d_model = m.d_model;
+        cfg->n_layers = m.n_layers;
+        cfg->n_heads = m.n_heads;
+        cfg->n_kv_heads = m.n_kv_heads;
+        cfg->d_head = m.d_head;
+        cfg->d_mlp = m.d_mlp;
+        cfg->max_positions = m.max_positions;
+        cfg->norm_eps = m.norm_eps;
+        cfg->rope_theta = m.rope_theta;
+        cfg->tied_head = 1;
+        cfg->weight_dtype = ESPEC_F32;
+        cfg->kv_dtype = ESPEC_F32;
+        cfg->seed = m.seed;
+    });
+}
+
+espec_status espec_load_model_file(espec_engine* eng, int which, const char* path) {
+    if (!path || which < 0 || which > 1) return ESPEC_CONFIG;
+    return guard(eng, [&] { load_model_file(*eng->impl, which, eng->cfg[which], path); });
+}
+
+espec_status espec_save_model_file(espec_engine* eng, int which, const char* path) {
+    if (!path || which < 0 || which > 1) return ESPEC_CONFIG;
+    return guard(eng, [&] { save_model_file(*eng->impl, which, eng->cfg[which], path); });
+}
+
+espec_status espec_probe_similarity(espec_engine* eng, const int* lp_sizes, int n_lp, const int32_t* tokens,
+                                    const int* offsets, int n_seqs, espec_similarity_row* rows) {
+    if (!eng) return ESPEC_CONFIG;
+    if ((n_lp > 0 && (!lp_sizes || !rows)) || (n_seqs > 0 && (!tokens || !offsets))) return ESPEC_CONFIG;
+    return guard(eng, [&] {
+        std::vector<std::vector<int>> corpus;
+        for (int s = 0; s < n_seqs; ++s) {
+            if (offsets[s + 1] <= offsets[s]) throw Error(ST_CONFIG, "similarity probe sequences must be non-empty");
+            corpus.emplace_back(tokens + offsets[s], tokens + offsets[s + 1]);
+        }
+        const auto r = probe_similarity(*eng->impl, eng->cfg[0].n_layers, std::vector<int>(lp_sizes, lp_sizes + n_lp),
+                                        corpus);
+        for (size_t i = 0; i < r.size(); ++i) rows[i] = {r[i].lp_size, r[i].h, r[i].q, r[i].k, r[i].v, r[i].attn_out};
+    });
 }
 
 }  // extern "C"

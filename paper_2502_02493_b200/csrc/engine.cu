@@ -1204,7 +1204,7 @@ public:
     // (decode_mk.cu) executing the op list forward_body records; the op list
     // depends only on (model, plan, T), so it is built once and cached.
     void forward(ModelDev& M, Cache& C, Workspace& W, const LayerPlan* plan, const Pass& ps) {
-        if (mk_usable(M, ps.T)) {
+        if (mk_usable(M, ps.T) && !cap_) {
             forward_mk(M, C, W, plan, ps);
             return;
         }
@@ -1220,6 +1220,7 @@ public:
         return mk_mode_ && !tp() && T >= 1 && T <= mk_max_rows() && M.c.weight_dtype == DT_BF16 &&
                M.c.kv_dtype == DT_BF16 && (M.c.d_head == 64 || M.c.d_head == 128);
     }
+    std::vector<LayerCapture>* cap_ = nullptr;  // forward_capture in progress
     void mk_clear() {
         for (auto& kv : mk_progs_)
             if (kv.second.dev) cudaFree(kv.second.dev);
@@ -1371,8 +1372,14 @@ public:
             for (int l = 0; l < c.n_layers; ++l) groups.push_back({l});
         // fuzzy groups: the residual adds h += attn_i ride on the O / down GEMV
         // epilogues (bf16 decode GEMV, one GPU); otherwise separate add kernels
-        const bool fuse = wdt == DT_BF16 && !tp() && T <= 16 && fuse_adds_;
+        const bool fuse = wdt == DT_BF16 && !tp() && T <= 16 && fuse_adds_ && !cap_;
         const int b16 = attn_b16(M, T) ? 1 : 0;
+        // similarity-probe capture (LayerProbe, proj/include/espec/draft_engine.hpp:24-37):
+        // every group takes the unfused path so attn_out exists on its own
+        auto grab = [&](std::vector<float>& dst, const float* src, int cols) {
+            dst.resize((size_t)T * cols);
+            CUDA_OK(cudaMemcpyAsync(dst.data(), src, sizeof(float) * dst.size(), cudaMemcpyDeviceToHost, stream_));
+        };
         for (const auto& g : groups) {
             const int n = (int)g.size();
             // attention of every layer in the group reads the group-entry state
@@ -1387,8 +1394,10 @@ public:
                 qb.p[i] = p;
             }
             g_gemv(M, 0, gemv_bytes(M, d, M.qkv_ld(), M.qkv_N(), T, n), EPI_QKV, qb, n, T, ps, kv);
+            if (cap_)
+                for (int i = 0; i < n; ++i) grab((*cap_)[g[i]].q, W.q + (size_t)i * kChunk * qd, qd);
             attention(M, C, W, g, ps);
-            if (n == 1) {
+            if (n == 1 && !cap_) {
                 row_parallel_resid(M, W, M.L[g[0]].wo, qd, b16 ? (const float*)W.mixed_b16 : W.mixed, qd, 2, T, ps, kv,
                                    nullptr, b16);
             } else {
@@ -1405,6 +1414,8 @@ public:
                     ob.p[i] = p;
                 }
                 g_gemv(M, 2, gemv_bytes(M, qd, d, d, T, n), EPI_STORE, ob, n, T, ps, kv);
+                if (cap_)
+                    for (int i = 0; i < n; ++i) grab((*cap_)[g[i]].attn_out, W.attn + (size_t)i * kChunk * d, d);
                 if (tp()) {
                     // ONE all-reduce for the whole group's attention outputs
                     const int per = (size_t)n * T * d <= comm_.slot_floats ? n : 1;
@@ -1422,7 +1433,10 @@ public:
             // residual / MLP chain stays sequential (proj/src/draft_engine.cpp:112-130)
             for (int i = 0; i < n; ++i) {
                 const LayerDev& L = M.L[g[i]];
-                if (n > 1 && !fuse) {
+                // LayerProbe::h_in is the running state before this layer's residual add
+                // (proj/src/draft_engine.cpp:112-124)
+                if (cap_) grab((*cap_)[g[i]].h_in, W.h, d);
+                if ((n > 1 || cap_) && !fuse) {
                     g_add(W, W.attn + (size_t)i * kChunk * d, d, T);
                 }
                 GemvBatch ub;
@@ -2285,6 +2299,29 @@ public:
         CUDA_OK(cudaStreamSynchronize(stream_));
         CUDA_OK(cudaGetLastError());
         committed_.clear();
+    }
+
+    // forward_chain with every layer's LayerProbe captured (h_in, q, k, v,
+    // attn_out; proj/src/draft_engine.cpp:291-330)
+    void forward_capture(int which, const std::vector<int>& tokens, const std::string& plan_spec,
+                         std::vector<LayerCapture>& out) override {
+        if (tp()) cfg_fail("the similarity probe runs on one GPU");
+        ModelDev& M = which ? base_ : draft_;
+        out.assign(M.c.n_layers, LayerCapture{});
+        cap_ = &out;
+        try {
+            forward_chain(which, tokens, plan_spec, nullptr, nullptr);
+        } catch (...) {
+            cap_ = nullptr;
+            throw;
+        }
+        cap_ = nullptr;
+        const int n = (int)tokens.size(), kvd = M.kvh() * M.c.d_head;
+        for (int l = 0; l < M.c.n_layers; ++l) {
+            out[l].k.resize((size_t)n * kvd);
+            out[l].v.resize((size_t)n * kvd);
+            cache_rows(which, l, 0, n, out[l].k.data(), out[l].v.data());
+        }
     }
 
     int cache_rows(int which, int layer, int row0, int n, float* k, float* v) override {

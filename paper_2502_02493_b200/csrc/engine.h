@@ -92,6 +92,12 @@ struct OutcomeOut {
     std::vector<int> path, tokens;
 };
 
+// One layer's intermediates of a probed pass (LayerProbe + AttnCapture,
+// proj/include/espec/draft_engine.hpp:24-37, model.hpp:67-69): T rows each.
+struct LayerCapture {
+    std::vector<float> h_in, q, k, v, attn_out;
+};
+
 class Engine;
 // tp > 1: this engine is shard `rank` of a tensor-parallel group (one per
 // GPU); link the group with comm_link (one process) or comm_ipc_* (one
@@ -130,6 +136,8 @@ public:
     virtual void forward_tree(int which, const std::vector<int>& prompt, const std::vector<int>& tokens,
                               const std::vector<int>& parents, const std::string& plan, float* logits,
                               float* hidden) = 0;
+    virtual void forward_capture(int which, const std::vector<int>& tokens, const std::string& plan,
+                                 std::vector<LayerCapture>& out) = 0;
     virtual int cache_rows(int which, int layer, int row0, int n, float* k, float* v) = 0;
     virtual int cache_committed(int which) const = 0;
     virtual const std::vector<int>& committed() const = 0;

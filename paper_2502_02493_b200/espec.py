@@ -81,6 +81,20 @@ class _Iter(C.Structure):
                [(n, C.c_float) for n in ("calibrate_ms", "draft_ms", "verify_ms")]
 
 
+class _Report(C.Structure):
+    """espec_report = RunReport's derived metrics (report.hpp:40-57)."""
+    _fields_ = [("n_iterations", C.c_int), ("has_alpha", C.c_int), ("alpha", C.c_double),
+                ("tokens_emitted", C.c_int64), ("mean_accept_len", C.c_double), ("tokens_per_s", C.c_double),
+                ("draft_per_100_s", C.c_double), ("verify_per_100_s", C.c_double),
+                ("calibrate_per_100_s", C.c_double), ("draft_total_per_100_s", C.c_double),
+                ("total_s", C.c_double), ("speedup_vs_vanilla", C.c_double)]
+
+
+class _SimRow(C.Structure):
+    """espec_similarity_row = SimilarityRow (draft_engine.hpp:124-127)."""
+    _fields_ = [("lp_size", C.c_int)] + [(n, C.c_double) for n in ("h", "q", "k", "v", "attn_out")]
+
+
 _lib = None
 
 
@@ -137,6 +151,13 @@ def lib():
         L.espec_verify.argtypes = [V, P(_Tree), P(_Outcome)]
         L.espec_resolve_draft_cache.argtypes = [V, P(_Outcome)]
         L.espec_commit_outcome.argtypes = [V, P(C.c_int32), P(C.c_int), P(_Iter)]
+        L.espec_aggregate.argtypes = [P(_Iter), C.c_int, C.c_double, P(_Report)]
+        L.espec_report_emit.argtypes = [P(_Report), P(_Iter), C.c_int, C.c_char_p, C.c_int, P(C.c_int), C.c_int,
+                                        C.c_int, C.c_int, C.c_char_p, C.c_int, P(C.c_int)]
+        L.espec_model_file_config.argtypes = [C.c_char_p, P(_ModelCfg)]
+        L.espec_load_model_file.argtypes = [V, C.c_int, C.c_char_p]
+        L.espec_save_model_file.argtypes = [V, C.c_int, C.c_char_p]
+        L.espec_probe_similarity.argtypes = [V, P(C.c_int), C.c_int, P(C.c_int32), P(C.c_int), C.c_int, P(_SimRow)]
         _lib = L
     return _lib
 
@@ -333,6 +354,25 @@ class Engine:
         self._check(lib().espec_generate_tokens(self._h, _i(t), len(t), _i(out), C.byref(n_out), traces,
                                                 C.byref(n_it)))
         return list(out[: n_out.value]), [_trace(traces[i]) for i in range(n_it.value)]
+
+    def load_model_file(self, which: int, path: str):
+        """load_model (model_io.cpp:106-190) into the drafter (0) or base (1)."""
+        self._check(lib().espec_load_model_file(self._h, which, os.fsencode(path)))
+
+    def save_model_file(self, which: int, path: str):
+        """save_model (model_io.cpp:76-104) of the drafter (0) or base (1)."""
+        self._check(lib().espec_save_model_file(self._h, which, os.fsencode(path)))
+
+    def probe_similarity(self, lp_sizes: Sequence[int], corpus: Sequence[Sequence[int]]) -> List["SimilarityRow"]:
+        """probe_similarity (draft_engine.cpp:337-357) on the drafter."""
+        lps = np.ascontiguousarray(lp_sizes, np.int32)
+        toks = np.ascontiguousarray([t for seq in corpus for t in seq], np.int32)
+        offs = np.ascontiguousarray(np.cumsum([0] + [len(s) for s in corpus]), np.int32)
+        rows = (_SimRow * max(len(lps), 1))()
+        self._check(lib().espec_probe_similarity(self._h, lps.ctypes.data_as(C.POINTER(C.c_int)), len(lps),
+                                                 _i(toks), offs.ctypes.data_as(C.POINTER(C.c_int)), len(corpus),
+                                                 rows))
+        return [SimilarityRow(r.lp_size, r.h, r.q, r.k, r.v, r.attn_out) for r in rows[: len(lps)]]
 
     def stream(self) -> int:
         """cudaStream_t (as an int) all of this engine's kernels run on."""
@@ -631,6 +671,87 @@ def total_variation(a: dict, b: dict, runs_a: int, runs_b: int) -> float:
     P64 = C.POINTER(C.c_int64)
     return lib().espec_total_variation(_i(pa), ca.ctypes.data_as(P64), len(keys_a), _i(pb), cb.ctypes.data_as(P64),
                                        len(keys_b), n, runs_a, runs_b)
+
+
+@dataclass
+class SimilarityRow:
+    """SimilarityRow (draft_engine.hpp:124-127)."""
+    lp_size: int
+    h: float
+    q: float
+    k: float
+    v: float
+    attn_out: float
+
+
+def similarity_csv(rows: Sequence[SimilarityRow]) -> str:
+    """similarity_csv (draft_engine.cpp:359-370)."""
+    out = "lp_size,h,q,k,v,attnoutput\n"
+    for r in rows:
+        out += f"{r.lp_size},{r.h:.6f},{r.q:.6f},{r.k:.6f},{r.v:.6f},{r.attn_out:.6f}\n"
+    return out
+
+
+@dataclass
+class RunReport:
+    """RunReport's derived metrics (report.hpp:40-57), device seconds."""
+    n_iterations: int
+    has_alpha: bool
+    alpha: float
+    tokens_emitted: int
+    mean_accept_len: float
+    tokens_per_s: float
+    draft_per_100_s: float
+    verify_per_100_s: float
+    calibrate_per_100_s: float
+    draft_total_per_100_s: float
+    total_s: float
+    speedup_vs_vanilla: float
+    _c: object = field(default=None, repr=False, compare=False)
+
+
+def _iters(traces: Sequence[IterationTrace]):
+    arr = (_Iter * max(len(traces), 1))()
+    for i, t in enumerate(traces):
+        arr[i] = _Iter(*(getattr(t, n) for n, _ in _Iter._fields_))
+    return arr
+
+
+def aggregate(traces: Sequence[IterationTrace], vanilla_baseline_s: float) -> RunReport:
+    """aggregate(traces, vanilla_baseline_sim) (report.cpp:51-95) through the C ABI."""
+    r = _Report()
+    st = lib().espec_aggregate(_iters(traces), len(traces), vanilla_baseline_s, C.byref(r))
+    if st:
+        raise EspecError(st, lib().espec_create_error().decode())
+    vals = [getattr(r, n) for n, _ in _Report._fields_]
+    vals[1] = bool(vals[1])
+    return RunReport(*vals, _c=r)
+
+
+def emit_report(report: RunReport, traces: Sequence[IterationTrace], algorithm: str, n: int, widths: Sequence[int],
+                lp_size: int, fmt: str = "json") -> str:
+    """emit_report (report.cpp:97-171): fmt "json" or "csv"."""
+    w = np.ascontiguousarray(widths, np.int32)
+    need = C.c_int(0)
+    cap = 4096 + 512 * len(traces)
+    buf = C.create_string_buffer(cap)
+    st = lib().espec_report_emit(C.byref(report._c), _iters(traces), len(traces), algorithm.encode(), n,
+                                 w.ctypes.data_as(C.POINTER(C.c_int)), len(w), lp_size, 0 if fmt == "json" else 1,
+                                 buf, cap, C.byref(need))
+    if st:
+        raise EspecError(st, lib().espec_create_error().decode())
+    return buf.value.decode()
+
+
+def model_file_config(path: str) -> ModelConfig:
+    """Validate an ESPEC1 file (load_model's checks) and return its config."""
+    c = _ModelCfg()
+    st = lib().espec_model_file_config(os.fsencode(path), C.byref(c))
+    if st:
+        raise EspecError(st, lib().espec_create_error().decode())
+    return ModelConfig(vocab_size=c.vocab_size, d_model=c.d_model, n_layers=c.n_layers, n_heads=c.n_heads,
+                       d_head=c.d_head, d_mlp=c.d_mlp, max_positions=c.max_positions, norm_eps=c.norm_eps,
+                       seed=c.seed, n_kv_heads=c.n_kv_heads, rope_theta=c.rope_theta, tied_head=True)
 
 
 def plan_groups(n_layers: int, lp_size: int) -> str:

@@ -363,6 +363,7 @@ struct Cache {
     KvView view() const {
         KvView v;
         v.pool = pool;
+        v.pool_pages = n_pages;
         v.page_table = table_dev;
         v.page_rows = page_rows;
         v.n_layers = n_layers;
@@ -1111,6 +1112,7 @@ public:
         p.view.anc = staging_.push(anc.data(), T, stream_);
         p.view.tree_base = tree_base;
         p.view.total = C.total();
+        p.view.new_lo = rows.empty() ? 0 : *std::min_element(rows.begin(), rows.end());
         p.tok_idx = staging_.push(tok_idx.data(), T, stream_);
         return p;
     }

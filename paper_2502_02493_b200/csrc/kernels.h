@@ -58,6 +58,7 @@ struct KvView {
     int n_layers = 0, n_kv = 0, dh = 0;
     int dtype = 0;                    // DType
     long long page_elems = 0;         // elements per page (all layers)
+    int pool_pages = 0;               // pages in the pool (tensor-map extent)
     // 64-row pages per attention item (bf16 path). A function of the cache
     // capacity only — never of the pass — so every row's reduction tree is
     // the same in any pass (batch invariance).
@@ -74,6 +75,10 @@ struct PassView {
     const unsigned long long* anc = nullptr;      // tree rows visible: bit i -> row tree_base+i
     int tree_base = 0;
     int total = 0;             // rows stored in the cache during this pass
+    // lowest cache row this pass writes (0 = unknown): K/V pages wholly below
+    // it are final before the pass starts (attention may load them before
+    // its dependency wait)
+    int new_lo = 0;
 };
 
 struct GemvProblem {

@@ -146,6 +146,7 @@ static espec_status espec_bench_attn_impl(int T, int n_heads, int n_kv, int dh, 
     kv.dh = dh;
     kv.dtype = DT_BF16;
     kv.page_elems = page_elems;
+    kv.pool_pages = n_pages;
     {
         const int cap = (ctx + 64 + page_rows - 1) / page_rows * page_rows;  // as Cache::view()
         kv.attn_ppi = attn_pages_per_item(cap);
@@ -158,6 +159,7 @@ static espec_status espec_bench_attn_impl(int T, int n_heads, int n_kv, int dh, 
     pv.anc = anc;
     pv.tree_base = ctx;
     pv.total = ctx;
+    pv.new_lo = ctx - T;  // as in the engine: the pass's own rows are the last T
     AttnBatch b;
     for (int p = 0; p < nprob; ++p) {
         b.p[p].q = q + (size_t)p * 16 * n_heads * dh;

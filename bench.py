@@ -392,11 +392,9 @@ def main():
         return dict(ms=ms, emitted=emitted, traces=traces, launches=launches, site=site_stats,
                     clocks=sampler.summary() if sampler else None)
 
-    # main arm: EasySpec. Roofline site: the base verify pass — one decode
-    # megakernel launch (80 layers, T = n+1 rows) — or, with ESPEC_MK=0, the
-    # base gate/up GEMV (the largest per-kernel launch)
-    mk = os.environ.get("ESPEC_MK", "0") != "0"
-    site_kind = 6 if mk else 3
+    # main arm: EasySpec. Roofline site: the base gate/up GEMV (the largest
+    # launch of the step)
+    site_kind = 3
     # headline: no per-launch events inside the timed region (they would
     # break PDL overlap of the timed kernel site); the roofline comes from a
     # separate pass of the same arm below
@@ -430,7 +428,7 @@ def main():
     gu_shape = f"{wl['base']['d_model']}x{2 * wl['base']['d_mlp'] // ws}"
     traffic, traffic_src = None, None
     tp = os.path.join(ROOT, "profiles", "roofline_traffic.json")
-    if os.path.exists(tp) and not mk and ws == 1:
+    if os.path.exists(tp) and ws == 1:
         try:  # ncu --set full dram__bytes of this workload's gate/up launch
             ent = json.load(open(tp)).get("workloads", {}).get(args.workload)
             if ent and ent.get("shape") == gu_shape:
@@ -509,9 +507,7 @@ def main():
                                 "speedup_vs_vanilla": (proj_tok_s / arms["vanilla"]["tokens_per_s"])
                                 if "vanilla" in arms else None,
                                 "note": "projection, tokens/iteration = n*alpha+1 (proj/src/cli.cpp:403)"},
-            "roofline": {"kernel": "decode_mk_kernel (one launch = base verify pass: all layers x [QKV, attention, O, "
-                                   "gate/up, down], T=n+1 rows; bytes = bf16 weights + KV + activations)" if mk else
-                                   f"sgemv_kernel<8,EPI_SILU> (stream-K bf16 GEMV, base gate/up {gu_shape}, "
+            "roofline": {"kernel": f"sgemv_kernel<8,EPI_SILU> (stream-K bf16 GEMV, base gate/up {gu_shape}, "
                                    f"T={n + 1})",
                          "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": (achieved / hbm) if achieved else None, "traffic": traffic,

@@ -578,9 +578,6 @@ public:
         CUDA_OK(cudaSetDevice(device));
         if (const char* e = std::getenv("ESPEC_PDL")) set_pdl(std::atoi(e) != 0);
         CUDA_OK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
-        CUDA_OK(cudaMalloc(&mk_counter_, sizeof(unsigned long long)));
-        CUDA_OK(cudaMemset(mk_counter_, 0, sizeof(unsigned long long)));
-        if (const char* e = std::getenv("ESPEC_MK")) mk_mode_ = std::atoi(e);
         if (const char* e = std::getenv("ESPEC_WIDE_DRAFT")) wide_draft_ = std::atoi(e);
         if (const char* e = std::getenv("ESPEC_FUSE_ADDS")) fuse_adds_ = std::atoi(e);
         if (const char* e = std::getenv("ESPEC_B16_ACTS")) b16_acts_ = std::atoi(e);
@@ -659,8 +656,6 @@ public:
         if (comm_.ticket) cudaFree(comm_.ticket);
         for (auto& e : ev_) cudaEventDestroy(e);
         for (auto& e : site_ev_) cudaEventDestroy(e);
-        mk_clear();
-        if (mk_counter_) cudaFree(mk_counter_);
         cudaStreamDestroy(stream_);
     }
 
@@ -720,11 +715,9 @@ public:
         draft_.release();
         draft_.allocate(true, &base_);
         draft_allocated_ = true;
-        mk_clear();
     }
 
     void init_weights_seeded(int which, uint64_t seed, bool parity) override {
-        mk_clear();
         ModelDev& M = which ? base_ : draft_;
         M.c.seed = seed;
         ensure_allocated(which);
@@ -1202,14 +1195,7 @@ public:
     }
 
     // forward_sequential / forward_fuzzy (proj/src/draft_engine.cpp:35-133).
-    // Decode-sized single-GPU bf16 passes run as ONE megakernel launch
-    // (decode_mk.cu) executing the op list forward_body records; the op list
-    // depends only on (model, plan, T), so it is built once and cached.
     void forward(ModelDev& M, Cache& C, Workspace& W, const LayerPlan* plan, const Pass& ps) {
-        if (mk_usable(M, ps.T) && !cap_) {
-            forward_mk(M, C, W, plan, ps);
-            return;
-        }
         forward_body(M, C, W, plan, ps);
     }
     // decode passes whose attention takes the bf16 item path: its output (and
@@ -1218,111 +1204,11 @@ public:
         return M.c.weight_dtype == DT_BF16 && M.c.kv_dtype == DT_BF16 && T <= 16 &&
                (M.c.d_head == 64 || M.c.d_head == 128) && b16_acts_;
     }
-    bool mk_usable(const ModelDev& M, int T) const {
-        return mk_mode_ && !tp() && T >= 1 && T <= mk_max_rows() && M.c.weight_dtype == DT_BF16 &&
-               M.c.kv_dtype == DT_BF16 && (M.c.d_head == 64 || M.c.d_head == 128);
-    }
     std::vector<LayerCapture>* cap_ = nullptr;  // forward_capture in progress
-    void mk_clear() {
-        for (auto& kv : mk_progs_)
-            if (kv.second.dev) cudaFree(kv.second.dev);
-        mk_progs_.clear();
-    }
-    void forward_mk(ModelDev& M, Cache& C, Workspace& W, const LayerPlan* plan, const Pass& ps) {
-        const std::string key =
-            std::string(&M == &base_ ? "base" : "draft") + "|" + (plan ? format_plan(*plan) : "-") + "|" + std::to_string(ps.T);
-        auto it = mk_progs_.find(key);
-        if (it == mk_progs_.end()) {
-            MkProg P;
-            mk_rec_ = &P;
-            try {
-                forward_body(M, C, W, plan, ps);
-            } catch (...) {
-                mk_rec_ = nullptr;
-                throw;
-            }
-            mk_rec_ = nullptr;
-            const unsigned long long G = (unsigned long long)mk_grid();
-            unsigned long long acc = 0;
-            for (auto& op : P.ops) {
-                op.arrivals = mk_op_arrivals(op.type);
-                acc += G * (unsigned long long)op.arrivals;
-                op.target = acc;
-            }
-            P.arrivals = acc;
-            const size_t b0 = sizeof(MkOp) * P.ops.size(), b1 = sizeof(GemvProblem) * P.probs.size(),
-                         b2 = sizeof(AttnProblem) * P.aprobs.size();
-            const size_t o1 = (b0 + 255) / 256 * 256, o2 = o1 + (b1 + 255) / 256 * 256;
-            CUDA_OK(cudaMalloc(&P.dev, o2 + b2 + 16));
-            char* d = static_cast<char*>(P.dev);
-            CUDA_OK(cudaMemcpy(d, P.ops.data(), b0, cudaMemcpyHostToDevice));
-            if (b1) CUDA_OK(cudaMemcpy(d + o1, P.probs.data(), b1, cudaMemcpyHostToDevice));
-            if (b2) CUDA_OK(cudaMemcpy(d + o2, P.aprobs.data(), b2, cudaMemcpyHostToDevice));
-            P.d_ops = reinterpret_cast<MkOp*>(d);
-            P.d_probs = reinterpret_cast<GemvProblem*>(d + o1);
-            P.d_aprobs = reinterpret_cast<AttnProblem*>(d + o2);
-            it = mk_progs_.emplace(key, std::move(P)).first;
-        }
-        MkProg& P = it->second;
-        MkArgs a;
-        a.ops = P.d_ops;
-        a.n_ops = (int)P.ops.size();
-        a.probs = P.d_probs;
-        a.aprobs = P.d_aprobs;
-        a.pass = ps.view;
-        a.kv = C.view();
-        a.tok_arena = arena_;
-        a.tok_idx = ps.tok_idx;
-        a.counter = mk_counter_;
-        a.base = mk_base_;
-        const double bytes =
-            P.weight_bytes + (double)M.c.n_layers * 2.0 * ps.view.total * M.kvdim() * dsize(M.c.kv_dtype);
-        static const char* trace_path = std::getenv("ESPEC_MK_TRACE");
-        unsigned long long* tr = nullptr;
-        const size_t tr_n = P.ops.size() * (size_t)mk_grid() * 8;
-        if (trace_path) {
-            CUDA_OK(cudaMalloc(&tr, sizeof(unsigned long long) * tr_n));
-            CUDA_OK(cudaMemsetAsync(tr, 0, sizeof(unsigned long long) * tr_n, stream_));
-            a.trace = tr;
-        }
-        site(M, 6, bytes, [&] { CUDA_OK(launch_decode_mk(a, stream_)); });
-        mk_base_ += P.arrivals;
-        ++launches_;
-        if (trace_path) {
-            // debug timeline: <path>.<model>.T<T>.txt, one line per op:
-            // type epi units then grid x {start, staged, done, arrive} (ns)
-            std::vector<unsigned long long> h(tr_n);
-            CUDA_OK(cudaMemcpyAsync(h.data(), tr, sizeof(unsigned long long) * tr_n, cudaMemcpyDeviceToHost, stream_));
-            CUDA_OK(cudaStreamSynchronize(stream_));
-            cudaFree(tr);
-            const std::string fn = std::string(trace_path) + "." + (&M == &base_ ? "base" : "draft") + ".T" +
-                                   std::to_string(ps.T) + ".txt";
-            if (FILE* f = std::fopen(fn.c_str(), "w")) {
-                const int G = mk_grid();
-                for (size_t k = 0; k < P.ops.size(); ++k) {
-                    std::fprintf(f, "%d %d %d", P.ops[k].type, P.ops[k].epi, P.ops[k].units);
-                    for (int c = 0; c < G; ++c)
-                        for (int e = 0; e < 8; ++e) std::fprintf(f, " %llu", h[(k * G + c) * 8 + e]);
-                    std::fprintf(f, "\n");
-                }
-                std::fclose(f);
-            }
-        }
-    }
 
-    // ---- launch-or-record wrappers (forward_body under forward_mk records ops)
+    // ---- launch wrappers
     void g_gemv(ModelDev& M, int kind, double bytes, int epi, const GemvBatch& b, int n, int T, const Pass& ps,
                 const KvView& kv) {
-        if (mk_rec_) {
-            MkOp op;
-            mk_plan_gemv(op, b.p[0].K, b.p[0].ldw, n);
-            op.epi = epi;
-            op.prob0 = (int)mk_rec_->probs.size();
-            for (int i = 0; i < n; ++i) mk_rec_->probs.push_back(b.p[i]);
-            mk_rec_->ops.push_back(op);
-            mk_rec_->weight_bytes += bytes;
-            return;
-        }
         set_sgemv_wide(&M == &draft_ && wide_draft_);
         site(M, kind, bytes, [&] { launch_gemv(epi, M.c.weight_dtype, b, n, T, ps.view, kv, stream_, &pool_); });
         set_sgemv_wide(false);
@@ -1330,32 +1216,10 @@ public:
     }
     void g_embed(ModelDev& M, Workspace& W, const Pass& ps) {
         const int d = M.c.d_model;
-        if (mk_rec_) {
-            MkOp op;
-            op.type = MK_EMBED;
-            op.emb = M.emb;
-            op.h = W.h;
-            op.stats = W.stats;
-            op.d = d;
-            op.stat_tiles = (d + kStatTile - 1) / kStatTile;
-            mk_rec_->ops.push_back(op);
-            return;
-        }
         launch_embed(M.c.weight_dtype, M.emb, d, arena_, ps.tok_idx, ps.T, W.h, W.stats, stream_);
         ++launches_;
     }
     void g_add(Workspace& W, const float* a, int d, int T) {
-        if (mk_rec_) {
-            MkOp op;
-            op.type = MK_ADD;
-            op.h = W.h;
-            op.a = a;
-            op.stats = W.stats;
-            op.d = d;
-            op.stat_tiles = (d + kStatTile - 1) / kStatTile;
-            mk_rec_->ops.push_back(op);
-            return;
-        }
         launch_add_stats(W.h, a, d, T, W.stats, stream_);
         ++launches_;
     }
@@ -1477,21 +1341,9 @@ public:
                 a.tickets = W.attn_tickets + (size_t)W.attn_ticket_slot * i;
                 ab.p[i] = a;
             }
-            if (mk_rec_) {
-                MkOp op;
-                op.type = MK_ATTN;
-                op.nprob = (int)g.size();
-                op.prob0 = (int)mk_rec_->aprobs.size();
-                op.n_heads = M.qh();
-                op.G = M.qh() / M.kvh();
-                op.dh = M.c.d_head;
-                for (size_t i = 0; i < g.size(); ++i) mk_rec_->aprobs.push_back(ab.p[i]);
-                mk_rec_->ops.push_back(op);
-                continue;
-            }
             const double kvb = (double)g.size() * 2.0 * ps.view.total * M.kvdim() * dsize(M.c.kv_dtype);
             site(M, 1, kvb, [&] { launch_attention(ab, (int)g.size(), M.qh(), v, kv, stream_); });
-            ++launches_;
+            launches_ += attention_launches(v, kv);
         }
     }
 
@@ -2455,27 +2307,9 @@ private:
     int site_which_ = -1, site_kind_ = -1, site_n_ = 0;
     double site_ms_ = 0, site_bytes_ = 0;
     long long h2d_bytes_ = 0, d2h_bytes_ = 0;
-    // decode megakernel: programs cached per (model, plan, T); the recording
-    // target while forward() builds one; the device arrival counter
-    struct MkProg {
-        std::vector<MkOp> ops;
-        std::vector<GemvProblem> probs;
-        std::vector<AttnProblem> aprobs;
-        void* dev = nullptr;  // ops | probs | aprobs
-        MkOp* d_ops = nullptr;
-        GemvProblem* d_probs = nullptr;
-        AttnProblem* d_aprobs = nullptr;
-        unsigned long long arrivals = 0;
-        double weight_bytes = 0;
-    };
-    std::map<std::string, MkProg> mk_progs_;
-    MkProg* mk_rec_ = nullptr;
-    unsigned long long* mk_counter_ = nullptr;
-    unsigned long long mk_base_ = 0;
     int wide_draft_ = 1;  // ESPEC_WIDE_DRAFT=0: drafter on the (K, N)-only GEMV plan too
     int fuse_adds_ = 1;   // ESPEC_FUSE_ADDS=0: fuzzy-group residual adds as separate kernels
     int b16_acts_ = 1;    // ESPEC_B16_ACTS=0: attention / SiLU outputs in fp32
-    int mk_mode_ = 0;  // ESPEC_MK=1 enables the decode megakernel (measured slower than the per-kernel path today)
 };
 
 std::unique_ptr<Engine> make_engine(const ModelCfg& base, const ModelCfg& draft, const RunCfg& run, int device,

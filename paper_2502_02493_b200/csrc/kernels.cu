@@ -9,19 +9,15 @@
 // from row sum-of-squares partials (one per 32 columns), residual add + row
 // stats, SiLU over [gate16 | up16] packed groups, RoPE + paged-KV write,
 // argmax. Reduction order never depends on T (batch invariance).
-#include <cuda.h>
-#include <cudaTypedefs.h>
-
 #include <cstdio>
 #include <cstdlib>
 #include <type_traits>
-#include <mutex>
 #include <vector>
 
 #include "common.cuh"
 #include "kernels.h"
 #include "ptx.cuh"
-#include "attn_mma.cuh"
+#include "attn_common.cuh"
 
 namespace espec_dev {
 
@@ -513,7 +509,9 @@ size_t attn_ws_floats(int T, int n_heads, int dh, int max_rows) {
     const size_t splits = (size_t)(max_rows + kAttnRows - 1) / kAttnRows;
     // covers both layouts: fp32 [split][n_kv][T*G][dh+2] and bf16 mma
     // [chunk][n_kv * mtiles][16][dh+4]
-    return splits * (size_t)(T * n_heads + 16 * n_heads) * (dh + 4);
+    // tcgen05 kernel: [chunk][n_kv * pair groups][128][dh + 4], at most
+    // T * H + 128 * H rows per chunk (chunks <= splits)
+    return splits * (size_t)(T * n_heads + 128 * n_heads) * (dh + 4);
 }
 int attn_pages_per_item(int cap) {
     static const int forced = [] {
@@ -521,9 +519,10 @@ int attn_pages_per_item(int cap) {
         return e ? std::atoi(e) : 0;
     }();
     if (forced > 0) return forced;
-    // a chunk of 4-8 pages per CTA: few enough chunks that the fixed-order
-    // cross-chunk combine stays short, enough CTAs to fill the SMs at long context
-    return cap <= 4096 ? 4 : cap <= 16384 ? 8 : 16;
+    // tcgen05 attention (attn_tc.cu), measured (profiles/r2_attn_tc.txt): 2 pages
+    // per CTA at short context, 4-8 as the context grows (fewer chunk partials
+    // for the combine kernel, pages processed two per softmax step)
+    return cap <= 2048 ? 2 : cap <= 4096 ? 4 : cap <= 32768 ? 8 : 16;
 }
 
 size_t attn_tickets(int T, int n_heads, int n_kv) {
@@ -533,55 +532,11 @@ size_t attn_tickets(int T, int n_heads, int n_kv) {
 }
 
 struct AttnLaunch {
-    CUtensorMap kvmap;  // bf16 whole-head kernel: 4-D swizzled view of the KV pool (kv_tensor_map)
     AttnBatch b;
     PassView pass;
     KvView kv;
     int n_heads, G, splits, pblocks;
-    unsigned long long* trace = nullptr;  // diagnostic timeline (ESPEC_ATTN_TRACE) or nullptr
 };
-
-// 4-D tensor map of a bf16 KV pool for attn_mma_kernel's page loads:
-// {dh, 64 rows, (layer, k|v, kv head), page}, box {64, 64, 1, 1}, 128-byte
-// swizzle. Encoded once per pool (cuTensorMapEncodeTiled through the
-// runtime's driver entry point, no -lcuda).
-static void kv_tensor_map(CUtensorMap& m, const KvView& kv) {
-    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
-        void* fn = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess)
-            fn = nullptr;
-        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-    }();
-    if (!encode) dev_fail(DEV_ERR_CUDA, "attention: cuTensorMapEncodeTiled is unavailable");
-    if (kv.pool_pages <= 0) dev_fail(DEV_ERR_CUDA, "attention: KvView.pool_pages is not set");
-    struct Entry {
-        const void* pool;
-        long long page_elems;
-        int n_layers, n_kv, dh, pages;
-        CUtensorMap map;
-    };
-    static std::mutex mu;
-    static std::vector<Entry> cache;
-    std::lock_guard<std::mutex> lk(mu);
-    for (const Entry& e : cache)
-        if (e.pool == kv.pool && e.page_elems == kv.page_elems && e.n_layers == kv.n_layers && e.n_kv == kv.n_kv &&
-            e.dh == kv.dh && e.pages == kv.pool_pages) {
-            m = e.map;
-            return;
-        }
-    const cuuint64_t dims[4] = {(cuuint64_t)kv.dh, 64, (cuuint64_t)kv.n_layers * 2 * kv.n_kv,
-                                (cuuint64_t)kv.pool_pages};
-    const cuuint64_t strides[3] = {(cuuint64_t)kv.dh * 2, (cuuint64_t)64 * kv.dh * 2, (cuuint64_t)kv.page_elems * 2};
-    const cuuint32_t box[4] = {64, 64, 1, 1};
-    const cuuint32_t estr[4] = {1, 1, 1, 1};
-    const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, kv.pool, dims, strides, box, estr,
-                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) dev_fail(DEV_ERR_CUDA, "attention: cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
-    cache.push_back({kv.pool, kv.page_elems, kv.n_layers, kv.n_kv, kv.dh, kv.pool_pages, m});
-}
 
 template <typename KT>
 __global__ void __launch_bounds__(kAttnThreads) attn_kernel(const __grid_constant__ AttnLaunch L) {
@@ -730,190 +685,13 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(const __grid_constan
 // combine through a split workspace, last CTA in fixed order.
 // ---------------------------------------------------------------------------
 
-// Whole-kv-head CTA: one CTA per (chunk of kv.attn_ppi pages, kv head, group
-// of <= 3 m-tiles); every m-tile of the group shares the CTA's page loads (no
-// replicated K/V traffic up to 48 query pairs, e.g. T = 6 at G = 8). Warps
-// 4 * mtl + kq compute m-tile mtl over key quarter kq of every page
-// (attn_warp_page); the chunk's K/V pages stream through a kAttnStages-deep
-// TMA ring refilled after each page. Pages wholly below the pass's first
-// written row are issued before griddepcontrol.wait: they were written by
-// kernels that completed before this kernel's predecessor started (every
-// kernel in the chain waits before it writes), so their loads overlap the QKV
-// GEMV's tail. Rows are bit-identical to attn_mma_item's (same per-warp
-// arithmetic, same chunking). 3 m-tiles = 384 threads keeps the per-warp
-// state (Q fragments + P V accumulators, ~170 registers) spill-free.
-constexpr int kAttnStages = 6;
-constexpr int kAttnCtaTiles = 3;
-constexpr int kAttnCtaMaxChunks = 64;
-constexpr int kAttnMaxPpi = 64;
-template <int DH>
-__host__ __device__ constexpr int attn_cta_group_bytes() {
-    return (attn_tile_scratch_floats<DH>() > attn_combine_scratch_floats(kAttnCtaMaxChunks)
-                ? attn_tile_scratch_floats<DH>()
-                : attn_combine_scratch_floats(kAttnCtaMaxChunks)) * 4;
+static bool attn_tc_path(const KvView& kv) {
+    return kv.dtype == DT_BF16 && kv.page_rows == 64 && (kv.dh == 64 || kv.dh == 128);
 }
-template <int DH>
-__host__ __device__ constexpr int attn_cta_bar_offset(int mtc) {
-    const int ring = kAttnStages * 2 * 64 * DH * 2;
-    const int scr = mtc * attn_cta_group_bytes<DH>();
-    return ((ring > scr ? ring : scr) + 127) / 128 * 128;
-}
-
-template <int DH>
-__global__ void __launch_bounds__(kAttnCtaTiles * 128, 1) attn_mma_kernel(const __grid_constant__ AttnLaunch L) {
-    extern __shared__ __align__(128) unsigned char smraw[];
-    __shared__ unsigned s_last;
-    constexpr int S = kAttnStages;
-    constexpr int PS = DH + 4;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int NC = blockDim.x, mtc = NC / 128;  // m-tiles in this CTA
-    const AttnProblem& A = L.b.p[blockIdx.z];
-    const PassView& pass = L.pass;
-    const KvView& kv = L.kv;
-    const int G = L.G, H = L.n_heads, P = pass.T * G, n_kv = kv.n_kv;
-    const int hk = blockIdx.y % n_kv, mg = blockIdx.y / n_kv;
-    const int mtiles = (P + 15) / 16, ny = n_kv * mtiles;
-    const int bx = blockIdx.x, nchunks = gridDim.x;
-    const int pg0 = bx * kv.attn_ppi, pg1 = min((pass.total + 63) / 64, pg0 + kv.attn_ppi);
-    // the swizzled TMA boxes need 1024-byte aligned destinations
-    unsigned char* sm = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);
-    __nv_bfloat16* ring = reinterpret_cast<__nv_bfloat16*>(sm);
-    uint64_t* full = reinterpret_cast<uint64_t*>(sm + attn_cta_bar_offset<DH>(mtc));  // [S][K|V]
-    unsigned long long* tr =
-        L.trace ? L.trace + (((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 8 : nullptr;
-    auto kbuf = [&](int st) { return ring + (size_t)(st * 2) * 64 * DH; };
-    auto vbuf = [&](int st) { return ring + (size_t)(st * 2 + 1) * 64 * DH; };
-    // physical pages of the chunk, looked up once (the refills then issue
-    // without a dependent global load in warp 0's path)
-    int* s_page = reinterpret_cast<int*>(full + 2 * S);  // [kAttnMaxPpi]
-    auto issue = [&](int pg, int page) {  // tid 0 only
-        const int st = (pg - pg0) % S;
-        attn_issue_page_tmap<DH>(kv, &L.kvmap, A.layer, hk, page, kbuf(st), vbuf(st), &full[2 * st],
-                                 &full[2 * st + 1]);
-    };
-    auto stable = [&](int pg) { return (pg + 1) * 64 <= pass.new_lo; };
-    if (tr && tid == 0) atomicMax(tr, gtimer());
-    if (tid == 0) {
-        for (int i = 0; i < 2 * S; ++i) mbar_init(&full[i], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int pg = pg0; pg < pg1 && pg < pg0 + S; ++pg)
-            if (stable(pg)) issue(pg, kv.page_table[pg]);
-    }
-    pdl_wait();
-    if (tr && tid == 0) atomicMax(tr + 1, gtimer());
-    pdl_trigger();
-    if (tid < pg1 - pg0) s_page[tid] = kv.page_table[pg0 + tid];
-    if (tid == 0)
-        for (int pg = pg0; pg < pg1 && pg < pg0 + S; ++pg)
-            if (!stable(pg)) issue(pg, kv.page_table[pg]);
-    const int mtl = warp >> 2, kq = warp & 3;
-    const int mt = mg * kAttnCtaTiles + mtl;  // this warp's m-tile
-    AttnWarp<DH> W;
-    attn_warp_init<DH>(W, A, pass, H, G, hk, mt, lane);
-    named_bar(1, NC);  // barriers initialised before anyone waits on them
-    // steps of two pages; the two stages of a step are refilled after it
-    for (int pg = pg0; pg < pg1; pg += 2) {
-        const int i = pg - pg0;
-        if (tr && i == 0 && tid == 0) {
-            mbar_wait(&full[0], 0);
-            atomicMax(tr + 2, gtimer());
-        }
-        const int st[2] = {i % S, (i + 1) % S};
-        const __nv_bfloat16* const Ks[2] = {kbuf(st[0]), kbuf(st[1])};
-        const __nv_bfloat16* const Vs[2] = {vbuf(st[0]), vbuf(st[1])};
-        uint64_t* const mk[2] = {&full[2 * st[0]], &full[2 * st[1]]};
-        uint64_t* const mv[2] = {&full[2 * st[0] + 1], &full[2 * st[1] + 1]};
-        const uint32_t ph[2] = {(uint32_t)(i / S) & 1u, (uint32_t)((i + 1) / S) & 1u};
-        const int j0[2] = {pg * 64 + kq * 16, (pg + 1) * 64 + kq * 16};
-        attn_warp_step<DH, true>(W, Ks, Vs, mk, mv, ph, min(2, pg1 - pg), pass, P, j0, kq, lane);
-        named_bar(1, NC);  // both stages consumed by every warp (and s_page written)
-        if (tid == 0) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            for (int q = pg + S; q < pg1 && q < pg + S + 2; ++q) issue(q, s_page[q - pg0]);
-        }
-    }
-    if (tr && lane == 0) atomicMax(tr + 3, gtimer());
-    // the ring is combine scratch from here on (every issued page was consumed:
-    // a page always holds keys 0..15 of the kq = 0 warps)
-    float* scr = reinterpret_cast<float*>(sm + (size_t)mtl * attn_cta_group_bytes<DH>());
-    const int t = tid & 127;
-    const bool live = mt < mtiles;
-    if (live)
-        attn_tile_finish<DH>(W, scr, t, 2 + mtl, A, H, G, hk, mt, P, nchunks,
-                             A.ws + (((size_t)bx * ny + mt * n_kv + hk) * 16) * PS);
-    if (nchunks == 1) return;
-    // the last CTA of this (kv head, m-tile group) combines the chunks in order
-    // (the barrier orders every thread's partial stores before thread 0's
-    // acq_rel ticket, as in attn_mma_item)
-    named_bar(1, NC);
-    if (tr && tid == 0) atomicMax(tr + 4, gtimer());
-    if (tid == 0) {
-        unsigned* ticket = A.tickets + blockIdx.y;
-        unsigned tk;
-        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(tk) : "l"(ticket) : "memory");
-        s_last = (tk == (unsigned)nchunks - 1) ? 1u : 0u;
-        if (s_last) *ticket = 0u;
-    }
-    named_bar(1, NC);
-    if (!s_last || !live) return;
-    attn_tile_combine<DH>(scr, t, 2 + mtl, A, H, G, hk, mt, P, nchunks, A.ws + ((size_t)(mt * n_kv + hk) * 16) * PS,
-                          (size_t)ny * 16 * PS);
-    if (tr && tid == 0) atomicMax(tr + 5, gtimer());
-}
-
-template <int DH>
-static void attn_mma_launch(const AttnLaunch& L, int nprob, cudaStream_t s) {
-    const int splits = (L.pass.total + 63) / 64;
-    const int chunks = (splits + L.kv.attn_ppi - 1) / L.kv.attn_ppi;
-    if (chunks > kAttnCtaMaxChunks)
-        dev_fail(DEV_ERR_CUDA, "attention: context of " + std::to_string(L.pass.total) + " rows exceeds the " +
-                                   std::to_string(kAttnCtaMaxChunks * L.kv.attn_ppi * 64) +
-                                   "-row split-combine limit of this cache capacity");
-    const int mtiles = (L.pass.T * L.G + 15) / 16;
-    const int mtc = std::min(kAttnCtaTiles, mtiles), mgroups = (mtiles + kAttnCtaTiles - 1) / kAttnCtaTiles;
-    dim3 grid(chunks, L.kv.n_kv * mgroups, nprob);
-    if (L.kv.attn_ppi > kAttnMaxPpi) dev_fail(DEV_ERR_CUDA, "attention: more than 64 pages per chunk");
-    const size_t smem = 1024 + attn_cta_bar_offset<DH>(mtc) + 2 * kAttnStages * 8 + 4 * kAttnMaxPpi;
-    static unsigned long long configured = 0;
-    ensure_smem((const void*)attn_mma_kernel<DH>,
-                1024 + attn_cta_bar_offset<DH>(kAttnCtaTiles) + 2 * kAttnStages * 8 + 4 * kAttnMaxPpi, configured);
-    // diagnostic: ESPEC_ATTN_TRACE=T,n traces the n-th launch with T pass rows (per CTA, %globaltimer
-    // at 0 start, 1 past griddepcontrol.wait, 2 first K page, 3 pages done,
-    // 4 partial written, 5 combine done) into gpurun_out/attn_trace.txt
-    static int tT = -1, tn = -1;
-    static bool parsed = false;
-    if (!parsed) {
-        parsed = true;
-        if (const char* e = std::getenv("ESPEC_ATTN_TRACE")) std::sscanf(e, "%d,%d", &tT, &tn);
-    }
-    static unsigned long long* tbuf = nullptr;
-    static int seen = 0;
-    const size_t nblk = (size_t)grid.x * grid.y * grid.z;
-    AttnLaunch Lt = L;
-    kv_tensor_map(Lt.kvmap, L.kv);
-    bool traced = false;
-    if (tn >= 0 && L.pass.T == tT && seen++ == tn && nblk <= 4096) {
-        if (!tbuf) CK(cudaMalloc(&tbuf, sizeof(unsigned long long) * 8 * 4096));
-        CK(cudaMemset(tbuf, 0, sizeof(unsigned long long) * 8 * 4096));
-        CK(cudaDeviceSynchronize());
-        Lt.trace = tbuf;
-        traced = true;
-    }
-    CK(launch_pdl(attn_mma_kernel<DH>, grid, dim3(128 * mtc), smem, s, Lt));
-    if (traced) {
-        std::vector<unsigned long long> h(8 * nblk);
-        CK(cudaStreamSynchronize(s));
-        CK(cudaMemcpy(h.data(), tbuf, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost));
-        if (FILE* f = std::fopen("gpurun_out/attn_trace.txt", "w")) {
-            std::fprintf(f, "grid %d %d %d T %d total %d ppi %d\n", grid.x, grid.y, grid.z, L.pass.T, L.pass.total,
-                         L.kv.attn_ppi);
-            for (size_t b = 0; b < nblk; ++b) {
-                for (int e = 0; e < 8; ++e) std::fprintf(f, " %llu", h[b * 8 + e]);
-                std::fprintf(f, "\n");
-            }
-            std::fclose(f);
-        }
-    }
+int attention_launches(const PassView& pass, const KvView& kv) {
+    if (!attn_tc_path(kv)) return 1;
+    const int pages = (pass.total + 63) / 64;
+    return (pages + kv.attn_ppi - 1) / kv.attn_ppi > 1 ? 2 : 1;
 }
 
 void launch_attention(const AttnBatch& b, int nprob, int n_heads, const PassView& pass, const KvView& kv,
@@ -930,9 +708,8 @@ void launch_attention(const AttnBatch& b, int nprob, int n_heads, const PassView
     const size_t smem = sizeof(float) * ((size_t)(kAttnPairs + kAttnRows) * (kv.dh + 1) + kAttnPairs * kAttnRows);
     static unsigned long long configured[2] = {0, 0};
     dim3 grid(L.splits, kv.n_kv * L.pblocks, nprob);
-    if (kv.dtype == DT_BF16 && kv.page_rows == 64 && (kv.dh == 64 || kv.dh == 128)) {
-        if (kv.dh == 128) attn_mma_launch<128>(L, nprob, s);
-        else attn_mma_launch<64>(L, nprob, s);
+    if (attn_tc_path(kv)) {
+        launch_attention_tc(b, nprob, n_heads, pass, kv, s);
     } else if (kv.dtype == DT_BF16) {
         ensure_smem((const void*)attn_kernel<__nv_bfloat16>, 200 * 1024, configured[1]);
         CK(launch_pdl(attn_kernel<__nv_bfloat16>, grid, dim3(kAttnThreads), smem, s, L));

@@ -214,6 +214,12 @@ int attn_pages_per_item(int capacity_rows);
 size_t attn_tickets(int T, int n_heads, int n_kv);
 void launch_attention(const AttnBatch& b, int nprob, int n_heads, const PassView& pass, const KvView& kv,
                       cudaStream_t s);
+// bf16 paged KV, 64-row pages, d_head 64 / 128: the tcgen05 kernel (attn_tc.cu)
+void launch_attention_tc(const AttnBatch& b, int nprob, int n_heads, const PassView& pass, const KvView& kv,
+                         cudaStream_t s);
+// kernels one launch_attention call issues (the tcgen05 path adds a combine
+// kernel when the context spans more than one chunk)
+int attention_launches(const PassView& pass, const KvView& kv);
 
 // Copy cache rows src[i] -> dst[i] for every layer (commit_path compaction).
 void launch_kv_move(const KvView& kv, const int* src, const int* dst, int n, cudaStream_t s);
@@ -354,44 +360,6 @@ struct GatherColsArgs {
 void launch_allgather_cols(CommView& c, const GatherColsArgs& a, cudaStream_t s);
 // vocab-parallel argmax: (val, idx) per row from every rank -> first maximum
 void launch_allgather_argmax(CommView& c, int T, const float* val, const int* idx, int* tok_out, cudaStream_t s);
-
-// ---- decode megakernel (decode_mk.cu): one persistent launch per decode pass
-enum MkOpType : int { MK_EMBED = 0, MK_GEMV = 1, MK_ATTN = 2, MK_ADD = 3 };
-struct MkOp {
-    int type = 0, epi = 0, nprob = 0, prob0 = 0;
-    // GEMV: the stream-K plan of sgemv_plan (identical units and reduction order)
-    int KT = 0, kcb = 0, nK = 0, ngroups = 0, units = 0, xld = 0;
-    int rotate = 0;                  // rotated unit order (split-K ops)
-    int arrivals = 0;                // arrivals per CTA when the op completes (1)
-    unsigned long long target = 0;   // cumulative arrivals (launch-relative) at completion
-    // ATTN: AttnProblem[prob0 .. prob0+nprob)
-    int n_heads = 0, G = 0, dh = 0;
-    // EMBED (h = emb[tok]) / ADD (h += a); both write row stats
-    const void* emb = nullptr;
-    float* h = nullptr;
-    const float* a = nullptr;
-    float* stats = nullptr;
-    int d = 0, stat_tiles = 0;
-};
-struct MkArgs {
-    const MkOp* ops = nullptr;
-    int n_ops = 0;
-    const GemvProblem* probs = nullptr;
-    const AttnProblem* aprobs = nullptr;
-    PassView pass;
-    KvView kv;
-    const int* tok_arena = nullptr;  // EMBED: token of row t = tok_arena[tok_idx[t]]
-    const int* tok_idx = nullptr;
-    unsigned long long* counter = nullptr;  // monotonic arrival counter
-    unsigned long long base = 0;            // its value when this launch starts
-    unsigned long long* trace = nullptr;    // optional [n_ops][grid][4] timeline
-    int stages = 0;
-};
-int mk_max_rows();                                   // T limit of a megakernel pass
-int mk_grid();                                       // CTAs (one per SM)
-int mk_op_arrivals(int type);
-void mk_plan_gemv(MkOp& op, int K, int ldw, int nprob);
-cudaError_t launch_decode_mk(const MkArgs& a, cudaStream_t s);
 
 // Deterministic N(0, sd) init from a counter hash (perf-mode weights).
 void launch_fill_normal(int dtype, void* dst, long long n, float sd, uint64_t seed, cudaStream_t s);

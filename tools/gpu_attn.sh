@@ -1,9 +1,11 @@
-# attention rework check: GPU tests, isolated attention sweep, default bench
-tag=${1:-r2e}
+# decode attention evidence: isolated sweep over C2 shapes, per-CTA timelines,
+# pages-per-chunk sweep, in-stream site times -> gpurun_out/<tag>_*
+tag=${1:-r2attn}
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/${tag}_gpu.log 2>&1; echo "gpu tests rc=$?"; tail -3 gpurun_out/${tag}_gpu.log
-timeout 300 python tools/bench_attn.py > gpurun_out/${tag}_attn.txt 2>&1; echo "attn rc=$?"; cat gpurun_out/${tag}_attn.txt
-timeout 1200 python bench.py > gpurun_out/${tag}_bench.json 2> gpurun_out/${tag}_bench.err; echo "bench rc=$?"
-python -c "
-import json; d=json.load(open('gpurun_out/${tag}_bench.json'))
-print('value %.2f tok/s'%d['value'], 'ms/step %.2f'%d['ms_per_step'], 'stages', {k:round(v,2) for k,v in d['stage_ms_per_step'].items()}, 'vanilla %.2f tok/s'%d['arms']['vanilla']['tokens_per_s'], 'e2e %.2f'%d['e2e']['value'], 'frac %.3f'%d['roofline']['frac'])"
+timeout 120 python tools/bench_attn.py > gpurun_out/${tag}_attn.txt 2>&1; cat gpurun_out/${tag}_attn.txt
+for ppi in 2 4 8 16; do echo "== ppi $ppi"; ESPEC_ATTN_PPI=$ppi timeout 120 python tools/bench_attn.py; done > gpurun_out/${tag}_ppi.txt 2>&1
+for spec in "6 64 8 128 4096" "1 32 8 128 600" "6 64 8 128 600"; do set -- $spec
+  ESPEC_ATTN_TRACE="$1,5" timeout 120 python tools/one_attn.py $1 $2 $3 $4 $5 1 10 > /dev/null 2>&1
+  echo "== T=$1 H=$2 ctx=$5"; python tools/attn_trace.py gpurun_out/attn_trace.txt
+done > gpurun_out/${tag}_trace.txt 2>&1
+timeout 900 python tools/site_times.py > gpurun_out/${tag}_sites.txt 2>&1

@@ -285,6 +285,12 @@ def main():
     ap.add_argument("--e2e-tokens", type=int, default=128)  # the paper protocol: 128 new tokens
     ap.add_argument("--no-arms", action="store_true", help="skip the vanilla / sd comparison arms")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--tp-proxy", type=int, default=0,
+                    help="shard proxy: run rank 0 of a TP-N group alone on one GPU, collectives looped back "
+                         "(per-GPU step time at TP-N shard shapes; outputs are not the model's)")
+    ap.add_argument("--draft-layout", default="tp", choices=["tp", "lp"],
+                    help="drafter across the GPUs: tensor-parallel (tp) or the paper's layer-parallel placement "
+                         "(lp: fuzzy-group slot j on GPU j, MLP / head tensor-parallel)")
     ap.add_argument("--temperature", type=float, default=0.0,
                     help="sampling temperature of every arm (0 = greedy, the BASELINE metric)")
     args = ap.parse_args()
@@ -329,9 +335,14 @@ def main():
                           **wl["draft"])
     run = E.RunConfig(algorithm="easyspec", n=n, lp_size=lp, temperature=args.temperature,
                       max_new_tokens=(warm + steps + 2) * (n + 1))
-    eng = E.Engine(base, draft, run, device=dev, tp_size=ws, tp_rank=rank)
+    proxy = args.tp_proxy if ws == 1 else 0
+    tp = proxy or ws  # tensor-parallel degree whose per-GPU shard this process runs
+    layout = args.draft_layout if tp > 1 else "tp"
+    eng = E.Engine(base, draft, run, device=dev, tp_size=tp, tp_rank=rank, draft_layout=layout)
     if ws > 1:
         eng.link_process_group()  # all-gather the NVLink receive-region IPC handles
+    elif proxy > 1:
+        eng.link_loopback()
     eng.init_weights(E.Engine.BASE, base.seed, parity=False)
     eng.init_weights(E.Engine.DRAFT, draft.seed, parity=False)
     rng = np.random.default_rng(1234)  # the same prompt on every TP rank
@@ -425,12 +436,12 @@ def main():
     hbm, peak_kind = peaks()
     cnt, site_ms, site_bytes = rf["site"]
     achieved = site_bytes / (site_ms / cnt / 1000.0) / 1e9 if cnt else None
-    gu_shape = f"{wl['base']['d_model']}x{2 * wl['base']['d_mlp'] // ws}"
+    gu_shape = f"{wl['base']['d_model']}x{2 * wl['base']['d_mlp'] // tp}"
     traffic, traffic_src = None, None
-    tp = os.path.join(ROOT, "profiles", "roofline_traffic.json")
-    if os.path.exists(tp) and ws == 1:
+    tpath = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+    if os.path.exists(tpath) and tp == 1:
         try:  # ncu --set full dram__bytes of this workload's gate/up launch
-            ent = json.load(open(tp)).get("workloads", {}).get(args.workload)
+            ent = json.load(open(tpath)).get("workloads", {}).get(args.workload)
             if ent and ent.get("shape") == gu_shape:
                 traffic, traffic_src = ent["dram_bytes_per_launch"], ent["source"]
         except Exception:
@@ -482,8 +493,14 @@ def main():
             "vs_baseline": None,
             "dtype": "bf16", "data": "synthetic (random-init weights, uniform-random prompt ids)",
             "config": {"workload": wl["name"], "ctx": args.ctx, "n": n, "lp": lp,
-                       "plan": E.plan_groups(draft.n_layers, lp), "tp": ws,
-                       "parallelism": f"tp{ws} (base + drafter)" if ws > 1 else "single GPU",
+                       "plan": E.plan_groups(draft.n_layers, lp), "tp": tp,
+                       "draft_layout": layout,
+                       "parallelism": (f"tp{ws} (base + drafter)" if layout == "tp" else
+                                       f"base tp{ws}, drafter layer-parallel over {ws} GPUs (MLP / head tp{ws})")
+                       if ws > 1 else
+                       (f"tp{proxy} shard proxy: rank 0 of a TP-{proxy} group alone on one GPU, collectives "
+                        f"looped back (per-GPU step at TP-{proxy} shard shapes; tokens are not the model's)"
+                        if proxy > 1 else "single GPU"),
                        "l2": "no flush: the weights streamed per step (GBs) >> 126 MB L2"},
             "speedup_vs_vanilla": (value / arms["vanilla"]["tokens_per_s"]) if "vanilla" in arms else None,
             "draft_ms_per_token": (calib_ms + draft_ms) * per_tok,
@@ -493,10 +510,10 @@ def main():
             # passes / the stage's device time; calibrate = 1 drafter pass + head,
             # draft = (n-1) fuzzy passes + heads, verify = 1 base pass + head
             "stage_roofline": {
-                "calibrate": pass_bytes(wl["draft"], args.ctx, ws) / (calib_ms / steps / 1e3) / 1e9 / hbm,
-                "draft": (n - 1) * pass_bytes(wl["draft"], args.ctx, ws) / (draft_ms / steps / 1e3) / 1e9 / hbm,
-                "verify": pass_bytes(wl["base"], args.ctx, ws) / (verify_ms / steps / 1e3) / 1e9 / hbm,
-                "vanilla": (pass_bytes(wl["base"], args.ctx, ws) / (arms["vanilla"]["ms_per_step"] / 1e3) / 1e9 / hbm)
+                "calibrate": pass_bytes(wl["draft"], args.ctx, tp) / (calib_ms / steps / 1e3) / 1e9 / hbm,
+                "draft": (n - 1) * pass_bytes(wl["draft"], args.ctx, tp) / (draft_ms / steps / 1e3) / 1e9 / hbm,
+                "verify": pass_bytes(wl["base"], args.ctx, tp) / (verify_ms / steps / 1e3) / 1e9 / hbm,
+                "vanilla": (pass_bytes(wl["base"], args.ctx, tp) / (arms["vanilla"]["ms_per_step"] / 1e3) / 1e9 / hbm)
                 if "vanilla" in arms else None,
                 "unit": "fraction of measured HBM GB/s"},
             "stage_ms_per_step": {"calibrate": calib_ms / steps, "draft": draft_ms / steps,

@@ -81,10 +81,15 @@ typedef struct {
 } espec_run_cfg;
 
 /* Devices used by one engine. One engine drives one GPU; a tensor-parallel
- * group of tp_size engines (one per GPU, usually one per process) shards both
- * models Megatron-style and exchanges partial sums over
- * NVLink peer memory. Layer-parallel fuzzy groups run on every GPU of the
- * group (n_lp_devices must be 0 or 1). */
+ * group of tp_size engines (one per GPU, usually one per process) shards the
+ * base Megatron-style and exchanges partial sums over NVLink
+ * peer memory. The drafter either follows the same tensor-parallel split
+ * (n_lp_devices 0 or 1: every GPU runs a head slice of every layer of a fuzzy
+ * group), or takes the paper's layer-parallel placement (n_lp_devices ==
+ * tp_size, lp_devices = {0, 1, ..., tp_size - 1}): group slot j runs on rank
+ * j with full heads and owns that layer's draft KV, one exchange per group
+ * delivers the slots' attention outputs to every rank, and the MLPs / LM head
+ * stay tensor-parallel (draft_engine.cpp:89-130, cost_sim.cpp:127-143). */
 typedef struct {
     int device;
     int n_lp_devices;
@@ -123,6 +128,12 @@ void espec_engine_destroy(espec_engine* eng);
  * imports the world * 64 bytes in rank order. */
 espec_status espec_comm_link(espec_engine** engines, int world);
 espec_status espec_comm_export(espec_engine* eng, void* handle64);
+/* Shard proxy (measurement only): a tp_size = N engine of rank 0 stands in for
+ * the whole group on one GPU — every collective pushes into all N slots of its
+ * own receive region — so a single GPU exposes the per-GPU step time of a TP-N
+ * deployment (its shard shapes and N-slot collectives). Outputs are not the
+ * model's (each sum is N x this shard's partial). */
+espec_status espec_comm_loopback(espec_engine* eng);
 espec_status espec_comm_import(espec_engine* eng, const void* handles, int world);
 const char* espec_last_error(const espec_engine* eng);
 /* Error text for a failed espec_engine_create (no engine exists yet). */

@@ -142,13 +142,26 @@ espec_status espec_engine_create(const espec_model_cfg* base, const espec_model_
     if (!base || !draft || !run || !out) return ESPEC_CONFIG;
     *out = nullptr;
     try {
-        if (devices && devices->n_lp_devices > 1)
-            throw Error(ST_CONFIG, "layer-parallel groups run tensor-parallel: use tp_size (one engine per GPU)");
         const int tp = devices && devices->tp_size > 0 ? devices->tp_size : 1;
         const int rank = devices ? devices->tp_rank : 0;
+        // n_lp_devices > 1: the drafter's layer-parallel placement over the
+        // group's GPUs (group slot j -> lp_devices[j] = rank j); 0 / 1: the
+        // drafter is tensor-parallel like the base
+        bool draft_lp = false;
+        if (devices && devices->n_lp_devices > 1) {
+            if (devices->n_lp_devices != tp)
+                throw Error(ST_CONFIG, "layer-parallel placement spans the tensor-parallel group: n_lp_devices must "
+                                       "equal tp_size");
+            if (!devices->lp_devices) throw Error(ST_CONFIG, "lp_devices is NULL");
+            for (int j = 0; j < tp; ++j)
+                if (devices->lp_devices[j] != j)
+                    throw Error(ST_CONFIG, "lp_devices must list the group's ranks in order (slot j -> rank j)");
+            draft_lp = true;
+        }
         auto e = new espec_engine();
         try {
-            e->impl = make_engine(to_model(base), to_model(draft), to_run(run), devices ? devices->device : 0, tp, rank);
+            e->impl = make_engine(to_model(base), to_model(draft), to_run(run), devices ? devices->device : 0, tp, rank,
+                                  draft_lp);
         } catch (...) {
             delete e;
             throw;
@@ -185,6 +198,10 @@ espec_status espec_comm_link(espec_engine** engines, int world) {
         if (st != ESPEC_OK) return st;
     }
     return ESPEC_OK;
+}
+
+espec_status espec_comm_loopback(espec_engine* eng) {
+    return guard(eng, [&] { eng->impl->comm_loopback(); });
 }
 
 espec_status espec_comm_export(espec_engine* eng, void* handle64) {

@@ -22,6 +22,9 @@
 // (the single-device test harness) must not: a pre-launched successor
 // parked on every SM could starve the peer shard that this kernel waits on.
 // Sequence numbers only grow, so flags never need resetting.
+// Shard proxy (CommView::loopback): one engine impersonates every rank of a
+// TP-N group on one GPU, so a single-GPU run exposes the per-GPU step of a
+// TP-N deployment (shard-sized GEMVs, N-slot collectives) without peers.
 #include <cstdio>
 #include <cstdlib>
 
@@ -59,7 +62,8 @@ __device__ void comm_signal_wait(const CommView& c, uint64_t seq, int par) {
         if (tk == gridDim.x - 1) {
             *c.ticket = 0u;
             __threadfence_system();
-            for (int p = 0; p < c.world; ++p) st_release_sys(c.peer_flags[p] + (size_t)par * c.world + c.rank, seq);
+            for (int p = 0; p < c.world; ++p)
+                st_release_sys(c.peer_flags[p] + (size_t)par * c.world + (c.loopback ? p : c.rank), seq);
         }
         const long long t0 = clock64();
         for (int s = 0; s < c.world; ++s) {
@@ -109,8 +113,9 @@ __global__ void __launch_bounds__(kCommThreads, 6) allreduce_rows_kernel(CommVie
     for (int g = g0 + warp; g < g1; g += kCommThreads / 32) {
         const int r = g / gpr, col = (g - r * gpr) * 32 + lane;
         if (col < d) {
-            const float v = a.src[ar_row(a, r, a.ld_src) + col];
-            for (int p = 0; p < c.world; ++p) slot(c, c.peer_recv[p], par, c.rank)[(size_t)r * d + col] = v;
+            const bool zero = a.rows_per_block > 0 && ((a.zero_blocks >> (r / a.rows_per_block)) & 1u);
+            const float v = zero ? 0.f : a.src[ar_row(a, r, a.ld_src) + col];
+            for (int p = 0; p < c.world; ++p) slot(c, c.peer_recv[p], par, c.loopback ? p : c.rank)[(size_t)r * d + col] = v;
         }
     }
     if (phases & PH_SYNC) comm_signal_wait(c, seq, par);
@@ -173,7 +178,7 @@ __global__ void __launch_bounds__(kCommThreads, 6) allgather_cols_kernel(CommVie
         for (long long i = i0; i < n; i += stride) {
             const int r = (int)(i / a.cols), j = (int)(i - (long long)r * a.cols);
             const float v = a.src[(size_t)r * a.ld_src + j];
-            for (int p = 0; p < c.world; ++p) slot(c, c.peer_recv[p], par, c.rank)[i] = v;
+            for (int p = 0; p < c.world; ++p) slot(c, c.peer_recv[p], par, c.loopback ? p : c.rank)[i] = v;
         }
     if (phases & PH_SYNC) comm_signal_wait(c, seq, par);
     if (!(phases & PH_COMBINE)) return;
@@ -218,7 +223,7 @@ __global__ void allgather_argmax_kernel(CommView c, uint64_t seq, int T, const f
         const float v = val[t];
         const float ib = __int_as_float(idx[t]);
         for (int p = 0; p < c.world; ++p) {
-            float* d = slot(c, c.peer_recv[p], par, c.rank);
+            float* d = slot(c, c.peer_recv[p], par, c.loopback ? p : c.rank);
             d[2 * t] = v;
             d[2 * t + 1] = ib;
         }

@@ -212,6 +212,13 @@ struct LayerDev {
 struct ModelDev {
     ModelCfg c;
     int tp = 1, rank = 0;
+    // attention split: atp ranks share each layer's heads (Megatron, = tp), or
+    // under the layer-parallel placement (lp, drafter only: the paper layout)
+    // atp = 1 and owner[l] is the one rank that runs layer l's attention (full
+    // heads) and holds its KV; the MLP and the head stay tensor-parallel
+    int atp = 1, arank = 0;
+    bool lp = false;
+    std::vector<int> owner;
     void* emb = nullptr;   // [V][d] (replicated)
     void* head = nullptr;  // [d][head_ld]: this rank's vocabulary slice
     int head_ld = 0;
@@ -219,8 +226,8 @@ struct ModelDev {
     float2* rope = nullptr;  // [max_positions][d_head/2] (cos, sin) of apply_rope's angles
     std::vector<LayerDev> L;
     std::vector<void*> owned;
-    int qh() const { return c.n_heads / tp; }
-    int kvh() const { return c.n_kv_heads / tp; }
+    int qh() const { return c.n_heads / atp; }
+    int kvh() const { return c.n_kv_heads / atp; }
     int f_loc() const { return c.d_mlp / tp; }
     int V_loc() const { return c.vocab_size / tp; }
     int qkv_N() const { return (qh() + 2 * kvh()) * c.d_head; }
@@ -558,15 +565,18 @@ struct Workspace {
 
 class EngineImpl final : public Engine {
 public:
-    EngineImpl(const ModelCfg& bc, const ModelCfg& dc, const RunCfg& run, int device, int tp, int rank)
+    EngineImpl(const ModelCfg& bc, const ModelCfg& dc, const RunCfg& run, int device, int tp, int rank,
+               bool draft_lp)
         : device_(device) {
         bc.validate();
         dc.validate();
         if (bc.vocab_size != dc.vocab_size) cfg_fail("base and draft models must share the vocabulary");
         if (tp < 1 || tp > kMaxTp) cfg_fail("tp_size must lie in [1, 8]");
         if (rank < 0 || rank >= tp) cfg_fail("tp_rank must lie in [0, tp_size)");
+        if (draft_lp && tp < 2) cfg_fail("layer-parallel placement needs tp_size > 1 (one GPU per group slot)");
         for (const ModelCfg* c : {&bc, &dc}) {
-            if (c->n_heads % tp || c->n_kv_heads % tp) cfg_fail("attention heads must divide by tp_size");
+            if ((c->n_heads % tp || c->n_kv_heads % tp) && !(c == &dc && draft_lp))
+                cfg_fail("attention heads must divide by tp_size");
             if (c->d_mlp % (16 * tp)) cfg_fail("d_mlp must be a multiple of 16 * tp_size");
             if (c->vocab_size % tp) cfg_fail("vocab_size must divide by tp_size");
         }
@@ -574,6 +584,11 @@ public:
         draft_.c = dc;
         base_.tp = draft_.tp = tp;
         base_.rank = draft_.rank = rank;
+        base_.atp = tp;
+        base_.arank = rank;
+        draft_.lp = draft_lp;
+        draft_.atp = draft_lp ? 1 : tp;
+        draft_.arank = draft_lp ? 0 : rank;
         set_run(run);
         CUDA_OK(cudaSetDevice(device));
         if (const char* e = std::getenv("ESPEC_PDL")) set_pdl(std::atoi(e) != 0);
@@ -671,6 +686,12 @@ public:
             cfg_fail("layer plan covers " + std::to_string(plan_.n_layers()) + " layers, drafter has " +
                      std::to_string(draft_.c.n_layers));
         if (plan_.max_group_size() > kMaxGroup) cfg_fail("layer-parallel groups are limited to 8 layers");
+        // layer-parallel placement: group slot j -> rank j (mod the group size
+        // of GPUs); sequential drafting (sd / vanilla plans) keeps every layer
+        // on rank 0, the lead GPU
+        draft_.owner.assign(draft_.c.n_layers, 0);
+        for (const auto& grp : plan_.groups)
+            for (size_t j = 0; j < grp.size(); ++j) draft_.owner[grp[j]] = (int)(j % std::max(1, draft_.tp));
         // validate_run_config (proj/src/orchestrator.cpp:95-118)
         if (run.n < 1) cfg_fail("speculation length must be >= 1");
         if (run.max_new_tokens < 1) cfg_fail("max_new_tokens must be >= 1");
@@ -705,6 +726,9 @@ public:
         // make_truncated_draft (proj/src/model.cpp:86-99): the drafter reuses the
         // base's embedding, final norm and first L_d blocks (no copy in HBM).
         if (!base_allocated_) throw Error(ST_CONFIG, "initialise the base model first");
+        if (draft_.lp)
+            cfg_fail("the layer-parallel drafter holds full-head attention while the base is head-sharded: "
+                     "initialise it on its own (init_model(keep layers, same seed) is the same truncated model)");
         const ModelCfg& b = base_.c;
         const ModelCfg& d = draft_.c;
         if (d.n_layers < 2 || d.n_layers >= b.n_layers)
@@ -785,14 +809,15 @@ public:
         }
         for (int l = 0; l < c.n_layers; ++l) {
             LayerDev& L = M.L[l];
-            ColMap mq = seg({{0, r * qh * dh, qh * dh},
-                             {qh * dh, H * dh + r * kvh * dh, kvh * dh},
-                             {(qh + kvh) * dh, (H + Hkv) * dh + r * kvh * dh, kvh * dh}});
+            const int ar = M.arank;  // attention heads of this rank (all of them under lp)
+            ColMap mq = seg({{0, ar * qh * dh, qh * dh},
+                             {qh * dh, H * dh + ar * kvh * dh, kvh * dh},
+                             {(qh + kvh) * dh, (H + Hkv) * dh + ar * kvh * dh, kvh * dh}});
             mq.seed = k++;
             mat_fill_map(L.wqkv, dt, d, M.qkv_ld(), mq, 0, (long long)(H + 2 * Hkv) * dh, proj_sd);
             ColMap mo = seg({{0, 0, d}});
             mo.seed = k++;
-            mat_fill_map(L.wo, dt, qh * dh, d, mo, r * qh * dh, d, proj_sd * resid);
+            mat_fill_map(L.wo, dt, qh * dh, d, mo, ar * qh * dh, d, proj_sd * resid);
             ColMap mg;
             mg.gateup = 1;
             mg.f_loc = fl;
@@ -909,21 +934,22 @@ public:
         LayerDev& L = M.L[layer];
         const int qd = M.qdim(), kd = M.kvdim();
         const int qd_full = c.n_heads * c.d_head, kd_full = c.n_kv_heads * c.d_head;
+        const int ar = M.arank;  // attention heads of this rank (all of them under lp)
         if (name == "wq") {
             expect(d, qd_full);
-            const auto sl = cslice((long long)r * qd, qd);
+            const auto sl = cslice((long long)ar * qd, qd);
             mat_write(L.wqkv, dt, d, M.qkv_ld(), 0, sl.data(), qd);
         } else if (name == "wk") {
             expect(d, kd_full);
-            const auto sl = cslice((long long)r * kd, kd);
+            const auto sl = cslice((long long)ar * kd, kd);
             mat_write(L.wqkv, dt, d, M.qkv_ld(), qd, sl.data(), kd);
         } else if (name == "wv") {
             expect(d, kd_full);
-            const auto sl = cslice((long long)r * kd, kd);
+            const auto sl = cslice((long long)ar * kd, kd);
             mat_write(L.wqkv, dt, d, M.qkv_ld(), qd + kd, sl.data(), kd);
         } else if (name == "wo") {
             expect(qd_full, d);
-            mat_write(L.wo, dt, qd, d, 0, data + (size_t)r * qd * d, d);
+            mat_write(L.wo, dt, qd, d, 0, data + (size_t)ar * qd * d, d);
         } else if (name == "w_down") {
             expect(f, d);
             mat_write(L.wd, dt, fl, d, 0, data + (size_t)r * fl * d, d);
@@ -1248,42 +1274,61 @@ public:
         };
         for (const auto& g : groups) {
             const int n = (int)g.size();
+            // layer-parallel placement (the paper layout, ModelDev::lp): this
+            // rank runs the attention of the group's layers it owns, full
+            // heads, and the group's exchange delivers every slot to every rank
+            std::vector<int> sl, sg;  // slots computed here and their layers
+            for (int i = 0; i < n; ++i)
+                if (!M.lp || M.owner[g[i]] == comm_.rank) {
+                    sl.push_back(i);
+                    sg.push_back(g[i]);
+                }
+            const int m = (int)sl.size();
             // attention of every layer in the group reads the group-entry state
             GemvBatch qb;
-            for (int i = 0; i < n; ++i) {
+            for (int j = 0; j < m; ++j) {
+                const int i = j;
                 GemvProblem p = gp(W, i);
-                const LayerDev& L = M.L[g[i]];
+                const LayerDev& L = M.L[sg[j]];
                 p.W = L.wqkv; p.K = d; p.N = M.qkv_N(); p.ldw = M.qkv_ld();
                 p.x = W.h; p.ldx = d; p.gain = L.ga; p.stats_in = W.stats; p.stat_tiles_in = tiles; p.eps = c.norm_eps;
                 p.out = W.q + (size_t)i * kChunk * qd; p.ldo = qd;
-                p.n_heads = M.qh(); p.n_kv = M.kvh(); p.dh = c.d_head; p.layer = g[i]; p.rope = M.rope;
-                qb.p[i] = p;
+                p.n_heads = M.qh(); p.n_kv = M.kvh(); p.dh = c.d_head; p.layer = sg[j]; p.rope = M.rope;
+                qb.p[j] = p;
             }
-            g_gemv(M, 0, gemv_bytes(M, d, M.qkv_ld(), M.qkv_N(), T, n), EPI_QKV, qb, n, T, ps, kv);
-            if (cap_)
-                for (int i = 0; i < n; ++i) grab((*cap_)[g[i]].q, W.q + (size_t)i * kChunk * qd, qd);
-            attention(M, C, W, g, ps);
-            if (n == 1 && !cap_) {
+            if (m > 0) {
+                g_gemv(M, 0, gemv_bytes(M, d, M.qkv_ld(), M.qkv_N(), T, m), EPI_QKV, qb, m, T, ps, kv);
+                if (cap_)
+                    for (int i = 0; i < n; ++i) grab((*cap_)[g[i]].q, W.q + (size_t)i * kChunk * qd, qd);
+                attention(M, C, W, sg, ps);
+            }
+            if (n == 1 && !cap_ && !M.lp) {
                 row_parallel_resid(M, W, M.L[g[0]].wo, qd, b16 ? (const float*)W.mixed_b16 : W.mixed, qd, 2, T, ps, kv,
                                    nullptr, b16);
             } else {
-                GemvBatch ob;
-                for (int i = 0; i < n; ++i) {
-                    GemvProblem p = gp(W, i);
-                    p.W = M.L[g[i]].wo; p.K = qd; p.N = d; p.ldw = d;
-                    p.x = b16 ? (const float*)(W.mixed_b16 + (size_t)i * kChunk * qd) : W.mixed + (size_t)i * kChunk * qd;
-                    p.ldx = qd; p.x_bf16 = b16;
-                    p.out = W.attn + (size_t)i * kChunk * d; p.ldo = d;
-                    if (i == 0 && fuse) {  // h += attn_0 in the epilogue (+ row stats)
-                        p.out = W.h; p.resid = W.h; p.ldr = d; p.stats_out = W.stats; p.stat_tiles_out = tiles;
+                if (m > 0) {
+                    GemvBatch ob;
+                    for (int j = 0; j < m; ++j) {
+                        const int i = sl[j];
+                        GemvProblem p = gp(W, j);
+                        p.W = M.L[sg[j]].wo; p.K = qd; p.N = d; p.ldw = d;
+                        p.x = b16 ? (const float*)(W.mixed_b16 + (size_t)j * kChunk * qd) : W.mixed + (size_t)j * kChunk * qd;
+                        p.ldx = qd; p.x_bf16 = b16;
+                        p.out = W.attn + (size_t)i * kChunk * d; p.ldo = d;
+                        if (i == 0 && fuse) {  // h += attn_0 in the epilogue (+ row stats)
+                            p.out = W.h; p.resid = W.h; p.ldr = d; p.stats_out = W.stats; p.stat_tiles_out = tiles;
+                        }
+                        ob.p[j] = p;
                     }
-                    ob.p[i] = p;
+                    g_gemv(M, 2, gemv_bytes(M, qd, d, d, T, m), EPI_STORE, ob, m, T, ps, kv);
                 }
-                g_gemv(M, 2, gemv_bytes(M, qd, d, d, T, n), EPI_STORE, ob, n, T, ps, kv);
                 if (cap_)
                     for (int i = 0; i < n; ++i) grab((*cap_)[g[i]].attn_out, W.attn + (size_t)i * kChunk * d, d);
                 if (tp()) {
-                    // ONE all-reduce for the whole group's attention outputs
+                    // ONE exchange for the whole group's attention outputs: the
+                    // sum of the ranks' row-parallel partials (TP), or under the
+                    // layer-parallel placement the owners' outputs (every other
+                    // rank pushes exact zeros for a slot it does not own)
                     const int per = (size_t)n * T * d <= comm_.slot_floats ? n : 1;
                     for (int i0 = 0; i0 < n; i0 += per) {
                         AllreduceArgs a;
@@ -1291,6 +1336,9 @@ public:
                         a.src = W.attn + (size_t)i0 * kChunk * d; a.ld_src = d;
                         a.out = W.attn + (size_t)i0 * kChunk * d; a.ldo = d;
                         a.rows_per_block = T; a.block_stride = (size_t)kChunk * d;
+                        if (M.lp)
+                            for (int b = 0; b < per && i0 + b < n; ++b)
+                                if (M.owner[g[i0 + b]] != comm_.rank) a.zero_blocks |= 1u << b;
                         launch_allreduce_rows(comm_, a, stream_);
                         ++launches_;
                     }
@@ -1302,7 +1350,7 @@ public:
                 // LayerProbe::h_in is the running state before this layer's residual add
                 // (proj/src/draft_engine.cpp:112-124)
                 if (cap_) grab((*cap_)[g[i]].h_in, W.h, d);
-                if ((n > 1 || cap_) && !fuse) {
+                if ((n > 1 || cap_ || M.lp) && !fuse) {
                     g_add(W, W.attn + (size_t)i * kChunk * d, d, T);
                 }
                 GemvBatch ub;
@@ -2232,6 +2280,13 @@ public:
         comm_.local_sync = &local_sync_fn;
         comm_.local_ctx = local_group_.get();
     }
+    // shard proxy: this engine (rank 0 of a TP-N group) stands in for every
+    // rank; collectives loop back into its own receive region
+    void comm_loopback() override {
+        if (comm_.world < 2) cfg_fail("the shard proxy needs tp_size > 1");
+        for (int p = 0; p < comm_.world; ++p) set_peer(p, comm_region());
+        comm_.loopback = 1;
+    }
     void comm_ipc_export(void* handle64) override {
         if (!comm_mem_) cfg_fail("tp_size is 1: nothing to export");
         cudaIpcMemHandle_t h;
@@ -2313,8 +2368,8 @@ private:
 };
 
 std::unique_ptr<Engine> make_engine(const ModelCfg& base, const ModelCfg& draft, const RunCfg& run, int device,
-                                    int tp, int rank) {
-    return std::unique_ptr<Engine>(new EngineImpl(base, draft, run, device, tp, rank));
+                                    int tp, int rank, bool draft_lp) {
+    return std::unique_ptr<Engine>(new EngineImpl(base, draft, run, device, tp, rank, draft_lp));
 }
 
 }  // namespace espec

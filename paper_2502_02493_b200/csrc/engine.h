@@ -102,8 +102,10 @@ class Engine;
 // tp > 1: this engine is shard `rank` of a tensor-parallel group (one per
 // GPU); link the group with comm_link (one process) or comm_ipc_* (one
 // process per GPU) before loading weights' first use.
+// draft_lp: the drafter's layer-parallel placement (group slot j -> rank j,
+// full-head attention + KV on the owner, MLP / head tensor-parallel)
 std::unique_ptr<Engine> make_engine(const ModelCfg& base, const ModelCfg& draft, const RunCfg& run, int device,
-                                    int tp = 1, int rank = 0);
+                                    int tp = 1, int rank = 0, bool draft_lp = false);
 
 class Engine {
 public:
@@ -160,6 +162,8 @@ public:
     // one process per GPU: export this rank's cudaIpcMemHandle_t (64 bytes),
     // then import all ranks' handles in rank order
     virtual void comm_ipc_export(void* handle64) = 0;
+    // shard proxy: one engine stands in for all tp_size ranks (timing only)
+    virtual void comm_loopback() = 0;
     virtual void comm_ipc_import(const void* handles, int world) = 0;
     // device pointer of this shard's receive region (comm_link)
     virtual void* comm_region() = 0;

@@ -324,6 +324,11 @@ struct CommView {
     uint64_t seq = 0;                // collectives issued so far (host side)
     int early_trigger = 1;           // PDL-trigger the successor before waiting (GPUs not shared)
     int debug = 0;                   // ESPEC_TRACE_COMM: device-side trace
+    // shard proxy (one engine standing in for all `world` ranks on one GPU):
+    // every push lands in all sender slots of this rank's own region and every
+    // flag is set locally, so each collective moves and waits like a TP-N one
+    // (its sums are world x this rank's partial: timing, not numerics)
+    int loopback = 0;
     // Shards sharing ONE GPU (single-device harness): device-side spinning
     // could wait on a peer whose copies queue behind this rank's work, so the
     // push and combine run as two kernels and local_sync orders them with
@@ -348,6 +353,10 @@ struct AllreduceArgs {
     // + (r % rows_per_block) * ld (0 = one block)
     int rows_per_block = 0;
     size_t block_stride = 0;
+    // blocks (bit b = rows [b * rows_per_block, (b + 1) * rows_per_block)) this
+    // rank contributes as exact zeros without reading src: the layer-parallel
+    // placement's exchange, where only a slot's owner computed it
+    unsigned zero_blocks = 0;
 };
 void launch_allreduce_rows(CommView& c, const AllreduceArgs& a, cudaStream_t s);
 struct GatherColsArgs {

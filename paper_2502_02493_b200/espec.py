@@ -138,6 +138,7 @@ def lib():
         L.espec_comm_link.argtypes = [P(V), C.c_int]
         L.espec_comm_export.argtypes = [V, C.c_void_p]
         L.espec_comm_import.argtypes = [V, C.c_void_p, C.c_int]
+        L.espec_comm_loopback.argtypes = [V]
         L.espec_prefill.argtypes = [V, P(C.c_int32), C.c_int]
         L.espec_prefix_distribution.argtypes = [V, P(C.c_int32), C.c_int, C.c_int64, C.c_int64, C.c_int64,
                                                 P(C.c_int32), P(C.c_int64), C.c_int, P(C.c_int)]
@@ -253,13 +254,25 @@ class Engine:
     DRAFT, BASE = 0, 1
 
     def __init__(self, base: ModelConfig, draft: ModelConfig, run: RunConfig, device: int = 0, tp_size: int = 1,
-                 tp_rank: int = 0):
+                 tp_rank: int = 0, draft_layout: str = "tp"):
+        """draft_layout "tp": the drafter is tensor-parallel like the base;
+        "lp": the paper's layer-parallel placement (group slot j on rank j,
+        full-head attention + its KV on the owner, MLP / head tensor-parallel)."""
         L = lib()
         self.base_cfg, self.draft_cfg = base, draft
         self.tp_size, self.tp_rank = tp_size, tp_rank
         self._h = C.c_void_p()
         self._keep = []
-        dm = _DevMap(device, 1, None, tp_size, tp_rank)
+        if draft_layout == "lp":
+            if tp_size < 2:  # n_lp_devices <= 1 would silently mean the tensor-parallel drafter
+                raise EspecError(1, "layer-parallel placement needs tp_size > 1 (one GPU per group slot)")
+            lpd = (C.c_int * tp_size)(*range(tp_size))
+            self._lpd = lpd
+            dm = _DevMap(device, tp_size, lpd, tp_size, tp_rank)
+        elif draft_layout == "tp":
+            dm = _DevMap(device, 1, None, tp_size, tp_rank)
+        else:
+            raise ValueError(f"draft_layout must be 'tp' or 'lp', not {draft_layout!r}")
         st = L.espec_engine_create(C.byref(base._c()), C.byref(draft._c()), C.byref(self._run(run)), C.byref(dm),
                                    C.byref(self._h))
         if st:
@@ -306,6 +319,11 @@ class Engine:
     def ipc_import(self, handles: Sequence[bytes]):
         blob = b"".join(handles)
         self._check(lib().espec_comm_import(self._h, blob, len(handles)))
+
+    def link_loopback(self):
+        """Shard proxy: this rank-0 engine of a TP-N group stands in for all N
+        ranks (collectives loop back; timing only, outputs are not the model's)."""
+        self._check(lib().espec_comm_loopback(self._h))
 
     def link_process_group(self, group=None):
         """One process per GPU: all-gather the IPC handles over a
@@ -594,18 +612,21 @@ def exchange_ipc_handles(local: bytes, group=None) -> List[bytes]:
 
 
 def tp_group_local(base: ModelConfig, draft: ModelConfig, run: RunConfig, tp: int, device: int = 0,
-                   parity: bool = True, truncated: int = 0) -> List[Engine]:
+                   parity: bool = True, truncated: int = 0, draft_layout: str = "tp") -> List[Engine]:
     """All tp shards of one tensor-parallel group in this process (testing
     the sharded path on one GPU: the collectives run over plain device
     pointers instead of NVLink-mapped ones)."""
-    engines = [Engine(base, draft, run, device=device, tp_size=tp, tp_rank=r) for r in range(tp)]
+    engines = [Engine(base, draft, run, device=device, tp_size=tp, tp_rank=r, draft_layout=draft_layout)
+               for r in range(tp)]
     Engine.link_local(engines)
     for e in engines:
         e.init_weights(Engine.BASE, base.seed, parity=parity)
-        if truncated:
+        if truncated and draft_layout == "tp":
             e.share_truncated_draft()
         else:
-            e.init_weights(Engine.DRAFT, draft.seed, parity=parity)
+            # the layer-parallel drafter cannot alias the head-sharded base
+            # blocks; init_model(keep layers, same seed) is the same drafter
+            e.init_weights(Engine.DRAFT, base.seed if truncated else draft.seed, parity=parity)
     return engines
 
 

@@ -26,7 +26,7 @@ def _port():
     return p
 
 
-def _rank(rank, world, port, idx, q):
+def _rank(rank, world, port, idx, q, layout="tp"):
     import torch.distributed as dist
 
     from paper_2502_02493_b200 import espec as E
@@ -40,10 +40,14 @@ def _rank(rank, world, port, idx, q):
         run = E.RunConfig(algorithm=r["algorithm"], n=r["n"], widths=r["widths"], lp_size=r["lp_size"],
                           plan_override=r["plan_override"] or None, temperature=r["temperature"],
                           max_new_tokens=min(r["max_new_tokens"], 24), seed=r["seed"], calibration=r["calibration"])
-        eng = E.Engine(base, replace(base, n_layers=case["keep"]), run, device=0, tp_size=world, tp_rank=rank)
+        eng = E.Engine(base, replace(base, n_layers=case["keep"]), run, device=0, tp_size=world, tp_rank=rank,
+                       draft_layout=layout)
         eng.link_process_group()
         eng.init_weights(E.Engine.BASE, base.seed)
-        eng.share_truncated_draft()
+        if layout == "tp":
+            eng.share_truncated_draft()
+        else:  # the layer-parallel drafter: init_model(keep layers, same seed)
+            eng.init_weights(E.Engine.DRAFT, base.seed)
         toks, _ = eng.generate(case["prompt"].encode())
         q.put((rank, [int(t) for t in toks], case["tokens"][:len(toks)]))
         eng.close()
@@ -53,11 +57,12 @@ def _rank(rank, world, port, idx, q):
     dist.destroy_process_group()
 
 
-def test_tp2_two_processes_ipc_matches_reference():
+@pytest.mark.parametrize("layout", ["tp", "lp"])
+def test_tp2_two_processes_ipc_matches_reference(layout):
     world, port = 2, _port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_rank, args=(r, world, port, 3, q)) for r in range(world)]
+    procs = [ctx.Process(target=_rank, args=(r, world, port, 3, q, layout)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(world)]

@@ -15,7 +15,11 @@ wl = bench.WORKLOADS["c2"]
 mp = 512 + 200
 base = E.ModelConfig(max_positions=mp, seed=7, tied_head=False, weight_dtype=E.BF16, kv_dtype=E.BF16, **wl["base"])
 draft = E.ModelConfig(max_positions=mp, seed=9, tied_head=False, weight_dtype=E.BF16, kv_dtype=E.BF16, **wl["draft"])
-eng = E.Engine(base, draft, E.RunConfig(algorithm="easyspec", n=5, lp_size=4, max_new_tokens=100))
+# ESPEC_TP_PROXY=N: rank 0 of a TP-N group alone on this GPU (collectives loop back)
+tp = int(os.environ.get("ESPEC_TP_PROXY", "1"))
+eng = E.Engine(base, draft, E.RunConfig(algorithm="easyspec", n=5, lp_size=4, max_new_tokens=100), tp_size=tp)
+if tp > 1:
+    eng.link_loopback()
 eng.init_weights(E.Engine.BASE, 7, parity=False)
 eng.init_weights(E.Engine.DRAFT, 9, parity=False)
 prompt = [int(t) for t in np.random.default_rng(1234).integers(0, base.vocab_size, size=512)]
@@ -35,6 +39,6 @@ for alg in ("easyspec", "vanilla"):
                 eng.step()
             n, ms, by = eng.site_stats()
             eng.time_site(-1, -1)
-            row.append(f"{names[kind]} {1e3 * ms / max(n, 1):6.1f}us x{n // 4}/step ({by / max(ms / n, 1e-9) / 1e6 / 6543:.0%})")
+            row.append(f"{names[kind]} {1e3 * ms / max(n, 1):6.1f}us x{n // 4}/step ({by / max(ms / max(n, 1), 1e-9) / 1e6 / 6543:.0%})")
         print(f"{alg:8s} {wname:5s} " + " | ".join(row), flush=True)
 eng.close()

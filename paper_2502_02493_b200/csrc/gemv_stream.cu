@@ -218,7 +218,6 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
     constexpr int NE = sg_ne<TM>();
     __shared__ __align__(8) uint64_t red_full[NE];
     __shared__ __align__(8) uint64_t red_empty[NE];
-    __shared__ float inv_rms[kSgSlots][TM];
     __shared__ __align__(16) uint4 s_xzero[2];  // 32 zero bytes: A rows a slot does not hold
 
     constexpr int kStageBlocks = SB;  // == L.sblk (compile-time: a runtime stage size costs 13 % at T = 16)
@@ -348,6 +347,25 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
         if (e >= L.ne) return;
         __shared__ int s_pos[16];
         __shared__ long long s_kvrow[16];
+        __shared__ float s_rms[kMaxProblems][TM];
+        // RMSNorm prologue, second half: the consumers staged x * gain (no
+        // statistics on their critical path); each row's 1/rms scales its sums
+        // here. Computed once per CTA while the consumers run their first unit.
+        const int nprob = L.units / (L.ngroups * L.nK);
+        for (int q = e; q < nprob * TM; q += L.ne) {
+            const int pb = q / TM, t = q - pb * TM;
+            const GemvProblem& P = L.b.p[pb];
+            float r = 1.f;
+            if (P.gain != nullptr && t < L.T) {
+                float ss = 0.f;
+                const float* st = P.stats_in + (size_t)(L.t0 + t) * P.stat_tiles_in;
+#pragma unroll 8
+                for (int i = lane; i < P.stat_tiles_in; i += 32) ss += __ldcg(st + i);
+                ss = warp_sum(ss);
+                r = 1.0f / sqrtf(ss / (float)P.K + P.eps);
+            }
+            if (lane == 0) s_rms[pb][t] = r;
+        }
         if constexpr (EPI == EPI_QKV) {
             // the pass's row metadata (rotary position, paged-KV row base),
             // once per CTA while the consumers run their first unit — not two
@@ -358,8 +376,8 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
                 s_kvrow[lane] = (long long)L.kv.page_table[row / L.kv.page_rows] * L.kv.page_elems +
                                 (long long)(row % L.kv.page_rows) * L.kv.dh;
             }
-            named_bar(3, L.ne * 32);
         }
+        named_bar(3, L.ne * 32);
         constexpr bool kResid = TM == 8 && (EPI == EPI_RESID || EPI == EPI_STORE);
         int i = e;
         for (;; i += L.ne) {
@@ -445,6 +463,9 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
                             if (jj + c < L.nK) v[t] += ld[c][t];
                 }
             }
+            if (P.gain != nullptr)
+#pragma unroll
+                for (int t = 0; t < TM; ++t) v[t] = __fmul_rn(v[t], s_rms[prob][t]);
             SgEpiCtx ctx{L.pass, L.kv, L.T, L.t0, L.ngroups};
             if constexpr (EPI == EPI_QKV) {
                 ctx.pos = s_pos;
@@ -465,57 +486,48 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
     for (int s = 0; s <= pair1 - pair0; ++s) {
         const int pair = pair0 + s, prob = pair / L.nK, j = pair - prob * L.nK;
         const GemvProblem& P = L.b.p[prob];
-        // RMSNorm statistics: warp w sums row w's per-32-column partials
-        // (lane-strided, then a fixed shuffle tree; independent of T)
-        for (int t = warp; t < TM; t += kSgConsumers) {
-            float r = 1.f;
-            if (P.gain != nullptr && t < T) {
-                float ss = 0.f;
-                const float* st = P.stats_in + (size_t)(t0 + t) * P.stat_tiles_in;
-#pragma unroll 8
-                for (int i = lane; i < P.stat_tiles_in; i += 32) ss += __ldcg(st + i);
-                ss = warp_sum(ss);
-                r = 1.0f / sqrtf(ss / (float)P.K + P.eps);
-            }
-            if (lane == 0) inv_rms[s][t] = r;
-        }
-        named_bar(1, kSgConsumers * 32);
         __nv_bfloat16* xd = xs + (size_t)s * xslot;
         const int k0 = j * kc;
         const int kq = kc >> 2;
-        // rows >= T are zero; rows < T: batches of 8 independent float4 loads
-        // per thread so the L2 round trips overlap
+        // rows >= T are zero
         for (int i = T * kq + tid; i < L.xrows * kq; i += kSgConsumers * 32) {
             const int t = i / kq, kk = (i - t * kq) * 4;
             *reinterpret_cast<uint2*>(xd + t * L.xld + kk) = make_uint2(0u, 0u);
         }
-        constexpr int U = 8;
+        constexpr int NT = kSgConsumers * 32;
         if (P.x_bf16) {
             // activations already bf16 (producer-rounded): straight copy
+            constexpr int U = TM == 8 ? 16 : 8;
             const __nv_bfloat16* xb16 = reinterpret_cast<const __nv_bfloat16*>(P.x);
-            for (int i0 = tid; i0 < T * kq; i0 += (kSgConsumers * 32) * U) {
+            for (int i0 = tid; i0 < T * kq; i0 += NT * U) {
                 uint2 v[U];
 #pragma unroll
                 for (int q = 0; q < U; ++q) {
-                    const int i = i0 + q * (kSgConsumers * 32);
+                    const int i = i0 + q * NT;
                     const int t = i / kq, k = k0 + (i - t * kq) * 4;
                     v[q] = make_uint2(0u, 0u);
                     if (i < T * kq && k < P.K) v[q] = __ldcg(reinterpret_cast<const uint2*>(xb16 + (size_t)(t0 + t) * P.ldx + k));
                 }
 #pragma unroll
                 for (int q = 0; q < U; ++q) {
-                    const int i = i0 + q * (kSgConsumers * 32);
+                    const int i = i0 + q * NT;
                     if (i >= T * kq) break;
                     const int t = i / kq, kk = (i - t * kq) * 4;
                     *reinterpret_cast<uint2*>(xd + t * L.xld + kk) = v[q];
                 }
             }
-        } else
-        for (int i0 = tid; i0 < T * kq; i0 += kSgConsumers * 32 * U) {
+            continue;
+        }
+        // fp32 rows with the RMSNorm prologue's first half: x * gain rounded to
+        // bf16 (the epilogue applies each row's 1/rms to its sums, so the row
+        // statistics are off the consumers' critical path), batches of U
+        // independent row and gain loads per thread in flight per round trip
+        constexpr int U = TM == 8 ? 8 : 4;  // (the 16-row variant's registers are tighter)
+        for (int i0 = tid; i0 < T * kq; i0 += NT * U) {
             float4 v[U], gn[U];
 #pragma unroll
             for (int q = 0; q < U; ++q) {
-                const int i = i0 + q * kSgConsumers * 32;
+                const int i = i0 + q * NT;
                 const int t = i / kq, k = k0 + (i - t * kq) * 4;
                 v[q] = make_float4(0.f, 0.f, 0.f, 0.f);
                 gn[q] = make_float4(1.f, 1.f, 1.f, 1.f);
@@ -524,18 +536,21 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
                     if (P.gain != nullptr) gn[q] = __ldg(reinterpret_cast<const float4*>(P.gain + k));
                 }
             }
+            if (tid == 0 && s == 0 && i0 == tid && L.trace) {  // diagnostic: the first rows landed
+                if (v[0].x + gn[U - 1].w == 12345.f) asm volatile("trap;");
+                sg_tr(L.trace, 5);
+            }
 #pragma unroll
             for (int q = 0; q < U; ++q) {
-                const int i = i0 + q * kSgConsumers * 32;
+                const int i = i0 + q * NT;
                 if (i >= T * kq) break;
                 const int t = i / kq, kk = (i - t * kq) * 4;
                 float4 w = v[q];
                 if (P.gain != nullptr) {
-                    const float r = inv_rms[s][t];
-                    w.x = __fmul_rn(__fmul_rn(w.x, r), gn[q].x);
-                    w.y = __fmul_rn(__fmul_rn(w.y, r), gn[q].y);
-                    w.z = __fmul_rn(__fmul_rn(w.z, r), gn[q].z);
-                    w.w = __fmul_rn(__fmul_rn(w.w, r), gn[q].w);
+                    w.x = __fmul_rn(w.x, gn[q].x);
+                    w.y = __fmul_rn(w.y, gn[q].y);
+                    w.z = __fmul_rn(w.z, gn[q].z);
+                    w.w = __fmul_rn(w.w, gn[q].w);
                 }
                 const __nv_bfloat162 lo = __floats2bfloat162_rn(w.x, w.y), hi = __floats2bfloat162_rn(w.z, w.w);
                 uint2 pk;
@@ -543,6 +558,7 @@ __global__ void __launch_bounds__(sg_threads<TM>(), 1) sgemv_kernel(const __grid
                 pk.y = *reinterpret_cast<const uint32_t*>(&hi);
                 *reinterpret_cast<uint2*>(xd + t * L.xld + kk) = pk;
             }
+            if (tid == 0 && s == 0 && i0 == tid && L.trace) sg_tr(L.trace, 6);  // diagnostic: the first batch stored
         }
     }
     named_bar(1, kSgConsumers * 32);

@@ -11,10 +11,11 @@ heads = [l for l in lines if l.startswith("epi")]
 rows = [l for l in lines if l.strip() and not l.startswith("epi")]
 t = np.array([[int(x) for x in l.split()] for l in rows], dtype=np.int64).reshape(len(heads), -1, 16)
 t0 = t[0][t[0][:, 0] > 0, 0].min()
-names = {0: "cta start", 1: "dep released", 2: "staged", 3: "consumers done", 4: "epilogues done"}
+names = {0: "cta start", 1: "dep released", 5: "x rows landed", 6: "x batch stored", 2: "staged", 3: "consumers done",
+         4: "epilogues done"}
 for h, tl in zip(heads, t):
     print(h)
-    for e in (0, 1, 2, 3, 4):
+    for e in (0, 1, 5, 6, 2, 3, 4):
         v = tl[:, e]
         v = (v[v > 0] - t0) / 1e3
         if len(v):

@@ -153,12 +153,22 @@ void launch_allreduce_rows(CommView& c, const AllreduceArgs& a, cudaStream_t s) 
     int ctas = (groups + 7) / 8;
     if (ctas > kCommMaxCtas) ctas = kCommMaxCtas;
     if (c.local_sync) {
-        CCK(launch_pdl(allreduce_rows_kernel, dim3(ctas), dim3(kCommThreads), 0, s, c, seq, a, (int)PH_PUSH));
+        if (!a.prepushed)
+            CCK(launch_pdl(allreduce_rows_kernel, dim3(ctas), dim3(kCommThreads), 0, s, c, seq, a, (int)PH_PUSH));
         c.local_sync(c.local_ctx, c.rank, s);
         CCK(launch_pdl(allreduce_rows_kernel, dim3(ctas), dim3(kCommThreads), 0, s, c, seq, a, (int)PH_COMBINE));
     } else {
-        CCK(launch_pdl(allreduce_rows_kernel, dim3(ctas), dim3(kCommThreads), 0, s, c, seq, a, (int)PH_ALL));
+        CCK(launch_pdl(allreduce_rows_kernel, dim3(ctas), dim3(kCommThreads), 0, s, c, seq, a,
+                       a.prepushed ? (int)(PH_SYNC | PH_COMBINE) : (int)PH_ALL));
     }
+}
+
+// The receive slot that rank `c.rank` fills in every rank's region for the
+// NEXT collective call (its parity), as a GEMV epilogue push target.
+float* comm_push_slot(const CommView& c, int p) {
+    const uint64_t par = (c.seq + 1) & 1;
+    const int sender = c.loopback ? p : c.rank;
+    return c.peer_recv[p] + ((size_t)par * c.world + sender) * c.slot_floats;
 }
 
 // ---------------------------------------------------------------------------

@@ -1211,13 +1211,25 @@ public:
             return;
         }
         p.out = W.part; p.ldo = d;
+        // bf16 decode GEMV: its epilogue pushes the partial straight into every
+        // rank's receive slot (the all-reduce's push fused into the GEMV)
+        const bool fused = gemv_fused_push_ok(wdt, T) && (size_t)T * d <= comm_.slot_floats;
+        if (fused) set_push(p, 0);
         b.p[0] = p;
         g_gemv(M, kind, gemv_bytes(M, K, d, d, T, 1), EPI_STORE, b, 1, T, ps, kv);
         AllreduceArgs a;
+        a.prepushed = fused ? 1 : 0;
         a.rows = T; a.d = d; a.src = W.part; a.ld_src = d; a.mode = AR_RESID;
         a.out = W.h; a.ldo = d; a.resid = W.h; a.ldr = d; a.stats = W.stats; a.stat_tiles = tiles;
         launch_allreduce_rows(comm_, a, stream_);
         ++launches_;
+    }
+
+    // GEMV epilogue push targets: every rank's receive slot for the next
+    // collective call, rows from `row0` (packed [rows][d])
+    void set_push(GemvProblem& p, int row0) {
+        p.push_n = comm_.world;
+        for (int q = 0; q < comm_.world; ++q) p.push[q] = comm_push_slot(comm_, q) + (size_t)row0 * p.N;
     }
 
     // forward_sequential / forward_fuzzy (proj/src/draft_engine.cpp:35-133).
@@ -1306,6 +1318,9 @@ public:
                 row_parallel_resid(M, W, M.L[g[0]].wo, qd, b16 ? (const float*)W.mixed_b16 : W.mixed, qd, 2, T, ps, kv,
                                    nullptr, b16);
             } else {
+                // tensor-parallel drafter (not lp): the O partials go straight
+                // into the receive slots when one exchange carries the group
+                const bool fused = tp() && !M.lp && gemv_fused_push_ok(wdt, T) && (size_t)n * T * d <= comm_.slot_floats;
                 if (m > 0) {
                     GemvBatch ob;
                     for (int j = 0; j < m; ++j) {
@@ -1318,6 +1333,7 @@ public:
                         if (i == 0 && fuse) {  // h += attn_0 in the epilogue (+ row stats)
                             p.out = W.h; p.resid = W.h; p.ldr = d; p.stats_out = W.stats; p.stat_tiles_out = tiles;
                         }
+                        if (fused) set_push(p, i * T);
                         ob.p[j] = p;
                     }
                     g_gemv(M, 2, gemv_bytes(M, qd, d, d, T, m), EPI_STORE, ob, m, T, ps, kv);
@@ -1339,6 +1355,7 @@ public:
                         if (M.lp)
                             for (int b = 0; b < per && i0 + b < n; ++b)
                                 if (M.owner[g[i0 + b]] != comm_.rank) a.zero_blocks |= 1u << b;
+                        a.prepushed = fused ? 1 : 0;
                         launch_allreduce_rows(comm_, a, stream_);
                         ++launches_;
                     }

@@ -369,6 +369,8 @@ int gemv_col_tiles(int K, int N, int wdtype) {
     return gemv_plan(K, N).tiles;
 }
 
+bool gemv_fused_push_ok(int wdtype, int T) { return wdtype == DT_BF16 && !(g_prefill && T > 16); }
+
 void launch_gemv(int epi, int wdtype, const GemvBatch& b, int nprob, int T, const PassView& pass,
                  const KvView& kv, cudaStream_t s, SgPool* pool) {
     if (T <= 0 || nprob <= 0) return;

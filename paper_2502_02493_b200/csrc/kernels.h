@@ -81,6 +81,8 @@ struct PassView {
     int new_lo = 0;
 };
 
+constexpr int kMaxTp = 8;  // tensor-parallel group size limit
+
 struct GemvProblem {
     const void* W = nullptr;
     int K = 0, N = 0, ldw = 0;
@@ -124,6 +126,12 @@ struct GemvProblem {
     float* tc_rms = nullptr;
     float* tc_part = nullptr;        // split-K partial tiles (nullptr: no split)
     unsigned* tc_tickets = nullptr;
+    // EPI_STORE, bf16 decode GEMV: the tensor-parallel partial goes straight
+    // into every rank's NVLink receive slot (push[p] = rank p's slot for this
+    // rank and call, rows packed [t][N]) as each output tile finishes, instead
+    // of to `out` — the all-reduce's push phase fused into the GEMV epilogue
+    float* push[kMaxTp] = {};
+    int push_n = 0;
 };
 
 constexpr int kMaxProblems = 8;
@@ -187,6 +195,9 @@ size_t packed_elems(int K, int ldw);
 void launch_pack(const void* logical, int K, int ldw, void* packed, bool unpack, cudaStream_t s);
 
 // y = epilogue(norm?(x) · W) for T rows, over nprob same-shape problems.
+// true when launch_gemv(wdtype, T) runs the bf16 decode GEMV (the kernel with
+// the fused TP push epilogue), i.e. not the fp32 GEMV or the tcgen05 prefill
+bool gemv_fused_push_ok(int wdtype, int T);
 void launch_gemv(int epi, int wdtype, const GemvBatch& b, int nprob, int T, const PassView& pass,
                  const KvView& kv, cudaStream_t s, SgPool* pool = nullptr);
 
@@ -310,7 +321,6 @@ struct VerifyArgs {
 void launch_verify_sample(const VerifyArgs& a, cudaStream_t s);
 
 // ---- tensor-parallel collectives over NVLink peer memory (comm.cu) ----
-constexpr int kMaxTp = 8;
 constexpr int kCommErrTimeout = 6;  // engine error-slot code (see EngineImpl::sync_outcome)
 struct CommView {
     int rank = 0, world = 1;
@@ -357,6 +367,9 @@ struct AllreduceArgs {
     // rank contributes as exact zeros without reading src: the layer-parallel
     // placement's exchange, where only a slot's owner computed it
     unsigned zero_blocks = 0;
+    // every rank's slot was already filled by the producing GEMV's epilogue
+    // (GemvProblem::push): only signal, wait and combine
+    int prepushed = 0;
 };
 void launch_allreduce_rows(CommView& c, const AllreduceArgs& a, cudaStream_t s);
 struct GatherColsArgs {
@@ -367,6 +380,8 @@ struct GatherColsArgs {
     int ld_dst = 0;
 };
 void launch_allgather_cols(CommView& c, const GatherColsArgs& a, cudaStream_t s);
+// rank p's receive slot that this rank fills for the next collective call
+float* comm_push_slot(const CommView& c, int p);
 // vocab-parallel argmax: (val, idx) per row from every rank -> first maximum
 void launch_allgather_argmax(CommView& c, int T, const float* val, const int* idx, int* tok_out, cudaStream_t s);
 

@@ -52,9 +52,18 @@ __device__ __forceinline__ void sg_epilogue(const SgEpiCtx& L, const GemvProblem
             if (lane == 0) P.stats_out[(t0 + t) * P.stat_tiles_out + g] = sq;
         }
     } else if constexpr (EPI == EPI_STORE) {
+        if (P.push_n > 0) {
+            // tensor-parallel partial: straight into every rank's receive slot
+            // (NVLink stores, tile by tile as the GEMV finishes its columns)
 #pragma unroll
-        for (int t = 0; t < TM; ++t)
-            if (t < T && c < P.N) P.out[(size_t)(t0 + t) * P.ldo + c] = v[t];
+            for (int t = 0; t < TM; ++t)
+                if (t < T && c < P.N)
+                    for (int p = 0; p < P.push_n; ++p) P.push[p][(size_t)(t0 + t) * P.N + c] = v[t];
+        } else {
+#pragma unroll
+            for (int t = 0; t < TM; ++t)
+                if (t < T && c < P.N) P.out[(size_t)(t0 + t) * P.ldo + c] = v[t];
+        }
     }
     if constexpr (EPI == EPI_SILU) {
         // packed group = [gate 16 | up 16]: silu(gate) * up (proj/src/model.cpp:197-210)

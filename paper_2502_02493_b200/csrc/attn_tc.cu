@@ -114,6 +114,70 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
     for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(u[j]);
 }
 
+__device__ __forceinline__ uint32_t dsmem_addr(uint32_t local, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ float2 ld_dsmem2(uint32_t addr) {
+    float2 v;
+    asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr) : "memory");
+    return v;
+}
+__device__ __forceinline__ float4 ld_dsmem4(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(addr)
+                 : "memory");
+    return v;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// Fixed-order combine of one row's 16 output dims over the chunk partials
+// (values, max in the log2 domain, denominator): chunk weights 2^(m_ch - M),
+// denominator and weighted sum in chunk order, CB chunks' loads in flight per
+// round trip (CB changes only the load schedule, not the arithmetic). ml(ch) -> (m, l), x(ch, v) -> dims [4 v, 4 v + 4) of the slice.
+// One arithmetic for the combine kernel (global partials) and the cluster
+// path (partials in the cluster's shared memory), so a row is bit-identical
+// whichever path its pass takes.
+template <int CB, class ML, class X>
+__device__ __forceinline__ void tca_combine(int nchunks, ML ml, X x, float4 (&acc)[4], float& den) {
+    float M = -INFINITY;
+    for (int ch = 0; ch < nchunks; ++ch) M = fmaxf(M, ml(ch).x);
+#pragma unroll
+    for (int v = 0; v < 4; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    den = 0.f;
+    for (int ch0 = 0; ch0 < nchunks; ch0 += CB) {
+        float4 xv[CB][4];
+        float2 mv[CB];
+#pragma unroll
+        for (int q = 0; q < CB; ++q) {
+            const bool in = ch0 + q < nchunks;
+            mv[q] = in ? ml(ch0 + q) : make_float2(-INFINITY, 0.f);
+#pragma unroll
+            for (int v = 0; v < 4; ++v) xv[q][v] = in ? x(ch0 + q, v) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int q = 0; q < CB; ++q) {
+            if (ch0 + q >= nchunks) break;
+            float f = 0.f;
+            if (M != -INFINITY && mv[q].x != -INFINITY) {
+                f = tca_ex2(mv[q].x - M);
+                den = __fmaf_rn(f, mv[q].y, den);
+            }
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                acc[v].x = __fmaf_rn(f, xv[q][v].x, acc[v].x);
+                acc[v].y = __fmaf_rn(f, xv[q][v].y, acc[v].y);
+                acc[v].z = __fmaf_rn(f, xv[q][v].z, acc[v].z);
+                acc[v].w = __fmaf_rn(f, xv[q][v].w, acc[v].w);
+            }
+        }
+    }
+}
+
 struct TcaLaunch {
     CUtensorMap kvmap;  // 4-D swizzled view of the KV pool (tca_tensor_map)
     AttnBatch b;
@@ -121,6 +185,7 @@ struct TcaLaunch {
     KvView kv;
     int n_heads, G;
     unsigned long long* trace = nullptr;
+    int cluster = 0;  // 1: the chunks of a (kv head, pair group) form one cluster and combine through DSMEM
 };
 
 // Pages are processed in steps of two (pages 2s, 2s + 1 of the chunk): one
@@ -430,15 +495,43 @@ __global__ void __launch_bounds__(kTcaThreads, 1) attn_tc_kernel(const __grid_co
                         attn_store_row<DH>(A, off + c * 16, acc, l);
                     }
                 } else {
-                    float* wsrow = A.ws + (((size_t)bx * (n_kv * ngroups) + blockIdx.y) * kTcaRows + r) * PS;
+                    // chunk partial: to this CTA's shared memory (cluster path;
+                    // the ring is dead: every page's MMAs completed) or to the
+                    // split workspace for the combine kernel
+                    float* prow = L.cluster ? reinterpret_cast<float*>(sm + LY::kRing) + (size_t)r * PS
+                                            : A.ws + (((size_t)bx * (n_kv * ngroups) + blockIdx.y) * kTcaRows + r) * PS;
 #pragma unroll
                     for (int c = 0; c < DQ / 4; ++c)
-                        *reinterpret_cast<float4*>(wsrow + grp * DQ + 4 * c) =
+                        *reinterpret_cast<float4*>(prow + grp * DQ + 4 * c) =
                             make_float4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
-                    if (grp == 0) *reinterpret_cast<float2*>(wsrow + DH) = make_float2(m, l);
+                    if (grp == 0) *reinterpret_cast<float2*>(prow + DH) = make_float2(m, l);
                 }
             }
         }
+    }
+    if (L.cluster) {
+        __syncwarp();
+        // the cluster's CTAs hold the chunks of this (kv head, pair group):
+        // CTA c combines rows [c R / chunks, (c + 1) R / chunks) reading every
+        // chunk's partial from its shared memory, then waits until no CTA
+        // reads its own any more
+        cluster_sync_all();
+        const int R = min(kTcaRows, P - mg * kTcaRows);
+        const int r0 = bx * R / nchunks, r1 = (bx + 1) * R / nchunks;
+        const uint32_t part = smem_u32(sm + LY::kRing);
+        for (int it = tid; it < (r1 - r0) * (DH / 16) && tid < kTcaSoftmax; it += kTcaSoftmax) {
+            const int rr = r0 + it / (DH / 16), c0 = (it % (DH / 16)) * 16;
+            const uint32_t row = part + (uint32_t)(rr * PS) * 4u;
+            float4 acc[4];
+            float den;
+            tca_combine<2>(
+                nchunks, [&](int ch) { return ld_dsmem2(dsmem_addr(row + DH * 4, (uint32_t)ch)); },
+                [&](int ch, int v) { return ld_dsmem4(dsmem_addr(row + (uint32_t)(c0 + 4 * v) * 4u, (uint32_t)ch)); },
+                acc, den);
+            const int pp = mg * kTcaRows + rr;
+            attn_store_row<DH>(A, (size_t)(pp / G) * H * DH + (hk * G + pp % G) * DH + c0, acc, den);
+        }
+        cluster_sync_all();
     }
     // TMEM is no longer read: release it
     tca_fence_before();
@@ -473,42 +566,12 @@ __global__ void __launch_bounds__(32 * (DH / 16)) attn_tc_combine_kernel(const _
     if (r >= kTcaRows || p >= P) return;
     const size_t cstride = (size_t)(n_kv * ngroups) * kTcaRows * PS;
     const float* base = A.ws + ((size_t)by * kTcaRows + r) * PS;
-    float M = -INFINITY;
-    for (int ch = 0; ch < nchunks; ++ch) M = fmaxf(M, __ldcg(base + ch * cstride + DH));
     float4 acc[4];
-#pragma unroll
-    for (int v = 0; v < 4; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-    float den = 0.f;
-    constexpr int CB = 8;
-    for (int ch0 = 0; ch0 < nchunks; ch0 += CB) {
-        float4 x[CB][4];
-        float2 ml[CB];
-#pragma unroll
-        for (int q = 0; q < CB; ++q) {
-            const bool in = ch0 + q < nchunks;
-            const float* src = base + (ch0 + q) * cstride;
-            ml[q] = in ? __ldcg(reinterpret_cast<const float2*>(src + DH)) : make_float2(-INFINITY, 0.f);
-#pragma unroll
-            for (int v = 0; v < 4; ++v)
-                x[q][v] = in ? __ldcg(reinterpret_cast<const float4*>(src + c0 + 4 * v)) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-#pragma unroll
-        for (int q = 0; q < CB; ++q) {
-            if (ch0 + q >= nchunks) break;
-            float f = 0.f;
-            if (M != -INFINITY && ml[q].x != -INFINITY) {
-                f = tca_ex2(ml[q].x - M);
-                den = __fmaf_rn(f, ml[q].y, den);
-            }
-#pragma unroll
-            for (int v = 0; v < 4; ++v) {
-                acc[v].x = __fmaf_rn(f, x[q][v].x, acc[v].x);
-                acc[v].y = __fmaf_rn(f, x[q][v].y, acc[v].y);
-                acc[v].z = __fmaf_rn(f, x[q][v].z, acc[v].z);
-                acc[v].w = __fmaf_rn(f, x[q][v].w, acc[v].w);
-            }
-        }
-    }
+    float den;
+    tca_combine<8>(
+        nchunks, [&](int ch) { return __ldcg(reinterpret_cast<const float2*>(base + ch * cstride + DH)); },
+        [&](int ch, int v) { return __ldcg(reinterpret_cast<const float4*>(base + ch * cstride + c0 + 4 * v)); }, acc,
+        den);
     attn_store_row<DH>(A, (size_t)(p / G) * H * DH + (hk * G + p % G) * DH + c0, acc, den);
 }
 
@@ -551,6 +614,18 @@ static void tca_tensor_map(CUtensorMap& m, const KvView& kv) {
     if (r != CUDA_SUCCESS)
         dev_fail(DEV_ERR_CUDA, "attention: cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
     cache.push_back({kv.pool, kv.page_elems, kv.n_layers, kv.n_kv, kv.dh, kv.pool_pages, m});
+}
+
+// Chunks of one (kv head, pair group) combine inside their cluster when
+// they fit one (2..ESPEC_ATTN_CLUSTER CTAs, default 16: above the portable 8
+// the kernel opts in to non-portable clusters): no workspace round trip, no
+// combine launch. ESPEC_ATTN_CLUSTER=0 keeps the combine kernel.
+int attn_tc_cluster(int chunks) {
+    static const int cap = [] {
+        const char* e = std::getenv("ESPEC_ATTN_CLUSTER");
+        return e ? std::min(16, std::atoi(e)) : 16;
+    }();
+    return chunks >= 2 && chunks <= cap ? 1 : 0;
 }
 
 template <int DH>
@@ -596,8 +671,20 @@ static void attn_tc_launch(const AttnBatch& b, int nprob, int n_heads, const Pas
         L.trace = tbuf;
         traced = true;
     }
-    DEV_CK(launch_pdl(attn_tc_kernel<DH>, grid, dim3(kTcaThreads), smem, s, L));
-    if (chunks > 1) {
+    L.cluster = attn_tc_cluster(chunks);
+    if (L.cluster && chunks > 8) {
+        static bool nonportable = false;
+        if (!nonportable) {
+            DEV_CK(cudaFuncSetAttribute((const void*)attn_tc_kernel<DH>,
+                                        cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            nonportable = true;
+        }
+    }
+    if (L.cluster)
+        DEV_CK(launch_pdl_cluster(attn_tc_kernel<DH>, grid, dim3(kTcaThreads), smem, s, chunks, L));
+    else
+        DEV_CK(launch_pdl(attn_tc_kernel<DH>, grid, dim3(kTcaThreads), smem, s, L));
+    if (chunks > 1 && !L.cluster) {
         const int rows = std::min(kTcaRows, pass.T * L.G);
         DEV_CK(launch_pdl(attn_tc_combine_kernel<DH>, dim3((rows + 31) / 32, kv.n_kv * groups, nprob),
                           dim3(32 * (DH / 16)), 0, s, L, chunks));

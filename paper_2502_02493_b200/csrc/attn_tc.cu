@@ -617,13 +617,15 @@ static void tca_tensor_map(CUtensorMap& m, const KvView& kv) {
 }
 
 // Chunks of one (kv head, pair group) combine inside their cluster when
-// they fit one (2..ESPEC_ATTN_CLUSTER CTAs, default 16: above the portable 8
-// the kernel opts in to non-portable clusters): no workspace round trip, no
-// combine launch. ESPEC_ATTN_CLUSTER=0 keeps the combine kernel.
+// they fit one (2..ESPEC_ATTN_CLUSTER CTAs, default the portable 8; up to 16
+// opts in to non-portable clusters, which measured 1.8x slower at 16 chunks
+// as a 16-SM cluster rarely finds a free GPC): no workspace round trip, no
+// combine launch (~1 us per attention isolated, profiles/r2_cluster.txt).
+// ESPEC_ATTN_CLUSTER=0 keeps the combine kernel.
 int attn_tc_cluster(int chunks) {
     static const int cap = [] {
         const char* e = std::getenv("ESPEC_ATTN_CLUSTER");
-        return e ? std::min(16, std::atoi(e)) : 16;
+        return e ? std::min(16, std::atoi(e)) : 8;
     }();
     return chunks >= 2 && chunks <= cap ? 1 : 0;
 }

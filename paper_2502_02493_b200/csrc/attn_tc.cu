@@ -116,19 +116,20 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 
 __device__ __forceinline__ uint32_t dsmem_addr(uint32_t local, uint32_t rank) {
     uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+    asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
     return r;
 }
 __device__ __forceinline__ float2 ld_dsmem2(uint32_t addr) {
     float2 v;
-    asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr) : "memory");
+    asm("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
     return v;
 }
 __device__ __forceinline__ float4 ld_dsmem4(uint32_t addr) {
     float4 v;
-    asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                 : "r"(addr)
-                 : "memory");
+    // not volatile: ordered by the cluster barriers around the combine, so
+    // the loads of one row's chunks can all be in flight at once
+    asm("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+        : "r"(addr));
     return v;
 }
 __device__ __forceinline__ void cluster_sync_all() {
@@ -178,6 +179,12 @@ __device__ __forceinline__ void tca_combine(int nchunks, ML ml, X x, float4 (&ac
     }
 }
 
+// ESPEC_ATTN_TRACE slots per CTA (%globaltimer): 0 start, 1 past
+// griddepcontrol.wait, 2 first K page, 3 pages done, 4 end, 5 cluster
+// synced; per step s < 8: 8+s QK(s) issued, 16+s PV(s) issued (MMA thread),
+// 24+s S(s) seen, 32+s PV(s) seen, 40+s P(s) written (softmax thread 0)
+constexpr int kTcaTraceSlots = 48;
+
 struct TcaLaunch {
     CUtensorMap kvmap;  // 4-D swizzled view of the KV pool (tca_tensor_map)
     AttnBatch b;
@@ -226,7 +233,7 @@ __global__ void __launch_bounds__(kTcaThreads, 1) attn_tc_kernel(const __grid_co
     int* s_page = reinterpret_cast<int*>(sm + LY::kBars + 256);
     float* red = reinterpret_cast<float*>(sm + LY::kRed);  // [4][128]
     unsigned long long* tr =
-        L.trace ? L.trace + (((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 8 : nullptr;
+        L.trace ? L.trace + (((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * kTcaTraceSlots : nullptr;
     auto kbuf = [&](int st) { return sm + LY::kRing + st * LY::kStage; };
     auto vbuf = [&](int st) { return sm + LY::kRing + st * LY::kStage + LY::kStage / 2; };
     auto pbuf = [&](int s, int pp) {  // P tile of page 2 s + pp
@@ -306,6 +313,7 @@ __global__ void __launch_bounds__(kTcaThreads, 1) attn_tc_kernel(const __grid_co
                                 tca_desc(qaddr + (kk >> 2) * (kTcaRows * 128) + (kk & 3) * 32, 16, 1024),
                                 tca_desc(kaddr + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024), id_s, kk > 0);
                 }
+                if (tr && s < 8) tr[8 + s] = gtimer();
                 tca_commit(&s_full[s & 1]);
             };
             mbar_wait(q_full, 0);
@@ -313,12 +321,23 @@ __global__ void __launch_bounds__(kTcaThreads, 1) attn_tc_kernel(const __grid_co
             if (nsteps > 0) qk(0);
             for (int s = 0; s < nsteps; ++s) {
                 const int b = s & 1;
+                // refill the previous step's stages with the pages of step
+                // s + 2 as soon as PV(s - 1) (issued one iteration ago) has
+                // released them, before this step's waits
+                if (s >= 1)
+                    for (int pp = 0; pp < 2; ++pp) {
+                        const int j = 2 * (s - 1) + pp;
+                        if (j + S >= n) break;
+                        mbar_wait(&kv_empty[j % S], (uint32_t)(j / S) & 1u);
+                        issue(j + S, s_page[j + S]);
+                    }
                 if (s + 1 < nsteps) qk(s + 1);
                 mbar_wait(&p_full[b], (uint32_t)(s >> 1) & 1u);
                 if (s >= 2) mbar_wait(&pv_free[b], (uint32_t)((s - 2) >> 1) & 1u);
                 for (int pp = 0; pp < 2 && 2 * s + pp < n; ++pp) {
                     const int i = 2 * s + pp, st = i % S;
                     mbar_wait(&v_full[st], (uint32_t)(i / S) & 1u);
+                    if (tr && pp == 0 && s < 8) tr[16 + s] = gtimer();
                     tca_fence_after();
                     const uint32_t paddr = smem_u32(pbuf(s, pp)), vaddr = smem_u32(vbuf(st));
 #pragma unroll
@@ -328,15 +347,6 @@ __global__ void __launch_bounds__(kTcaThreads, 1) attn_tc_kernel(const __grid_co
                 }
                 tca_commit(&pv_full[b]);
                 for (int pp = 0; pp < 2 && 2 * s + pp < n; ++pp) tca_commit(&kv_empty[(2 * s + pp) % S]);
-                // refill the previous step's stages with the pages of step s + 2
-                // (the previous step's PV was issued one iteration ago)
-                if (s >= 1)
-                    for (int pp = 0; pp < 2; ++pp) {
-                        const int j = 2 * (s - 1) + pp;
-                        if (j + S >= n) break;
-                        mbar_wait(&kv_empty[j % S], (uint32_t)(j / S) & 1u);
-                        issue(j + S, s_page[j + S]);
-                    }
             }
         }
     } else {
@@ -385,6 +395,7 @@ __global__ void __launch_bounds__(kTcaThreads, 1) attn_tc_kernel(const __grid_co
         auto fold = [&](int s) {  // o = o * alpha(s) + PV(s) over this thread's dims
             const int b = s & 1;
             mbar_wait(&pv_full[b], (uint32_t)(s >> 1) & 1u);
+            if (tr && tid == 0 && s < 8) tr[32 + s] = gtimer();
             if (idle) {
                 mbar_arrive(&pv_free[b]);
                 return;
@@ -403,6 +414,7 @@ __global__ void __launch_bounds__(kTcaThreads, 1) attn_tc_kernel(const __grid_co
         for (int s = 0; s < nsteps; ++s) {
             const int b = s & 1;
             mbar_wait(&s_full[b], (uint32_t)(s >> 1) & 1u);
+            if (tr && tid == 0 && s < 8) tr[24 + s] = gtimer();
             if (idle) {
                 if (s > 0) fold(s - 1);
                 mbar_arrive(&p_full[b]);
@@ -474,6 +486,7 @@ __global__ void __launch_bounds__(kTcaThreads, 1) attn_tc_kernel(const __grid_co
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             tca_fence_before();
             mbar_arrive(&p_full[b]);
+            if (tr && tid == 0 && s < 8) tr[40 + s] = gtimer();
         }
         if (nsteps > 0) fold(nsteps - 1);
         if (!idle) {  // (an idle quarter's four warps skip this together)
@@ -516,6 +529,7 @@ __global__ void __launch_bounds__(kTcaThreads, 1) attn_tc_kernel(const __grid_co
         // chunk's partial from its shared memory, then waits until no CTA
         // reads its own any more
         cluster_sync_all();
+        if (tr && tid == 0) tr[5] = gtimer();
         const int R = min(kTcaRows, P - mg * kTcaRows);
         const int r0 = bx * R / nchunks, r1 = (bx + 1) * R / nchunks;
         const uint32_t part = smem_u32(sm + LY::kRing);
@@ -524,7 +538,7 @@ __global__ void __launch_bounds__(kTcaThreads, 1) attn_tc_kernel(const __grid_co
             const uint32_t row = part + (uint32_t)(rr * PS) * 4u;
             float4 acc[4];
             float den;
-            tca_combine<2>(
+            tca_combine<4>(
                 nchunks, [&](int ch) { return ld_dsmem2(dsmem_addr(row + DH * 4, (uint32_t)ch)); },
                 [&](int ch, int v) { return ld_dsmem4(dsmem_addr(row + (uint32_t)(c0 + 4 * v) * 4u, (uint32_t)ch)); },
                 acc, den);
@@ -653,9 +667,7 @@ static void attn_tc_launch(const AttnBatch& b, int nprob, int n_heads, const Pas
     static unsigned long long configured = 0;
     ensure_smem((const void*)attn_tc_kernel<DH>, (int)smem, configured);
     // diagnostic: ESPEC_ATTN_TRACE=T,n traces the n-th launch with T pass rows
-    // (per CTA %globaltimer: 0 start, 1 past griddepcontrol.wait, 2 first K
-    // page, 3 pages done, 4 partial written, 5 combine done) into
-    // gpurun_out/attn_trace.txt
+    // (kTcaTraceSlots %globaltimer stamps per CTA) into gpurun_out/attn_trace.txt
     static int tT = -1, tn = -1;
     static bool parsed = false;
     if (!parsed) {
@@ -667,8 +679,8 @@ static void attn_tc_launch(const AttnBatch& b, int nprob, int n_heads, const Pas
     const size_t nblk = (size_t)grid.x * grid.y * grid.z;
     bool traced = false;
     if (tn >= 0 && pass.T == tT && seen++ == tn && nblk <= 4096) {
-        if (!tbuf) DEV_CK(cudaMalloc(&tbuf, sizeof(unsigned long long) * 8 * 4096));
-        DEV_CK(cudaMemset(tbuf, 0, sizeof(unsigned long long) * 8 * 4096));
+        if (!tbuf) DEV_CK(cudaMalloc(&tbuf, sizeof(unsigned long long) * kTcaTraceSlots * 4096));
+        DEV_CK(cudaMemset(tbuf, 0, sizeof(unsigned long long) * kTcaTraceSlots * 4096));
         DEV_CK(cudaDeviceSynchronize());
         L.trace = tbuf;
         traced = true;
@@ -692,14 +704,14 @@ static void attn_tc_launch(const AttnBatch& b, int nprob, int n_heads, const Pas
                           dim3(32 * (DH / 16)), 0, s, L, chunks));
     }
     if (traced) {
-        std::vector<unsigned long long> h(8 * nblk);
+        std::vector<unsigned long long> h(kTcaTraceSlots * nblk);
         DEV_CK(cudaStreamSynchronize(s));
         DEV_CK(cudaMemcpy(h.data(), tbuf, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost));
         if (FILE* f = std::fopen("gpurun_out/attn_trace.txt", "w")) {
             std::fprintf(f, "grid %d %d %d T %d total %d ppi %d\n", grid.x, grid.y, grid.z, pass.T, pass.total,
                          kv.attn_ppi);
             for (size_t i = 0; i < nblk; ++i) {
-                for (int e = 0; e < 8; ++e) std::fprintf(f, " %llu", h[i * 8 + e]);
+                for (int e = 0; e < kTcaTraceSlots; ++e) std::fprintf(f, " %llu", h[i * kTcaTraceSlots + e]);
                 std::fprintf(f, "\n");
             }
             std::fclose(f);

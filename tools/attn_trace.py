@@ -1,7 +1,8 @@
-"""Summarise an attention timeline (ESPEC_ATTN_TRACE=n): per CTA the times of
-start, dependency release, first K page, pages done, partial written and (the
-last CTA of each kv head / m-tile) combine done, in us relative to the earliest
-CTA start."""
+"""Summarise an attention timeline (ESPEC_ATTN_TRACE=T,n; slots in attn_tc.cu
+kTcaTraceSlots): per CTA the times of start, dependency release, first K page,
+pages done, end and cluster sync in us relative to the earliest CTA start, then
+the per-step pipeline (median over CTAs, us from the CTA's first K page):
+QK(s) issued, S(s) seen by softmax, P(s) written, PV(s) issued, PV(s) seen."""
 import sys
 
 import numpy as np
@@ -10,10 +11,19 @@ lines = open(sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/attn_trace.txt").
 print(lines[0])
 t = np.array([[int(x) for x in l.split()] for l in lines[1:] if l.strip()], dtype=np.int64)
 t0 = t[t[:, 0] > 0, 0].min()
-names = ["cta start", "dep released", "first K page", "pages done", "partial written", "combine done",
-         "cluster synced", "rank0 combined"]
-for e, n in sorted(enumerate(names), key=lambda x: [0, 1, 2, 3, 4, 6, 7, 5][x[0]]):
+names = {0: "cta start", 1: "dep released", 2: "first K page", 3: "pages done", 5: "cluster synced", 4: "end"}
+for e in (0, 1, 2, 3, 5, 4):
     v = t[:, e]
     v = (v[v > 0] - t0) / 1e3
     if len(v):
-        print(f"  {n:18s} n {len(v):4d} min {v.min():8.2f}  median {np.median(v):8.2f}  max {v.max():8.2f} us")
+        print(f"  {names[e]:18s} n {len(v):4d} min {v.min():8.2f}  median {np.median(v):8.2f}  max {v.max():8.2f} us")
+if t.shape[1] >= 48:
+    print("  step   QK issued   S seen  P written  PV issued  PV seen   (median us from first K page)")
+    k0 = t[:, 2]
+    for s in range(8):
+        cols = [8 + s, 24 + s, 40 + s, 16 + s, 32 + s]
+        ok = (t[:, cols] > 0).all(axis=1) & (k0 > 0)
+        if not ok.any():
+            break
+        med = [np.median((t[ok, c] - k0[ok]) / 1e3) for c in cols]
+        print(f"  {s:4d} " + " ".join(f"{x:9.2f}" for x in med))

@@ -68,7 +68,7 @@ struct TcaLayout {
     static constexpr bool kPInK = DH >= 128;
     static constexpr int kP = kRing + kTcaStages * kStage;
     static constexpr int kPBuf = kTcaRows * 64 * 2;
-    static constexpr int kRed = kP + (kPInK ? 0 : 4 * kPBuf);      // [4][128] partial row maxima / sums
+    static constexpr int kRed = kP + (kPInK ? 0 : 4 * kPBuf);      // [workers][rows] partial row maxima / sums (512)
     static constexpr int kBars = kRed + 4 * kTcaRows * 4;          // mbarriers, tmem base, page table
     static constexpr int kBytes = kBars + 256 + 4 * kTcaMaxPpi;
 };
@@ -112,6 +112,46 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
     for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(u[j]);
+}
+
+// the scores of one worker in both pages of a step: KW columns at each of two
+// TMEM addresses, one wait
+template <int KW>
+__device__ __forceinline__ void tmem_ld_pair(uint32_t a0, uint32_t a1, float (&v0)[KW], float (&v1)[KW]) {
+    if constexpr (KW == 16) {
+        tmem_ld16(a0, v0);
+        tmem_ld16(a1, v1);
+    } else if constexpr (KW == 8) {
+        uint32_t u[16];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%16];\n"
+            "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%8,%9,%10,%11,%12,%13,%14,%15}, [%17];\n"
+            "tcgen05.wait::ld.sync.aligned;"
+            : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7]),
+              "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]), "=r"(u[14]), "=r"(u[15])
+            : "r"(a0), "r"(a1)
+            : "memory");
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            v0[j] = __uint_as_float(u[j]);
+            v1[j] = __uint_as_float(u[8 + j]);
+        }
+    } else {
+        static_assert(KW == 4, "4, 8 or 16 keys per worker");
+        uint32_t u[8];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%8];\n"
+            "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%4,%5,%6,%7}, [%9];\n"
+            "tcgen05.wait::ld.sync.aligned;"
+            : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7])
+            : "r"(a0), "r"(a1)
+            : "memory");
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            v0[j] = __uint_as_float(u[j]);
+            v1[j] = __uint_as_float(u[4 + j]);
+        }
+    }
 }
 
 __device__ __forceinline__ uint32_t dsmem_addr(uint32_t local, uint32_t rank) {
@@ -182,8 +222,10 @@ __device__ __forceinline__ void tca_combine(int nchunks, ML ml, X x, float4 (&ac
 // ESPEC_ATTN_TRACE slots per CTA (%globaltimer): 0 start, 1 past
 // griddepcontrol.wait, 2 first K page, 3 pages done, 4 end, 5 cluster
 // synced; per step s < 8: 8+s QK(s) issued, 16+s PV(s) issued (MMA thread),
-// 24+s S(s) seen, 32+s PV(s) seen, 40+s P(s) written (softmax thread 0)
-constexpr int kTcaTraceSlots = 48;
+// 24+s S(s) seen, 32+s PV(s) seen, 40+s P(s) written (softmax thread 0);
+// step 2 phases (softmax thread 0): 48 scores loaded, 49 row max exchanged,
+// 50 exponentials summed, 51 fold done, 52 P stored
+constexpr int kTcaTraceSlots = 64;
 
 struct TcaLaunch {
     CUtensorMap kvmap;  // 4-D swizzled view of the KV pool (tca_tensor_map)
@@ -197,8 +239,9 @@ struct TcaLaunch {
 
 // Pages are processed in steps of two (pages 2s, 2s + 1 of the chunk): one
 // softmax round trip (scores, row max, probabilities, output fold) per step.
-template <int DH>
+template <int DH, int REP>
 __global__ void __launch_bounds__(kTcaThreads, 1) attn_tc_kernel(const __grid_constant__ TcaLaunch L) {
+    static_assert(REP == 1 || REP == 2 || REP == 4, "row copies per tile");
     using LY = TcaLayout<DH>;
     constexpr int S = kTcaStages;   // = two steps of two pages
     constexpr int PS = DH + 4;      // workspace row: DH values, max, denominator
@@ -231,7 +274,7 @@ __global__ void __launch_bounds__(kTcaThreads, 1) attn_tc_kernel(const __grid_co
     uint64_t* pv_free = pv_full + 2;    // [2]  PV tile read (softmax arrivals)
     uint32_t* s_tmem = reinterpret_cast<uint32_t*>(pv_free + 2);
     int* s_page = reinterpret_cast<int*>(sm + LY::kBars + 256);
-    float* red = reinterpret_cast<float*>(sm + LY::kRed);  // [4][128]
+    float* red = reinterpret_cast<float*>(sm + LY::kRed);  // [4 REP workers][128 / REP rows]
     unsigned long long* tr =
         L.trace ? L.trace + (((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * kTcaTraceSlots : nullptr;
     auto kbuf = [&](int st) { return sm + LY::kRing + st * LY::kStage; };
@@ -351,11 +394,28 @@ __global__ void __launch_bounds__(kTcaThreads, 1) attn_tc_kernel(const __grid_co
         }
     } else {
         // ---------------- softmax warps
+        // REP copies of the group's rows fill the 128-row tile (REP 4: <= 32
+        // rows, 2: <= 64, else 1): tile row t holds pair row t % R, so every
+        // TMEM lane quarter (a warp reads only its own quarter's lanes) has
+        // live rows, and the 4 REP warps of a row split its keys: KW = 16 /
+        // REP keys of each page per worker (the exponentials per warp fall by
+        // REP and spread over all four SM sub-partitions). A row's arithmetic
+        // does not depend on REP (batch invariance): 16 key units of 4 keys
+        // per page, each with its own running denominator, summed by one
+        // pairwise tree at the end.
+        constexpr int R = kTcaRows / REP;  // canonical rows
+        constexpr int KW = 16 / REP;       // keys of each page per worker
+        constexpr int U = KW / 4;          // key units per worker
+        constexpr int NW = 4 * REP;        // workers per row
         const int qtr = warp & 3, grp = warp >> 2;
-        const int r = qtr * 32 + lane;  // query pair row = TMEM lane
+        const int t = qtr * 32 + lane;  // tile row = TMEM lane
+        const int r = t % R;            // the pair row it holds
+        const int w = (t / R) * 4 + grp;  // worker: keys [w KW, w KW + KW) of each page
+        const bool owner = t < R;       // copy 0: folds PV and holds output dims [grp DQ, grp DQ + DQ)
         const int p = mg * kTcaRows + r;
         const bool valid = p < P;
-        const int bar_row = 2 + qtr;  // named barrier of the four warps sharing these rows
+        const int bar_row = 2 + qtr % (4 / REP);  // named barrier of the 4 REP warps sharing these rows
+        constexpr int bar_n = 128 * REP;
         int ve = 0;
         unsigned long long an = 0ull;
         {
@@ -365,7 +425,7 @@ __global__ void __launch_bounds__(kTcaThreads, 1) attn_tc_kernel(const __grid_co
                 ve = pass.vis_end[p / G];
                 an = pass.anc[p / G];
             }
-            unsigned char* qrow = sm + LY::kQ + r * 128;
+            unsigned char* qrow = sm + LY::kQ + t * 128;
 #pragma unroll
             for (int cc = 0; cc < DQ / 8; ++cc) {  // 16-byte chunks of 8 dims
                 const int c = grp * (DQ / 8) + cc;
@@ -376,7 +436,7 @@ __global__ void __launch_bounds__(kTcaThreads, 1) attn_tc_kernel(const __grid_co
                 }
                 const uint4 u = make_uint4(pack_bf16x2(a.x, a.y), pack_bf16x2(a.z, a.w), pack_bf16x2(b.x, b.y),
                                            pack_bf16x2(b.z, b.w));
-                *reinterpret_cast<uint4*>(qrow + (c >> 3) * (kTcaRows * 128) + (((c & 7) ^ (r & 7)) * 16)) = u;
+                *reinterpret_cast<uint4*>(qrow + (c >> 3) * (kTcaRows * 128) + (((c & 7) ^ (t & 7)) * 16)) = u;
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_arrive(q_full);
@@ -384,19 +444,22 @@ __global__ void __launch_bounds__(kTcaThreads, 1) attn_tc_kernel(const __grid_co
         const int vmin = valid ? min(ve, pass.total) : 0x7fffffff;
         // scores in the log2 domain: s * log2(e) / sqrt(dh), probabilities by ex2
         const float qscale = 1.4426950408889634f / sqrtf((float)DH);
-        // a lane quarter with no valid pair (e.g. rows 64-127 of a 48-pair
+        // a lane quarter with no valid pair (e.g. rows 64-127 of a 96-pair
         // pass) only keeps the barrier counts: its P / PV rows are never read
-        const bool idle = mg * kTcaRows + qtr * 32 >= P;
+        const bool idle = mg * kTcaRows + (qtr * 32) % R >= P;
         const uint32_t trow = tmem + ((uint32_t)(qtr * 32) << 16);
         float o[DQ];
 #pragma unroll
         for (int d = 0; d < DQ; ++d) o[d] = 0.f;
-        float m = -INFINITY, l = 0.f, alpha_prev = 0.f;
+        float m = -INFINITY, alpha_prev = 0.f;
+        float lu[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) lu[u] = 0.f;
         auto fold = [&](int s) {  // o = o * alpha(s) + PV(s) over this thread's dims
             const int b = s & 1;
             mbar_wait(&pv_full[b], (uint32_t)(s >> 1) & 1u);
             if (tr && tid == 0 && s < 8) tr[32 + s] = gtimer();
-            if (idle) {
+            if (idle || !owner) {
                 mbar_arrive(&pv_free[b]);
                 return;
             }
@@ -421,81 +484,109 @@ __global__ void __launch_bounds__(kTcaThreads, 1) attn_tc_kernel(const __grid_co
                 continue;
             }
             tca_fence_after();
-            // this thread's keys: [16 grp, 16 grp + 16) of each page of the step
-            float sc[2][16];
-            tmem_ld16(trow + b * 128 + grp * 16, sc[0]);
-            tmem_ld16(trow + b * 128 + 64 + grp * 16, sc[1]);
+            // this worker's keys of each page of the step
+            float sc[2][KW];
+            tmem_ld_pair<KW>(trow + b * 128 + w * KW, trow + b * 128 + 64 + w * KW, sc[0], sc[1]);
+            const bool ph = tr && tid == 0 && s == 2;
+            if (ph) tr[48] = gtimer();
             float mx = -INFINITY;
 #pragma unroll
             for (int pp = 0; pp < 2; ++pp) {
-                const int j0 = (pg0 + 2 * s + pp) * 64 + grp * 16;
-                if (j0 + 16 <= vmin) {  // below every causal prefix: no per-key test
+                const int j0 = (pg0 + 2 * s + pp) * 64 + w * KW;
+                if (j0 + KW <= vmin) {  // below every causal prefix: no per-key test
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) {
+                    for (int j = 0; j < KW; ++j) {
                         sc[pp][j] = __fmul_rn(sc[pp][j], qscale);
                         mx = fmaxf(mx, sc[pp][j]);
                     }
                 } else {
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) {
+                    for (int j = 0; j < KW; ++j) {
                         const bool ok = valid && visible_rows(pass, ve, an, j0 + j);
                         sc[pp][j] = ok ? __fmul_rn(sc[pp][j], qscale) : -INFINITY;
                         mx = fmaxf(mx, sc[pp][j]);
                     }
                 }
             }
-            // row max over the four key groups, fixed order (the second
-            // barrier: every group has read before the next step writes)
-            red[grp * kTcaRows + r] = mx;
-            named_bar(bar_row, 128);
-            mx = fmaxf(fmaxf(red[r], red[kTcaRows + r]), fmaxf(red[2 * kTcaRows + r], red[3 * kTcaRows + r]));
-            named_bar(bar_row, 128);
+            // row max over the workers (exact in any order; the second
+            // barrier: every worker has read before the next step writes)
+            red[w * R + r] = mx;
+            named_bar(bar_row, bar_n);
+#pragma unroll
+            for (int k = 0; k < NW; ++k) mx = fmaxf(mx, red[k * R + r]);
+            named_bar(bar_row, bar_n);
+            if (ph) tr[49] = gtimer();
             const float mn = fmaxf(m, mx);
             // rescale of the running sums (exactly 1 while the max holds, 0
             // while nothing was visible yet)
             const float alpha = m == -INFINITY ? 0.f : (mn == m ? 1.f : tca_ex2(m - mn));
             m = mn;
-            float sum = 0.f;
             const float mo = m == -INFINITY ? 0.f : m;  // ex2(-inf - 0) = 0 for masked keys
 #pragma unroll
             for (int pp = 0; pp < 2; ++pp)
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    sc[pp][j] = tca_ex2(sc[pp][j] - mo);
-                    sum += sc[pp][j];
-                }
-            l = __fmaf_rn(l, alpha, sum);  // this group's share of the denominator
-            if (s > 0) fold(s - 1);
-            alpha_prev = alpha;
+                for (int j = 0; j < KW; ++j) sc[pp][j] = tca_ex2(sc[pp][j] - mo);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {  // a unit's 8 keys of the step in order
+                float su = 0.f;
+#pragma unroll
+                for (int pp = 0; pp < 2; ++pp)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) su += sc[pp][4 * u + j];
+                lu[u] = __fmaf_rn(lu[u], alpha, su);
+            }
+            if (ph) tr[50] = gtimer();
             // P (bf16) -> the K-major 128-byte-swizzled tile of each page of the
-            // step (its K buffer, dead since QK(s) completed, or a P buffer
-            // whose previous reader PV(s - 2) completed before fold(s - 2))
+            // step, row r (its K buffer, dead since QK(s) completed, or a P
+            // buffer whose previous reader PV(s - 2) completed before fold(s - 2))
 #pragma unroll
             for (int pp = 0; pp < 2; ++pp) {
                 if (pp == 1 && 2 * s + 1 >= n) break;
                 unsigned char* prow = pbuf(s, pp) + r * 128;
+                const float* v = sc[pp];
+                if constexpr (KW >= 8) {
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int c = grp * 2 + h;
-                    const float* v = sc[pp] + 8 * h;
-                    const uint4 u = make_uint4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]),
-                                               pack_bf16x2(v[4], v[5]), pack_bf16x2(v[6], v[7]));
-                    *reinterpret_cast<uint4*>(prow + ((c ^ (r & 7)) * 16)) = u;
+                    for (int h = 0; h < KW / 8; ++h) {
+                        const int c = w * (KW / 8) + h;
+                        const uint4 u = make_uint4(pack_bf16x2(v[8 * h], v[8 * h + 1]), pack_bf16x2(v[8 * h + 2], v[8 * h + 3]),
+                                                   pack_bf16x2(v[8 * h + 4], v[8 * h + 5]), pack_bf16x2(v[8 * h + 6], v[8 * h + 7]));
+                        *reinterpret_cast<uint4*>(prow + ((c ^ (r & 7)) * 16)) = u;
+                    }
+                } else {
+                    const int c = w >> 1;
+                    *reinterpret_cast<uint2*>(prow + ((c ^ (r & 7)) * 16) + (w & 1) * 8) =
+                        make_uint2(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]));
                 }
             }
+            if (ph) tr[52] = gtimer();
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             tca_fence_before();
             mbar_arrive(&p_full[b]);
             if (tr && tid == 0 && s < 8) tr[40 + s] = gtimer();
+            // the previous step's PV (issued one step ago) into the output
+            if (s > 0) fold(s - 1);
+            if (ph) tr[51] = gtimer();
+            alpha_prev = alpha;
         }
         if (nsteps > 0) fold(nsteps - 1);
-        if (!idle) {  // (an idle quarter's four warps skip this together)
-            // the row's denominator: the four groups' shares in fixed order
-            red[grp * kTcaRows + r] = l;
-            named_bar(bar_row, 128);
-            l = ((red[r] + red[kTcaRows + r]) + red[2 * kTcaRows + r]) + red[3 * kTcaRows + r];
+        if (!idle) {  // (an idle quarter's warps skip this together)
+            // the row's denominator: the pairwise tree over the 16 key units
+            // (each worker's own units first, then the workers')
+            float lw = lu[0];
+            if constexpr (U == 2) lw = lu[0] + lu[1];
+            if constexpr (U == 4) lw = (lu[0] + lu[1]) + (lu[2] + lu[3]);
+            red[w * R + r] = lw;
+            named_bar(bar_row, bar_n);
+            float v[NW];
+#pragma unroll
+            for (int k = 0; k < NW; ++k) v[k] = red[k * R + r];
+#pragma unroll
+            for (int k = NW; k > 1; k >>= 1)
+#pragma unroll
+                for (int i = 0; i < k / 2; ++i) v[i] = v[2 * i] + v[2 * i + 1];
+            const float l = v[0];
             if (tr && tid == 0) atomicMax(tr + 3, gtimer());
-            if (valid) {
+            if (valid && owner) {
                 if (nchunks == 1) {
                     const size_t off = (size_t)(p / G) * H * DH + (hk * G + p % G) * DH + grp * DQ;
 #pragma unroll
@@ -664,8 +755,17 @@ static void attn_tc_launch(const AttnBatch& b, int nprob, int n_heads, const Pas
     dim3 grid(chunks, kv.n_kv * groups, nprob);
     const size_t smem = TcaLayout<DH>::kBytes;
     static_assert(TcaLayout<128>::kBytes <= 227 * 1024, "attention tiles exceed the shared-memory opt-in");
-    static unsigned long long configured = 0;
-    ensure_smem((const void*)attn_tc_kernel<DH>, (int)smem, configured);
+    // row copies per tile: all four TMEM lane quarters busy for small passes
+    // (ESPEC_ATTN_REP=1 forces one copy; the results do not depend on it)
+    static const int rep_cap = [] {
+        const char* e = std::getenv("ESPEC_ATTN_REP");
+        return e ? std::atoi(e) : 4;
+    }();
+    const int P = pass.T * L.G;
+    const int rep = groups > 1 ? 1 : (P <= 32 && rep_cap >= 4) ? 4 : (P <= 64 && rep_cap >= 2) ? 2 : 1;
+    auto kernel = rep == 4 ? attn_tc_kernel<DH, 4> : rep == 2 ? attn_tc_kernel<DH, 2> : attn_tc_kernel<DH, 1>;
+    static unsigned long long configured[3] = {0, 0, 0};
+    ensure_smem((const void*)kernel, (int)smem, configured[rep >> 1]);
     // diagnostic: ESPEC_ATTN_TRACE=T,n traces the n-th launch with T pass rows
     // (kTcaTraceSlots %globaltimer stamps per CTA) into gpurun_out/attn_trace.txt
     static int tT = -1, tn = -1;
@@ -687,17 +787,16 @@ static void attn_tc_launch(const AttnBatch& b, int nprob, int n_heads, const Pas
     }
     L.cluster = attn_tc_cluster(chunks);
     if (L.cluster && chunks > 8) {
-        static bool nonportable = false;
-        if (!nonportable) {
-            DEV_CK(cudaFuncSetAttribute((const void*)attn_tc_kernel<DH>,
-                                        cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-            nonportable = true;
+        static bool nonportable[3] = {false, false, false};
+        if (!nonportable[rep >> 1]) {
+            DEV_CK(cudaFuncSetAttribute((const void*)kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            nonportable[rep >> 1] = true;
         }
     }
     if (L.cluster)
-        DEV_CK(launch_pdl_cluster(attn_tc_kernel<DH>, grid, dim3(kTcaThreads), smem, s, chunks, L));
+        DEV_CK(launch_pdl_cluster(kernel, grid, dim3(kTcaThreads), smem, s, chunks, L));
     else
-        DEV_CK(launch_pdl(attn_tc_kernel<DH>, grid, dim3(kTcaThreads), smem, s, L));
+        DEV_CK(launch_pdl(kernel, grid, dim3(kTcaThreads), smem, s, L));
     if (chunks > 1 && !L.cluster) {
         const int rows = std::min(kTcaRows, pass.T * L.G);
         DEV_CK(launch_pdl(attn_tc_combine_kernel<DH>, dim3((rows + 31) / 32, kv.n_kv * groups, nprob),

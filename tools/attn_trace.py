@@ -27,3 +27,11 @@ if t.shape[1] >= 48:
             break
         med = [np.median((t[ok, c] - k0[ok]) / 1e3) for c in cols]
         print(f"  {s:4d} " + " ".join(f"{x:9.2f}" for x in med))
+if t.shape[1] >= 64:
+    ok = (t[:, 26] > 0) & (t[:, 48] > 0)
+    if ok.any():
+        base = t[ok, 26]
+        lab = ["scores loaded", "row max exchanged", "exp summed", "fold done", "P stored", "P arrived"]
+        cols = [48, 49, 50, 51, 52, 42]
+        print("  step 2 softmax phases (median us from S(2) seen): " +
+              ", ".join(f"{n} {np.median((t[ok, c] - base) / 1e3):.2f}" for n, c in zip(lab, cols)))

@@ -343,12 +343,15 @@ __global__ void __launch_bounds__(kTcaThreads, 1) attn_tc_kernel(const __grid_co
                 if (!stable(pg0 + i)) issue(i, s_page[i]);
             const uint32_t qaddr = smem_u32(sm + LY::kQ);
             const uint32_t id_s = tca_idesc(64, 0), id_pv = tca_idesc(DH, 1);
+            // one thread issues three independent streams as their inputs
+            // land (polling, so none waits behind another): QK(s) when the
+            // step's K pages are in and S buffer s & 1 is free, PV(s) when
+            // P(s), the V pages and PV buffer s & 1 are ready, and the refill
+            // of a page's stage with the page S later once PV released it
             auto qk = [&](int s) {  // S[s & 1] = Q [K(2s) | K(2s + 1)]^T
                 for (int pp = 0; pp < 2 && 2 * s + pp < n; ++pp) {
                     const int i = 2 * s + pp, st = i % S;
-                    mbar_wait(&k_full[st], (uint32_t)(i / S) & 1u);
                     if (tr && i == 0) atomicMax(tr + 2, gtimer());
-                    tca_fence_after();
                     const uint32_t kaddr = smem_u32(kbuf(st));
 #pragma unroll
                     for (int kk = 0; kk < DH / 16; ++kk)
@@ -359,29 +362,11 @@ __global__ void __launch_bounds__(kTcaThreads, 1) attn_tc_kernel(const __grid_co
                 if (tr && s < 8) tr[8 + s] = gtimer();
                 tca_commit(&s_full[s & 1]);
             };
-            mbar_wait(q_full, 0);
-            tca_fence_after();
-            if (nsteps > 0) qk(0);
-            for (int s = 0; s < nsteps; ++s) {
+            auto pv = [&](int s) {  // PV[s & 1] = P(2s) V(2s) + P(2s + 1) V(2s + 1)
                 const int b = s & 1;
-                // refill the previous step's stages with the pages of step
-                // s + 2 as soon as PV(s - 1) (issued one iteration ago) has
-                // released them, before this step's waits
-                if (s >= 1)
-                    for (int pp = 0; pp < 2; ++pp) {
-                        const int j = 2 * (s - 1) + pp;
-                        if (j + S >= n) break;
-                        mbar_wait(&kv_empty[j % S], (uint32_t)(j / S) & 1u);
-                        issue(j + S, s_page[j + S]);
-                    }
-                if (s + 1 < nsteps) qk(s + 1);
-                mbar_wait(&p_full[b], (uint32_t)(s >> 1) & 1u);
-                if (s >= 2) mbar_wait(&pv_free[b], (uint32_t)((s - 2) >> 1) & 1u);
+                if (tr && s < 8) tr[16 + s] = gtimer();
                 for (int pp = 0; pp < 2 && 2 * s + pp < n; ++pp) {
                     const int i = 2 * s + pp, st = i % S;
-                    mbar_wait(&v_full[st], (uint32_t)(i / S) & 1u);
-                    if (tr && pp == 0 && s < 8) tr[16 + s] = gtimer();
-                    tca_fence_after();
                     const uint32_t paddr = smem_u32(pbuf(s, pp)), vaddr = smem_u32(vbuf(st));
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk)  // 16 keys per MMA
@@ -390,6 +375,32 @@ __global__ void __launch_bounds__(kTcaThreads, 1) attn_tc_kernel(const __grid_co
                 }
                 tca_commit(&pv_full[b]);
                 for (int pp = 0; pp < 2 && 2 * s + pp < n; ++pp) tca_commit(&kv_empty[(2 * s + pp) % S]);
+            };
+            auto pages_in = [&](uint64_t* full, int s) {
+                for (int pp = 0; pp < 2 && 2 * s + pp < n; ++pp) {
+                    const int i = 2 * s + pp;
+                    if (!mbar_test(&full[i % S], (uint32_t)(i / S) & 1u)) return false;
+                }
+                return true;
+            };
+            mbar_wait(q_full, 0);
+            tca_fence_after();
+            int qn = 0, pn = 0, rn = 0;  // next QK step, next PV step, next page to refill
+            while (pn < nsteps) {
+                // S buffer qn & 1 is free once PV(qn - 2) was issued (after P(qn - 2))
+                if (qn < nsteps && qn <= pn + 1 && pages_in(k_full, qn)) {
+                    tca_fence_after();
+                    qk(qn++);
+                }
+                if (pn < qn && mbar_test(&p_full[pn & 1], (uint32_t)(pn >> 1) & 1u) &&
+                    (pn < 2 || mbar_test(&pv_free[pn & 1], (uint32_t)((pn - 2) >> 1) & 1u)) && pages_in(v_full, pn)) {
+                    tca_fence_after();
+                    pv(pn++);
+                }
+                while (rn + S < n && rn / 2 < pn && mbar_test(&kv_empty[rn % S], (uint32_t)(rn / S) & 1u)) {
+                    issue(rn + S, s_page[rn + S]);
+                    ++rn;
+                }
             }
         }
     } else {

@@ -317,8 +317,14 @@ __global__ void __launch_bounds__(kTcaThreads, 1) attn_tc_kernel(const __grid_co
             mbar_init(&pv_free[b], kTcaSoftmax);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int i = 0; i < n && i < S; ++i)
-            if (stable(pg0 + i)) issue(i, kv.page_table[pg0 + i]);
+        // the ring's page ids in one round trip (a load per issue would
+        // serialise behind each TMA issue's memory clobber)
+        int pt[S];
+#pragma unroll
+        for (int i = 0; i < S; ++i) pt[i] = i < n ? kv.page_table[pg0 + i] : 0;
+#pragma unroll
+        for (int i = 0; i < S; ++i)
+            if (i < n && stable(pg0 + i)) issue(i, pt[i]);
     }
     // S tiles (two pages each) at columns [0, 256), PV tiles at [256, 256 + 2 DH):
     // 512 columns, allocated before the dependent grid may launch (no TMEM wait cycles)
@@ -338,7 +344,14 @@ __global__ void __launch_bounds__(kTcaThreads, 1) attn_tc_kernel(const __grid_co
     if (warp == kTcaSoftmaxWarps) {
         // ---------------- producer + MMA issuer
         if (lane == 0) {
-            for (int i = 0; i < n; ++i) s_page[i] = kv.page_table[pg0 + i];
+            for (int i0 = 0; i0 < n; i0 += 8) {  // 8 loads in flight per round trip
+                int v[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) v[k] = i0 + k < n ? kv.page_table[pg0 + i0 + k] : 0;
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    if (i0 + k < n) s_page[i0 + k] = v[k];
+            }
             for (int i = 0; i < n && i < S; ++i)
                 if (!stable(pg0 + i)) issue(i, s_page[i]);
             const uint32_t qaddr = smem_u32(sm + LY::kQ);

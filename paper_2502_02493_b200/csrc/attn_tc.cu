@@ -221,7 +221,8 @@ __device__ __forceinline__ void tca_combine(int nchunks, ML ml, X x, float4 (&ac
 
 // ESPEC_ATTN_TRACE slots per CTA (%globaltimer): 0 start, 1 past
 // griddepcontrol.wait, 2 first K page, 3 pages done, 4 end, 5 cluster
-// synced; per step s < 8: 8+s QK(s) issued, 16+s PV(s) issued (MMA thread),
+// synced, 6 prologue page loads issued, 7 first K page landed, 53 Q tile
+// written; per step s < 8: 8+s QK(s) issued, 16+s PV(s) issued (MMA thread),
 // 24+s S(s) seen, 32+s PV(s) seen, 40+s P(s) written (softmax thread 0);
 // step 2 phases (softmax thread 0): 48 scores loaded, 49 row max exchanged,
 // 50 exponentials summed, 51 fold done, 52 P stored
@@ -325,6 +326,7 @@ __global__ void __launch_bounds__(kTcaThreads, 1) attn_tc_kernel(const __grid_co
 #pragma unroll
         for (int i = 0; i < S; ++i)
             if (i < n && stable(pg0 + i)) issue(i, pt[i]);
+        if (tr) tr[6] = gtimer();
     }
     // S tiles (two pages each) at columns [0, 256), PV tiles at [256, 256 + 2 DH):
     // 512 columns, allocated before the dependent grid may launch (no TMEM wait cycles)
@@ -354,6 +356,7 @@ __global__ void __launch_bounds__(kTcaThreads, 1) attn_tc_kernel(const __grid_co
             }
             for (int i = 0; i < n && i < S; ++i)
                 if (!stable(pg0 + i)) issue(i, s_page[i]);
+            if (tr) tr[55] = gtimer();
             const uint32_t qaddr = smem_u32(sm + LY::kQ);
             const uint32_t id_s = tca_idesc(64, 0), id_pv = tca_idesc(DH, 1);
             // one thread issues three independent streams as their inputs
@@ -396,7 +399,12 @@ __global__ void __launch_bounds__(kTcaThreads, 1) attn_tc_kernel(const __grid_co
                 }
                 return true;
             };
+            if (tr) {
+                mbar_wait(&k_full[0], 0);
+                tr[7] = gtimer();
+            }
             mbar_wait(q_full, 0);
+            if (tr) tr[53] = gtimer();
             tca_fence_after();
             int qn = 0, pn = 0, rn = 0;  // next QK step, next PV step, next page to refill
             while (pn < nsteps) {
@@ -462,6 +470,7 @@ __global__ void __launch_bounds__(kTcaThreads, 1) attn_tc_kernel(const __grid_co
                                            pack_bf16x2(b.z, b.w));
                 *reinterpret_cast<uint4*>(qrow + (c >> 3) * (kTcaRows * 128) + (((c & 7) ^ (t & 7)) * 16)) = u;
             }
+            if (tr && tid == 0) tr[54] = gtimer();
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_arrive(q_full);
         }

@@ -11,8 +11,11 @@ lines = open(sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/attn_trace.txt").
 print(lines[0])
 t = np.array([[int(x) for x in l.split()] for l in lines[1:] if l.strip()], dtype=np.int64)
 t0 = t[t[:, 0] > 0, 0].min()
-names = {0: "cta start", 1: "dep released", 2: "first K page", 3: "pages done", 5: "cluster synced", 4: "end"}
-for e in (0, 1, 2, 3, 5, 4):
+names = {0: "cta start", 6: "prologue issued", 7: "K page 0 landed", 1: "dep released", 54: "Q rows stored (t0)", 55: "page ids read", 53: "Q tile written",
+         2: "first QK issued", 3: "pages done", 5: "cluster synced", 4: "end"}
+for e in (0, 6, 7, 1, 54, 55, 53, 2, 3, 5, 4):
+    if e >= t.shape[1]:
+        continue
     v = t[:, e]
     v = (v[v > 0] - t0) / 1e3
     if len(v):

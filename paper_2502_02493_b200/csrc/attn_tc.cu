@@ -159,19 +159,6 @@ __device__ __forceinline__ uint32_t dsmem_addr(uint32_t local, uint32_t rank) {
     asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
     return r;
 }
-__device__ __forceinline__ float2 ld_dsmem2(uint32_t addr) {
-    float2 v;
-    asm("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
-    return v;
-}
-__device__ __forceinline__ float4 ld_dsmem4(uint32_t addr) {
-    float4 v;
-    // not volatile: ordered by the cluster barriers around the combine, so
-    // the loads of one row's chunks can all be in flight at once
-    asm("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-        : "r"(addr));
-    return v;
-}
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -185,8 +172,14 @@ __device__ __forceinline__ void cluster_sync_all() {
 // whichever path its pass takes.
 template <int CB, class ML, class X>
 __device__ __forceinline__ void tca_combine(int nchunks, ML ml, X x, float4 (&acc)[4], float& den) {
-    float M = -INFINITY;
-    for (int ch = 0; ch < nchunks; ++ch) M = fmaxf(M, ml(ch).x);
+    float M = -INFINITY;  // (exact in any order; 8 loads in flight per round trip)
+    for (int ch0 = 0; ch0 < nchunks; ch0 += 8) {
+        float mm[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) mm[q] = ch0 + q < nchunks ? ml(ch0 + q).x : -INFINITY;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) M = fmaxf(M, mm[q]);
+    }
 #pragma unroll
     for (int v = 0; v < 4; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
     den = 0.f;
@@ -648,28 +641,43 @@ __global__ void __launch_bounds__(kTcaThreads, 1) attn_tc_kernel(const __grid_co
     }
     if (L.cluster) {
         __syncwarp();
-        // the cluster's CTAs hold the chunks of this (kv head, pair group):
-        // CTA c combines rows [c R / chunks, (c + 1) R / chunks) reading every
-        // chunk's partial from its shared memory, then waits until no CTA
-        // reads its own any more
-        cluster_sync_all();
-        if (tr && tid == 0) tr[5] = gtimer();
+        // the cluster's CTAs hold the chunks of this (kv head, pair group);
+        // CTA c combines rows [c R / chunks, (c + 1) R / chunks). Every CTA
+        // pushes each partial row to its combiner's shared memory (remote
+        // stores: no round trips), then each combines from local memory.
         const int R = min(kTcaRows, P - mg * kTcaRows);
-        const int r0 = bx * R / nchunks, r1 = (bx + 1) * R / nchunks;
-        const uint32_t part = smem_u32(sm + LY::kRing);
-        for (int it = tid; it < (r1 - r0) * (DH / 16) && tid < kTcaSoftmax; it += kTcaSoftmax) {
-            const int rr = r0 + it / (DH / 16), c0 = (it % (DH / 16)) * 16;
-            const uint32_t row = part + (uint32_t)(rr * PS) * 4u;
+        const int RPO = (R + nchunks - 1) / nchunks + 1;  // rows per combiner, bound
+        auto r_lo = [&](int c) { return c * R / nchunks; };
+        float* part = reinterpret_cast<float*>(sm + LY::kRing);  // [128][PS] own partial rows
+        float* recv = part + kTcaRows * PS;                          // [chunk][RPO][PS] rows to combine
+        cluster_sync_all();  // every CTA's ring is dead: receive areas may be written
+        if (tr && tid == 0) tr[5] = gtimer();
+        for (int it = tid; it < R * (PS / 4); it += kTcaThreads) {
+            const int rr = it / (PS / 4), q4 = it % (PS / 4);
+            int c = rr * nchunks / R;
+            while (c + 1 < nchunks && rr >= r_lo(c + 1)) ++c;
+            while (rr < r_lo(c)) --c;
+            const float4 v = *reinterpret_cast<const float4*>(part + rr * PS + 4 * q4);
+            const uint32_t dst = dsmem_addr(smem_u32(recv + ((bx * RPO) + (rr - r_lo(c))) * PS + 4 * q4), (uint32_t)c);
+            asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "f"(v.x), "f"(v.y), "f"(v.z),
+                         "f"(v.w)
+                         : "memory");
+        }
+        cluster_sync_all();  // the pushed rows are visible; no remote access after this
+        const int r0 = r_lo(bx), r1 = r_lo(bx + 1);
+        for (int it = tid; it < (r1 - r0) * (DH / 16); it += kTcaThreads) {
+            const int lr = it / (DH / 16), c0 = (it % (DH / 16)) * 16;
+            const float* row = recv + lr * PS;
             float4 acc[4];
             float den;
-            tca_combine<4>(
-                nchunks, [&](int ch) { return ld_dsmem2(dsmem_addr(row + DH * 4, (uint32_t)ch)); },
-                [&](int ch, int v) { return ld_dsmem4(dsmem_addr(row + (uint32_t)(c0 + 4 * v) * 4u, (uint32_t)ch)); },
+            tca_combine<2>(
+                nchunks, [&](int ch) { return *reinterpret_cast<const float2*>(row + (size_t)ch * RPO * PS + DH); },
+                [&](int ch, int v) { return *reinterpret_cast<const float4*>(row + (size_t)ch * RPO * PS + c0 + 4 * v); },
                 acc, den);
-            const int pp = mg * kTcaRows + rr;
+            const int pp = mg * kTcaRows + r0 + lr;
             attn_store_row<DH>(A, (size_t)(pp / G) * H * DH + (hk * G + pp % G) * DH + c0, acc, den);
         }
-        cluster_sync_all();
+        if (tr) atomicMax(tr + 56, gtimer());
     }
     // TMEM is no longer read: release it
     tca_fence_before();

@@ -12,8 +12,8 @@ print(lines[0])
 t = np.array([[int(x) for x in l.split()] for l in lines[1:] if l.strip()], dtype=np.int64)
 t0 = t[t[:, 0] > 0, 0].min()
 names = {0: "cta start", 6: "prologue issued", 7: "K page 0 landed", 1: "dep released", 54: "Q rows stored (t0)", 55: "page ids read", 53: "Q tile written",
-         2: "first QK issued", 3: "pages done", 5: "cluster synced", 4: "end"}
-for e in (0, 6, 7, 1, 54, 55, 53, 2, 3, 5, 4):
+         2: "first QK issued", 3: "pages done", 5: "cluster synced", 56: "combine done", 57: "cluster synced 2", 4: "end"}
+for e in (0, 6, 7, 1, 54, 55, 53, 2, 3, 5, 56, 57, 4):
     if e >= t.shape[1]:
         continue
     v = t[:, e]

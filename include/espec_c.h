@@ -98,14 +98,16 @@ typedef struct {
     int tp_rank;
 } espec_device_map;
 
-/* espec::IterationTrace (proj/include/espec/report.hpp:12-28) with real
- * device stage times in place of the simulated units. */
+/* espec::IterationTrace (proj/include/espec/report.hpp:12-28): the *_ms
+ * fields are measured device stage times (the reference's *_wall), the *_sim
+ * fields the cost model's units (espec_set_cost; orchestrator.cpp:263-386). */
 typedef struct {
     int m, n, drafted_nodes, emitted;
     int sequential_forwards, fuzzy_forwards, base_forwards;
     int committed, draft_committed, base_committed;
     int bonus;
     float calibrate_ms, draft_ms, verify_ms;
+    double calibrate_sim, draft_sim, verify_sim;
 } espec_iteration;
 
 typedef struct espec_engine espec_engine;
@@ -298,22 +300,58 @@ typedef struct {
     double calibrate_per_100_s;
     double draft_total_per_100_s; /* draft + calibrate (report.cpp:85) */
     double total_s;
-    double speedup_vs_vanilla; /* vanilla_baseline_s / total_s (report.cpp:87-90), 1 if total is 0 */
+    double speedup_vs_vanilla; /* vanilla_baseline_sim / total_sim (report.cpp:87-90), 1 if total_sim is 0 */
+    /* the same in the cost model's units (report.cpp:83-87) */
+    double draft_per_100_sim, verify_per_100_sim, calibrate_per_100_sim, draft_total_per_100_sim;
+    double total_sim;
 } espec_report;
 
 /* aggregate(traces, vanilla_baseline_sim) (proj/src/report.cpp:51-95):
  * ESPEC_CONFIG "cannot aggregate an empty trace list" / "traces emitted zero
- * tokens" as the reference throws. vanilla_baseline_s: device seconds the
- * vanilla arm takes for the same number of tokens. */
-espec_status espec_aggregate(const espec_iteration* traces, int n_traces, double vanilla_baseline_s,
+ * tokens" as the reference throws. vanilla_baseline_sim: the cost model's
+ * vanilla generation of the same tokens (espec_cost_eval
+ * ESPEC_COST_VANILLA_BASELINE, orchestrator.cpp:72-77). */
+espec_status espec_aggregate(const espec_iteration* traces, int n_traces, double vanilla_baseline_sim,
                              espec_report* out);
 /* emit_report (report.cpp:97-171): format 0 = JSON (the reference's keys;
- * "sim" and "wall" both carry measured device seconds — no cost simulator on
- * this path), 1 = CSV header + row. *len receives the text length;
- * ESPEC_SHAPE if it does not fit in cap bytes (NUL included). */
+ * "sim" in cost-model units, "wall" in measured device seconds; "config" is
+ * left empty), 1 = CSV header + row (the sim numbers, as the reference).
+ * *len receives the text length; ESPEC_SHAPE if it does not fit in cap bytes
+ * (NUL included). */
 espec_status espec_report_emit(const espec_report* report, const espec_iteration* traces, int n_traces,
                                const char* algorithm, int n, const int* widths, int n_widths, int lp_size,
                                int format, char* out, int cap, int* len);
+
+/* Cost simulator (proj/include/espec/cost_sim.hpp, proj/src/cost_sim.cpp):
+ * the affine device-cost model c_fixed + c_mem (w / tp) + c_comp (w / tp) s
+ * (+ t_addi when tp > 1) behind the reports' simulated stage units. Doubles in
+ * the reference's order: every number matches the reference bit for bit. */
+typedef struct {
+    double c_fixed, c_mem, c_comp, t_addi;
+    double attn_workload, mlp_workload, base_layer_workload;
+    int tp_size_base, tp_size_draft, devices;
+} espec_cost_params;
+espec_status espec_cost_defaults(espec_cost_params* out); /* CostParams{} */
+typedef enum {
+    ESPEC_COST_VALIDATE = 0,         /* CostParams::validate; out = 0 */
+    ESPEC_COST_T_EXE = 1,            /* t_exe(p, workload a, s b, tp n_layers) */
+    ESPEC_COST_GROUP_ATTENTION = 2,  /* group_attention_time(p, group size n_layers, s a) */
+    ESPEC_COST_DRAFT_GROUP = 3,      /* simulate_draft_group(p, plan, s a); plan in the reference's grammar */
+    ESPEC_COST_SEQUENTIAL_DRAFT = 4, /* sequential_draft_forward_time(p, n_layers, s a) */
+    ESPEC_COST_BASE_FORWARD = 5,     /* base_forward_time(p, n_layers, s a) */
+    ESPEC_COST_VANILLA_BASELINE = 6  /* vanilla_baseline_sim(p, n_layers, prompt_len a, tokens b) */
+} espec_cost_fn;
+/* ESPEC_CONFIG with the reference's ConfigError texts on invalid input. */
+espec_status espec_cost_eval(const espec_cost_params* params, int what, double a, double b, int n_layers,
+                             const char* plan, double* out);
+/* total_time_model: ESPEC_DOMAIN at alpha <= 0, ESPEC_CONFIG outside (0, 1] or n < 1. */
+espec_status espec_cost_total_time(double n_tokens, double t_draft, double t_base, int n, double alpha, double* out);
+/* RunConfig::cost of an engine (validated; default CostParams{}); the stages
+ * advance a SimClock per generation (reset by begin / prefill / generate)
+ * exactly as Generation does, so traces carry the reference's *_sim values. */
+espec_status espec_set_cost(espec_engine* eng, const espec_cost_params* params);
+/* GenerateResult::occupancy_csv of the current generation (cost_sim.cpp:102-117). */
+espec_status espec_occupancy_csv(espec_engine* eng, char* out, int cap, int* len);
 
 /* ESPEC1 model file (proj/include/espec/model_io.hpp, proj/src/model_io.cpp):
  * "ESPEC1\n", u64 header length, JSON header (config + tensor manifest), raw

@@ -80,6 +80,12 @@ public:
         const espec_device_map dm = {device, 1, &device, /*tp_size*/ 1, /*tp_rank*/ 0};
         b200_check(espec_engine_create(&bc, &dc, &rc, &dm, &e_), nullptr);
         try {
+            // RunConfig::cost: the engine's stages advance the same simulated clock
+            const CostParams& c = cfg.cost;
+            const espec_cost_params cp = {c.c_fixed,       c.c_mem,         c.c_comp,        c.t_addi,
+                                          c.attn_workload, c.mlp_workload,  c.base_layer_workload,
+                                          c.tp_size_base,  c.tp_size_draft, c.devices};
+            b200_check(espec_set_cost(e_, &cp), e_);
             b200_upload(e_, 1, base);
             b200_upload(e_, 0, draft);
         } catch (...) {
@@ -165,8 +171,10 @@ private:
 
 // Same signature and semantics as espec::generate (orchestrator.cpp:488-492).
 // The report comes from the reference's own aggregate() (report.cpp:51-95)
-// over the engine's iteration traces, device stage times in the *_wall slots
-// (there is no simulated clock on the B200 path).
+// over the engine's iteration traces: device stage times in the *_wall slots,
+// the engine's simulated units (RunConfig::cost) in the *_sim slots, the
+// vanilla baseline from vanilla_baseline_sim (orchestrator.cpp:72-77), and the
+// engine's SimClock occupancy CSV.
 inline GenerateResult generate_b200(const Model& base, const Model& draft, const RunConfig& cfg,
                                     std::span<const std::uint8_t> prompt, int device = 0) {
     B200Generation g(base, draft, cfg, device);
@@ -189,14 +197,25 @@ inline GenerateResult generate_b200(const Model& base, const Model& draft, const
         t.draft_wall = e.draft_ms * 1e-3;
         t.verify_wall = e.verify_ms * 1e-3;
         t.calibrate_wall = e.calibrate_ms * 1e-3;
+        t.draft_sim = e.draft_sim;
+        t.verify_sim = e.verify_sim;
+        t.calibrate_sim = e.calibrate_sim;
         t.fuzzy_forwards = e.fuzzy_forwards;
         t.sequential_forwards = e.sequential_forwards;
         t.base_forwards = e.base_forwards;
         traces.push_back(t);
     }
-    out.report = aggregate(traces, 0.0);
+    const int prompt_len = static_cast<int>(tokenize_prompt(prompt, base.config.vocab_size).size());
+    out.report = aggregate(traces, vanilla_baseline_sim(cfg.cost, base.config.n_layers, prompt_len,
+                                                        static_cast<long>(out.tokens.size())));
     out.report.algorithm = to_string(cfg.algorithm);
     out.report.n = cfg.algorithm == Algorithm::vanilla ? 0 : cfg.n;
+    int len = 0;
+    espec_occupancy_csv(g.handle(), nullptr, 0, &len);
+    std::string occ(static_cast<std::size_t>(len) + 1, '\0');
+    b200_check(espec_occupancy_csv(g.handle(), occ.data(), len + 1, &len), g.handle());
+    occ.resize(static_cast<std::size_t>(len));
+    out.occupancy_csv = occ;
     return out;
 }
 

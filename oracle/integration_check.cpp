@@ -153,6 +153,13 @@ int main() {
             ok &= gpu.tokens == ref.tokens && staged == ref.tokens && trees_ok;
             ok &= gpu.report.has_alpha == ref.report.has_alpha && gpu.report.alpha == ref.report.alpha;
             ok &= gpu.report.tokens_emitted == ref.report.tokens_emitted;
+            // the simulated report and occupancy, bit for bit (cost_sim.cpp)
+            ok &= gpu.report.total_sim == ref.report.total_sim &&
+                  gpu.report.speedup_vs_vanilla == ref.report.speedup_vs_vanilla &&
+                  gpu.report.per100_sim.draft == ref.report.per100_sim.draft &&
+                  gpu.report.per100_sim.verify == ref.report.per100_sim.verify &&
+                  gpu.report.per100_sim.calibrate == ref.report.per100_sim.calibrate &&
+                  gpu.occupancy_csv == ref.occupancy_csv;
         }
         all_ok &= ok;
         std::cout << (ci ? ", " : "") << "{\"name\": \"" << c.name << "\", \"ok\": " << (ok ? "true" : "false")

@@ -20,6 +20,7 @@
 #include <string>
 #include <vector>
 
+#include "espec/cost_sim.hpp"
 #include "espec/draft_engine.hpp"
 #include "espec/errors.hpp"
 #include "espec/kv_cache.hpp"
@@ -720,6 +721,174 @@ int main(int argc, char** argv) {
         }
         std::ofstream f(out_dir + "/ref_hostapi.json");
         f << host.dump() << "\n";
+    }
+    // ---- cost simulator -> proj/src/cost_sim.cpp, the sim
+    // fields of every generation's traces and report (orchestrator.cpp:72-77,
+    // 256-466; report.cpp:51-95)
+    {
+        json cost;
+        auto pj = [](const CostParams& p) {
+            return json{{"c_fixed", p.c_fixed}, {"c_mem", p.c_mem}, {"c_comp", p.c_comp}, {"t_addi", p.t_addi},
+                        {"attn_workload", p.attn_workload}, {"mlp_workload", p.mlp_workload},
+                        {"base_layer_workload", p.base_layer_workload}, {"tp_size_base", p.tp_size_base},
+                        {"tp_size_draft", p.tp_size_draft}, {"devices", p.devices}};
+        };
+        CostParams p0;
+        CostParams p1;
+        p1.c_fixed = 0.05;
+        p1.c_mem = 0.7;
+        p1.c_comp = 0.3;
+        p1.t_addi = 0.25;
+        p1.attn_workload = 0.2;
+        p1.mlp_workload = 0.08;
+        p1.base_layer_workload = 1.5;
+        p1.tp_size_base = 4;
+        p1.tp_size_draft = 2;
+        p1.devices = 4;
+        CostParams p2;
+        p2.tp_size_base = 1;
+        p2.devices = 1;
+        json fns = json::array();
+        for (const CostParams* pp : {&p0, &p1, &p2}) {
+            const CostParams& p = *pp;
+            json f;
+            f["params"] = pj(p);
+            json te = json::array();
+            for (double w : {0.0, 0.15, 2.0})
+                for (double sv : {1.0, 3.0, 7.5})
+                    for (int tp : {1, 2, 8}) te.push_back(json{w, sv, tp, t_exe(p, w, sv, tp)});
+            f["t_exe"] = te;
+            json ga = json::array();
+            for (int g : {1, 2, 4})
+                for (double sv : {1.0, 2.5}) ga.push_back(json{g, sv, group_attention_time(p, g, sv)});
+            f["group_attention"] = ga;
+            json dg = json::array();
+            for (const std::string& pl : {format_plan(plan_groups(32, 4)), format_plan(plan_groups(12, 2)),
+                                          format_plan(plan_groups(8, 1)), std::string("0|1-3|4-7|8"),
+                                          std::string("0|1-5|6")})
+                for (double sv : {1.0, 6.0}) {
+                    try {
+                        dg.push_back(json{pl, sv, simulate_draft_group(p, parse_plan_override(pl), sv)});
+                    } catch (const Error& e) {
+                        dg.push_back(json{pl, sv, e.what()});
+                    }
+                }
+            f["draft_group"] = dg;
+            json sq = json::array(), bf = json::array(), vb = json::array();
+            for (int L : {1, 8, 32})
+                for (double sv : {1.0, 5.0}) {
+                    sq.push_back(json{L, sv, sequential_draft_forward_time(p, L, sv)});
+                    bf.push_back(json{L, sv, base_forward_time(p, L, sv)});
+                }
+            for (int pl : {0, 1, 20})
+                for (long tk : {0L, 1L, 48L}) vb.push_back(json{12, pl, tk, vanilla_baseline_sim(p, 12, pl, tk)});
+            f["sequential"] = sq;
+            f["base"] = bf;
+            f["vanilla_baseline"] = vb;
+            fns.push_back(f);
+        }
+        cost["functions"] = fns;
+        json tt = json::array();
+        for (double al : {0.25, 0.8, 1.0}) tt.push_back(json{128.0, 0.3, 2.5, 5, al, total_time_model(128.0, 0.3, 2.5, 5, al)});
+        cost["total_time"] = tt;
+        // error texts
+        json errs;
+        auto catch_text = [](auto&& f) -> std::string {
+            try {
+                f();
+            } catch (const Error& e) {
+                return e.what();
+            }
+            return std::string();
+        };
+        {
+            CostParams b = p0;
+            b.c_mem = -1.0;
+            errs["negative"] = catch_text([&] { b.validate(); });
+            CostParams c = p0;
+            c.tp_size_base = 0;
+            errs["tp_zero"] = catch_text([&] { c.validate(); });
+            CostParams d = p0;
+            d.tp_size_draft = 9;
+            errs["tp_over"] = catch_text([&] { d.validate(); });
+            errs["t_exe_s"] = catch_text([&] { t_exe(p0, 0.1, 0.5, 1); });
+            errs["group_zero"] = catch_text([&] { group_attention_time(p0, 0, 1.0); });
+            errs["plan_over"] = catch_text([&] { simulate_draft_group(p1, parse_plan_override("0|1-5|6"), 1.0); });
+            errs["alpha_zero"] = catch_text([&] { total_time_model(10, 1, 1, 2, 0.0); });
+            errs["alpha_over"] = catch_text([&] { total_time_model(10, 1, 1, 2, 1.5); });
+            errs["n_zero"] = catch_text([&] { total_time_model(10, 1, 1, 0, 0.5); });
+        }
+        cost["errors"] = errs;
+        // every generation case's simulated stage units, occupancy and report,
+        // at the default cost and (three cases) at p1
+        json runs = json::array();
+        for (const auto& gc : cases) {
+            for (int variant = 0; variant < 2; ++variant) {
+                if (variant == 1 && gc.name != "fixa_easyspec" && gc.name != "t3_chain_easyspec" &&
+                    gc.name != "fixa_sd")
+                    continue;
+                const Model base = init_model(gc.base);
+                Model draft;
+                if (gc.draft_seed != 0) {
+                    ModelConfig dc = gc.base;
+                    dc.n_layers = gc.keep;
+                    dc.seed = gc.draft_seed;
+                    draft = init_model(dc);
+                } else {
+                    draft = gc.keep == 0 ? base : make_truncated_draft(base, gc.keep);
+                }
+                RunConfig rc = gc.run;
+                if (variant == 1) rc.cost = p1;
+                json r{{"name", gc.name}, {"cost", pj(rc.cost)}};
+                try {
+                    const GenerateResult res = generate(
+                        base, draft, rc, {reinterpret_cast<const std::uint8_t*>(gc.prompt.data()), gc.prompt.size()},
+                        nullptr);
+                    json sims = json::array();
+                    for (const auto& t : res.report.iterations)
+                        sims.push_back(json{t.calibrate_sim, t.draft_sim, t.verify_sim});
+                    const int prompt_len = static_cast<int>(tokenize_prompt(
+                        {reinterpret_cast<const std::uint8_t*>(gc.prompt.data()), gc.prompt.size()},
+                        base.config.vocab_size).size());
+                    r["sims"] = sims;
+                    r["prompt_len"] = prompt_len;
+                    r["n_tokens"] = res.tokens.size();
+                    r["vanilla_baseline"] = vanilla_baseline_sim(rc.cost, base.config.n_layers, prompt_len,
+                                                                 static_cast<long>(res.tokens.size()));
+                    r["per100_sim"] = {res.report.per100_sim.draft, res.report.per100_sim.verify,
+                                       res.report.per100_sim.calibrate};
+                    r["draft_total_per100_sim"] = res.report.draft_total_per100_sim;
+                    r["total_sim"] = res.report.total_sim;
+                    r["speedup"] = res.report.speedup_vs_vanilla;
+                    r["csv"] = emit_report(res.report, ReportFormat::csv);
+                    r["occupancy"] = res.occupancy_csv;
+                    r["error"] = nullptr;
+                } catch (const Error& e) {
+                    r["error"] = e.what();
+                }
+                runs.push_back(r);
+            }
+        }
+        // a plan wider than the simulated device count fails the run
+        {
+            const GenCase* gc = nullptr;
+            for (const auto& c : cases)
+                if (c.name == "fixa_easyspec") gc = &c;
+            const Model base = init_model(gc->base);
+            const Model draft = make_truncated_draft(base, gc->keep);
+            RunConfig rc = gc->run;
+            rc.cost.devices = 1;
+            rc.cost.tp_size_base = 1;
+            json r{{"name", "fixa_easyspec"}, {"cost", pj(rc.cost)}};
+            r["error"] = catch_text([&] {
+                generate(base, draft, rc,
+                         {reinterpret_cast<const std::uint8_t*>(gc->prompt.data()), gc->prompt.size()}, nullptr);
+            });
+            runs.push_back(r);
+        }
+        cost["runs"] = runs;
+        std::ofstream f(out_dir + "/ref_cost.json");
+        f << cost.dump() << "\n";
     }
     std::cout << "wrote " << out_dir << "/ref_numerics.json and ref_generate.json (" << cases.size()
               << " generation cases)\n";

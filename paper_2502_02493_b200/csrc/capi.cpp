@@ -6,6 +6,7 @@
 
 #include "../../include/espec_c.h"
 #include "engine.h"
+#include "cost_sim.h"
 #include "host_api.h"
 
 using namespace espec;
@@ -71,6 +72,9 @@ void fill_trace(const IterationTrace& t, espec_iteration* o) {
     o->calibrate_ms = t.calibrate_ms;
     o->draft_ms = t.draft_ms;
     o->verify_ms = t.verify_ms;
+    o->calibrate_sim = t.calibrate_sim;
+    o->draft_sim = t.draft_sim;
+    o->verify_sim = t.verify_sim;
 }
 
 template <typename F>
@@ -123,6 +127,9 @@ IterationTrace from_c(const espec_iteration& o) {
     t.calibrate_ms = o.calibrate_ms;
     t.draft_ms = o.draft_ms;
     t.verify_ms = o.verify_ms;
+    t.calibrate_sim = o.calibrate_sim;
+    t.draft_sim = o.draft_sim;
+    t.verify_sim = o.verify_sim;
     return t;
 }
 
@@ -517,13 +524,13 @@ double espec_total_variation(const int32_t* pa, const int64_t* ca, int na, const
     return dist / 2.0;
 }
 
-espec_status espec_aggregate(const espec_iteration* traces, int n_traces, double vanilla_baseline_s,
+espec_status espec_aggregate(const espec_iteration* traces, int n_traces, double vanilla_baseline_sim,
                              espec_report* out) {
     if (!out || (n_traces > 0 && !traces)) return ESPEC_CONFIG;
     return guard_free([&] {
         std::vector<IterationTrace> t;
         for (int i = 0; i < n_traces; ++i) t.push_back(from_c(traces[i]));
-        const ReportAgg r = aggregate_traces(t, vanilla_baseline_s);
+        const ReportAgg r = aggregate_traces(t, vanilla_baseline_sim);
         out->n_iterations = r.iterations;
         out->has_alpha = r.has_alpha;
         out->alpha = r.alpha;
@@ -536,6 +543,11 @@ espec_status espec_aggregate(const espec_iteration* traces, int n_traces, double
         out->draft_total_per_100_s = r.draft_total_per100;
         out->total_s = r.total;
         out->speedup_vs_vanilla = r.speedup_vs_vanilla;
+        out->draft_per_100_sim = r.draft_per100_sim;
+        out->verify_per_100_sim = r.verify_per100_sim;
+        out->calibrate_per_100_sim = r.calibrate_per100_sim;
+        out->draft_total_per_100_sim = r.draft_total_per100_sim;
+        out->total_sim = r.total_sim;
     });
 }
 
@@ -557,6 +569,11 @@ espec_status espec_report_emit(const espec_report* report, const espec_iteration
         r.draft_total_per100 = report->draft_total_per_100_s;
         r.total = report->total_s;
         r.speedup_vs_vanilla = report->speedup_vs_vanilla;
+        r.draft_per100_sim = report->draft_per_100_sim;
+        r.verify_per100_sim = report->verify_per_100_sim;
+        r.calibrate_per100_sim = report->calibrate_per_100_sim;
+        r.draft_total_per100_sim = report->draft_total_per_100_sim;
+        r.total_sim = report->total_sim;
         std::vector<IterationTrace> t;
         for (int i = 0; i < n_traces; ++i) t.push_back(from_c(traces[i]));
         std::string text;
@@ -565,6 +582,73 @@ espec_status espec_report_emit(const espec_report* report, const espec_iteration
         else throw Error(ST_CONFIG, "report format must be 0 (json) or 1 (csv)");
         if (len) *len = (int)text.size();
         if (!out || (int)text.size() + 1 > cap) throw Error(ST_SHAPE, "report text does not fit the buffer");
+        std::memcpy(out, text.c_str(), text.size() + 1);
+    });
+}
+
+// ---- cost simulator (proj/src/cost_sim.cpp) -------------------------------
+namespace {
+CostParams cost_from_c(const espec_cost_params* c) {
+    CostParams p;
+    p.c_fixed = c->c_fixed;
+    p.c_mem = c->c_mem;
+    p.c_comp = c->c_comp;
+    p.t_addi = c->t_addi;
+    p.attn_workload = c->attn_workload;
+    p.mlp_workload = c->mlp_workload;
+    p.base_layer_workload = c->base_layer_workload;
+    p.tp_size_base = c->tp_size_base;
+    p.tp_size_draft = c->tp_size_draft;
+    p.devices = c->devices;
+    return p;
+}
+}  // namespace
+
+espec_status espec_cost_defaults(espec_cost_params* out) {
+    if (!out) return ESPEC_CONFIG;
+    const CostParams d;
+    *out = espec_cost_params{d.c_fixed,      d.c_mem,         d.c_comp,        d.t_addi,  d.attn_workload,
+                             d.mlp_workload, d.base_layer_workload, d.tp_size_base, d.tp_size_draft, d.devices};
+    return ESPEC_OK;
+}
+
+espec_status espec_cost_eval(const espec_cost_params* params, int what, double a, double b, int n_layers,
+                             const char* plan, double* out) {
+    if (!params || !out) return ESPEC_CONFIG;
+    return guard_free([&] {
+        const CostParams p = cost_from_c(params);
+        switch (what) {
+            case ESPEC_COST_VALIDATE: p.validate(); *out = 0.0; break;
+            case ESPEC_COST_T_EXE: *out = t_exe(p, a, b, n_layers); break;
+            case ESPEC_COST_GROUP_ATTENTION: *out = group_attention_time(p, n_layers, a); break;
+            case ESPEC_COST_DRAFT_GROUP: {
+                if (!plan) throw Error(ST_CONFIG, "cost: a layer plan is required");
+                *out = simulate_draft_group(p, parse_plan_override(plan), a);
+                break;
+            }
+            case ESPEC_COST_SEQUENTIAL_DRAFT: *out = sequential_draft_forward_time(p, n_layers, a); break;
+            case ESPEC_COST_BASE_FORWARD: *out = base_forward_time(p, n_layers, a); break;
+            case ESPEC_COST_VANILLA_BASELINE: *out = vanilla_baseline_sim(p, n_layers, (int)a, (long)b); break;
+            default: throw Error(ST_CONFIG, "cost: unknown function " + std::to_string(what));
+        }
+    });
+}
+
+espec_status espec_cost_total_time(double n_tokens, double t_draft, double t_base, int n, double alpha, double* out) {
+    if (!out) return ESPEC_CONFIG;
+    return guard_free([&] { *out = total_time_model(n_tokens, t_draft, t_base, n, alpha); });
+}
+
+espec_status espec_set_cost(espec_engine* eng, const espec_cost_params* params) {
+    if (!params) return ESPEC_CONFIG;
+    return guard(eng, [&] { eng->impl->set_cost(cost_from_c(params)); });
+}
+
+espec_status espec_occupancy_csv(espec_engine* eng, char* out, int cap, int* len) {
+    return guard(eng, [&] {
+        const std::string text = eng->impl->occupancy_csv();
+        if (len) *len = (int)text.size();
+        if (!out || (int)text.size() + 1 > cap) throw Error(ST_SHAPE, "occupancy text does not fit the buffer");
         std::memcpy(out, text.c_str(), text.size() + 1);
     });
 }

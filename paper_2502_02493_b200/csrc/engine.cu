@@ -14,6 +14,7 @@
 #include <mutex>
 
 #include "common.cuh"
+#include "cost_sim.h"
 #include "engine.h"
 
 namespace espec {
@@ -675,6 +676,12 @@ public:
     }
 
     // ---------------- setup ----------------
+
+    void set_cost(const CostParams& cost) override {
+        cost.validate();
+        cost_ = cost;
+    }
+    std::string occupancy_csv() const override { return clock_.occupancy_csv(); }
 
     void set_run(const RunCfg& run) override {
         run_ = run;
@@ -1498,6 +1505,8 @@ public:
         generated_ = 0;
         it_.phase = 0;
         draft_cached_ = 0;
+        clock_ = SimClock(cost_.devices);
+        sim_dpre_ = sim_bpre_ = 0;
         rng_ = Xoshiro(run_.seed);  // Generation's RNG (proj/src/orchestrator.cpp:150)
         bcache_.reset();
         dcache_.reset();
@@ -1583,6 +1592,12 @@ public:
         }
         CUDA_OK(cudaEventRecord(ev_[0], stream_));
         const int n0 = (int)committed_.size();
+        {  // sim_base_forward over the uncached suffix (orchestrator.cpp:441-466)
+            const double before = clock_.stage_elapsed(SIM_VERIFY);
+            sim_base_forward(cost_, base_.c.n_layers, n0 - bcache_.committed + sim_bpre_, clock_, SIM_VERIFY);
+            sim_bpre_ = 0;
+            tr.verify_sim = clock_.stage_elapsed(SIM_VERIFY) - before;
+        }
         // the prompt but its last token is prefilled (tcgen05 when long); the
         // last token always goes through a decode-sized pass, exactly like the
         // frontier row of a speculative verify, so greedy outputs agree
@@ -1704,6 +1719,15 @@ public:
         if (I.fuzzy_lead) ++I.tr.fuzzy_forwards;
         else ++I.tr.sequential_forwards;
         I.lead_T = (int)lead_rows.size();
+        {  // StageSimDelta of drafter_leading_pass (orchestrator.cpp:262-298)
+            const int stage = I.calibrated ? SIM_CALIBRATE : SIM_DRAFT;
+            const double before = clock_.stage_elapsed(stage);
+            const int s_rows = I.lead_T + sim_dpre_;
+            sim_dpre_ = 0;
+            if (I.fuzzy_lead) sim_fuzzy_draft_forward(cost_, plan_, s_rows, clock_, stage);
+            else sim_sequential_draft_forward(cost_, draft_.c.n_layers, s_rows, clock_, stage);
+            (I.calibrated ? I.tr.calibrate_sim : I.tr.draft_sim) += clock_.stage_elapsed(stage) - before;
+        }
         const bool store = I.need_logits || root_logits_host;
         head(draft_, dws_, I.lead_T - 1, 1, I.need_logits ? arena_ + am_off_ : arena_ + tree_off_,
              store ? dlogits_ : nullptr);
@@ -1734,6 +1758,7 @@ public:
         }
         I.n_dists = 1;
         if (I.need_logits) select_level(0, 1, {widths_[0]}, {0}, V);
+        const double sim_before = clock_.stage_elapsed(SIM_DRAFT);  // draft_stage's StageSimDelta (302-331)
         for (int level = 1; level <= run_.n - 1 && !frontier.empty(); ++level) {
             std::vector<int> parents, tok;
             for (int idx : frontier) {
@@ -1747,6 +1772,9 @@ public:
             forward(draft_, dcache_, dws_, I.easy ? &plan_ : nullptr, ps);
             if (I.easy) ++I.tr.fuzzy_forwards;
             else ++I.tr.sequential_forwards;
+            // one simulated forward per forwarded level of frontier-size rows
+            if (I.easy) sim_fuzzy_draft_forward(cost_, plan_, (int)frontier.size(), clock_, SIM_DRAFT);
+            else sim_sequential_draft_forward(cost_, draft_.c.n_layers, (int)frontier.size(), clock_, SIM_DRAFT);
             std::vector<int> next, first_child, widths;
             const int dist0 = I.n_dists;
             for (size_t i = 0; i < frontier.size(); ++i) {
@@ -1771,6 +1799,7 @@ public:
             I.n_dists += nf;
             frontier = next;
         }
+        I.tr.draft_sim += clock_.stage_elapsed(SIM_DRAFT) - sim_before;
         I.tr.drafted_nodes = (int)nodes.size();
         CUDA_OK(cudaEventRecord(ev_[2], stream_));
         I.phase = 2;
@@ -1840,6 +1869,13 @@ public:
                                     sizeof(int) * nn, cudaMemcpyDeviceToDevice, stream_));
         }
         const int n_comm = I.n_comm;
+        {  // verify_stage's StageSimDelta (orchestrator.cpp:336-386): one base
+           // forward over the uncached suffix plus the tree nodes
+            const double before = clock_.stage_elapsed(SIM_VERIFY);
+            sim_base_forward(cost_, base_.c.n_layers, n_comm - bcache_.committed + sim_bpre_ + nn, clock_, SIM_VERIFY);
+            sim_bpre_ = 0;
+            I.tr.verify_sim += clock_.stage_elapsed(SIM_VERIFY) - before;
+        }
         // committed tokens the base has no rows for: all but the frontier token
         // are prefilled chunk-wise first (equivalent to one pass: causal rows).
         if (n_comm - 1 > bcache_.committed)
@@ -1996,10 +2032,12 @@ public:
         // it with the tree); drafter: the whole chunks before the final one, so
         // the leading pass runs exactly the chunk step() would run.
         if (n - 1 > 0) chain_pass(base_, bcache_, bws_, 0, n - 1, nullptr, false, true, 0);
+        sim_bpre_ = n - 1;
         const int dpre = ((n - 1) / kChunk) * kChunk;
         if (dpre > 0 && run_.algorithm != ALG_VANILLA) {
             chain_pass(draft_, dcache_, dws_, 0, dpre, nullptr, false, true, 0);
             draft_cached_ = dpre;
+            sim_dpre_ = dpre;
         }
         CUDA_OK(cudaStreamSynchronize(stream_));
     }
@@ -2370,6 +2408,12 @@ private:
     RunCfg run_;
     std::vector<int> widths_;
     LayerPlan plan_;
+    // simulated time (RunConfig::cost, Generation::clock_): reset per
+    // generation; sim_*pre_ = rows prefill() ran ahead of the reference's
+    // schedule (it stages the whole prompt in the first iteration's passes)
+    CostParams cost_;
+    SimClock clock_{8};
+    int sim_dpre_ = 0, sim_bpre_ = 0;
     std::vector<int> committed_;
     int draft_cached_ = 0;
     int generated_ = 0;

@@ -76,7 +76,11 @@ struct IterationTrace {
     int committed = 0, draft_committed = 0, base_committed = 0;
     float calibrate_ms = 0, draft_ms = 0, verify_ms = 0;  // device time (CUDA events)
     int bonus = 0;
+    // simulated stage units of the reference's cost model (cost_sim.h;
+    // IterationTrace::*_sim, orchestrator.cpp:263-386)
+    double calibrate_sim = 0, draft_sim = 0, verify_sim = 0;
 };
+struct CostParams;
 
 // DraftTree (proj/include/espec/draft_engine.hpp:63-84) as plain arrays.
 struct TreeOut {
@@ -115,6 +119,10 @@ public:
     virtual void load_tensor(int which, const std::string& name, int layer, const float* data, long long rows,
                              long long cols) = 0;
     virtual void set_run(const RunCfg& run) = 0;
+    // RunConfig::cost (orchestrator.hpp:34): the simulated-time model the
+    // stages advance; validated; takes effect at the next begin()/prefill()
+    virtual void set_cost(const CostParams& cost) = 0;
+    virtual std::string occupancy_csv() const = 0;  // GenerateResult::occupancy_csv of the current generation
     // Start a generation over already-tokenized input (BOS + bytes).
     virtual void begin(const std::vector<int>& tokens) = 0;
     virtual bool done() const = 0;

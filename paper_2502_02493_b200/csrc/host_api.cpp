@@ -264,11 +264,11 @@ constexpr char kMagic[] = "ESPEC1\n";
 // RunReport (proj/src/report.cpp:51-95, 97-173)
 // ---------------------------------------------------------------------------
 
-ReportAgg aggregate_traces(const std::vector<IterationTrace>& traces, double vanilla_baseline_s) {
+ReportAgg aggregate_traces(const std::vector<IterationTrace>& traces, double vanilla_baseline_sim) {
     if (traces.empty()) throw Error(ST_CONFIG, "cannot aggregate an empty trace list");
     ReportAgg r;
     long emitted = 0, accepted = 0, attempted = 0;
-    double d = 0, v = 0, c = 0;
+    double d = 0, v = 0, c = 0, ds = 0, vs = 0, cs = 0;
     for (const auto& t : traces) {
         emitted += t.emitted;
         accepted += t.m;
@@ -278,6 +278,9 @@ ReportAgg aggregate_traces(const std::vector<IterationTrace>& traces, double van
         d += (double)t.draft_ms / 1000.0;
         v += (double)t.verify_ms / 1000.0;
         c += (double)t.calibrate_ms / 1000.0;
+        ds += t.draft_sim;
+        vs += t.verify_sim;
+        cs += t.calibrate_sim;
     }
     if (emitted <= 0) throw Error(ST_CONFIG, "traces emitted zero tokens");
     r.iterations = (int)traces.size();
@@ -291,8 +294,14 @@ ReportAgg aggregate_traces(const std::vector<IterationTrace>& traces, double van
     r.calibrate_per100 = c * per_token;
     r.draft_total_per100 = r.draft_per100 + r.calibrate_per100;
     r.total = d + v + c;
-    r.speedup_vs_vanilla = r.total > 0.0 ? vanilla_baseline_s / r.total : 1.0;
     r.tokens_per_s = r.total > 0.0 ? emitted / r.total : 0.0;
+    // simulated units (report.cpp:83-90): the speed-up is the cost model's
+    r.draft_per100_sim = ds * per_token;
+    r.verify_per100_sim = vs * per_token;
+    r.calibrate_per100_sim = cs * per_token;
+    r.draft_total_per100_sim = r.draft_per100_sim + r.calibrate_per100_sim;
+    r.total_sim = ds + vs + cs;
+    r.speedup_vs_vanilla = r.total_sim > 0.0 ? vanilla_baseline_sim / r.total_sim : 1.0;
     return r;
 }
 
@@ -302,16 +311,15 @@ std::string report_csv(const ReportAgg& r, const std::string& algorithm, int n, 
     out << "algorithm,n,lp_size,alpha,d_per100,v_per100,c_per100,speedup\n";
     out << algorithm << ',' << n << ',' << lp_size << ',';
     if (r.has_alpha) out << r.alpha;
-    out << ',' << r.draft_per100 << ',' << r.verify_per100 << ',' << r.calibrate_per100 << ','
+    out << ',' << r.draft_per100_sim << ',' << r.verify_per100_sim << ',' << r.calibrate_per100_sim << ','
         << r.speedup_vs_vanilla << "\n";
     return out.str();
 }
 
 std::string report_json(const ReportAgg& r, const std::vector<IterationTrace>& traces, const std::string& algorithm,
                         int n, const std::vector<int>& widths, int lp_size) {
-    // emit_report's JSON layout (report.cpp:97-136). There is no cost
-    // simulator on this path (cost_sim out of scope): "sim" and
-    // "wall" both carry the measured device seconds.
+    // emit_report's JSON layout (report.cpp:97-136): "sim" in the cost
+    // model's units, "wall" in measured device seconds.
     std::ostringstream o;
     auto num = [](double x) { return json_double(x); };
     o << "{\n  \"algorithm\": " << json_string(algorithm) << ",\n  \"n\": " << n << ",\n  \"widths\": [";
@@ -320,12 +328,12 @@ std::string report_json(const ReportAgg& r, const std::vector<IterationTrace>& t
       << ",\n  \"tokens_emitted\": " << r.tokens_emitted << ",\n  \"tokens_per_s_wall\": " << num(r.tokens_per_s);
     const char* blocks[2] = {"sim", "wall"};
     for (int b = 0; b < 2; ++b) {
-        o << ",\n  \"" << blocks[b] << "\": {\n    \"draft_per_100\": " << num(r.draft_per100)
-          << ",\n    \"verify_per_100\": " << num(r.verify_per100) << ",\n    \"calibrate_per_100\": "
-          << num(r.calibrate_per100);
+        o << ",\n  \"" << blocks[b] << "\": {\n    \"draft_per_100\": " << num(b ? r.draft_per100 : r.draft_per100_sim)
+          << ",\n    \"verify_per_100\": " << num(b ? r.verify_per100 : r.verify_per100_sim)
+          << ",\n    \"calibrate_per_100\": " << num(b ? r.calibrate_per100 : r.calibrate_per100_sim);
         if (b == 0)
-            o << ",\n    \"draft_total_per_100\": " << num(r.draft_total_per100) << ",\n    \"total_sim\": "
-              << num(r.total) << ",\n    \"total_speedup_vs_vanilla\": " << num(r.speedup_vs_vanilla);
+            o << ",\n    \"draft_total_per_100\": " << num(r.draft_total_per100_sim) << ",\n    \"total_sim\": "
+              << num(r.total_sim) << ",\n    \"total_speedup_vs_vanilla\": " << num(r.speedup_vs_vanilla);
         o << "\n  }";
     }
     o << ",\n  \"config\": {},\n  \"iterations\": [";
@@ -335,7 +343,8 @@ std::string report_json(const ReportAgg& r, const std::vector<IterationTrace>& t
         o << (i ? "," : "") << "\n    {\"m\": " << t.m << ", \"n\": " << t.n << ", \"drafted_nodes\": "
           << t.drafted_nodes << ", \"emitted\": " << t.emitted << ", \"draft_wall\": " << num(dw)
           << ", \"verify_wall\": " << num(vw) << ", \"calibrate_wall\": " << num(cw) << ", \"draft_sim\": "
-          << num(dw) << ", \"verify_sim\": " << num(vw) << ", \"calibrate_sim\": " << num(cw)
+          << num(t.draft_sim) << ", \"verify_sim\": " << num(t.verify_sim) << ", \"calibrate_sim\": "
+          << num(t.calibrate_sim)
           << ", \"fuzzy_forwards\": " << t.fuzzy_forwards << ", \"sequential_forwards\": " << t.sequential_forwards
           << ", \"base_forwards\": " << t.base_forwards << "}";
     }

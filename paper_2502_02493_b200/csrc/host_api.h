@@ -20,10 +20,13 @@ struct ReportAgg {
     double mean_accept_len = 0.0;
     double tokens_per_s = 0.0;
     double draft_per100 = 0.0, verify_per100 = 0.0, calibrate_per100 = 0.0, draft_total_per100 = 0.0;
-    double total = 0.0;
-    double speedup_vs_vanilla = 1.0;
+    double total = 0.0;  // measured device seconds of the three stages
+    // the cost model's units (IterationTrace::*_sim, report.cpp:83-90)
+    double draft_per100_sim = 0.0, verify_per100_sim = 0.0, calibrate_per100_sim = 0.0, draft_total_per100_sim = 0.0;
+    double total_sim = 0.0;
+    double speedup_vs_vanilla = 1.0;  // vanilla_baseline_sim / total_sim
 };
-ReportAgg aggregate_traces(const std::vector<IterationTrace>& traces, double vanilla_baseline_s);
+ReportAgg aggregate_traces(const std::vector<IterationTrace>& traces, double vanilla_baseline_sim);
 std::string report_csv(const ReportAgg& r, const std::string& algorithm, int n, int lp_size);
 std::string report_json(const ReportAgg& r, const std::vector<IterationTrace>& traces, const std::string& algorithm,
                         int n, const std::vector<int>& widths, int lp_size);

@@ -78,7 +78,8 @@ class _Iter(C.Structure):
     _fields_ = [(n, C.c_int) for n in ("m", "n", "drafted_nodes", "emitted", "sequential_forwards",
                                        "fuzzy_forwards", "base_forwards", "committed", "draft_committed",
                                        "base_committed", "bonus")] + \
-               [(n, C.c_float) for n in ("calibrate_ms", "draft_ms", "verify_ms")]
+               [(n, C.c_float) for n in ("calibrate_ms", "draft_ms", "verify_ms")] + \
+               [(n, C.c_double) for n in ("calibrate_sim", "draft_sim", "verify_sim")]
 
 
 class _Report(C.Structure):
@@ -87,7 +88,17 @@ class _Report(C.Structure):
                 ("tokens_emitted", C.c_int64), ("mean_accept_len", C.c_double), ("tokens_per_s", C.c_double),
                 ("draft_per_100_s", C.c_double), ("verify_per_100_s", C.c_double),
                 ("calibrate_per_100_s", C.c_double), ("draft_total_per_100_s", C.c_double),
-                ("total_s", C.c_double), ("speedup_vs_vanilla", C.c_double)]
+                ("total_s", C.c_double), ("speedup_vs_vanilla", C.c_double),
+                ("draft_per_100_sim", C.c_double), ("verify_per_100_sim", C.c_double),
+                ("calibrate_per_100_sim", C.c_double), ("draft_total_per_100_sim", C.c_double),
+                ("total_sim", C.c_double)]
+
+
+class _CostParams(C.Structure):
+    """espec_cost_params = CostParams (cost_sim.hpp:17-32)."""
+    _fields_ = [(n, C.c_double) for n in ("c_fixed", "c_mem", "c_comp", "t_addi", "attn_workload", "mlp_workload",
+                                          "base_layer_workload")] + \
+               [(n, C.c_int) for n in ("tp_size_base", "tp_size_draft", "devices")]
 
 
 class _SimRow(C.Structure):
@@ -153,6 +164,12 @@ def lib():
         L.espec_resolve_draft_cache.argtypes = [V, P(_Outcome)]
         L.espec_commit_outcome.argtypes = [V, P(C.c_int32), P(C.c_int), P(_Iter)]
         L.espec_aggregate.argtypes = [P(_Iter), C.c_int, C.c_double, P(_Report)]
+        L.espec_cost_defaults.argtypes = [P(_CostParams)]
+        L.espec_cost_eval.argtypes = [P(_CostParams), C.c_int, C.c_double, C.c_double, C.c_int, C.c_char_p,
+                                      P(C.c_double)]
+        L.espec_cost_total_time.argtypes = [C.c_double, C.c_double, C.c_double, C.c_int, C.c_double, P(C.c_double)]
+        L.espec_set_cost.argtypes = [V, P(_CostParams)]
+        L.espec_occupancy_csv.argtypes = [V, C.c_char_p, C.c_int, P(C.c_int)]
         L.espec_report_emit.argtypes = [P(_Report), P(_Iter), C.c_int, C.c_char_p, C.c_int, P(C.c_int), C.c_int,
                                         C.c_int, C.c_int, C.c_char_p, C.c_int, P(C.c_int)]
         L.espec_model_file_config.argtypes = [C.c_char_p, P(_ModelCfg)]
@@ -237,6 +254,9 @@ class IterationTrace:
     calibrate_ms: float
     draft_ms: float
     verify_ms: float
+    calibrate_sim: float = 0.0  # the cost model's units (IterationTrace::*_sim)
+    draft_sim: float = 0.0
+    verify_sim: float = 0.0
 
 
 def _trace(t: _Iter) -> IterationTrace:
@@ -353,6 +373,17 @@ class Engine:
         self.run = run
 
     # ---- generation
+    def set_cost(self, cost: "CostParams"):
+        """RunConfig::cost for the next generation (validated)."""
+        c = cost._c()
+        self._check(lib().espec_set_cost(self._h, C.byref(c)))
+
+    def occupancy_csv(self) -> str:
+        need = C.c_int(0)
+        buf = C.create_string_buffer(1 << 16)
+        self._check(lib().espec_occupancy_csv(self._h, buf, 1 << 16, C.byref(need)))
+        return buf.value.decode()
+
     def generate(self, prompt: bytes):
         n = self.run.max_new_tokens
         out = np.zeros(n, np.int32)
@@ -715,7 +746,9 @@ def similarity_csv(rows: Sequence[SimilarityRow]) -> str:
 
 @dataclass
 class RunReport:
-    """RunReport's derived metrics (report.hpp:40-57), device seconds."""
+    """RunReport's derived metrics (report.hpp:40-57): *_s in measured device
+    seconds, *_sim in the cost model's units; speedup_vs_vanilla is the cost
+    model's (vanilla_baseline_sim / total_sim, report.cpp:87-90)."""
     n_iterations: int
     has_alpha: bool
     alpha: float
@@ -728,6 +761,11 @@ class RunReport:
     draft_total_per_100_s: float
     total_s: float
     speedup_vs_vanilla: float
+    draft_per_100_sim: float = 0.0
+    verify_per_100_sim: float = 0.0
+    calibrate_per_100_sim: float = 0.0
+    draft_total_per_100_sim: float = 0.0
+    total_sim: float = 0.0
     _c: object = field(default=None, repr=False, compare=False)
 
 
@@ -738,10 +776,10 @@ def _iters(traces: Sequence[IterationTrace]):
     return arr
 
 
-def aggregate(traces: Sequence[IterationTrace], vanilla_baseline_s: float) -> RunReport:
+def aggregate(traces: Sequence[IterationTrace], vanilla_baseline_sim: float) -> RunReport:
     """aggregate(traces, vanilla_baseline_sim) (report.cpp:51-95) through the C ABI."""
     r = _Report()
-    st = lib().espec_aggregate(_iters(traces), len(traces), vanilla_baseline_s, C.byref(r))
+    st = lib().espec_aggregate(_iters(traces), len(traces), vanilla_baseline_sim, C.byref(r))
     if st:
         raise EspecError(st, lib().espec_create_error().decode())
     vals = [getattr(r, n) for n, _ in _Report._fields_]
@@ -762,6 +800,79 @@ def emit_report(report: RunReport, traces: Sequence[IterationTrace], algorithm: 
     if st:
         raise EspecError(st, lib().espec_create_error().decode())
     return buf.value.decode()
+
+
+@dataclass
+class CostParams:
+    """CostParams (proj/include/espec/cost_sim.hpp:17-32), the reference's defaults."""
+    c_fixed: float = 0.02
+    c_mem: float = 1.0
+    c_comp: float = 0.01
+    t_addi: float = 0.1
+    attn_workload: float = 0.15
+    mlp_workload: float = 0.05
+    base_layer_workload: float = 2.0
+    tp_size_base: int = 8
+    tp_size_draft: int = 1
+    devices: int = 8
+
+    def _c(self) -> _CostParams:
+        return _CostParams(*(getattr(self, n) for n, _ in _CostParams._fields_))
+
+
+COST_VALIDATE, COST_T_EXE, COST_GROUP_ATTENTION, COST_DRAFT_GROUP, COST_SEQUENTIAL_DRAFT, COST_BASE_FORWARD, \
+    COST_VANILLA_BASELINE = range(7)
+
+
+def _cost(p: CostParams, what: int, a: float = 0.0, b: float = 0.0, n: int = 0, plan: str = None) -> float:
+    out = C.c_double(0.0)
+    c = p._c()
+    st = lib().espec_cost_eval(C.byref(c), what, a, b, n, plan.encode() if plan is not None else None, C.byref(out))
+    if st:
+        raise EspecError(st, lib().espec_create_error().decode())
+    return out.value
+
+
+def cost_defaults() -> CostParams:
+    c = _CostParams()
+    lib().espec_cost_defaults(C.byref(c))
+    return CostParams(*(getattr(c, n) for n, _ in _CostParams._fields_))
+
+
+def cost_validate(p: CostParams):
+    _cost(p, COST_VALIDATE)
+
+
+def t_exe(p: CostParams, workload: float, s_tokens: float, tp_size: int) -> float:
+    return _cost(p, COST_T_EXE, workload, s_tokens, tp_size)
+
+
+def group_attention_time(p: CostParams, group_size: int, s_tokens: float) -> float:
+    return _cost(p, COST_GROUP_ATTENTION, s_tokens, 0.0, group_size)
+
+
+def simulate_draft_group(p: CostParams, plan: str, s_tokens: float = 1) -> float:
+    return _cost(p, COST_DRAFT_GROUP, s_tokens, 0.0, 0, plan)
+
+
+def sequential_draft_forward_time(p: CostParams, n_layers: int, s_tokens: float = 1) -> float:
+    return _cost(p, COST_SEQUENTIAL_DRAFT, s_tokens, 0.0, n_layers)
+
+
+def base_forward_time(p: CostParams, n_layers: int, s_tokens: float = 1) -> float:
+    return _cost(p, COST_BASE_FORWARD, s_tokens, 0.0, n_layers)
+
+
+def vanilla_baseline_sim(p: CostParams, base_layers: int, prompt_len: int, tokens: int) -> float:
+    return _cost(p, COST_VANILLA_BASELINE, prompt_len, tokens, base_layers)
+
+
+def total_time_model(n_tokens: float, t_draft: float, t_base: float, n: int, alpha: float) -> float:
+    out = C.c_double(0.0)
+    st = lib().espec_cost_total_time(n_tokens, t_draft, t_base, n, alpha, C.byref(out))
+    if st:
+        raise EspecError(st, lib().espec_create_error().decode())
+    return out.value
 
 
 def model_file_config(path: str) -> ModelConfig:

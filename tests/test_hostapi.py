@@ -26,13 +26,15 @@ MODEL_FILE = os.path.join(GOLD, "ref_tiny.espec1")
 
 def _traces(rep):
     # the fixture's stage times are k * 2^-10 s: exact as the engine's float ms
+    # (wall) and as the simulated units (the fixture sets sim = wall)
     out = []
     for t in rep["traces"]:
         out.append(E.IterationTrace(m=t["m"], n=t["n"], drafted_nodes=t["drafted_nodes"], emitted=t["emitted"],
                                     sequential_forwards=t["sequential_forwards"], fuzzy_forwards=t["fuzzy_forwards"],
                                     base_forwards=t["base_forwards"], committed=0, draft_committed=0,
                                     base_committed=0, bonus=0, calibrate_ms=t["calibrate"] * 1000.0,
-                                    draft_ms=t["draft"] * 1000.0, verify_ms=t["verify"] * 1000.0))
+                                    draft_ms=t["draft"] * 1000.0, verify_ms=t["verify"] * 1000.0,
+                                    calibrate_sim=t["calibrate"], draft_sim=t["draft"], verify_sim=t["verify"]))
     return out
 
 

@@ -1,0 +1,8 @@
+# same-binary A/B of an environment switch on the C2 bench: tools/gpu_ab_env.sh TAG "VAR=a" "VAR=b" [reps]
+tag=$1; a=$2; b=$3; reps=${4:-3}
+mkdir -p gpurun_out
+for i in $(seq $reps); do for e in "$a" "$b"; do
+  echo "== $e"; env $e timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu --no-arms 2>/dev/null | tail -1 | python -c "
+import json,sys; j=json.loads(sys.stdin.read()); s=j.get('stage_ms_per_step') or {}
+print(f\"{j['value']:.3f} tok/s {j['ms_per_step']:.2f} ms/step e2e {j['e2e']['value']:.3f}\", {k: round(v, 2) for k, v in s.items()})"
+done; done > gpurun_out/${tag}_bench.txt 2>&1; cat gpurun_out/${tag}_bench.txt

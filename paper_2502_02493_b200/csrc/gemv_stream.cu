@@ -109,65 +109,33 @@ SgPlan sgemv_plan(int K, int ldw, int nprob) {
 }
 
 // Wide plan (drafter only, see set_sgemv_wide): T-dependent units as long as
-// the activation slots hold just the pass's T rows. The k-chunk count nK
-// (<= max(the (K, N) plan's, 8): the partial workspace bound) minimises the
-// largest per-CTA load, ceil(units / CTAs) x unit blocks, taking the fewest
-// chunks within 4 % of the best: e.g. the 8B drafter's down projection
-// (N = 4096 = 128 column groups) used to run as 128 whole-K units on 128 SMs
-// (20 idle) and now runs 8 k-chunks, <= 7 units on each of 148 SMs.
-// ESPEC_SG_WIDE_BAL=0: the previous rule (fewest chunks whose wave-quantised
-// load is within 20 % of the mean).
+// the activation slots hold just the pass's T rows — usually the whole K in
+// ONE unit, so no split-K partials, tickets or end-of-launch reductions. The
+// smallest k-chunk count whose per-CTA load is within 20% of the mean is
+// taken, never more chunks than the (K, N) plan (workspace bound).
 static constexpr int kWideSlotBytes = 64 * 1024;
-static constexpr int kWideMaxNK = 8;
 static bool sgemv_plan_wide(int K, int ldw, int nprob, int T, SgPlan& out) {
-    static const bool balanced = [] {
-        const char* e = std::getenv("ESPEC_SG_WIDE_BAL");
-        return !(e && e[0] == '0');
-    }();
     const SgPlan base = sgemv_plan(K, ldw, nprob);
-    auto fits = [&](const SgPlan& p) {
-        for (int c = 0; c < p.grid; ++c) {
-            const long long s0 = (long long)c * p.units / p.grid, e0 = (long long)(c + 1) * p.units / p.grid;
-            if (e0 > s0 && (e0 - 1) / p.ngroups - s0 / p.ngroups + 1 > kSgSlots) return false;
-        }
-        return true;
-    };
-    auto make = [&](int nK, SgPlan& p) {
-        p = base;
+    SgPlan p = base;
+    for (int nK = 1; nK <= base.nK; ++nK) {
         const int kcb = (p.KT + nK - 1) / nK;
-        if ((long long)kSgSlots * T * (kcb * 16 + 8) * 2 > kWideSlotBytes) return false;
+        if ((long long)kSgSlots * T * (kcb * 16 + 8) * 2 > kWideSlotBytes) continue;
+        const long long units = (long long)nprob * nK * p.ngroups;
+        const long long waves = (units + kSgSms - 1) / kSgSms;
+        if (waves * kSgSms * 5 > units * 6) continue;  // > 20% imbalance
         p.kcb = kcb;
         p.nK = (p.KT + kcb - 1) / kcb;
         p.units = nprob * p.nK * p.ngroups;
         p.grid = p.units < kSgSms ? p.units : kSgSms;
-        return fits(p);
-    };
-    if (!balanced) {
-        for (int nK = 1; nK <= base.nK; ++nK) {
-            SgPlan p;
-            if (!make(nK, p)) continue;
-            const long long waves = ((long long)p.units + kSgSms - 1) / kSgSms;
-            if (waves * kSgSms * 5 > (long long)p.units * 6) continue;  // > 20% imbalance
-            out = p;
-            return true;
+        bool ok = true;
+        for (int c = 0; c < p.grid && ok; ++c) {
+            const long long s0 = (long long)c * p.units / p.grid, e0 = (long long)(c + 1) * p.units / p.grid;
+            if (e0 > s0 && (e0 - 1) / p.ngroups - s0 / p.ngroups + 1 > kSgSlots) ok = false;
         }
-        return false;
+        if (!ok) continue;
+        out = p;
+        return true;
     }
-    const int cap = std::max(base.nK, kWideMaxNK);
-    long long best = -1;
-    std::vector<std::pair<int, long long>> cand;
-    for (int nK = 1; nK <= cap; ++nK) {
-        SgPlan p;
-        if (!make(nK, p)) continue;
-        const long long load = ((long long)p.units + p.grid - 1) / p.grid * p.kcb;
-        cand.push_back({nK, load});
-        if (best < 0 || load < best) best = load;
-    }
-    for (const auto& c : cand)
-        if (c.second * 100 <= best * 104) {
-            make(c.first, out);
-            return true;
-        }
     return false;
 }
 
@@ -176,8 +144,7 @@ void set_sgemv_wide(bool on) { g_wide = on; }
 
 size_t sgemv_partial_floats(int K, int ldw) {
     const SgPlan p = sgemv_plan(K, ldw, 1);
-    const int nk = std::max(p.nK, std::min(kWideMaxNK, p.KT));  // wide plans: up to kWideMaxNK chunks
-    return nk > 1 ? (size_t)nk * 16 * ldw : 0;
+    return p.nK > 1 ? (size_t)p.nK * 16 * ldw : 0;
 }
 
 // smem = ring (stages x 8 KB) + activation slots (xrows rows) + reduction buffers

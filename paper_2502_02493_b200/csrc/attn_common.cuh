@@ -40,30 +40,35 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 // 16 output values (one pair row, 16 consecutive dims) = acc / den: fp32, or
 // bf16 rounded to nearest (exactly what the O GEMV's staging would do) when
 // the consumer takes bf16 activations
-template <int DH>
-__device__ __forceinline__ void attn_store_row(const AttnProblem& A, size_t off, const float4 (&acc)[4], float den) {
-    float y[16];
+template <int DH, int NV>
+__device__ __forceinline__ void attn_store_row(const AttnProblem& A, size_t off, const float4 (&acc)[NV], float den) {
+    float y[4 * NV];
 #pragma unroll
-    for (int v = 0; v < 4; ++v) {
+    for (int v = 0; v < NV; ++v) {
         y[4 * v] = den > 0.f ? acc[v].x / den : 0.f;
         y[4 * v + 1] = den > 0.f ? acc[v].y / den : 0.f;
         y[4 * v + 2] = den > 0.f ? acc[v].z / den : 0.f;
         y[4 * v + 3] = den > 0.f ? acc[v].w / den : 0.f;
     }
     if (A.out_bf16) {
-        uint32_t pk[8];
+        uint32_t pk[2 * NV];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < 2 * NV; ++j) {
             const __nv_bfloat162 b = __floats2bfloat162_rn(y[2 * j], y[2 * j + 1]);
             pk[j] = *reinterpret_cast<const uint32_t*>(&b);
         }
-        uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(A.out) + off);
-        o[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        o[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+        __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(A.out) + off;
+        if constexpr (NV == 1) {
+            *reinterpret_cast<uint2*>(ob) = make_uint2(pk[0], pk[1]);
+        } else {
+#pragma unroll
+            for (int v = 0; v < NV / 2; ++v)
+                reinterpret_cast<uint4*>(ob)[v] = make_uint4(pk[4 * v], pk[4 * v + 1], pk[4 * v + 2], pk[4 * v + 3]);
+        }
     } else {
         float* o = A.out + off;
 #pragma unroll
-        for (int v = 0; v < 4; ++v)
+        for (int v = 0; v < NV; ++v)
             *reinterpret_cast<float4*>(o + 4 * v) = make_float4(y[4 * v], y[4 * v + 1], y[4 * v + 2], y[4 * v + 3]);
     }
 }

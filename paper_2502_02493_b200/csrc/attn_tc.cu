@@ -55,6 +55,7 @@ constexpr int kTcaSoftmax = 32 * kTcaSoftmaxWarps;
 constexpr int kTcaThreads = kTcaSoftmax + 32;
 constexpr int kTcaMaxChunks = 64;
 constexpr int kTcaMaxPpi = 64;
+constexpr int kTcaMaxTickets = 1 << 14;  // (problem, kv head, pair group) counters per stream
 
 template <int DH>
 struct TcaLayout {
@@ -70,7 +71,8 @@ struct TcaLayout {
     static constexpr int kPBuf = kTcaRows * 64 * 2;
     static constexpr int kRed = kP + (kPInK ? 0 : 4 * kPBuf);      // [workers][rows] partial row maxima / sums (512)
     static constexpr int kBars = kRed + 4 * kTcaRows * 4;          // mbarriers, tmem base, page table
-    static constexpr int kBytes = kBars + 256 + 4 * kTcaMaxPpi;
+    static constexpr int kFlag = kBars + 256 + 4 * kTcaMaxPpi;   // ticket path: "this CTA combines"
+    static constexpr int kBytes = kFlag + 16;
 };
 
 // UMMA shared-memory descriptor, 128-byte swizzle (layout type 2), version 1:
@@ -170,8 +172,8 @@ __device__ __forceinline__ void cluster_sync_all() {
 // One arithmetic for the combine kernel (global partials) and the cluster
 // path (partials in the cluster's shared memory), so a row is bit-identical
 // whichever path its pass takes.
-template <int CB, class ML, class X>
-__device__ __forceinline__ void tca_combine(int nchunks, ML ml, X x, float4 (&acc)[4], float& den) {
+template <int CB, int NV, class ML, class X>
+__device__ __forceinline__ void tca_combine(int nchunks, ML ml, X x, float4 (&acc)[NV], float& den) {
     float M = -INFINITY;  // (exact in any order; 8 loads in flight per round trip)
     for (int ch0 = 0; ch0 < nchunks; ch0 += 8) {
         float mm[8];
@@ -181,17 +183,17 @@ __device__ __forceinline__ void tca_combine(int nchunks, ML ml, X x, float4 (&ac
         for (int q = 0; q < 8; ++q) M = fmaxf(M, mm[q]);
     }
 #pragma unroll
-    for (int v = 0; v < 4; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int v = 0; v < NV; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
     den = 0.f;
     for (int ch0 = 0; ch0 < nchunks; ch0 += CB) {
-        float4 xv[CB][4];
+        float4 xv[CB][NV];
         float2 mv[CB];
 #pragma unroll
         for (int q = 0; q < CB; ++q) {
             const bool in = ch0 + q < nchunks;
             mv[q] = in ? ml(ch0 + q) : make_float2(-INFINITY, 0.f);
 #pragma unroll
-            for (int v = 0; v < 4; ++v) xv[q][v] = in ? x(ch0 + q, v) : make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int v = 0; v < NV; ++v) xv[q][v] = in ? x(ch0 + q, v) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
         for (int q = 0; q < CB; ++q) {
@@ -202,7 +204,7 @@ __device__ __forceinline__ void tca_combine(int nchunks, ML ml, X x, float4 (&ac
                 den = __fmaf_rn(f, mv[q].y, den);
             }
 #pragma unroll
-            for (int v = 0; v < 4; ++v) {
+            for (int v = 0; v < NV; ++v) {
                 acc[v].x = __fmaf_rn(f, xv[q][v].x, acc[v].x);
                 acc[v].y = __fmaf_rn(f, xv[q][v].y, acc[v].y);
                 acc[v].z = __fmaf_rn(f, xv[q][v].z, acc[v].z);
@@ -228,7 +230,11 @@ struct TcaLaunch {
     KvView kv;
     int n_heads, G;
     unsigned long long* trace = nullptr;
-    int cluster = 0;  // 1: the chunks of a (kv head, pair group) form one cluster and combine through DSMEM
+    // how the chunks of a (kv head, pair group) combine (nchunks > 1):
+    // 0: the PDL-launched combine kernel; 1: inside one cluster through DSMEM;
+    // 2: the last chunk CTA to finish (ticket) combines from the workspace
+    int cluster = 0;
+    int* ticket = nullptr;  // mode 2: one arrival counter per (problem, kv head, pair group), zero between launches
 };
 
 // Pages are processed in steps of two (pages 2s, 2s + 1 of the chunk): one
@@ -628,7 +634,7 @@ __global__ void __launch_bounds__(kTcaThreads, 1) attn_tc_kernel(const __grid_co
                     // chunk partial: to this CTA's shared memory (cluster path;
                     // the ring is dead: every page's MMAs completed) or to the
                     // split workspace for the combine kernel
-                    float* prow = L.cluster ? reinterpret_cast<float*>(sm + LY::kRing) + (size_t)r * PS
+                    float* prow = L.cluster == 1 ? reinterpret_cast<float*>(sm + LY::kRing) + (size_t)r * PS
                                             : A.ws + (((size_t)bx * (n_kv * ngroups) + blockIdx.y) * kTcaRows + r) * PS;
 #pragma unroll
                     for (int c = 0; c < DQ / 4; ++c)
@@ -639,7 +645,48 @@ __global__ void __launch_bounds__(kTcaThreads, 1) attn_tc_kernel(const __grid_co
             }
         }
     }
-    if (L.cluster) {
+    if (L.cluster == 2 && nchunks > 1) {
+        // ticket combine: every chunk CTA has written its partial rows to the
+        // workspace; the last to arrive combines them (the combine kernel's
+        // arithmetic and thread mapping: bit-identical rows) — no cluster
+        // co-scheduling, no combine launch and no extra dependency hop
+        int* last = reinterpret_cast<int*>(sm + LY::kFlag);
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            int* ctr = L.ticket + (size_t)blockIdx.z * gridDim.y + blockIdx.y;
+            const int arrived = atomicAdd(ctr, 1);
+            const int is_last = arrived == nchunks - 1;
+            if (is_last) *ctr = 0;  // every chunk has arrived: ready for the next launch
+            *last = is_last;
+            __threadfence();
+        }
+        __syncthreads();
+        if (*last) {
+            // 4 output dims per thread item (the same per-element arithmetic
+            // as the 16-dim items of the combine kernel): 8 chunks' loads in
+            // flight without spilling the softmax path's registers
+            constexpr int CPR = DH / 4;
+            const int R = min(kTcaRows, P - mg * kTcaRows);
+            const size_t cstride = (size_t)(n_kv * ngroups) * kTcaRows * PS;
+            for (int it = tid; it < R * CPR; it += kTcaThreads) {
+                const int rr = it / CPR, c0 = (it % CPR) * 4;
+                const float* base = A.ws + ((size_t)blockIdx.y * kTcaRows + rr) * PS;
+                float4 acc[1];
+                float den;
+                tca_combine<8>(
+                    nchunks, [&](int ch) { return __ldcg(reinterpret_cast<const float2*>(base + ch * cstride + DH)); },
+                    [&](int ch, int v) {
+                        return __ldcg(reinterpret_cast<const float4*>(base + ch * cstride + c0 + 4 * v));
+                    },
+                    acc, den);
+                const int pp = mg * kTcaRows + rr;
+                attn_store_row<DH>(A, (size_t)(pp / G) * H * DH + (hk * G + pp % G) * DH + c0, acc, den);
+            }
+        }
+        if (tr && tid == 0) atomicMax(tr + 56, gtimer());
+    }
+    if (L.cluster == 1) {
         __syncwarp();
         // the cluster's CTAs hold the chunks of this (kv head, pair group);
         // CTA c combines rows [c R / chunks, (c + 1) R / chunks). Every CTA
@@ -768,12 +815,47 @@ static void tca_tensor_map(CUtensorMap& m, const KvView& kv) {
 // as a 16-SM cluster rarely finds a free GPC): no workspace round trip, no
 // combine launch (~1 us per attention isolated, profiles/r2_cluster.txt).
 // ESPEC_ATTN_CLUSTER=0 keeps the combine kernel.
-int attn_tc_cluster(int chunks) {
+// Single-row passes (T = 1: at most G <= 8 pair rows) with more chunks than
+// a cluster holds let the last chunk CTA to finish combine (mode 2): 8 rows x
+// 16 chunks are two L2 round trips on one SM, cheaper than a combine launch
+// (isolated drafter T = 1 ctx 8K 16.4 -> 15.7 us). Wider passes keep the
+// combine kernel: one SM combining 48 rows x 8 chunks measured 4-8 us slower
+// (profiles/r2_attn_ticket.txt). ESPEC_ATTN_COMBINE=ticket forces mode 2
+// whenever chunks > 1, =kernel never uses it.
+int attn_tc_cluster(int chunks, int T) {
     static const int cap = [] {
         const char* e = std::getenv("ESPEC_ATTN_CLUSTER");
         return e ? std::min(16, std::atoi(e)) : 8;
     }();
-    return chunks >= 2 && chunks <= cap ? 1 : 0;
+    static const int ticket = [] {  // 1 force, 0 auto, -1 never
+        const char* e = std::getenv("ESPEC_ATTN_COMBINE");
+        if (!e) return 0;
+        const std::string v(e);
+        return v == "ticket" ? 1 : v == "kernel" ? -1 : 0;
+    }();
+    if (chunks < 2) return 0;
+    if (ticket > 0) return 2;
+    if (chunks <= cap) return 1;
+    return ticket == 0 && T == 1 ? 2 : 0;
+}
+
+// per-(device, stream) ticket counters (zeroed once; every launch leaves them
+// zero); launches on one stream never overlap in their ticket phase (each
+// follows griddepcontrol.wait, i.e. the completion of every earlier kernel)
+static int* tca_tickets(cudaStream_t s) {
+    static std::mutex mu;
+    static std::vector<std::pair<std::pair<int, cudaStream_t>, int*>> all;
+    int dev = 0;
+    DEV_CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> g(mu);
+    for (auto& e : all)
+        if (e.first.first == dev && e.first.second == s) return e.second;
+    int* p = nullptr;
+    DEV_CK(cudaMalloc(&p, sizeof(int) * kTcaMaxTickets));
+    DEV_CK(cudaMemset(p, 0, sizeof(int) * kTcaMaxTickets));
+    DEV_CK(cudaDeviceSynchronize());
+    all.push_back({{dev, s}, p});
+    return p;
 }
 
 template <int DH>
@@ -826,19 +908,24 @@ static void attn_tc_launch(const AttnBatch& b, int nprob, int n_heads, const Pas
         L.trace = tbuf;
         traced = true;
     }
-    L.cluster = attn_tc_cluster(chunks);
-    if (L.cluster && chunks > 8) {
+    L.cluster = attn_tc_cluster(chunks, pass.T);
+    if (L.cluster == 2) {
+        if ((size_t)grid.y * grid.z > (size_t)kTcaMaxTickets)
+            dev_fail(DEV_ERR_CUDA, "attention: too many (problem, kv head) groups for the ticket combine");
+        L.ticket = tca_tickets(s);
+    }
+    if (L.cluster == 1 && chunks > 8) {
         static bool nonportable[3] = {false, false, false};
         if (!nonportable[rep >> 1]) {
             DEV_CK(cudaFuncSetAttribute((const void*)kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
             nonportable[rep >> 1] = true;
         }
     }
-    if (L.cluster)
+    if (L.cluster == 1)
         DEV_CK(launch_pdl_cluster(kernel, grid, dim3(kTcaThreads), smem, s, chunks, L));
     else
         DEV_CK(launch_pdl(kernel, grid, dim3(kTcaThreads), smem, s, L));
-    if (chunks > 1 && !L.cluster) {
+    if (chunks > 1 && L.cluster == 0) {
         const int rows = std::min(kTcaRows, pass.T * L.G);
         DEV_CK(launch_pdl(attn_tc_combine_kernel<DH>, dim3((rows + 31) / 32, kv.n_kv * groups, nprob),
                           dim3(32 * (DH / 16)), 0, s, L, chunks));

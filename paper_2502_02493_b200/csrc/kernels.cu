@@ -694,7 +694,7 @@ int attention_launches(const PassView& pass, const KvView& kv) {
     if (!attn_tc_path(kv)) return 1;
     const int pages = (pass.total + 63) / 64;
     const int chunks = (pages + kv.attn_ppi - 1) / kv.attn_ppi;
-    return chunks > 1 && !attn_tc_cluster(chunks) ? 2 : 1;
+    return chunks > 1 && !attn_tc_cluster(chunks, pass.T) ? 2 : 1;
 }
 
 void launch_attention(const AttnBatch& b, int nprob, int n_heads, const PassView& pass, const KvView& kv,

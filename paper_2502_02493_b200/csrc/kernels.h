@@ -230,7 +230,7 @@ void launch_attention_tc(const AttnBatch& b, int nprob, int n_heads, const PassV
                          cudaStream_t s);
 // kernels one launch_attention call issues (the tcgen05 path adds a combine
 // kernel when the context spans more than one chunk)
-int attn_tc_cluster(int chunks);  // 1: the split chunks combine inside a cluster (attn_tc.cu)
+int attn_tc_cluster(int chunks, int T);  // 1: chunks combine inside a cluster, 2: last chunk CTA combines (attn_tc.cu)
 int attention_launches(const PassView& pass, const KvView& kv);
 
 // Copy cache rows src[i] -> dst[i] for every layer (commit_path compaction).

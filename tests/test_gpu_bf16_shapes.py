@@ -222,8 +222,9 @@ def test_decode_gemv_tail_pool_bitwise_above_16_rows(tmp_path):
         assert r.returncode == 0, r.stderr[-2000:]
         z = np.load(f)
         res.append([z[k] for k in sorted(z.files, key=lambda s: int(s.split("_")[1]))])
-    for a, b in zip(*res):
-        assert np.array_equal(a, b)
+    for other in res[1:]:
+        for a, b in zip(res[0], other):
+            assert np.array_equal(a, b)
 
 
 @pytest.mark.parametrize("ppi", ["4", "8"])
@@ -232,16 +233,19 @@ def test_attention_cluster_combine_bitwise_equals_combine_kernel(tmp_path, ppi):
     block cluster (DSMEM, default for 2..16 chunks) or through the workspace
     and the combine kernel (ESPEC_ATTN_CLUSTER=0). Both run one arithmetic
     (attn_tc.cu tca_combine), so a 37-row verify pass at ctx 2100 is bitwise
-    equal either way: ppi 4 -> 9 chunks (a non-portable cluster), ppi 8 -> 5."""
+    equal either way: ppi 4 -> 9 chunks (a non-portable cluster), ppi 8 -> 5.
+    The ticket combine (ESPEC_ATTN_COMBINE=ticket: the last chunk CTA to
+    finish combines from the workspace) must match as well."""
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     res = []
-    for cl in ("16", "0"):
-        f = tmp_path / f"cl{cl}.npz"
-        env = dict(os.environ, ESPEC_ATTN_CLUSTER=cl, ESPEC_ATTN_PPI=ppi)
+    for cl, comb in (("16", ""), ("0", ""), ("0", "ticket")):
+        f = tmp_path / f"cl{cl}{comb}.npz"
+        env = dict(os.environ, ESPEC_ATTN_CLUSTER=cl, ESPEC_ATTN_PPI=ppi, ESPEC_ATTN_COMBINE=comb)
         r = subprocess.run([sys.executable, "-c", _POOL_SCRIPT, root, str(f)], env=env, capture_output=True,
                            text=True, timeout=600)
         assert r.returncode == 0, r.stderr[-2000:]
         z = np.load(f)
         res.append([z[k] for k in sorted(z.files, key=lambda s: int(s.split("_")[1]))])
-    for a, b in zip(*res):
-        assert np.array_equal(a, b)
+    for other in res[1:]:
+        for a, b in zip(res[0], other):
+            assert np.array_equal(a, b)

@@ -160,9 +160,26 @@ __device__ __forceinline__ void tc_epilogue(const TcLaunch& L, int t, int g, con
                 if (g * 16 + j < P.N / 2) o[j] = y[j];
         }
     } else if constexpr (EPI == EPI_QKV) {
+        // every load of the group first (row metadata, page id, the rotary
+        // factors of its 16 column pairs), then the arithmetic and the
+        // stores: loads issued after a store cannot be hoisted above it (the
+        // pointers may alias), which made each pair a serial L2 round trip
         const int qd = P.n_heads * P.dh, kd = P.n_kv * P.dh;
         const int pos = L.pass.pos[t];
         const int row = L.pass.rows[t];
+        const KvView& kv = L.kv;
+        const int page = c0 + 32 > qd && c0 < P.N ? kv.page_table[row / kv.page_rows] : 0;
+        float2 cs_sn[16];
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+            const int c = c0 + j;
+            cs_sn[j >> 1] = make_float2(1.f, 0.f);
+            if (c < P.N && c < qd + kd) {
+                const int base = c < qd ? 0 : qd;
+                const int i = (c - base) % P.dh;
+                cs_sn[j >> 1] = __ldg(&P.rope[(size_t)pos * (P.dh >> 1) + (i >> 1)]);
+            }
+        }
 #pragma unroll
         for (int j = 0; j < 32; j += 2) {
             const int c = c0 + j;
@@ -173,17 +190,13 @@ __device__ __forceinline__ void tc_epilogue(const TcLaunch& L, int t, int g, con
             const int head = within / P.dh, i = within - head * P.dh;
             float y0 = v[j], y1 = v[j + 1];
             if (region < 2) {
-                const float2 cs_sn = P.rope[(size_t)pos * (P.dh >> 1) + (i >> 1)];
-                const float cs = cs_sn.x, sn = cs_sn.y;
+                const float cs = cs_sn[j >> 1].x, sn = cs_sn[j >> 1].y;
                 y0 = __fsub_rn(__fmul_rn(v[j], cs), __fmul_rn(v[j + 1], sn));
                 y1 = __fadd_rn(__fmul_rn(v[j], sn), __fmul_rn(v[j + 1], cs));
             }
             if (region == 0) {
-                P.out[(size_t)t * P.ldo + c] = y0;
-                P.out[(size_t)t * P.ldo + c + 1] = y1;
+                *reinterpret_cast<float2*>(P.out + (size_t)t * P.ldo + c) = make_float2(y0, y1);
             } else {
-                const KvView& kv = L.kv;
-                const int page = kv.page_table[row / kv.page_rows];
                 const long long off = (long long)page * kv.page_elems +
                                       ((((long long)P.layer * 2 + (region - 1)) * kv.n_kv + head) * kv.page_rows +
                                        row % kv.page_rows) * kv.dh + i;
@@ -236,27 +249,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
     if (warp == 0) {
-        // ---------------- producer (weights need no dependency; A does)
+        // ---------------- producer (weights need no dependency; A does: the
+        // first ring's weight boxes are issued before griddepcontrol.wait,
+        // overlapping the predecessor's tail)
         if (lane == 0) {
-            asm volatile("griddepcontrol.wait;" ::: "memory");
             const char* A = reinterpret_cast<const char*>(L.xa);
             const char* B = reinterpret_cast<const char*>(L.P.W);
             uint64_t pol;
             asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
             const size_t KT = (size_t)KS;
-            for (int st = st0; st < st1; ++st) {
-                const int i = st - st0, s = i % kTcStages;
-                tc_mbar_wait(&empty_bar[s], ((uint32_t)(i / kTcStages) & 1u) ^ 1u);
+            auto issue_b = [&](int st, int s) {
                 const int ks0 = st * kTcStepsPerStage;
                 const int nks = min(kTcStepsPerStage, KS - ks0);
                 // a tensor box always transfers its full 32 KB (out-of-range
                 // groups / k-steps arrive as zeros)
                 tc_mbar_expect(&full_bar[s], (uint32_t)(nm * nks * kTcABlock + (L.use_tma ? kTcBStage : nks * ng * 1024)));
-                unsigned char* sa = sm + (size_t)s * kTcStageBytes;
-                unsigned char* sb = sa + kTcAStage;
-                for (int m = 0; m < nm; ++m)
-                    tc_bulk(sa + (size_t)m * kTcStepsPerStage * kTcABlock,
-                            A + ((size_t)m * KS + ks0) * kTcABlock, (uint32_t)(nks * kTcABlock), &full_bar[s]);
+                unsigned char* sb = sm + (size_t)s * kTcStageBytes + kTcAStage;
                 if (L.use_tma) {
                     // weights are read once per launch: L2 evict-first
                     asm volatile(
@@ -271,6 +279,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
                             tc_bulk(sb + (size_t)k * (kTcN / 32) * 1024 + gl * 1024,
                                     B + (((size_t)(g0 + gl)) * KT + ks0 + k) * 1024, 1024u, &full_bar[s]);
                 }
+            };
+            const int npre = min(kTcStages, st1 - st0);
+            for (int i = 0; i < npre; ++i) issue_b(st0 + i, i);
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            for (int st = st0; st < st1; ++st) {
+                const int i = st - st0, s = i % kTcStages;
+                if (i >= npre) {
+                    tc_mbar_wait(&empty_bar[s], ((uint32_t)(i / kTcStages) & 1u) ^ 1u);
+                    issue_b(st, s);
+                }
+                const int ks0 = st * kTcStepsPerStage;
+                const int nks = min(kTcStepsPerStage, KS - ks0);
+                unsigned char* sa = sm + (size_t)s * kTcStageBytes;
+                for (int m = 0; m < nm; ++m)
+                    tc_bulk(sa + (size_t)m * kTcStepsPerStage * kTcABlock,
+                            A + ((size_t)m * KS + ks0) * kTcABlock, (uint32_t)(nks * kTcABlock), &full_bar[s]);
             }
         }
     } else if (warp == 1) {
@@ -354,16 +378,29 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
                         float v[32];
 #pragma unroll
                         for (int j = 0; j < 32; ++j) v[j] = 0.f;
-                        for (int zz = 0; zz < L.ksplits; ++zz) {
-                            const float4* pp =
-                                reinterpret_cast<const float4*>(L.part + ((size_t)zz * 256 + r) * ldw + (g0 + gl) * 32);
+                        // split order kept; the loads of up to 4 splits in
+                        // flight per round trip (one split per round trip
+                        // serialised the tail on L2 latency)
+                        for (int z0 = 0; z0 < L.ksplits; z0 += 4) {
+                            float4 q[4][8];
 #pragma unroll
-                            for (int j = 0; j < 8; ++j) {
-                                const float4 q = __ldcg(pp + j);
-                                v[4 * j] += q.x;
-                                v[4 * j + 1] += q.y;
-                                v[4 * j + 2] += q.z;
-                                v[4 * j + 3] += q.w;
+                            for (int b = 0; b < 4; ++b) {
+                                const float4* pp = reinterpret_cast<const float4*>(
+                                    L.part + ((size_t)(z0 + b) * 256 + r) * ldw + (g0 + gl) * 32);
+#pragma unroll
+                                for (int j = 0; j < 8; ++j)
+                                    q[b][j] = z0 + b < L.ksplits ? __ldcg(pp + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+                            }
+#pragma unroll
+                            for (int b = 0; b < 4; ++b) {
+                                if (z0 + b >= L.ksplits) break;
+#pragma unroll
+                                for (int j = 0; j < 8; ++j) {
+                                    v[4 * j] += q[b][j].x;
+                                    v[4 * j + 1] += q[b][j].y;
+                                    v[4 * j + 2] += q[b][j].z;
+                                    v[4 * j + 3] += q[b][j].w;
+                                }
                             }
                         }
                         tc_epilogue<EPI>(L, L.t0 + r, g0 + gl, v);

@@ -15,7 +15,8 @@
 //   warp 1  allocates all 512 TMEM columns; lane 0 issues tcgen05.mma
 //           (kind::f16, M=128, N=256, K=16, fp32 accumulate in TMEM) — eight
 //           per stage — and releases each stage with tcgen05.commit;
-//   warps 2-5 epilogue: tcgen05.ld 32 columns at a time (each thread one row),
+//   warps 2-9 epilogue: tcgen05.ld 32 columns at a time (each thread one row;
+//           two warps per TMEM lane quarter take alternate 32-column groups),
 //           then the same fused epilogues as the decode GEMV (residual + row
 //           statistics, SiLU(gate)*up, RoPE + paged-KV write, store).
 // Operands are UMMA canonical K-major "interleave" tiles: the weights are
@@ -44,7 +45,8 @@ constexpr int kTcABlock = kTcM * kTcKStep * 2;                      // 4 KB: 128
 constexpr int kTcAStage = kTcMSub * kTcABlock * kTcStepsPerStage;   // 32 KB
 constexpr int kTcBStage = kTcN * kTcKStep * kTcStepsPerStage * 2;   // 32 KB
 constexpr int kTcStageBytes = kTcAStage + kTcBStage;
-constexpr int kTcThreads = 6 * 32;
+constexpr int kTcEpiWarps = 8;  // two per TMEM lane quarter
+constexpr int kTcThreads = (2 + kTcEpiWarps) * 32;
 constexpr int kTcMinStagesPerSplit = 8;  // >= 512 k per K-split
 
 __device__ __forceinline__ uint32_t tc_smem(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -326,16 +328,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
                 tc_smem(&acc_bar)));
         }
     } else {
-        // ---------------- epilogue warps 2..5: TMEM lanes 32*(warp%4) ..
+        // ---------------- epilogue warps 2..9: TMEM lanes 32*(warp%4) .., column
+        // groups half, half + 2, ... (half = which of the quarter's two warps)
         asm volatile("griddepcontrol.wait;" ::: "memory");
         tc_mbar_wait(&acc_bar, 0);
         tc_fence_after();
         const int lane_base = 32 * (warp & 3);
+        const int half = (warp - 2) >> 2;
         const int ldw = L.P.ldw;
         for (int m = 0; m < nm; ++m) {
             const int r = m * kTcM + lane_base + lane;  // row within the CTA's 256
             const bool ok = r < L.T;
-            for (int gl = 0; gl < ng; ++gl) {
+            for (int gl = half; gl < ng; gl += 2) {
                 uint32_t u[32];
                 const uint32_t taddr = tmem_base + ((uint32_t)lane_base << 16) + (uint32_t)(m * kTcN + gl * 32);
                 asm volatile(
@@ -362,19 +366,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
         }
         if (L.ksplits > 1) {
             // last K-split CTA of this tile sums the partials in split order
-            asm volatile("bar.sync 1, 128;" ::: "memory");
+            asm volatile("bar.sync 1, %0;" ::"n"(kTcEpiWarps * 32) : "memory");
             if (threadIdx.x == 64) {
                 unsigned tk;
                 asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(tk) : "l"(L.tickets + ntile) : "memory");
                 s_last = tk == (unsigned)L.ksplits - 1 ? 1u : 0u;
                 if (s_last) L.tickets[ntile] = 0u;
             }
-            asm volatile("bar.sync 1, 128;" ::: "memory");
+            asm volatile("bar.sync 1, %0;" ::"n"(kTcEpiWarps * 32) : "memory");
             if (s_last) {
                 for (int m = 0; m < nm; ++m) {
                     const int r = m * kTcM + lane_base + lane;
                     if (r >= L.T) continue;
-                    for (int gl = 0; gl < ng; ++gl) {
+                    for (int gl = half; gl < ng; gl += 2) {
                         float v[32];
 #pragma unroll
                         for (int j = 0; j < 32; ++j) v[j] = 0.f;

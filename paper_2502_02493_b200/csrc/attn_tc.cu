@@ -858,9 +858,36 @@ static int* tca_tickets(cudaStream_t s) {
     return p;
 }
 
+// Pages per chunk CTA of a launch: the cache's capacity rule (kv.attn_ppi),
+// doubled while a batched launch (nprob > 1: a fuzzy group's layers) would
+// need more than one wave of CTAs — at ctx 512 a 4-layer group of the C2
+// drafter is 5 chunks x 8 kv heads x 4 = 160 CTAs, a second wave for 12 of
+// them — up to 8 pages per CTA (4 softmax steps): longer chunks lose more
+// to their serial step chain than the extra waves cost (C5 sweep, ctx 8K:
+// doubling 8 -> 32 pages per CTA made the lp 4 / 8 draft stage 0.4-0.7 ms
+// slower; ctx 512: draft stage -0.15 ms, ctx 2K -0.1 ms;
+// profiles/r2_attn_wave.txt). Single-problem launches (every base pass, so
+// verify and vanilla rows stay bitwise equal) keep the capacity rule.
+// ESPEC_ATTN_WAVE=0 disables.
+int attn_tc_ppi(const PassView& pass, const KvView& kv, int n_heads, int nprob) {
+    static const bool on = [] {
+        const char* e = std::getenv("ESPEC_ATTN_WAVE");
+        return !(e && std::atoi(e) == 0);
+    }();
+    int ppi = kv.attn_ppi;
+    if (!on || nprob <= 1) return ppi;
+    const int pages = (pass.total + 63) / 64;
+    const int groups = (pass.T * (n_heads / kv.n_kv) + kTcaRows - 1) / kTcaRows;
+    auto ctas = [&](int q) { return (long long)((pages + q - 1) / q) * kv.n_kv * groups * nprob; };
+    while (ctas(ppi) > 148 && ppi * 2 <= 8 && (pages + ppi - 1) / ppi > 1) ppi *= 2;
+    return ppi;
+}
+
 template <int DH>
-static void attn_tc_launch(const AttnBatch& b, int nprob, int n_heads, const PassView& pass, const KvView& kv,
+static void attn_tc_launch(const AttnBatch& b, int nprob, int n_heads, const PassView& pass, const KvView& kv_in,
                            cudaStream_t s) {
+    KvView kv = kv_in;
+    kv.attn_ppi = attn_tc_ppi(pass, kv_in, n_heads, nprob);
     TcaLaunch L;
     tca_tensor_map(L.kvmap, kv);
     L.b = b;

@@ -1415,7 +1415,7 @@ public:
             }
             const double kvb = (double)g.size() * 2.0 * ps.view.total * M.kvdim() * dsize(M.c.kv_dtype);
             site(M, 1, kvb, [&] { launch_attention(ab, (int)g.size(), M.qh(), v, kv, stream_); });
-            launches_ += attention_launches(v, kv);
+            launches_ += attention_launches(v, kv, M.qh(), (int)g.size());
         }
     }
 

@@ -690,10 +690,11 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(const __grid_constan
 static bool attn_tc_path(const KvView& kv) {
     return kv.dtype == DT_BF16 && kv.page_rows == 64 && (kv.dh == 64 || kv.dh == 128);
 }
-int attention_launches(const PassView& pass, const KvView& kv) {
+int attention_launches(const PassView& pass, const KvView& kv, int n_heads, int nprob) {
     if (!attn_tc_path(kv)) return 1;
     const int pages = (pass.total + 63) / 64;
-    const int chunks = (pages + kv.attn_ppi - 1) / kv.attn_ppi;
+    const int ppi = attn_tc_ppi(pass, kv, n_heads, nprob);
+    const int chunks = (pages + ppi - 1) / ppi;
     return chunks > 1 && !attn_tc_cluster(chunks, pass.T) ? 2 : 1;
 }
 

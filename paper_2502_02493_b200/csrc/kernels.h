@@ -231,7 +231,8 @@ void launch_attention_tc(const AttnBatch& b, int nprob, int n_heads, const PassV
 // kernels one launch_attention call issues (the tcgen05 path adds a combine
 // kernel when the context spans more than one chunk)
 int attn_tc_cluster(int chunks, int T);  // 1: chunks combine inside a cluster, 2: last chunk CTA combines (attn_tc.cu)
-int attention_launches(const PassView& pass, const KvView& kv);
+int attention_launches(const PassView& pass, const KvView& kv, int n_heads, int nprob);
+int attn_tc_ppi(const PassView& pass, const KvView& kv, int n_heads, int nprob);  // pages per chunk CTA of one launch
 
 // Copy cache rows src[i] -> dst[i] for every layer (commit_path compaction).
 void launch_kv_move(const KvView& kv, const int* src, const int* dst, int n, cudaStream_t s);

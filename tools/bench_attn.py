@@ -9,6 +9,7 @@ from paper_2502_02493_b200 import espec as E  # noqa: E402
 
 CASES = [  # name, T, n_heads, n_kv, dh, ctx, nprob
     ("draft T=1 ctx 600", 1, 32, 8, 128, 600, 1), ("draft T=1 ctx 600 x3", 1, 32, 8, 128, 600, 3),
+    ("draft T=1 ctx 600 x4", 1, 32, 8, 128, 600, 4),
     ("draft T=6 ctx 600", 6, 32, 8, 128, 600, 1), ("base T=6 ctx 600", 6, 64, 8, 128, 600, 1),
     ("base T=1 ctx 600", 1, 64, 8, 128, 600, 1), ("base T=6 ctx 4096", 6, 64, 8, 128, 4096, 1),
     ("base T=6 ctx 8192", 6, 64, 8, 128, 8192, 1), ("draft T=1 ctx 8192", 1, 32, 8, 128, 8192, 1),
